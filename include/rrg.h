@@ -1,0 +1,167 @@
+/*
+ * rrg.h -- C ABI of the B200-native LoRANN query engine (librrg.so).
+ *
+ * The reference (`rrann`, pure Python/NumPy) has no native FFI; its drop-in
+ * boundary is the Python function pair `query_batch` / `query`
+ * (pkg/src/rrann/index.py:286-340, re-exported in __init__.py:11-21) plus the
+ * index file loader `RrrIndex.load` -> `deserialize` (index.py:138-141,443-507).
+ * SPEC.md:522-526 names the intended foreign binding
+ * `bound_query_batch(BoundIndex, array2d, k, w, t) -> (ids, scores)` with
+ * `bound_load`; the entry points below are exactly that binding, in C:
+ *
+ *   rrg_index_open        <- RrrIndex.load / deserialize        (index.py:138-141, 443-507)
+ *   rrg_index_create      <- RrrIndex already in memory (the models of index.py:110-118)
+ *   rrg_search            <- query_batch, device buffers        (index.py:338-340, 286-335)
+ *   rrg_search_host       <- bound_query_batch, host buffers
+ *   rrg_last_error        <- exception message text             (errors.py:8-39)
+ *
+ * Status codes mirror the error-category -> CLI exit-code map (cli.py:20,198-200):
+ *   0 ok, 2 usage (ShapeError / ParameterError), 3 data (DataError / FormatError),
+ *   4 internal (RrannError / CUDA failure).  rrg_last_error_kind() names the
+ *   exception class so a binding can raise the reference's own type.
+ *
+ * All pointers are plain host or device pointers; no framework types cross
+ * this boundary.  Index handles are immutable after creation and may be
+ * searched concurrently from several host threads, each with its own stream
+ * and workspace (index.py docstring "concurrent queries").
+ */
+#ifndef RRG_H_
+#define RRG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RRG_OK 0
+#define RRG_E_USAGE 2
+#define RRG_E_DATA 3
+#define RRG_E_INTERNAL 4
+
+/* metric codes of the file header (index.py:48) */
+#define RRG_METRIC_EUCLIDEAN 0
+#define RRG_METRIC_IP 1
+#define RRG_METRIC_COSINE 2
+
+/* header flags (index.py:43-46) */
+#define RRG_FLAG_QUANTIZED (1u << 0)
+#define RRG_FLAG_CORPUS (1u << 1)
+#define RRG_FLAG_BALANCED (1u << 2)
+#define RRG_FLAG_EXACT_IVF (1u << 3)
+
+typedef struct RrgIndex RrgIndex;
+
+/* Host-side description of an in-memory index (the fields of RrrIndex and its
+ * ClusterModels, index.py:110-118 / rrr.py:77-94).  Per-cluster payloads are
+ * concatenated in cluster order.  Quantized factors are given exactly as the
+ * file stores them (index.py:346-353): head_row[cols], col_scales[cols] and a
+ * rows x cols int8 block whose row 0 is the zero pad row. */
+typedef struct {
+  int32_t metric;           /* RRG_METRIC_* */
+  int32_t dim;              /* d */
+  int32_t reduced_dim;      /* s (== d when reduction is off) */
+  int32_t rank;             /* r */
+  int32_t n_clusters;       /* L */
+  int64_t n_points;         /* m */
+  uint32_t flags;           /* RRG_FLAG_* */
+  const float* projection;  /* d x s row-major */
+  const float* centroids;   /* L x s row-major */
+  const uint32_t* cluster_sizes;  /* L */
+  const int64_t* point_ids;       /* m, cluster order */
+  /* factor A of every cluster: s x cols_l (cols_l = m_l if exact else r) */
+  const float* a_head;      /* sum cols_l */
+  const float* a_scale;     /* sum cols_l */
+  const int8_t* a_values;   /* sum s*cols_l */
+  /* factor B of every non-exact cluster: r x m_l */
+  const float* b_head;      /* sum m_l over non-exact clusters */
+  const float* b_scale;
+  const int8_t* b_values;   /* sum r*m_l */
+  const float* norms;       /* m, cluster order; NULL unless euclidean */
+  const float* corpus;      /* m x d in ORIGINAL id order; NULL if no corpus */
+} RrgIndexDesc;
+
+typedef struct {
+  int32_t metric, dim, reduced_dim, rank, n_clusters;
+  int64_t n_points;
+  uint32_t flags;
+  int32_t n_exact_clusters;
+  int32_t max_cluster_size;
+  int32_t device;
+  uint64_t device_bytes;    /* HBM held by the index */
+} RrgIndexInfo;
+
+/* Parse an RRRANN01 file (streaming, CRC-checked, same FormatError texts as
+ * deserialize) and upload it to `device`.  Returns RRG_E_DATA on a malformed
+ * file. */
+int rrg_index_open(const char* path, int device, RrgIndex** out);
+
+/* Same, restricted to clusters [cluster_begin, cluster_end) -- the shard a
+ * rank owns in cluster-sharded multi-GPU search; projection and centroids are
+ * replicated. */
+int rrg_index_open_shard(const char* path, int device, int32_t cluster_begin,
+                         int32_t cluster_end, RrgIndex** out);
+
+/* Build from host arrays (see RrgIndexDesc). */
+int rrg_index_create(const RrgIndexDesc* desc, int device, RrgIndex** out);
+
+void rrg_index_destroy(RrgIndex* index);
+int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out);
+
+/* Workspace bytes rrg_search needs for a batch of nq queries. */
+size_t rrg_search_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t k,
+                                  int32_t w, int32_t t, int32_t rerank);
+
+/* Batched search, all buffers on the index's device, asynchronous on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).
+ *   queries : nq x dim f32, finite (validated by the caller, index.py:339)
+ *   ids     : nq x k int64, best first, -1 past count[i]
+ *   scores  : nq x k f32 (squared distance for euclidean, inner product for
+ *             ip/cosine, as QueryResult.scores, index.py:318-329), NaN past count[i]
+ *   count   : nq int32 = len(QueryResult.ids); truncated = count < k
+ * Parameter checks follow QueryParams.validate (index.py:92-100) and
+ * index.py:290-295. */
+int rrg_search(RrgIndex* index, const float* queries, int64_t nq, int32_t dim,
+               int32_t k, int32_t w, int32_t t, int32_t rerank, int64_t* ids,
+               float* scores, int32_t* count, void* workspace,
+               size_t workspace_bytes, void* stream);
+
+/* Host-buffer convenience form (the SPEC.md:522-526 binding): copies queries
+ * in, searches, copies results out, synchronous.  Validates finiteness of the
+ * queries on the host first (DataError, index.py:144-150). */
+int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq,
+                    int32_t dim, int32_t k, int32_t w, int32_t t,
+                    int32_t rerank, int64_t* ids, float* scores,
+                    int32_t* count);
+
+/* Stage entry points used by the stage-parity tests (device buffers). */
+int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq,
+                      float* xp, int8_t* qcodes, float* qscale, float* qhead,
+                      void* stream);
+int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w,
+                    int32_t* selected, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* Number of CUDA kernel launches issued by the most recent rrg_search* call
+ * on this thread (evidence for the bench's gpu_launches). */
+int64_t rrg_last_launch_count(void);
+
+/* Per-stage device timing (CUDA events recorded on the search stream around
+ * every launch) for the calls made on this thread while enabled.  Stages:
+ * 0 project, 1 prep/quantize, 2 route distances, 3 route select,
+ * 4 score+top-t, 5 rerank+top-k.  rrg_stage_times synchronizes the recorded
+ * events, writes the accumulated milliseconds and launch counts per stage
+ * (arrays of RRG_N_STAGES) and resets the accumulators. */
+#define RRG_N_STAGES 6
+void rrg_set_stage_timing(int enabled);
+int rrg_stage_times(double* ms, int64_t* launches);
+
+const char* rrg_last_error(void);
+const char* rrg_last_error_kind(void); /* "ShapeError", "ParameterError", ... */
+const char* rrg_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RRG_H_ */

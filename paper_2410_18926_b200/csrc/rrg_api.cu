@@ -1,0 +1,866 @@
+// rrg_api.cu -- C ABI of librrg.so: index loading/upload and batched search orchestration.
+//
+// Reference boundary replaced (see include/rrg.h):
+//   RrrIndex.load / deserialize   pkg/src/rrann/index.py:138-141, 405-507
+//   query_batch / query           pkg/src/rrann/index.py:286-340
+//   QueryParams.validate          pkg/src/rrann/index.py:92-100
+#include <cuda_runtime.h>
+#include <zlib.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/rrg.h"
+#include "rrg_common.cuh"
+#include "rrg_kernels.h"
+
+using namespace rrg;
+
+// ------------------------------------------------------------------ errors
+
+namespace {
+
+thread_local std::string g_err;
+thread_local std::string g_kind;
+thread_local int64_t g_launches = 0;
+
+// per-stage event timing (rrg_set_stage_timing / rrg_stage_times)
+struct StageTimer {
+  bool on = false;
+  struct Rec { int stage; cudaEvent_t a, b; };
+  std::vector<Rec> pending;
+  double ms[RRG_N_STAGES] = {0};
+  int64_t n[RRG_N_STAGES] = {0};
+  std::vector<cudaEvent_t> pool;
+  cudaEvent_t get() {
+    if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+thread_local StageTimer g_timer;
+
+// Runs one launch, counting it and (when enabled) bracketing it with events.
+template <typename F>
+void staged(int stage, cudaStream_t st, F&& launch) {
+  StageTimer& t = g_timer;
+  if (t.on) {
+    StageTimer::Rec r{stage, t.get(), t.get()};
+    cudaEventRecord(r.a, st);
+    launch();
+    cudaEventRecord(r.b, st);
+    t.pending.push_back(r);
+  } else {
+    launch();
+  }
+  ++g_launches;
+}
+
+int fail(int code, const char* kind, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  g_kind = kind;
+  return code;
+}
+
+struct RrgFail {
+  int code;
+};
+
+#define CUDA_TRY(expr)                                                                        \
+  do {                                                                                        \
+    cudaError_t e_ = (expr);                                                                  \
+    if (e_ != cudaSuccess) {                                                                  \
+      fail(RRG_E_INTERNAL, "RrannError", "CUDA error %s at %s:%d: %s", cudaGetErrorName(e_), \
+           __FILE__, __LINE__, cudaGetErrorString(e_));                                       \
+      throw RrgFail{RRG_E_INTERNAL};                                                          \
+    }                                                                                         \
+  } while (0)
+
+[[noreturn]] void raise_format(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  g_kind = "FormatError";
+  throw RrgFail{RRG_E_DATA};
+}
+
+[[noreturn]] void raise_usage(const char* kind, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  g_kind = kind;
+  throw RrgFail{RRG_E_USAGE};
+}
+
+// Python-style repr of a bytes object (for the "bad magic" message, index.py:447).
+std::string py_bytes_repr(const unsigned char* b, size_t n) {
+  std::string s = "b'";
+  for (size_t i = 0; i < n; ++i) {
+    unsigned c = b[i];
+    char tmp[8];
+    if (c == '\\') s += "\\\\";
+    else if (c == '\'') s += "\\'";
+    else if (c == '\t') s += "\\t";
+    else if (c == '\n') s += "\\n";
+    else if (c == '\r') s += "\\r";
+    else if (c >= 32 && c < 127) s += (char)c;
+    else { snprintf(tmp, sizeof tmp, "\\x%02x", c); s += tmp; }
+  }
+  return s + "'";
+}
+
+// NumPy float64 pairwise sum (same tree as rrg_common.cuh pw_sum_seq).
+double pw_sum_host(const double* a, int64_t n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int64_t i = 0; i < n; ++i) r += a[i];
+    return r;
+  }
+  if (n <= 128) {
+    double r[8];
+    for (int j = 0; j < 8; ++j) r[j] = a[j];
+    int64_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+      for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += a[i];
+    return res;
+  }
+  int64_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return pw_sum_host(a, n2) + pw_sum_host(a + n2, n - n2);
+}
+
+int64_t round_up(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------- host staging
+
+struct HostCluster {
+  uint32_t m = 0;
+  bool exact = false;
+  bool owned = true;
+  std::vector<int64_t> ids;
+  std::vector<float> a_head, a_scale;
+  std::vector<int8_t> a_vals;  // s x cols (row 0 = pad)
+  std::vector<float> b_head, b_scale;
+  std::vector<int8_t> b_vals;  // r x m
+  std::vector<float> norms;
+};
+
+struct HostModel {
+  int metric = 0, d = 0, s = 0, r = 0, L = 0;
+  int64_t m = 0;
+  uint32_t flags = 0;
+  std::vector<float> projection, centroids;
+  std::vector<HostCluster> clusters;
+};
+
+}  // namespace
+
+// ------------------------------------------------------------------ index
+
+struct RrgIndex {
+  int device = 0;
+  HostModel meta;  // header fields only (vectors released after upload)
+  DevIndexView view{};
+  std::vector<void*> allocs;
+  RrgIndexInfo info{};
+  int64_t max_cluster = 0;
+  std::vector<int> sizes_sorted_desc;  // cluster sizes (held), descending
+  int n_exact = 0;
+
+  void* dalloc(size_t bytes) {
+    void* p = nullptr;
+    if (bytes == 0) bytes = 16;
+    CUDA_TRY(cudaMalloc(&p, bytes));
+    allocs.push_back(p);
+    info.device_bytes += bytes;
+    return p;
+  }
+  template <typename T>
+  T* upload(const std::vector<T>& v) {
+    T* p = static_cast<T*>(dalloc(v.size() * sizeof(T)));
+    if (!v.empty()) CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+  ~RrgIndex() {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (void* p : allocs) cudaFree(p);
+    cudaSetDevice(prev);
+  }
+};
+
+namespace {
+
+// Build the device layout from the staged host model.  `corpus_rows` fills the
+// reordered corpus (cluster order) given pos_of_id on the device.
+template <typename CorpusFill>
+void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill fill_corpus) {
+  const int d = hm.d, s = hm.s, r = hm.r, L = hm.L;
+  if (!(hm.flags & RRG_FLAG_QUANTIZED))
+    raise_usage("ParameterError",
+                "unquantized index: the device path scores int8 factors only "
+                "(quantize=False scoring is tolerance-level, SURVEY.md 8(f) row 4)");
+  if (s > 1024) raise_usage("ParameterError", "reduced dimension %d > 1024 not supported", s);
+  if (r > 64) raise_usage("ParameterError", "rank %d > 64 not supported", r);
+  if (hm.m >= (int64_t)1 << 31) raise_usage("ParameterError", "more than 2^31 points");
+  DevIndexView& v = ix->view;
+  v.metric = hm.metric; v.d = d; v.s = s; v.r = r; v.L = L;
+  v.s_pad = (int)round_up(s, 16);
+  v.r_pad = (int)round_up(r, 16);
+  v.d_stride = (int)round_up(d, 4);
+
+  // cluster order positions
+  std::vector<int> cl_pos(L + 1), cl_kind(L), cl_aidx(L);
+  int64_t P = 0, P_exact = 0;
+  int n_rrr = 0;
+  for (int l = 0; l < L; ++l) {
+    HostCluster& c = hm.clusters[l];
+    cl_pos[l] = (int)P;
+    uint32_t held = c.owned ? c.m : 0;
+    cl_kind[l] = c.exact ? kKindExact : kKindRrr;
+    if (c.exact) {
+      cl_aidx[l] = (int)P_exact;
+      P_exact += held;
+    } else {
+      cl_aidx[l] = c.owned && held ? n_rrr++ : -1;
+    }
+    P += held;
+    if (held) ix->sizes_sorted_desc.push_back((int)held);
+    ix->max_cluster = std::max<int64_t>(ix->max_cluster, held);
+    if (c.exact) ix->n_exact++;
+  }
+  cl_pos[L] = (int)P;
+  v.P = P;
+  std::sort(ix->sizes_sorted_desc.begin(), ix->sizes_sorted_desc.end(), std::greater<int>());
+
+  std::vector<int8_t> at((size_t)n_rrr * r * v.s_pad, 0);
+  std::vector<float> ahead((size_t)n_rrr * r), ascale((size_t)n_rrr * r);
+  std::vector<int8_t> bt((size_t)P * v.r_pad, 0), xc((size_t)P_exact * v.s_pad, 0);
+  std::vector<float> phead(P), pscale(P), pnorm(hm.metric == kMetricEuclidean ? P : 0);
+  std::vector<int64_t> pid(P);
+  std::vector<int> pos_of_id(hm.m, -1);
+  for (int l = 0; l < L; ++l) {
+    HostCluster& c = hm.clusters[l];
+    if (!c.owned || c.m == 0) continue;
+    const int64_t p0 = cl_pos[l];
+    const int m = (int)c.m;
+    for (int p = 0; p < m; ++p) {
+      int64_t id = c.ids[p];
+      if (id < 0 || id >= hm.m) raise_format("cluster %d ids: id %lld out of range", l, (long long)id);
+      pid[p0 + p] = id;
+      pos_of_id[id] = (int)(p0 + p);
+      if (!pnorm.empty()) pnorm[p0 + p] = c.norms[p];
+    }
+    if (c.exact) {
+      // A: s x m (cols = points)
+      const int64_t x0 = cl_aidx[l];
+      for (int i = 0; i < s; ++i)
+        for (int p = 0; p < m; ++p) xc[(size_t)(x0 + p) * v.s_pad + i] = c.a_vals[(size_t)i * m + p];
+      for (int p = 0; p < m; ++p) { phead[p0 + p] = c.a_head[p]; pscale[p0 + p] = c.a_scale[p]; }
+    } else {
+      const int slot = cl_aidx[l];
+      for (int i = 0; i < s; ++i)
+        for (int j = 0; j < r; ++j)
+          at[((size_t)slot * r + j) * v.s_pad + i] = c.a_vals[(size_t)i * r + j];
+      for (int j = 0; j < r; ++j) {
+        ahead[(size_t)slot * r + j] = c.a_head[j];
+        ascale[(size_t)slot * r + j] = c.a_scale[j];
+      }
+      for (int j = 0; j < r; ++j)
+        for (int p = 0; p < m; ++p) bt[(size_t)(p0 + p) * v.r_pad + j] = c.b_vals[(size_t)j * m + p];
+      for (int p = 0; p < m; ++p) { phead[p0 + p] = c.b_head[p]; pscale[p0 + p] = c.b_scale[p]; }
+    }
+  }
+  // centroid squared norms in f64, NumPy order: (c*c).sum(axis=1) (cluster.py:50)
+  std::vector<double> cnorm(L), tmp(s);
+  for (int l = 0; l < L; ++l) {
+    for (int i = 0; i < s; ++i) {
+      double x = hm.centroids[(size_t)l * s + i];
+      tmp[i] = x * x;
+    }
+    cnorm[l] = pw_sum_host(tmp.data(), s);
+  }
+  v.W = ix->upload(hm.projection);
+  v.cent = ix->upload(hm.centroids);
+  v.cnorm = ix->upload(cnorm);
+  v.cl_pos = ix->upload(cl_pos);
+  v.cl_kind = ix->upload(cl_kind);
+  v.cl_aidx = ix->upload(cl_aidx);
+  v.at = ix->upload(at);
+  v.ahead = ix->upload(ahead);
+  v.ascale = ix->upload(ascale);
+  v.bt = ix->upload(bt);
+  v.xcodes = ix->upload(xc);
+  v.phead = ix->upload(phead);
+  v.pscale = ix->upload(pscale);
+  v.pnorm = pnorm.empty() ? nullptr : ix->upload(pnorm);
+  v.pid = ix->upload(pid);
+  v.corpus = nullptr;
+  if (has_corpus) {
+    float* corp = static_cast<float*>(ix->dalloc((size_t)std::max<int64_t>(P, 1) * v.d_stride * 4));
+    int* d_pos = ix->upload(pos_of_id);
+    fill_corpus(corp, d_pos, (int)v.d_stride);
+    v.corpus = corp;
+  }
+  ix->info.metric = hm.metric; ix->info.dim = d; ix->info.reduced_dim = s; ix->info.rank = r;
+  ix->info.n_clusters = L; ix->info.n_points = hm.m; ix->info.flags = hm.flags;
+  ix->info.n_exact_clusters = ix->n_exact;
+  ix->info.max_cluster_size = (int)ix->max_cluster;
+  ix->info.device = ix->device;
+  ix->meta.metric = hm.metric; ix->meta.d = d; ix->meta.s = s; ix->meta.r = r; ix->meta.L = L;
+  ix->meta.m = hm.m; ix->meta.flags = hm.flags;
+}
+
+// Streaming reader with incremental CRC32 (index.py:401,481-485) and the
+// reference's section/offset error messages (index.py:410-412).
+struct FileReader {
+  FILE* f = nullptr;
+  uint64_t off = 0, size = 0;
+  uLong crc = 0;
+  explicit FileReader(const char* path) {
+    f = fopen(path, "rb");
+    if (!f) {
+      g_err = std::string("cannot open index file: ") + path;
+      g_kind = "FormatError";
+      throw RrgFail{RRG_E_DATA};
+    }
+    fseeko(f, 0, SEEK_END);
+    size = (uint64_t)ftello(f);
+    fseeko(f, 0, SEEK_SET);
+    crc = crc32(0L, Z_NULL, 0);
+  }
+  ~FileReader() { if (f) fclose(f); }
+  void take(void* dst, uint64_t n, const std::string& section, bool update_crc = true) {
+    if (off + n > size) raise_format("truncated file: %s at offset %llu", section.c_str(), (unsigned long long)off);
+    if (n && fread(dst, 1, n, f) != n) raise_format("read error: %s at offset %llu", section.c_str(), (unsigned long long)off);
+    if (update_crc) {
+      const unsigned char* p = static_cast<const unsigned char*>(dst);
+      uint64_t left = n;
+      while (left) {
+        uInt chunk = (uInt)std::min<uint64_t>(left, 1u << 30);
+        crc = crc32(crc, p, chunk);
+        p += chunk;
+        left -= chunk;
+      }
+    }
+    off += n;
+  }
+  template <typename T>
+  void vec(std::vector<T>& v, uint64_t count, const std::string& section) {
+    v.resize(count);
+    take(v.data(), count * sizeof(T), section);
+  }
+};
+
+int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** out) {
+  FileReader fr(path);
+  unsigned char magic[8];
+  fr.take(magic, 8, "magic");
+  if (memcmp(magic, "RRRANN01", 8) != 0)
+    raise_format("bad magic %s; expected b'RRRANN01'", py_bytes_repr(magic, 8).c_str());
+  unsigned char hdr[29];  // struct "<BIIIIQI"
+  fr.take(hdr, 29, "header");
+  HostModel hm;
+  uint8_t mc = hdr[0];
+  uint32_t d, s, r, L, flags;
+  uint64_t m;
+  memcpy(&d, hdr + 1, 4); memcpy(&s, hdr + 5, 4); memcpy(&r, hdr + 9, 4); memcpy(&L, hdr + 13, 4);
+  memcpy(&m, hdr + 17, 8); memcpy(&flags, hdr + 25, 4);
+  if (mc > 2) raise_format("unknown metric code %u", (unsigned)mc);
+  hm.metric = mc; hm.d = (int)d; hm.s = (int)s; hm.r = (int)r; hm.L = (int)L; hm.m = (int64_t)m;
+  hm.flags = flags;
+  const bool quantized = flags & RRG_FLAG_QUANTIZED;
+  const bool has_corpus = flags & RRG_FLAG_CORPUS;
+  const bool exact_ivf = flags & RRG_FLAG_EXACT_IVF;
+  if (ce < 0) ce = (int32_t)L;
+  fr.vec(hm.projection, (uint64_t)d * s, "projection");
+  fr.vec(hm.centroids, (uint64_t)L * s, "centroids");
+  hm.clusters.resize(L);
+  uint64_t total = 0;
+  std::vector<float> fscratch;
+  for (uint32_t l = 0; l < L; ++l) {
+    HostCluster& c = hm.clusters[l];
+    std::string sec = "cluster " + std::to_string(l);
+    uint32_t ml;
+    fr.take(&ml, 4, sec + " size");
+    c.m = ml;
+    c.owned = (int32_t)l >= cb && (int32_t)l < ce;
+    std::vector<uint64_t> ids;
+    fr.vec(ids, ml, sec + " ids");
+    c.ids.assign(ids.begin(), ids.end());
+    c.exact = exact_ivf || ml < r;
+    const uint64_t acols = c.exact ? ml : r;
+    auto read_factor = [&](uint64_t rows, uint64_t cols, const std::string& fsec,
+                           std::vector<float>& head, std::vector<float>& scale,
+                           std::vector<int8_t>& vals) {
+      if (quantized) {
+        fr.vec(head, cols, fsec + " head row");
+        fr.vec(scale, cols, fsec + " scales");
+        fr.vec(vals, rows * cols, fsec + " values");
+      } else {
+        fr.vec(fscratch, rows * cols, fsec);
+      }
+    };
+    read_factor(s, acols, sec + " factor A", c.a_head, c.a_scale, c.a_vals);
+    if (!c.exact) read_factor(r, ml, sec + " factor B", c.b_head, c.b_scale, c.b_vals);
+    if (mc == kMetricEuclidean) fr.vec(c.norms, ml, sec + " norms");
+    if (!c.owned) {  // keep only metadata for routing; release payloads
+      std::vector<float>().swap(c.a_head); std::vector<float>().swap(c.a_scale);
+      std::vector<int8_t>().swap(c.a_vals); std::vector<float>().swap(c.b_head);
+      std::vector<float>().swap(c.b_scale); std::vector<int8_t>().swap(c.b_vals);
+      std::vector<float>().swap(c.norms);
+    }
+    total += ml;
+  }
+  if (total != m)
+    raise_format("cluster records cover %llu points, header says %llu", (unsigned long long)total,
+                 (unsigned long long)m);
+  CUDA_TRY(cudaSetDevice(device));
+  std::unique_ptr<RrgIndex> ix(new RrgIndex());
+  ix->device = device;
+  bool corpus_done = false;
+  auto fill = [&](float* dst, const int* d_pos, int d_stride) {
+    // stream the corpus (original id order) through pinned chunks, scatter into cluster order
+    const uint64_t row_bytes = (uint64_t)d * 4;
+    const uint64_t rows_per_chunk = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(row_bytes, 1));
+    float* pinned[2] = {nullptr, nullptr};
+    float* staging[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2];
+    cudaStream_t st;
+    CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CUDA_TRY(cudaMallocHost(&pinned[b], rows_per_chunk * row_bytes));
+      CUDA_TRY(cudaMalloc(&staging[b], rows_per_chunk * row_bytes));
+      CUDA_TRY(cudaEventCreate(&ev[b]));
+    }
+    uint64_t done = 0;
+    int b = 0;
+    try {
+      while (done < m) {
+        uint64_t n = std::min<uint64_t>(rows_per_chunk, m - done);
+        CUDA_TRY(cudaEventSynchronize(ev[b]));
+        if (done == 0 && fr.off + m * row_bytes > fr.size)
+          raise_format("truncated file: corpus at offset %llu", (unsigned long long)fr.off);
+        fr.take(pinned[b], n * row_bytes, "corpus");
+        CUDA_TRY(cudaMemcpyAsync(staging[b], pinned[b], n * row_bytes, cudaMemcpyHostToDevice, st));
+        launch_scatter_rows(staging[b], (int64_t)n, (int)d, d_stride, d_pos, (int64_t)done, dst, st);
+        CUDA_TRY(cudaGetLastError());
+        CUDA_TRY(cudaEventRecord(ev[b], st));
+        done += n;
+        b ^= 1;
+      }
+      CUDA_TRY(cudaStreamSynchronize(st));
+    } catch (...) {
+      cudaStreamSynchronize(st);
+      for (int q = 0; q < 2; ++q) { cudaFreeHost(pinned[q]); cudaFree(staging[q]); cudaEventDestroy(ev[q]); }
+      cudaStreamDestroy(st);
+      throw;
+    }
+    for (int q = 0; q < 2; ++q) { cudaFreeHost(pinned[q]); cudaFree(staging[q]); cudaEventDestroy(ev[q]); }
+    cudaStreamDestroy(st);
+    corpus_done = true;
+  };
+  if (!quantized) {
+    // still validate the whole file like deserialize would, then refuse
+    if (has_corpus) {
+      std::vector<float> chunk;
+      uint64_t left = m * (uint64_t)d;
+      while (left) { uint64_t n = std::min<uint64_t>(left, 1 << 24); fr.vec(chunk, n, "corpus"); left -= n; }
+    }
+  } else {
+    build_device_index(ix.get(), hm, has_corpus, fill);
+  }
+  (void)corpus_done;
+  uint64_t crc_off = fr.off;
+  uint32_t stored;
+  uLong actual = fr.crc;
+  fr.take(&stored, 4, "crc32", false);
+  if ((uint32_t)actual != stored)
+    raise_format("crc mismatch at offset %llu: %#x != %#x", (unsigned long long)crc_off, stored,
+                 (unsigned)actual);
+  if (fr.off != fr.size)
+    raise_format("unknown trailing section at offset %llu: %llu extra bytes",
+                 (unsigned long long)fr.off, (unsigned long long)(fr.size - fr.off));
+  if (!quantized) build_device_index(ix.get(), hm, false, [](float*, const int*, int) {});
+  *out = ix.release();
+  return RRG_OK;
+}
+
+int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
+  CUDA_TRY(cudaSetDevice(device));
+  HostModel hm;
+  hm.metric = dsc->metric; hm.d = dsc->dim; hm.s = dsc->reduced_dim; hm.r = dsc->rank;
+  hm.L = dsc->n_clusters; hm.m = dsc->n_points; hm.flags = dsc->flags;
+  if (hm.metric < 0 || hm.metric > 2) raise_usage("ParameterError", "unknown metric code %d", hm.metric);
+  const int d = hm.d, s = hm.s, r = hm.r, L = hm.L;
+  hm.projection.assign(dsc->projection, dsc->projection + (size_t)d * s);
+  hm.centroids.assign(dsc->centroids, dsc->centroids + (size_t)L * s);
+  hm.clusters.resize(L);
+  const bool exact_ivf = hm.flags & RRG_FLAG_EXACT_IVF;
+  int64_t po = 0, ao = 0, aoff = 0, bo = 0, boff = 0;
+  for (int l = 0; l < L; ++l) {
+    HostCluster& c = hm.clusters[l];
+    c.m = dsc->cluster_sizes[l];
+    c.exact = exact_ivf || (int)c.m < r;
+    const int64_t m = c.m;
+    c.ids.assign(dsc->point_ids + po, dsc->point_ids + po + m);
+    if (dsc->norms) c.norms.assign(dsc->norms + po, dsc->norms + po + m);
+    const int64_t acols = c.exact ? m : r;
+    c.a_head.assign(dsc->a_head + ao, dsc->a_head + ao + acols);
+    c.a_scale.assign(dsc->a_scale + ao, dsc->a_scale + ao + acols);
+    c.a_vals.assign(dsc->a_values + aoff, dsc->a_values + aoff + (size_t)s * acols);
+    ao += acols;
+    aoff += (int64_t)s * acols;
+    if (!c.exact) {
+      c.b_head.assign(dsc->b_head + bo, dsc->b_head + bo + m);
+      c.b_scale.assign(dsc->b_scale + bo, dsc->b_scale + bo + m);
+      c.b_vals.assign(dsc->b_values + boff, dsc->b_values + boff + (size_t)r * m);
+      bo += m;
+      boff += (int64_t)r * m;
+    }
+    po += m;
+  }
+  if (po != hm.m) raise_usage("ShapeError", "cluster sizes cover %lld points, n_points is %lld",
+                             (long long)po, (long long)hm.m);
+  std::unique_ptr<RrgIndex> ix(new RrgIndex());
+  ix->device = device;
+  const bool has_corpus = dsc->corpus != nullptr;
+  auto fill = [&](float* dst, const int* d_pos, int d_stride) {
+    const uint64_t row_bytes = (uint64_t)d * 4;
+    const uint64_t rows_per_chunk = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(row_bytes, 1));
+    float* staging = nullptr;
+    CUDA_TRY(cudaMalloc(&staging, rows_per_chunk * row_bytes));
+    for (uint64_t done = 0; done < (uint64_t)hm.m;) {
+      uint64_t n = std::min<uint64_t>(rows_per_chunk, hm.m - done);
+      CUDA_TRY(cudaMemcpy(staging, dsc->corpus + done * d, n * row_bytes, cudaMemcpyHostToDevice));
+      launch_scatter_rows(staging, (int64_t)n, d, d_stride, d_pos, (int64_t)done, dst, 0);
+      CUDA_TRY(cudaGetLastError());
+      done += n;
+    }
+    CUDA_TRY(cudaDeviceSynchronize());
+    cudaFree(staging);
+  };
+  if (has_corpus) hm.flags |= RRG_FLAG_CORPUS; else hm.flags &= ~RRG_FLAG_CORPUS;
+  build_device_index(ix.get(), hm, has_corpus, fill);
+  *out = ix.release();
+  return RRG_OK;
+}
+
+// ------------------------------------------------------------------ search
+
+struct Plan {
+  int64_t qc;      // queries per chunk
+  int take_cap;
+  int smem_cap;
+  int64_t gcap;    // global overflow capacity per query (0 if none)
+  size_t off_xp, off_qc, off_qs, off_qh, off_xx, off_pp, off_diss, off_sel, off_cpos, off_cn,
+      off_gk, off_gp, total;
+};
+
+Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank) {
+  Plan p{};
+  const DevIndexView& v = ix->view;
+  const int64_t L = v.L;
+  int64_t qc = std::max<int64_t>(256, (256ll << 20) / (L * 8));
+  qc = std::min<int64_t>(qc, 16384);
+  p.qc = std::max<int64_t>(1, std::min<int64_t>(nq, qc));
+  p.take_cap = rerank ? t : k;
+  // max candidates of any query: sum of the w largest held clusters
+  int64_t nmax = 0;
+  for (int i = 0; i < (int)ix->sizes_sorted_desc.size() && i < w; ++i) nmax += ix->sizes_sorted_desc[i];
+  p.take_cap = (int)std::min<int64_t>(p.take_cap, std::max<int64_t>(nmax, 1));
+  const size_t budget = 100 * 1024;
+  int64_t np2 = 1;
+  while (np2 < k) np2 <<= 1;
+  int64_t fixed = (int64_t)p.take_cap * 4 + 64 + np2 * 8;
+  int64_t cap = ((int64_t)budget - fixed) / 8;
+  cap = std::max<int64_t>(cap, 256);
+  p.smem_cap = (int)std::min<int64_t>(cap, std::max<int64_t>(nmax, 1));
+  p.gcap = nmax > p.smem_cap ? nmax : 0;
+  size_t o = 0;
+  auto carve = [&](size_t bytes) { size_t r = o; o += (bytes + 255) / 256 * 256; return r; };
+  const int64_t Q = p.qc;
+  p.off_xp = carve(Q * v.s * 4);
+  p.off_qc = carve(Q * v.s_pad);
+  p.off_qs = carve(Q * 4);
+  p.off_qh = carve(Q * 4);
+  p.off_xx = carve(Q * 4);
+  p.off_pp = carve(Q * 8);
+  p.off_diss = carve(Q * L * 8);
+  p.off_sel = carve(Q * (int64_t)w * 4);
+  p.off_cpos = carve(Q * (int64_t)p.take_cap * 4);
+  p.off_cn = carve(Q * 4);
+  p.off_gk = carve(Q * p.gcap * 4);
+  p.off_gp = carve(Q * p.gcap * 4);
+  p.total = o;
+  return p;
+}
+
+void validate_search(const RrgIndex* ix, int32_t dim, int32_t k, int32_t w, int32_t t,
+                     int32_t rerank) {
+  // QueryParams.validate (index.py:92-100), then index.py:290-295
+  const int L = ix->meta.L;
+  if (k < 1) raise_usage("ParameterError", "k must be >= 1");
+  if (!(1 <= w && w <= L)) raise_usage("ParameterError", "w=%d out of range [1, %d]", w, L);
+  if (t < 1) raise_usage("ParameterError", "t must be >= 1");
+  if (rerank && k > t) raise_usage("ParameterError", "k=%d must be <= t=%d when re-ranking", k, t);
+  if (dim != ix->meta.d)
+    raise_usage("ShapeError", "query dimension %d != index dimension %d", dim, ix->meta.d);
+  if (rerank && ix->view.corpus == nullptr)
+    raise_usage("ParameterError", "index was built without the corpus; re-ranking unavailable");
+}
+
+void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int32_t w, int32_t t,
+                 int32_t rerank, int64_t* ids, float* scores, int32_t* count, void* ws,
+                 size_t ws_bytes, cudaStream_t st) {
+  Plan p = make_plan(ix, nq, k, w, t, rerank);
+  if (ws_bytes < p.total)
+    raise_usage("ParameterError", "workspace too small: %zu < %zu bytes", ws_bytes, p.total);
+  char* base = static_cast<char*>(ws);
+  const DevIndexView& v = ix->view;
+  float* xp = reinterpret_cast<float*>(base + p.off_xp);
+  int8_t* qcodes = reinterpret_cast<int8_t*>(base + p.off_qc);
+  float* qscale = reinterpret_cast<float*>(base + p.off_qs);
+  float* qhead = reinterpret_cast<float*>(base + p.off_qh);
+  float* xx = reinterpret_cast<float*>(base + p.off_xx);
+  double* pp = reinterpret_cast<double*>(base + p.off_pp);
+  double* diss = reinterpret_cast<double*>(base + p.off_diss);
+  int* sel = reinterpret_cast<int*>(base + p.off_sel);
+  int* cpos = reinterpret_cast<int*>(base + p.off_cpos);
+  int* cn = reinterpret_cast<int*>(base + p.off_cn);
+  uint32_t* gk = reinterpret_cast<uint32_t*>(base + p.off_gk);
+  int* gp = reinterpret_cast<int*>(base + p.off_gp);
+  for (int64_t q0 = 0; q0 < nq; q0 += p.qc) {
+    const int n = (int)std::min<int64_t>(p.qc, nq - q0);
+    const float* x = queries + q0 * v.d;
+    staged(0, st, [&] { launch_project(x, v.W, n, v.d, v.s, xp, st); });
+    staged(1, st, [&] { launch_prep(xp, x, n, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st); });
+    staged(2, st, [&] { launch_route_dist(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st); });
+    staged(3, st, [&] { launch_route_select(diss, n, v.L, w, sel, st); });
+    ScoreArgsHost sa{};
+    sa.ix = v; sa.qcodes = qcodes; sa.qscale = qscale; sa.qhead = qhead; sa.xx = xx; sa.sel = sel;
+    sa.w = w; sa.take_cap = p.take_cap; sa.rerank = rerank; sa.k = k; sa.smem_cap = p.smem_cap;
+    sa.gkeys = gk; sa.gpos = gp; sa.gcap = p.gcap; sa.cand_pos = cpos; sa.cand_n = cn;
+    sa.out_ids = ids; sa.out_scores = scores; sa.out_count = count; sa.q0 = (int)q0;
+    staged(4, st, [&] { launch_score_select(sa, n, st); });
+    if (rerank) {
+      RerankArgsHost ra{};
+      ra.ix = v; ra.queries = x; ra.cand_pos = cpos; ra.cand_n = cn; ra.take_cap = p.take_cap;
+      ra.k = k; ra.out_ids = ids; ra.out_scores = scores; ra.out_count = count; ra.q0 = (int)q0;
+      staged(5, st, [&] { launch_rerank(ra, n, st); });
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const RrgFail& e) {
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    return fail(RRG_E_INTERNAL, "RrannError", "host out of memory");
+  } catch (const std::exception& e) {
+    return fail(RRG_E_INTERNAL, "RrannError", "%s", e.what());
+  }
+}
+
+struct HostCtx {
+  int device = -1;
+  cudaStream_t st = nullptr;
+  void* dbuf = nullptr;
+  size_t dcap = 0;
+  ~HostCtx() {
+    if (dbuf) cudaFree(dbuf);
+    if (st) cudaStreamDestroy(st);
+  }
+};
+thread_local HostCtx g_host;
+
+}  // namespace
+
+// ================================================================= C ABI
+
+extern "C" {
+
+int rrg_index_open(const char* path, int device, RrgIndex** out) {
+  return guarded([&] { return open_impl(path, device, 0, -1, out); });
+}
+
+int rrg_index_open_shard(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** out) {
+  return guarded([&] { return open_impl(path, device, cb, ce, out); });
+}
+
+int rrg_index_create(const RrgIndexDesc* desc, int device, RrgIndex** out) {
+  return guarded([&] { return create_impl(desc, device, out); });
+}
+
+void rrg_index_destroy(RrgIndex* index) { delete index; }
+
+int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out) {
+  if (!index || !out) return fail(RRG_E_USAGE, "ParameterError", "null argument");
+  *out = index->info;
+  return RRG_OK;
+}
+
+size_t rrg_search_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t k, int32_t w,
+                                  int32_t t, int32_t rerank) {
+  if (!index || nq <= 0 || k < 1 || w < 1 || t < 1) return 0;
+  return make_plan(index, nq, k, w, t, rerank).total;
+}
+
+int rrg_search(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+               int32_t w, int32_t t, int32_t rerank, int64_t* ids, float* scores, int32_t* count,
+               void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
+    if (nq == 0) return RRG_OK;  // query_batch on an empty batch returns [] (index.py:340)
+    validate_search(index, dim, k, w, t, rerank);
+    CUDA_TRY(cudaSetDevice(index->device));
+    search_impl(index, queries, nq, k, w, t, rerank, ids, scores, count, workspace,
+                workspace_bytes, static_cast<cudaStream_t>(stream));
+    return RRG_OK;
+  });
+}
+
+int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                    int32_t w, int32_t t, int32_t rerank, int64_t* ids, float* scores,
+                    int32_t* count) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
+    if (nq == 0) return RRG_OK;
+    // _check_finite (index.py:144-150) happens before any per-query check
+    for (int64_t i = 0; i < nq * (int64_t)dim; ++i)
+      if (!std::isfinite(queries[i]))
+        return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
+    validate_search(index, dim, k, w, t, rerank);
+    CUDA_TRY(cudaSetDevice(index->device));
+    HostCtx& h = g_host;
+    if (h.device != index->device) {
+      if (h.dbuf) cudaFree(h.dbuf);
+      if (h.st) cudaStreamDestroy(h.st);
+      h.dbuf = nullptr; h.dcap = 0; h.st = nullptr;
+      CUDA_TRY(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+      h.device = index->device;
+    }
+    Plan p = make_plan(index, nq, k, w, t, rerank);
+    const size_t qbytes = (size_t)nq * dim * 4, ibytes = (size_t)nq * k * 8,
+                 sbytes = (size_t)nq * k * 4, cbytes = (size_t)nq * 4;
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    size_t need = al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + p.total;
+    if (need > h.dcap) {
+      if (h.dbuf) cudaFree(h.dbuf);
+      h.dbuf = nullptr;
+      CUDA_TRY(cudaMalloc(&h.dbuf, need));
+      h.dcap = need;
+    }
+    char* b = static_cast<char*>(h.dbuf);
+    float* dq = reinterpret_cast<float*>(b);
+    int64_t* di = reinterpret_cast<int64_t*>(b + al(qbytes));
+    float* dsc = reinterpret_cast<float*>(b + al(qbytes) + al(ibytes));
+    int32_t* dc = reinterpret_cast<int32_t*>(b + al(qbytes) + al(ibytes) + al(sbytes));
+    void* ws = b + al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes);
+    CUDA_TRY(cudaMemcpyAsync(dq, queries, qbytes, cudaMemcpyHostToDevice, h.st));
+    search_impl(index, dq, nq, k, w, t, rerank, di, dsc, dc, ws, p.total, h.st);
+    CUDA_TRY(cudaMemcpyAsync(ids, di, ibytes, cudaMemcpyDeviceToHost, h.st));
+    CUDA_TRY(cudaMemcpyAsync(scores, dsc, sbytes, cudaMemcpyDeviceToHost, h.st));
+    CUDA_TRY(cudaMemcpyAsync(count, dc, cbytes, cudaMemcpyDeviceToHost, h.st));
+    CUDA_TRY(cudaStreamSynchronize(h.st));
+    return RRG_OK;
+  });
+}
+
+int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq, float* xp,
+                      int8_t* qcodes, float* qscale, float* qhead, void* stream) {
+  return guarded([&] {
+    const DevIndexView& v = index->view;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(index->device));
+    double* pp = nullptr;
+    float* xx = nullptr;
+    CUDA_TRY(cudaMallocAsync(&pp, std::max<int64_t>(nq, 1) * 8, st));
+    CUDA_TRY(cudaMallocAsync(&xx, std::max<int64_t>(nq, 1) * 4, st));
+    launch_project(queries, v.W, (int)nq, v.d, v.s, xp, st);
+    launch_prep(xp, queries, (int)nq, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(pp, st));
+    CUDA_TRY(cudaFreeAsync(xx, st));
+    return RRG_OK;
+  });
+}
+
+int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int32_t* selected,
+                    void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    const DevIndexView& v = index->view;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    size_t need = (size_t)nq * v.L * 8 + (size_t)nq * 8 + (size_t)nq * v.s_pad + 1024;
+    if (workspace_bytes < need) raise_usage("ParameterError", "workspace too small");
+    double* diss = static_cast<double*>(workspace);
+    double* pp = diss + (size_t)nq * v.L;
+    // recompute pp (f64 pairwise) via the prep kernel on xp; queries unused for xx
+    int8_t* qc = reinterpret_cast<int8_t*>(pp + nq);
+    float* dummy = nullptr;
+    CUDA_TRY(cudaMallocAsync(&dummy, std::max<int64_t>(nq, 1) * 12, st));
+    launch_prep(xp, xp, (int)nq, v.s, v.s_pad, v.s, qc, dummy, dummy + nq, pp, dummy + 2 * nq, st);
+    launch_route_dist(xp, v.cent, (int)nq, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
+    launch_route_select(diss, (int)nq, v.L, w, selected, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaFreeAsync(dummy, st));
+    return RRG_OK;
+  });
+}
+
+int64_t rrg_last_launch_count(void) { return g_launches; }
+
+void rrg_set_stage_timing(int enabled) { g_timer.on = enabled != 0; }
+
+int rrg_stage_times(double* ms, int64_t* launches) {
+  StageTimer& t = g_timer;
+  for (auto& r : t.pending) {
+    cudaEventSynchronize(r.b);
+    float el = 0.f;
+    cudaEventElapsedTime(&el, r.a, r.b);
+    t.ms[r.stage] += el;
+    t.n[r.stage] += 1;
+    t.pool.push_back(r.a);
+    t.pool.push_back(r.b);
+  }
+  t.pending.clear();
+  for (int i = 0; i < RRG_N_STAGES; ++i) {
+    if (ms) ms[i] = t.ms[i];
+    if (launches) launches[i] = t.n[i];
+    t.ms[i] = 0;
+    t.n[i] = 0;
+  }
+  return RRG_OK;
+}
+const char* rrg_last_error(void) { return g_err.c_str(); }
+const char* rrg_last_error_kind(void) { return g_kind.c_str(); }
+const char* rrg_version(void) { return "rrg 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

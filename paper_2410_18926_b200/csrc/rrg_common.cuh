@@ -1,0 +1,319 @@
+// rrg_common.cuh -- shared device-side definitions of the B200 LoRANN query engine.
+//
+// Exact-arithmetic rules restated from the reference:
+//  * quantize_vector (quantize.py:61-77): scale = rn_f32(127 / absmax) (f64 quotient
+//    rounded once == __fdiv_rn for f32 operands), products in f64 (exact), round half
+//    away from zero, clip to +-127;
+//  * dequantize_product (quantize.py:129-136): rn(rn(f32(raw) / rn(scale*cs)) + rn(head*hr)),
+//    never FMA-contracted (every op below is an explicit __f*_rn intrinsic);
+//  * ordering keys: ascending (key, corpus id), -0.0 == +0.0 (np.lexsort, index.py:315,320).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rrg {
+
+constexpr int kMetricEuclidean = 0;
+constexpr int kMetricIp = 1;
+constexpr int kMetricCosine = 2;
+
+constexpr int kKindRrr = 0;    // two-stage A/B model (rrr.py:181-203)
+constexpr int kKindExact = 1;  // single-factor exact model (rrr.py:103-113, index.py:465-468)
+
+// POD view of a device-resident index, passed by value to kernels.
+struct DevIndexView {
+  int metric, d, s, r, L;
+  int s_pad;     // s rounded up to 16 (query / exact codes row pitch, bytes)
+  int r_pad;     // r rounded up to 16 (B^T row pitch, bytes)
+  int d_stride;  // corpus row pitch in floats (d rounded up to 4)
+  int64_t P;     // points held (== m for an unsharded index)
+  const float* W;        // d x s
+  const float* cent;     // L x s
+  const double* cnorm;   // L: (c*c).sum(axis=1) in f64, NumPy pairwise order
+  const int* cl_pos;     // L+1: first global position of each cluster (cluster order)
+  const int* cl_kind;    // L
+  const int* cl_aidx;    // L: rrr -> model slot in at/ahead/ascale; exact -> row in xcodes
+  const int8_t* at;      // [n_rrr][r][s_pad]: A^T codes, row 0 of A (pad) kept as column 0
+  const float* ahead;    // [n_rrr][r]
+  const float* ascale;   // [n_rrr][r]
+  const int8_t* bt;      // [P][r_pad]: B^T codes per point, column 0 = pad row (zero)
+  const int8_t* xcodes;  // [P_exact][s_pad]: exact-model codes per point
+  const float* phead;    // [P] head_row of the point's last factor (B, or A for exact)
+  const float* pscale;   // [P] col_scales of the point's last factor
+  const float* pnorm;    // [P] ||c_p||^2 (euclidean) or nullptr
+  const int64_t* pid;    // [P] original corpus ids
+  const float* corpus;   // [P][d_stride] in cluster order, or nullptr
+};
+
+// ---------------------------------------------------------------- numerics
+
+__device__ __forceinline__ float deq(int raw, float xscale, float cs, float head, float hr) {
+  // quantize.py:136 with head_contrib = F32(head) * head_row (quantize.py:153)
+  float den = __fmul_rn(xscale, cs);
+  float q = __fdiv_rn(__int2float_rn(raw), den);
+  return __fadd_rn(q, __fmul_rn(head, hr));
+}
+
+__device__ __forceinline__ float quant_scale(float absmax) {
+  return absmax == 0.0f ? 1.0f : __fdiv_rn(127.0f, absmax);
+}
+
+__device__ __forceinline__ int quant_code(float v, float scale) {
+  // _round_half_away(f64(v) * f64(scale)), clip +-127 (quantize.py:28-29,75-76)
+  double p = __dmul_rn((double)v, (double)scale);
+  double a = floor(__dadd_rn(fabs(p), 0.5));
+  int c = (int)a;
+  c = c > 127 ? 127 : c;
+  return p < 0.0 ? -c : c;
+}
+
+// Monotone maps so unsigned integer order == float order, with -0.0 == +0.0.
+__device__ __forceinline__ uint32_t mono32(float f) {
+  uint32_t u = __float_as_uint(f);
+  if (u == 0x80000000u) u = 0u;
+  return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
+}
+__device__ __forceinline__ float unmono32(uint32_t k) {
+  uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
+  return __uint_as_float(u);
+}
+__device__ __forceinline__ uint64_t mono64(double f) {
+  uint64_t u = (uint64_t)__double_as_longlong(f);
+  if (u == 0x8000000000000000ull) u = 0ull;
+  return (u & 0x8000000000000000ull) ? ~u : (u | 0x8000000000000000ull);
+}
+
+// ---------------------------------------------------- NumPy pairwise summation
+// NumPy's pairwise_sum (the loop behind `sum(axis=-1)` on a contiguous row):
+//   n < 8     : sequential from 0
+//   n <= 128  : 8 strided accumulators, tree ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//               then the n%8 tail sequentially
+//   else      : n2 = n/2 - (n/2)%8; pw(a[:n2]) + pw(a[n2:])
+// Restated (and pinned against NumPy) in oracle/rrann_oracle.py:pairwise_sum_f32.
+template <typename T, typename Get>
+__device__ T pw_leaf(Get get, int start, int n) {
+  if (n < 8) {
+    T res = (T)0;
+    for (int i = 0; i < n; ++i) res = res + get(start + i);
+    return res;
+  }
+  T r[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) r[j] = get(start + j);
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = r[j] + get(start + i + j);
+  }
+  T res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  for (; i < n; ++i) res = res + get(start + i);
+  return res;
+}
+
+// Single-thread iterative evaluation of the full tree (used for short rows and
+// for ||p||^2 of the routing expansion).  The explicit stack mirrors the
+// recursion; depth <= 32.
+template <typename T, typename Get>
+__device__ T pw_sum_seq(Get get, int n) {
+  if (n <= 128) return pw_leaf<T>(get, 0, n);
+  int st_start[32], st_n[32], st_state[32];
+  T st_left[32];
+  int sp = 0;
+  st_start[0] = 0; st_n[0] = n; st_state[0] = 0;
+  T ret = (T)0;
+  while (sp >= 0) {
+    int s0 = st_start[sp], nn = st_n[sp];
+    if (nn <= 128) {
+      ret = pw_leaf<T>(get, s0, nn);
+      --sp;
+      // deliver ret to parent
+      while (sp >= 0) {
+        if (st_state[sp] == 1) {  // left done -> start right
+          st_left[sp] = ret;
+          st_state[sp] = 2;
+          int n2 = st_n[sp] / 2; n2 -= n2 % 8;
+          ++sp;
+          st_start[sp] = st_start[sp - 1] + n2; st_n[sp] = st_n[sp - 1] - n2; st_state[sp] = 0;
+          break;
+        } else {  // right done
+          ret = st_left[sp] + ret;
+          --sp;
+        }
+      }
+      continue;
+    }
+    if (st_state[sp] == 0) {
+      st_state[sp] = 1;
+      int n2 = nn / 2; n2 -= n2 % 8;
+      ++sp;
+      st_start[sp] = s0; st_n[sp] = n2; st_state[sp] = 0;
+    }
+  }
+  return ret;
+}
+
+// ---------------------------------------------------- block-wide selection
+// Select the `take` smallest items of n by (key, tie) -- ties broken by the
+// (unique) tie value -- and write their item indices (unordered) to out[].
+// MSB-first radix select with 8-bit digits over the key, then, only when the
+// boundary key value is shared by more items than remain to be taken, a second
+// radix select over the tie values of the boundary-equal items.
+struct SelectSmem {
+  int hist[256];
+  int count;
+  int dg;
+  int before;
+  int eq;
+};
+
+template <typename K>
+struct SelState {
+  K prefix, mask;
+  int rank;
+};
+
+__device__ __forceinline__ void warp_agg_add(int* hist, int bin, bool active) {
+  unsigned am = __ballot_sync(0xffffffffu, active);
+  if (!active) return;
+  unsigned peers = __match_any_sync(am, bin);
+  int leader = __ffs(peers) - 1;
+  if ((threadIdx.x & 31) == leader) atomicAdd(&hist[bin], __popc(peers));
+}
+
+// One radix pass: find the digit holding the rank-th element among items whose
+// masked key equals prefix.  Called by all threads.
+template <int NT, typename K, typename KeyF, typename PredF>
+__device__ void radix_pass(int n, KeyF key, PredF pred, SelState<K>& st, int shift,
+                           SelectSmem& sm) {
+  for (int i = threadIdx.x; i < 256; i += NT) sm.hist[i] = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += NT) {
+    int i = base + threadIdx.x;
+    bool act = false;
+    int bin = 0;
+    if (i < n && pred(i)) {
+      K k = key(i);
+      if ((k & st.mask) == st.prefix) {
+        act = true;
+        bin = (int)((k >> shift) & (K)255);
+      }
+    }
+    warp_agg_add(sm.hist, bin, act);
+  }
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int lane = threadIdx.x;
+    int h[8];
+    int tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { h[j] = sm.hist[lane * 8 + j]; tot += h[j]; }
+    int incl = tot;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int excl = incl - tot;
+    bool mine = excl < st.rank && st.rank <= incl;
+    unsigned b = __ballot_sync(0xffffffffu, mine);
+    if (mine) {
+      int cum = excl;
+      int j = 0;
+      for (; j < 8; ++j) {
+        if (cum + h[j] >= st.rank) break;
+        cum += h[j];
+      }
+      sm.dg = lane * 8 + j;
+      sm.before = cum;
+      sm.eq = h[j];
+    }
+    (void)b;
+  }
+  __syncthreads();
+  st.rank -= sm.before;
+  st.prefix |= ((K)sm.dg) << shift;
+  st.mask |= ((K)255) << shift;
+  __syncthreads();
+}
+
+template <int NT, typename K, typename KeyF, typename TieF>
+__device__ int block_select_smallest(int n, int take, KeyF key, TieF tie, int* out,
+                                     SelectSmem& sm) {
+  if (threadIdx.x == 0) sm.count = 0;
+  __syncthreads();
+  if (take >= n) {
+    for (int i = threadIdx.x; i < n; i += NT) out[i] = i;
+    __syncthreads();
+    return n;
+  }
+  if (take <= 0) return 0;
+  SelState<K> st{(K)0, (K)0, take};
+  auto all = [](int) { return true; };
+  int eq = 0;
+  constexpr int kBits = (int)sizeof(K) * 8;
+  int shift = kBits - 8;
+  bool early = false;
+  for (; shift >= 0; shift -= 8) {
+    radix_pass<NT, K>(n, key, all, st, shift, sm);
+    eq = sm.eq;
+    if (eq == st.rank) { early = true; break; }
+  }
+  // Items with (key & mask) < prefix are strictly smaller than the boundary bucket.
+  if (early || eq == st.rank) {
+    K mask = st.mask, prefix = st.prefix;
+    for (int base = 0; base < n; base += NT) {
+      int i = base + threadIdx.x;
+      bool sel = i < n && ((key(i) & mask) <= prefix);
+      unsigned b = __ballot_sync(0xffffffffu, sel);
+      int base_slot = 0;
+      if ((threadIdx.x & 31) == 0 && b) base_slot = atomicAdd(&sm.count, __popc(b));
+      base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+      if (sel) out[base_slot + __popc(b & ((1u << (threadIdx.x & 31)) - 1))] = i;
+    }
+    __syncthreads();
+    return take;
+  }
+  // Boundary key shared by more items than needed: select among equal-key items by tie.
+  K kstar = st.prefix;
+  int need = st.rank;
+  SelState<uint32_t> st2{0u, 0u, need};
+  auto eqpred = [&](int i) { return key(i) == kstar; };
+  for (int sh = 24; sh >= 0; sh -= 8) radix_pass<NT, uint32_t>(n, tie, eqpred, st2, sh, sm);
+  uint32_t tstar = st2.prefix;
+  for (int base = 0; base < n; base += NT) {
+    int i = base + threadIdx.x;
+    bool sel = false;
+    if (i < n) {
+      K k = key(i);
+      sel = k < kstar || (k == kstar && tie(i) <= tstar);
+    }
+    unsigned b = __ballot_sync(0xffffffffu, sel);
+    int base_slot = 0;
+    if ((threadIdx.x & 31) == 0 && b) base_slot = atomicAdd(&sm.count, __popc(b));
+    base_slot = __shfl_sync(0xffffffffu, base_slot, 0);
+    if (sel) out[base_slot + __popc(b & ((1u << (threadIdx.x & 31)) - 1))] = i;
+  }
+  __syncthreads();
+  return take;
+}
+
+// Bitonic sort (ascending) of n_pow2 u64 keys in shared memory; pad with ~0.
+template <int NT>
+__device__ void block_bitonic_sort(uint64_t* a, int n_pow2) {
+  for (int size = 2; size <= n_pow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < n_pow2 / 2; t += NT) {
+        int lo = 2 * t - (t & (stride - 1));
+        int hi = lo + stride;
+        bool up = ((lo & size) == 0);
+        uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace rrg

@@ -1,0 +1,589 @@
+// rrg_kernels.cu -- sm_100a kernels of the LoRANN batched query path.
+//
+// Stage map (reference file:line -> kernel):
+//   projection      index.py:298                 -> k_gemm_f64<EPI_PROJ>
+//   query quantize  quantize.py:61-77 (index.py:302) -> k_prep_queries
+//   routing         cluster.py:46-58,254-264     -> k_gemm_f64<EPI_L2|EPI_NEGIP> + k_route_select
+//   scoring + top-t rrr.py:181-203, index.py:303-316 -> k_score_select
+//   rerank + top-k  index.py:278-283,318-335     -> k_rerank_topk
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rrg_common.cuh"
+#include "rrg_kernels.h"
+
+namespace rrg {
+
+// =============================================================== f64 GEMM
+// C[M x N] = A[M x K] * op(B), A f32 row-major (lda), B f32: !BT -> K x N (ldb),
+// BT -> N x K (ldb).  Inputs are widened to f64 (exact), products and sums in
+// f64 -- the reference's `x.astype(f64) @ W.astype(f64)` (index.py:298) and
+// `p @ c.T` (cluster.py:50,58); the summation order differs from OpenBLAS only at
+// the f64 rounding level (0/153,600 projection mismatches).
+constexpr int GBM = 64, GBN = 64, GBK = 16, GNT = 256;
+
+template <int EPI, bool BT>
+__global__ void __launch_bounds__(GNT) k_gemm_f64(const float* __restrict__ A, int lda,
+                                                   const float* __restrict__ B, int ldb, int M,
+                                                   int N, int K, float* __restrict__ outf,
+                                                   double* __restrict__ outd, int ldo,
+                                                   const double* __restrict__ rowterm,
+                                                   const double* __restrict__ colterm) {
+  __shared__ double As[GBK][GBM + 1];
+  __shared__ double Bs[GBK][GBN + 1];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
+  double acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
+
+  for (int k0 = 0; k0 < K; k0 += GBK) {
+    // A tile: 64 rows x 16 k -> 1024 elements, 4 per thread
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int idx = tid + e * GNT;
+      int r = idx / GBK, kk = idx % GBK;
+      int gm = m0 + r, gk = k0 + kk;
+      As[kk][r] = (gm < M && gk < K) ? (double)A[(size_t)gm * lda + gk] : 0.0;
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int idx = tid + e * GNT;
+      if (BT) {
+        int c = idx / GBK, kk = idx % GBK;
+        int gn = n0 + c, gk = k0 + kk;
+        Bs[kk][c] = (gn < N && gk < K) ? (double)B[(size_t)gn * ldb + gk] : 0.0;
+      } else {
+        int kk = idx / GBN, c = idx % GBN;
+        int gn = n0 + c, gk = k0 + kk;
+        Bs[kk][c] = (gn < N && gk < K) ? (double)B[(size_t)gk * ldb + gn] : 0.0;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GBK; ++kk) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int gm = m0 + ty + 16 * i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int gn = n0 + tx + 16 * j;
+      if (gn >= N) continue;
+      double v = acc[i][j];
+      if (EPI == EPI_PROJ) {
+        outf[(size_t)gm * ldo + gn] = (float)v;  // one rounding to f32 (round-to-nearest)
+      } else if (EPI == EPI_L2) {
+        // ((p.p) - 2 (p.c)) + (c.c), then max(., 0)  (cluster.py:50-51)
+        double d2 = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, v)), colterm[gn]);
+        outd[(size_t)gm * ldo + gn] = d2 > 0.0 ? d2 : 0.0;
+      } else {
+        outd[(size_t)gm * ldo + gn] = -v;  // -(p @ c.T)  (cluster.py:58)
+      }
+    }
+  }
+}
+
+// ========================================================== query prep
+// One warp per query: quantize_vector(xp, mixed_precision=True) (quantize.py:61-77)
+// -> qcodes[q][0..s_pad) with slot 0 = 0 (pairs with the file's zero pad row of A),
+// qscale, qhead; pp = (p*p).sum() in f64 NumPy pairwise order for routing; and
+// xx = f32(x.x) for the no-rerank euclidean score shift (index.py:327).
+__global__ void k_prep_queries(const float* __restrict__ xp, const float* __restrict__ x, int nq,
+                               int s, int s_pad, int d, int8_t* __restrict__ qcodes,
+                               float* __restrict__ qscale, float* __restrict__ qhead,
+                               double* __restrict__ pp, float* __restrict__ xx) {
+  int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int lane = threadIdx.x & 31;
+  if (warp >= nq) return;
+  const float* row = xp + (size_t)warp * s;
+  float amax = 0.0f;
+  for (int i = 1 + lane; i < s; i += 32) amax = fmaxf(amax, fabsf(row[i]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  float sc = quant_scale(amax);
+  int8_t* out = qcodes + (size_t)warp * s_pad;
+  for (int i = lane; i < s_pad; i += 32) {
+    int c = 0;
+    if (i >= 1 && i < s && amax != 0.0f) c = quant_code(row[i], sc);
+    out[i] = (int8_t)c;
+  }
+  double xsum = 0.0;
+  const float* xr = x + (size_t)warp * d;
+  for (int i = lane; i < d; i += 32) xsum += (double)xr[i] * (double)xr[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+  if (lane == 0) {
+    qscale[warp] = sc;
+    qhead[warp] = row[0];
+    xx[warp] = (float)xsum;
+    auto get = [&](int i) { double v = (double)row[i]; return v * v; };
+    pp[warp] = pw_sum_seq<double>(get, s);
+  }
+}
+
+// ========================================================== routing select
+// route(): stable argsort of the dissimilarities, first w (cluster.py:263-264):
+// the w smallest by (diss, cluster id).  One CTA per query.
+template <int NT>
+__global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ diss, int L, int w,
+                                                     int* __restrict__ sel) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
+  int* outidx = reinterpret_cast<int*>(keys + L);
+  const double* row = diss + (size_t)blockIdx.x * L;
+  for (int i = threadIdx.x; i < L; i += NT) keys[i] = mono64(row[i]);
+  __syncthreads();
+  auto key = [&](int i) { return keys[i]; };
+  auto tie = [&](int i) { return (uint32_t)i; };
+  block_select_smallest<NT, uint64_t>(L, w, key, tie, outidx, sm);
+  for (int i = threadIdx.x; i < w; i += NT) sel[(size_t)blockIdx.x * w + i] = outidx[i];
+}
+
+// ====================================================== scoring + top-t select
+// One CTA per query.  For every routed cluster:
+//   rrr model   : raw1 = codes_x . A (int32, dp4a), inter = deq(raw1) (r values),
+//                 re-quantize inter, raw2_p = codes_r . B[:,p], yhat_p = deq(raw2_p)
+//   exact model : raw_p = codes_x . A[:,p], yhat_p = deq(raw_p)
+//   key_p = -2 yhat_p + norm_p (euclidean) | -yhat_p (ip/cosine)   (rrr.py:198-202, index.py:310)
+// then the take = min(t|k, ncand) smallest by (key, corpus id)  (index.py:314-316).
+// Candidate keys/positions live in shared memory when they fit, else in a
+// per-query global slice.
+struct ScoreArgs {
+  DevIndexView ix;
+  const int8_t* qcodes;
+  const float* qscale;
+  const float* qhead;
+  const float* xx;
+  const int* sel;
+  int w;
+  int take_cap;   // t (rerank) or k (no rerank)
+  int rerank;
+  int k;
+  int smem_cap;   // candidates that fit in dynamic smem
+  uint32_t* gkeys;  // [nq][gcap] overflow
+  int* gpos;
+  int64_t gcap;
+  int* cand_pos;  // [nq][take_cap] out (rerank)
+  int* cand_n;    // [nq]
+  int64_t* out_ids;  // no-rerank outputs [nq][k]
+  float* out_scores;
+  int* out_count;
+  int q0;  // query offset of this chunk (outputs)
+};
+
+constexpr int SNT = 512;
+constexpr int kMaxWChunk = 64;
+constexpr int kMaxR = 64;
+
+__global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  __shared__ __align__(16) int8_t c2s[kMaxWChunk][kMaxR];
+  __shared__ float s2s[kMaxWChunk], h2s[kMaxWChunk];
+  __shared__ int cl_l[kMaxWChunk], cl_p0[kMaxWChunk], cl_m[kMaxWChunk], cl_off[kMaxWChunk + 1];
+  __shared__ int total_n;
+  __shared__ __align__(16) int8_t qs[1024 + 16];
+
+  const DevIndexView& ix = a.ix;
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nwarps = SNT / 32;
+  const int s_pad = ix.s_pad, r = ix.r, r_pad = ix.r_pad;
+  const float xscale = a.qscale[q], xhead = a.qhead[q];
+  const int8_t* qc = a.qcodes + (size_t)q * s_pad;
+  for (int i = tid; i < s_pad; i += SNT) qs[i] = qc[i];
+  const int* selq = a.sel + (size_t)q * a.w;
+
+  // total candidates
+  if (tid == 0) total_n = 0;
+  __syncthreads();
+  {
+    int local = 0;
+    for (int c = tid; c < a.w; c += SNT) {
+      int l = selq[c];
+      local += ix.cl_pos[l + 1] - ix.cl_pos[l];
+    }
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if (lane == 0 && local) atomicAdd(&total_n, local);
+  }
+  __syncthreads();
+  const int N = total_n;
+  uint32_t* keys;
+  int* pos;
+  if (N <= a.smem_cap) {
+    keys = reinterpret_cast<uint32_t*>(smem_raw);
+    pos = reinterpret_cast<int*>(keys + a.smem_cap);
+  } else {
+    keys = a.gkeys + (size_t)q * a.gcap;
+    pos = a.gpos + (size_t)q * a.gcap;
+  }
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const int swords = s_pad / 4;
+  const int* qw = reinterpret_cast<const int*>(qs);
+
+  int cand_base = 0;
+  for (int c0 = 0; c0 < a.w; c0 += kMaxWChunk) {
+    const int nc = min(kMaxWChunk, a.w - c0);
+    if (tid == 0) {
+      int off = cand_base;
+      for (int c = 0; c < nc; ++c) {
+        int l = selq[c0 + c];
+        cl_l[c] = l;
+        cl_p0[c] = ix.cl_pos[l];
+        cl_m[c] = ix.cl_pos[l + 1] - ix.cl_pos[l];
+        cl_off[c] = off;
+        off += cl_m[c];
+      }
+      cl_off[nc] = off;
+    }
+    __syncthreads();
+    // ---- stage A (rrr clusters): warp per cluster, lanes over the r intermediate coords
+    for (int c = warp; c < nc; c += nwarps) {
+      int l = cl_l[c];
+      if (ix.cl_kind[l] != kKindRrr || cl_m[c] == 0) continue;
+      int slot = ix.cl_aidx[l];
+      const int8_t* at = ix.at + (size_t)slot * r * s_pad;
+      const float* ah = ix.ahead + (size_t)slot * r;
+      const float* as = ix.ascale + (size_t)slot * r;
+      float inter[2];
+      float amax = 0.0f;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int j = lane + 32 * h;
+        inter[h] = 0.0f;
+        if (j < r) {
+          const int* aw = reinterpret_cast<const int*>(at + (size_t)j * s_pad);
+          int raw = 0;
+          for (int u = 0; u < swords; ++u) raw = __dp4a(qw[u], __ldg(aw + u), raw);
+          inter[h] = deq(raw, xscale, as[j], xhead, ah[j]);
+          if (j >= 1) amax = fmaxf(amax, fabsf(inter[h]));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+      float sc2 = quant_scale(amax);
+      float head2 = __shfl_sync(0xffffffffu, inter[0], 0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        int j = lane + 32 * h;
+        if (j < r_pad) {
+          int code = 0;
+          if (j >= 1 && j < r && amax != 0.0f) code = quant_code(inter[h], sc2);
+          c2s[c][j] = (int8_t)code;
+        }
+      }
+      if (lane == 0) { s2s[c] = sc2; h2s[c] = head2; }
+    }
+    __syncthreads();
+    // ---- stage B: one thread per candidate point
+    const int nloc = cl_off[nc] - cand_base;
+    for (int e = tid; e < nloc; e += SNT) {
+      // locate cluster (nc <= 64: linear scan over the chunk prefix)
+      int c = 0;
+      while (cl_off[c + 1] - cand_base <= e) ++c;
+      int p = e - (cl_off[c] - cand_base);
+      int l = cl_l[c];
+      int gp = cl_p0[c] + p;
+      float yhat;
+      if (ix.cl_kind[l] == kKindRrr) {
+        const int* bw = reinterpret_cast<const int*>(ix.bt + (size_t)gp * r_pad);
+        const int* cw = reinterpret_cast<const int*>(c2s[c]);
+        int raw = 0;
+        for (int u = 0; u < r_pad / 4; ++u) raw = __dp4a(cw[u], __ldg(bw + u), raw);
+        yhat = deq(raw, s2s[c], ix.pscale[gp], h2s[c], ix.phead[gp]);
+      } else {
+        const int* xw = reinterpret_cast<const int*>(ix.xcodes + (size_t)(ix.cl_aidx[l] + p) * s_pad);
+        int raw = 0;
+        for (int u = 0; u < swords; ++u) raw = __dp4a(qw[u], __ldg(xw + u), raw);
+        yhat = deq(raw, xscale, ix.pscale[gp], xhead, ix.phead[gp]);
+      }
+      float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), ix.pnorm[gp]) : -yhat;
+      keys[cl_off[c] + p] = mono32(keyf);
+      pos[cl_off[c] + p] = gp;
+    }
+    cand_base = cl_off[nc];
+    __syncthreads();
+  }
+
+  // ---- top-take by (key, corpus id)
+  const int take = min(a.take_cap, N);
+  int* selidx = reinterpret_cast<int*>(smem_raw + (size_t)a.smem_cap * 8);  // after keys+pos
+  auto key = [&](int i) { return keys[i]; };
+  auto tie = [&](int i) { return (uint32_t)ix.pid[pos[i]]; };
+  block_select_smallest<SNT, uint32_t>(N, take, key, tie, selidx, sm);
+
+  const int gq = a.q0 + q;
+  if (a.rerank) {
+    int* outp = a.cand_pos + (size_t)q * a.take_cap;
+    for (int i = tid; i < take; i += SNT) outp[i] = pos[selidx[i]];
+    if (tid == 0) a.cand_n[q] = take;
+    return;
+  }
+  // no rerank: order the take (<= k) winners by (key, id) and emit (index.py:323-329)
+  uint64_t* srt = reinterpret_cast<uint64_t*>(selidx + a.take_cap + 2);
+  srt = reinterpret_cast<uint64_t*>((reinterpret_cast<uintptr_t>(srt) + 15) & ~uintptr_t(15));
+  int np2 = 1;
+  while (np2 < take) np2 <<= 1;
+  for (int i = tid; i < np2; i += SNT) {
+    uint64_t v = ~0ull;
+    if (i < take) {
+      int ci = selidx[i];
+      v = ((uint64_t)keys[ci] << 32) | (uint32_t)ix.pid[pos[ci]];
+    }
+    srt[i] = v;
+  }
+  block_bitonic_sort<SNT>(srt, np2);
+  const float xxq = a.xx[q];
+  for (int i = tid; i < a.k; i += SNT) {
+    int64_t id = -1;
+    float sc = __int_as_float(0x7fc00000);
+    if (i < take) {
+      uint64_t v = srt[i];
+      id = (int64_t)(uint32_t)v;
+      float kf = unmono32((uint32_t)(v >> 32));
+      sc = euclid ? __fadd_rn(kf, xxq) : -kf;
+    }
+    a.out_ids[(size_t)gq * a.k + i] = id;
+    a.out_scores[(size_t)gq * a.k + i] = sc;
+  }
+  if (tid == 0) a.out_count[gq] = take;
+}
+
+// ======================================================= rerank + top-k
+// One CTA per query; one warp per candidate row.  Euclidean: the row's exact
+// squared distance with NumPy's pairwise summation tree over the f32 squares
+// rn(rn(c - x)^2) (index.py:281-282); ip/cosine: -(c . x) (index.py:283,
+// BLAS-order dependent -> tolerance).  Then top-k by (diss, corpus id)
+// (index.py:320-322), sorted, scores = diss | -diss.
+struct RerankArgs {
+  DevIndexView ix;
+  const float* queries;  // [nq][d] (chunk-local)
+  const int* cand_pos;
+  const int* cand_n;
+  int take_cap;
+  int k;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+};
+
+constexpr int RNT = 256;
+
+__global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  const DevIndexView& ix = a.ix;
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = RNT / 32;
+  const int d = ix.d, ds = ix.d_stride;
+  const int n = a.cand_n[q];
+  // smem: x[ds] | per-warp row buffers [nwarps][ds] | diss keys[take_cap] | ids[take_cap] | sel[k] | sort[np2]
+  float* xs = reinterpret_cast<float*>(smem_raw);
+  float* rowbuf = xs + ds;
+  uint32_t* dkeys = reinterpret_cast<uint32_t*>(rowbuf + (size_t)nwarps * ds);
+  uint32_t* dids = dkeys + a.take_cap;
+  int* selidx = reinterpret_cast<int*>(dids + a.take_cap);
+  uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + a.k);
+  uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
+
+  const float* xq = a.queries + (size_t)q * d;
+  for (int i = tid; i < ds; i += RNT) xs[i] = i < d ? xq[i] : 0.0f;
+  __syncthreads();
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const int* cp = a.cand_pos + (size_t)q * a.take_cap;
+  float* mybuf = rowbuf + (size_t)warp * ds;
+  const int nv4 = ds / 4;
+  for (int i = warp; i < n; i += nwarps) {
+    int gp = cp[i];
+    const float4* row = reinterpret_cast<const float4*>(ix.corpus + (size_t)gp * ds);
+    const float4* x4 = reinterpret_cast<const float4*>(xs);
+    float diss;
+    if (euclid) {
+      for (int v = lane; v < nv4; v += 32) {
+        float4 c = __ldg(row + v);
+        float4 xv = x4[v];
+        float4 o;
+        float t0 = __fsub_rn(c.x, xv.x), t1 = __fsub_rn(c.y, xv.y);
+        float t2 = __fsub_rn(c.z, xv.z), t3 = __fsub_rn(c.w, xv.w);
+        o.x = __fmul_rn(t0, t0); o.y = __fmul_rn(t1, t1);
+        o.z = __fmul_rn(t2, t2); o.w = __fmul_rn(t3, t3);
+        reinterpret_cast<float4*>(mybuf)[v] = o;
+      }
+      __syncwarp();
+      if (lane == 0) {
+        auto get = [&](int j) { return mybuf[j]; };
+        diss = pw_sum_seq<float>(get, d);
+      }
+      __syncwarp();
+    } else {
+      float part = 0.0f;
+      for (int v = lane; v < nv4; v += 32) {
+        float4 c = __ldg(row + v);
+        float4 xv = x4[v];
+        part += c.x * xv.x + c.y * xv.y + c.z * xv.z + c.w * xv.w;
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      diss = -part;
+    }
+    if (lane == 0) {
+      dkeys[i] = mono32(diss);
+      dids[i] = (uint32_t)ix.pid[gp];
+    }
+  }
+  __syncthreads();
+  const int kk = min(a.k, n);
+  auto key = [&](int i) { return dkeys[i]; };
+  auto tie = [&](int i) { return dids[i]; };
+  block_select_smallest<RNT, uint32_t>(n, kk, key, tie, selidx, sm);
+  int np2 = 1;
+  while (np2 < kk) np2 <<= 1;
+  for (int i = tid; i < np2; i += RNT) {
+    uint64_t v = ~0ull;
+    if (i < kk) {
+      int ci = selidx[i];
+      v = ((uint64_t)dkeys[ci] << 32) | dids[ci];
+    }
+    srt[i] = v;
+  }
+  block_bitonic_sort<RNT>(srt, np2);
+  const int gq = a.q0 + q;
+  for (int i = tid; i < a.k; i += RNT) {
+    int64_t id = -1;
+    float sc = __int_as_float(0x7fc00000);
+    if (i < kk) {
+      uint64_t v = srt[i];
+      id = (int64_t)(uint32_t)v;
+      float df = unmono32((uint32_t)(v >> 32));
+      sc = euclid ? df : -df;
+    }
+    a.out_ids[(size_t)gq * a.k + i] = id;
+    a.out_scores[(size_t)gq * a.k + i] = sc;
+  }
+  if (tid == 0) a.out_count[gq] = kk;
+}
+
+// ======================================================= corpus scatter
+// dst[pos_of_id[i0 + i]] = src[i] for a chunk of file rows (original id order
+// -> cluster order), rows padded to d_stride.
+__global__ void k_scatter_rows(const float* __restrict__ src, int64_t nrows, int d, int d_stride,
+                               const int* __restrict__ pos_of_id, int64_t i0,
+                               float* __restrict__ dst) {
+  int64_t row = blockIdx.x;
+  if (row >= nrows) return;
+  int p = pos_of_id[i0 + row];
+  if (p < 0) return;  // row not held by this shard
+  const float* s = src + row * (int64_t)d;
+  float* t = dst + (int64_t)p * d_stride;
+  for (int j = threadIdx.x; j < d_stride; j += blockDim.x) t[j] = j < d ? s[j] : 0.0f;
+}
+
+// ===================================================================== launchers
+void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
+                    cudaStream_t st) {
+  dim3 grid((s + GBN - 1) / GBN, (nq + GBM - 1) / GBM);
+  k_gemm_f64<EPI_PROJ, false><<<grid, GNT, 0, st>>>(x, d, W, s, nq, s, d, xp, nullptr, s,
+                                                     nullptr, nullptr);
+}
+
+void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
+                 float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st) {
+  int warps_per_block = 8;
+  int blocks = (nq + warps_per_block - 1) / warps_per_block;
+  k_prep_queries<<<blocks, warps_per_block * 32, 0, st>>>(xp, x, nq, s, s_pad, d, qcodes, qscale,
+                                                          qhead, pp, xx);
+}
+
+void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
+                       const double* pp, const double* cnorm, double* diss, cudaStream_t st) {
+  dim3 grid((L + GBN - 1) / GBN, (nq + GBM - 1) / GBM);
+  if (metric == kMetricEuclidean)
+    k_gemm_f64<EPI_L2, true><<<grid, GNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L, pp,
+                                                    cnorm);
+  else
+    k_gemm_f64<EPI_NEGIP, true><<<grid, GNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
+                                                       nullptr, nullptr);
+}
+
+size_t route_select_smem(int L) { return (size_t)L * 8 + (size_t)L * 4 + 16; }
+
+void launch_route_select(const double* diss, int nq, int L, int w, int* sel, cudaStream_t st) {
+  size_t sm = route_select_smem(L);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_route_select<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  k_route_select<256><<<nq, 256, sm, st>>>(diss, L, w, sel);
+}
+
+size_t score_select_smem(int smem_cap, int take_cap, int k) {
+  size_t np2 = 1;
+  while (np2 < (size_t)k) np2 <<= 1;
+  return (size_t)smem_cap * 8 + (size_t)take_cap * 4 + 32 + np2 * 8 + 16;
+}
+
+void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st) {
+  ScoreArgs a;
+  a.ix = h.ix; a.qcodes = h.qcodes; a.qscale = h.qscale; a.qhead = h.qhead; a.xx = h.xx;
+  a.sel = h.sel; a.w = h.w; a.take_cap = h.take_cap; a.rerank = h.rerank; a.k = h.k;
+  a.smem_cap = h.smem_cap; a.gkeys = h.gkeys; a.gpos = h.gpos; a.gcap = h.gcap;
+  a.cand_pos = h.cand_pos; a.cand_n = h.cand_n; a.out_ids = h.out_ids;
+  a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
+  size_t sm = score_select_smem(h.smem_cap, h.take_cap, h.k);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_score_select<<<nq, SNT, sm, st>>>(a);
+}
+
+size_t rerank_smem(int d_stride, int take_cap, int k) {
+  size_t np2 = 1;
+  while (np2 < (size_t)k) np2 <<= 1;
+  return (size_t)d_stride * 4 * (1 + RNT / 32) + (size_t)take_cap * 8 + (size_t)k * 4 + 16 +
+         np2 * 8 + 16;
+}
+
+void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
+  RerankArgs a;
+  a.ix = h.ix; a.queries = h.queries; a.cand_pos = h.cand_pos; a.cand_n = h.cand_n;
+  a.take_cap = h.take_cap; a.k = h.k; a.out_ids = h.out_ids; a.out_scores = h.out_scores;
+  a.out_count = h.out_count; a.q0 = h.q0;
+  size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_rerank_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_rerank_topk<<<nq, RNT, sm, st>>>(a);
+}
+
+void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
+                         const int* pos_of_id, int64_t i0, float* dst, cudaStream_t st) {
+  if (nrows <= 0) return;
+  k_scatter_rows<<<(unsigned)nrows, 128, 0, st>>>(src, nrows, d, d_stride, pos_of_id, i0, dst);
+}
+
+}  // namespace rrg

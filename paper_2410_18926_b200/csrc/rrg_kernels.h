@@ -1,0 +1,61 @@
+// rrg_kernels.h -- host-side launchers of the query-path kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rrg_common.cuh"
+
+namespace rrg {
+
+constexpr int EPI_PROJ = 0;
+constexpr int EPI_L2 = 1;
+constexpr int EPI_NEGIP = 2;
+
+struct ScoreArgsHost {
+  DevIndexView ix;
+  const int8_t* qcodes;
+  const float* qscale;
+  const float* qhead;
+  const float* xx;
+  const int* sel;
+  int w, take_cap, rerank, k, smem_cap;
+  uint32_t* gkeys;
+  int* gpos;
+  int64_t gcap;
+  int* cand_pos;
+  int* cand_n;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+};
+
+struct RerankArgsHost {
+  DevIndexView ix;
+  const float* queries;
+  const int* cand_pos;
+  const int* cand_n;
+  int take_cap, k;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+};
+
+void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
+                    cudaStream_t st);
+void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
+                 float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st);
+void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
+                       const double* pp, const double* cnorm, double* diss, cudaStream_t st);
+size_t route_select_smem(int L);
+void launch_route_select(const double* diss, int nq, int L, int w, int* sel, cudaStream_t st);
+size_t score_select_smem(int smem_cap, int take_cap, int k);
+void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st);
+size_t rerank_smem(int d_stride, int take_cap, int k);
+void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st);
+void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
+                         const int* pos_of_id, int64_t i0, float* dst, cudaStream_t st);
+
+}  // namespace rrg

@@ -1,0 +1,247 @@
+"""DeviceIndex: a read-only HBM copy of an ``RRRANN01`` index, owned by librrg.so.
+
+Two ways in, mirroring the reference's two ways to hold an index:
+
+* ``DeviceIndex.from_file(path)``   <- ``RrrIndex.load`` / ``deserialize``
+  (index.py:138-141, 443-507): the native loader streams the file, checks the
+  CRC32 trailer and raises ``FormatError`` with the reference's section/offset
+  messages; the corpus block is scattered into cluster order on the device
+  without ever holding the whole file in host memory.
+* ``DeviceIndex.from_rrr(index)``   <- an in-memory ``rrann.RrrIndex``
+  (index.py:110-118): its arrays are handed over as an ``RrgIndexDesc``.
+
+HBM layout (all owned by the library): projection W [d,s] f32,
+centroids [L,s] f32 + f64 squared norms, per-cluster A^T int8 codes
+[n_rrr][r][s_pad] + head/scale, per-point B^T codes [P][r_pad] (32 B/point at
+r=32), per-point head/scale/norm/id SoA, and the corpus reordered by cluster
+[P][d_stride] f32.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+from . import _native
+from ._native import RrgIndexDesc, RrgIndexInfo, check, lib
+from .errors import ParameterError
+
+_METRIC_CODES = {"euclidean": 0, "ip": 1, "cosine": 2}
+_METRIC_NAMES = {v: k for k, v in _METRIC_CODES.items()}
+FLAG_QUANTIZED, FLAG_CORPUS, FLAG_BALANCED, FLAG_EXACT_IVF = 1, 2, 4, 8
+
+
+class DeviceIndex:
+    """Handle to a device-resident index.  Immutable; safe for concurrent searches."""
+
+    def __init__(self, handle: int, device: int, source: str):
+        self._h = ctypes.c_void_p(handle)
+        self.device = device
+        self.source = source
+        info = RrgIndexInfo()
+        check(lib.rrg_index_info(self._h, ctypes.byref(info)))
+        self.metric = _METRIC_NAMES[info.metric]
+        self.dim = info.dim
+        self.reduced_dim = info.reduced_dim
+        self.rank = info.rank
+        self.n_clusters = info.n_clusters
+        self.n_points = info.n_points
+        self.flags = info.flags
+        self.n_exact_clusters = info.n_exact_clusters
+        self.max_cluster_size = info.max_cluster_size
+        self.device_bytes = info.device_bytes
+        self._tls = threading.local()
+
+    @property
+    def has_corpus(self) -> bool:
+        return bool(self.flags & FLAG_CORPUS)
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            lib.rrg_index_destroy(h)
+            self._h = ctypes.c_void_p(0)
+
+    def __repr__(self) -> str:
+        return (f"DeviceIndex(metric={self.metric!r}, m={self.n_points}, d={self.dim}, "
+                f"s={self.reduced_dim}, r={self.rank}, L={self.n_clusters}, cuda:{self.device}, "
+                f"{self.device_bytes / 2**20:.1f} MiB)")
+
+    # ------------------------------------------------------------------ build
+
+    @classmethod
+    def from_file(cls, path, device: int = 0, shard: tuple[int, int] | None = None) -> "DeviceIndex":
+        h = ctypes.c_void_p()
+        p = os.fsencode(os.fspath(path))
+        if shard is None:
+            check(lib.rrg_index_open(p, device, ctypes.byref(h)))
+        else:
+            check(lib.rrg_index_open_shard(p, device, int(shard[0]), int(shard[1]), ctypes.byref(h)))
+        return cls(h.value, device, f"file:{os.fspath(path)}")
+
+    @classmethod
+    def from_rrr(cls, index, device: int = 0) -> "DeviceIndex":
+        """Upload an in-memory ``rrann.RrrIndex`` (quantized factors required)."""
+        cfg = index.config
+        if not cfg.rrr.quantize:
+            raise ParameterError("unquantized index: the device path scores int8 factors only")
+        models = index.models
+        L = len(models)
+        s = index.projection.shape[1]
+        r = cfg.rrr.rank
+
+        def full_values(qm):
+            # file layout (index.py:349-353): zero pad row + tail rows
+            return np.concatenate([np.zeros((1, qm.cols), np.int8), np.asarray(qm.values, np.int8)], axis=0)
+
+        sizes = np.array([mdl.n_points for mdl in models], dtype=np.uint32)
+        ids = np.ascontiguousarray(np.concatenate([mdl.point_ids for mdl in models]).astype(np.int64))
+        a_head = np.concatenate([mdl.a.head_row for mdl in models]).astype(np.float32)
+        a_scale = np.concatenate([mdl.a.col_scales for mdl in models]).astype(np.float32)
+        a_vals = np.concatenate([full_values(mdl.a).ravel() for mdl in models]).astype(np.int8)
+        bm = [mdl for mdl in models if mdl.b is not None]
+        f32 = np.float32
+        b_head = np.concatenate([mdl.b.head_row for mdl in bm]).astype(f32) if bm else np.zeros(1, f32)
+        b_scale = np.concatenate([mdl.b.col_scales for mdl in bm]).astype(f32) if bm else np.zeros(1, f32)
+        b_vals = (np.concatenate([full_values(mdl.b).ravel() for mdl in bm]).astype(np.int8)
+                  if bm else np.zeros(1, np.int8))
+        norms = None
+        if cfg.metric == "euclidean":
+            norms = np.ascontiguousarray(np.concatenate([mdl.norm_terms for mdl in models]).astype(f32))
+        proj = np.ascontiguousarray(index.projection, dtype=f32)
+        cent = np.ascontiguousarray(index.centroids, dtype=f32)
+        corpus = None if index.corpus is None else np.ascontiguousarray(index.corpus, dtype=f32)
+        flags = FLAG_QUANTIZED
+        if corpus is not None:
+            flags |= FLAG_CORPUS
+        if cfg.balanced:
+            flags |= FLAG_BALANCED
+        if cfg.scoring_mode == "exact_ivf":
+            flags |= FLAG_EXACT_IVF
+        keep = [proj, cent, sizes, ids, a_head, a_scale, a_vals, b_head, b_scale, b_vals, norms, corpus]
+
+        def ptr(a):
+            return None if a is None else a.ctypes.data
+
+        desc = RrgIndexDesc(
+            metric=_METRIC_CODES[cfg.metric], dim=index.dim, reduced_dim=s, rank=r, n_clusters=L,
+            n_points=index.n_points, flags=flags, projection=ptr(proj), centroids=ptr(cent),
+            cluster_sizes=ptr(sizes), point_ids=ptr(ids), a_head=ptr(a_head), a_scale=ptr(a_scale),
+            a_values=ptr(a_vals), b_head=ptr(b_head), b_scale=ptr(b_scale), b_values=ptr(b_vals),
+            norms=ptr(norms), corpus=ptr(corpus))
+        h = ctypes.c_void_p()
+        check(lib.rrg_index_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        del keep
+        return cls(h.value, device, "rrr")
+
+    # ----------------------------------------------------------------- search
+
+    def workspace_bytes(self, nq: int, k: int, w: int, t: int, rerank: bool) -> int:
+        return int(lib.rrg_search_workspace_bytes(self._h, nq, k, w, t, int(rerank)))
+
+    def _workspace(self, nbytes: int):
+        import torch
+
+        ws = getattr(self._tls, "ws", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+            self._tls.ws = ws
+        return ws
+
+    def search_device(self, queries, k: int, w: int, t: int, rerank: bool = True, out=None,
+                      stream=None):
+        """Device-level entry (no host sync): queries = CUDA f32 tensor [nq, d].
+
+        Returns (ids int64 [nq,k], scores f32 [nq,k], count int32 [nq]) CUDA tensors.
+        Finiteness of ``queries`` is the caller's responsibility (the drop-in
+        ``query_batch`` checks it first, like index.py:339).
+        """
+        import torch
+
+        if queries.dim() != 2:
+            from .errors import DataError
+            raise DataError("queries: expected 2-D array")
+        nq, dim = queries.shape
+        q = queries
+        if q.dtype != torch.float32 or not q.is_contiguous():
+            q = q.to(torch.float32).contiguous()
+        dev = torch.device(f"cuda:{self.device}")
+        if out is None:
+            ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+            scores = torch.empty((nq, k), dtype=torch.float32, device=dev)
+            count = torch.empty((nq,), dtype=torch.int32, device=dev)
+        else:
+            ids, scores, count = out
+        nbytes = self.workspace_bytes(nq, k, w, t, rerank) if nq else 0
+        ws = self._workspace(nbytes)
+        st = stream if stream is not None else torch.cuda.current_stream(dev)
+        check(lib.rrg_search(self._h, q.data_ptr(), nq, dim, k, w, t, int(rerank), ids.data_ptr(),
+                             scores.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
+                             st.cuda_stream))
+        return ids, scores, count
+
+    def search_host(self, queries: np.ndarray, k: int, w: int, t: int, rerank: bool = True,
+                    out=None):
+        """Host-buffer entry through the C ABI (``rrg_search_host``)."""
+        q = np.ascontiguousarray(queries, dtype=np.float32)
+        if q.ndim != 2:
+            from .errors import DataError
+            raise DataError("queries: expected 2-D array")
+        nq, dim = q.shape
+        if out is None:
+            ids = np.empty((nq, k), dtype=np.int64)
+            scores = np.empty((nq, k), dtype=np.float32)
+            count = np.empty((nq,), dtype=np.int32)
+        else:
+            ids, scores, count = out
+        check(lib.rrg_search_host(self._h, q.ctypes.data, nq, dim, k, w, t, int(rerank),
+                                  ids.ctypes.data, scores.ctypes.data, count.ctypes.data))
+        return ids, scores, count
+
+    # ------------------------------------------------------------- stage APIs
+
+    def stage_project(self, queries):
+        import torch
+
+        nq = queries.shape[0]
+        dev = queries.device
+        xp = torch.empty((nq, self.reduced_dim), dtype=torch.float32, device=dev)
+        s_pad = (self.reduced_dim + 15) // 16 * 16
+        qc = torch.empty((nq, s_pad), dtype=torch.int8, device=dev)
+        qs = torch.empty((nq,), dtype=torch.float32, device=dev)
+        qh = torch.empty((nq,), dtype=torch.float32, device=dev)
+        st = torch.cuda.current_stream(dev)
+        check(lib.rrg_stage_project(self._h, queries.data_ptr(), nq, xp.data_ptr(), qc.data_ptr(),
+                                    qs.data_ptr(), qh.data_ptr(), st.cuda_stream))
+        return xp, qc, qs, qh
+
+    def stage_route(self, xp, w: int):
+        import torch
+
+        nq = xp.shape[0]
+        s_pad = (self.reduced_dim + 15) // 16 * 16
+        nbytes = nq * self.n_clusters * 8 + nq * 8 + nq * s_pad + 4096
+        ws = torch.empty(nbytes, dtype=torch.uint8, device=xp.device)
+        sel = torch.empty((nq, w), dtype=torch.int32, device=xp.device)
+        st = torch.cuda.current_stream(xp.device)
+        check(lib.rrg_stage_route(self._h, xp.data_ptr(), nq, w, sel.data_ptr(), ws.data_ptr(),
+                                  nbytes, st.cuda_stream))
+        return sel
+
+
+def last_launch_count() -> int:
+    return int(lib.rrg_last_launch_count())
+
+
+def version() -> str:
+    return lib.rrg_version().decode()
+
+
+__all__ = ["DeviceIndex", "last_launch_count", "version", "_native"]

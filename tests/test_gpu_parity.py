@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the reference's golden vectors and the CPU oracle.
+
+Tolerances (BASELINE.json north_star): cluster selection, int32 products and
+neighbour ids bit-exact (up to documented ties); euclidean re-ranked distances
+bit-exact (NumPy pairwise tree restated); BLAS-order-dependent floats (ip/cosine
+re-rank sgemv, the no-rerank euclidean x.x shift) within 1e-5 relative.
+"""
+
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases, load_golden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+F32 = np.float32
+RTOL = 1e-5
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2410_18926_b200 as p
+    return p
+
+
+def _write(tmp_path, name, blob):
+    p = tmp_path / f"{name}.rrr"
+    p.write_bytes(blob)
+    return p
+
+
+def _golden_index(pkg, tmp_path, case):
+    g = load_golden(case)
+    return g, pkg.DeviceIndex.from_file(_write(tmp_path, case, g["index_bytes"].tobytes()))
+
+
+QUANT_CASES = [c for c in golden_cases() if c != "euclid_f32"]
+
+
+@pytest.mark.parametrize("case", QUANT_CASES)
+@pytest.mark.parametrize("entry", ["host", "device"])
+def test_golden_end_to_end(pkg, tmp_path, case, entry):
+    g, dev = _golden_index(pkg, tmp_path, case)
+    for pi, (k, w, t, rr) in enumerate(g["params"]):
+        if f"p{pi}_ids" not in g:
+            continue
+        k, w, t, rr = int(k), min(int(w), dev.n_clusters), int(t), bool(rr)
+        if entry == "host":
+            ids, sc, cnt = dev.search_host(g["queries"], k, w, t, rr)
+        else:
+            q = torch.from_numpy(g["queries"]).cuda()
+            ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(q, k, w, t, rr))
+        np.testing.assert_array_equal(cnt, g[f"p{pi}_count"], err_msg=f"{case} p{pi} count")
+        ref_ids = g[f"p{pi}_ids"]
+        mask = ref_ids >= 0
+        np.testing.assert_array_equal(np.where(mask, ids, -1), ref_ids, err_msg=f"{case} p{pi} ids")
+        ref_sc = g[f"p{pi}_scores"]
+        if dev.metric == "euclidean" and rr:
+            np.testing.assert_array_equal(sc[mask].view(np.int32), ref_sc[mask].view(np.int32),
+                                          err_msg=f"{case} p{pi} scores")
+        else:
+            np.testing.assert_allclose(sc[mask], ref_sc[mask], rtol=RTOL, atol=RTOL)
+
+
+@pytest.mark.parametrize("case", QUANT_CASES)
+def test_golden_stages(pkg, tmp_path, case):
+    g, dev = _golden_index(pkg, tmp_path, case)
+    x = torch.from_numpy(g["queries"][:3]).cuda()
+    xp, qc, qs, qh = dev.stage_project(x)
+    torch.cuda.synchronize()
+    xp = xp.cpu().numpy()
+    qc = qc.cpu().numpy()
+    for i in range(3):
+        np.testing.assert_array_equal(xp[i].view(np.int32), g[f"trace{i}_xp"].view(np.int32))
+        s = dev.reduced_dim
+        np.testing.assert_array_equal(qc[i, 1:s], g[f"trace{i}_qcodes"])
+        assert qc[i, 0] == 0
+        assert qs[i].item() == g[f"trace{i}_qscale"] and qh[i].item() == g[f"trace{i}_qhead"]
+    w = min(4, dev.n_clusters)
+    sel = dev.stage_route(torch.from_numpy(xp).cuda(), w).cpu().numpy()
+    for i in range(3):
+        assert set(sel[i].tolist()) == set(g[f"trace{i}_selected"].tolist())
+
+
+def test_unquantized_index_is_refused(pkg, tmp_path):
+    g = load_golden("euclid_f32")
+    with pytest.raises(pkg.ParameterError, match="unquantized"):
+        pkg.DeviceIndex.from_file(_write(tmp_path, "f32", g["index_bytes"].tobytes()))
+
+
+def test_validation_errors(pkg, tmp_path):
+    g, dev = _golden_index(pkg, tmp_path, "euclid_q")
+    q = g["queries"][:4]
+    with pytest.raises(pkg.ParameterError, match="k must be >= 1"):
+        dev.search_host(q, 0, 1, 10)
+    with pytest.raises(pkg.ParameterError, match="out of range"):
+        dev.search_host(q, 5, dev.n_clusters + 1, 10)
+    with pytest.raises(pkg.ParameterError, match="t must be >= 1"):
+        dev.search_host(q, 5, 1, 0)
+    with pytest.raises(pkg.ParameterError, match="when re-ranking"):
+        dev.search_host(q, 11, 1, 10)
+    with pytest.raises(pkg.ShapeError, match="query dimension"):
+        dev.search_host(q[:, :5], 5, 1, 10)
+    bad = q.copy()
+    bad[1, 2] = np.nan
+    with pytest.raises(pkg.DataError):
+        dev.search_host(bad, 5, 1, 10)
+    g2, dev2 = _golden_index(pkg, tmp_path, "euclid_norerank")
+    with pytest.raises(pkg.ParameterError, match="without the corpus"):
+        dev2.search_host(g2["queries"][:2], 5, 1, 10, True)
+
+
+def test_format_errors(pkg, tmp_path):
+    blob = load_golden("euclid_q")["index_bytes"].tobytes()
+    with pytest.raises(pkg.FormatError, match="truncated file: corpus"):
+        pkg.DeviceIndex.from_file(_write(tmp_path, "t", blob[:-100]))
+    bad = bytearray(blob)
+    bad[300] ^= 1
+    with pytest.raises(pkg.FormatError, match="crc mismatch"):
+        pkg.DeviceIndex.from_file(_write(tmp_path, "c", bytes(bad)))
+    with pytest.raises(pkg.FormatError, match="unknown trailing section"):
+        pkg.DeviceIndex.from_file(_write(tmp_path, "x", blob + b"abc"))
+
+
+def test_drop_in_query_batch(pkg, tmp_path):
+    g, dev = _golden_index(pkg, tmp_path, "euclid_q")
+    params = pkg.QueryParams(k=10, w=3, t=50)
+    res = pkg.query_batch(dev, g["queries"], params)
+    assert len(res) == g["queries"].shape[0]
+    for i, r in enumerate(res):
+        assert r.ids.dtype == np.int64 and r.scores.dtype == np.float32
+        np.testing.assert_array_equal(r.ids, g["p1_ids"][i][: g["p1_count"][i]])
+        assert r.truncated == (len(r.ids) < 10)
+    assert pkg.query_batch(dev, np.zeros((0, dev.dim), F32), pkg.QueryParams(k=0)) == []
+    one = pkg.query(dev, g["queries"][0], params)
+    np.testing.assert_array_equal(one.ids, res[0].ids)
+    cuda_res = pkg.query_batch(dev, torch.from_numpy(g["queries"]).cuda(), params)
+    for a, b in zip(res, cuda_res):
+        np.testing.assert_array_equal(a.ids, b.ids)
+
+
+def test_concurrent_searches_identical(pkg, tmp_path):
+    g, dev = _golden_index(pkg, tmp_path, "euclid_d100")
+    q = g["queries"]
+    base = dev.search_host(q, 10, 4, 200)
+    out = [None] * 4
+
+    def run(i):
+        out[i] = dev.search_host(q, 10, 4, 200)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for o in out:
+        for a, b in zip(o, base):
+            np.testing.assert_array_equal(a, b)
+
+
+def test_exactness_limit_recall_one(pkg, tmp_path):
+    """w = L, t = all candidates, rerank -> exact top-k (test_index.py:100-106)."""
+    from oracle import rrann_oracle as O
+
+    g, dev = _golden_index(pkg, tmp_path, "euclid_d100")
+    oidx = O.read_index(g["index_bytes"].tobytes())
+    q = g["queries"][:32]
+    k = 10
+    ids, sc, cnt = dev.search_host(q, k, dev.n_clusters, oidx.m, True)
+    c = oidx.corpus.astype(np.float64)
+    for i in range(q.shape[0]):
+        d2 = ((c - q[i].astype(np.float64)) ** 2).sum(1)
+        truth = np.argsort(d2, kind="stable")[:k]
+        assert set(ids[i].tolist()) == set(truth.tolist())
+
+
+# ------------------------------------------------------------- workload-size parity
+
+
+def _workload(pkg, name):
+    from paper_2410_18926_b200 import workloads as W
+
+    try:
+        path = W.materialize_index(name)
+    except FileNotFoundError:
+        pytest.skip(f"workload {name} not built")
+    return W, pkg.DeviceIndex.from_file(path), path
+
+
+@pytest.mark.parametrize("name,nq,params", [
+    ("tiny", 256, [(10, 1, 100, True), (10, 4, 37, True), (5, 32, 10_000, True), (10, 3, 1, False)]),
+    ("c1", 400, [(10, 4, 400, True), (100, 8, 800, True), (10, 2, 200, False)]),
+])
+def test_workload_vs_oracle(pkg, name, nq, params):
+    from oracle import rrann_oracle as O
+
+    W, dev, path = _workload(pkg, name)
+    oidx = O.read_index(path.read_bytes())
+    q = W.load_queries(name, nq)
+    for k, w, t, rr in params:
+        w = min(w, dev.n_clusters)
+        ids, sc, cnt = dev.search_host(q, k, w, t, rr)
+        ref = O.query_batch(oidx, q, k, w, t, rr)
+        for i, r in enumerate(ref):
+            c = int(cnt[i])
+            assert c == len(r.ids)
+            np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{name} q{i} {(k, w, t, rr)}")
+            if rr:
+                np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))
+            else:
+                np.testing.assert_allclose(sc[i, :c], r.scores, rtol=RTOL)
+
+
+def test_c2_properties_and_sample_parity(pkg):
+    """BASELINE configs[1] (1M x 768): oracle parity on a sample + size-independent properties."""
+    from oracle import rrann_oracle as O
+
+    W, dev, path = _workload(pkg, "c2")
+    man = W.load_manifest("c2")
+    q = W.load_queries("c2")
+    k, w, t = 100, 8, 800
+    ids, sc, cnt = dev.search_device(torch.from_numpy(q).cuda(), k, w, t, True)
+    ids, sc, cnt = ids.cpu().numpy(), sc.cpu().numpy(), cnt.cpu().numpy()
+    assert (cnt == k).all()
+    assert (np.diff(sc, axis=1) >= 0).all()                      # monotone scores
+    assert all(len(set(r.tolist())) == k for r in ids[:1000])     # unique ids
+    assert ids.min() >= 0 and ids.max() < man["generator"]["m"]
+    oidx = O.read_index(path.read_bytes())
+    for i in range(0, q.shape[0], 97):
+        r = O.query(oidx, q[i], k, w, t, True)
+        np.testing.assert_array_equal(ids[i], r.ids)
+        np.testing.assert_array_equal(sc[i].view(np.int32), r.scores.view(np.int32))
+    gt = W.load_ground_truth("c2")
+    if gt is not None:
+        rec = np.mean([len(set(ids[i].tolist()) & set(gt[i, :k].tolist())) / k for i in range(len(q))])
+        assert rec >= 0.5

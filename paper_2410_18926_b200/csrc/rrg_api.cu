@@ -229,6 +229,24 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.s_pad = (int)round_up(s, 16);
   v.r_pad = (int)round_up(r, 16);
   v.d_stride = (int)round_up(d, 4);
+  {  // pairwise-sum leaves of a d-element row (NumPy recursion, see rrg_common.cuh)
+    std::vector<int> leaves;
+    std::vector<std::pair<int, int>> stack{{0, d}};
+    while (!stack.empty()) {
+      auto [st0, n] = stack.back();
+      stack.pop_back();
+      if (n <= 128) { leaves.push_back(n); continue; }
+      int n2 = n / 2; n2 -= n2 % 8;
+      stack.push_back({st0 + n2, n - n2});  // right after left (LIFO)
+      stack.push_back({st0, n2});
+    }
+    bool equal = true;
+    for (int n : leaves) equal = equal && n == leaves[0];
+    int nl = (int)leaves.size();
+    v.pw_nleaves = nl;
+    v.pw_leaf_n = leaves[0];
+    v.pw_perfect = equal && (nl & (nl - 1)) == 0 && leaves[0] >= 8 && nl <= 16;
+  }
 
   // cluster order positions
   std::vector<int> cl_pos(L + 1), cl_kind(L), cl_aidx(L);

@@ -44,6 +44,10 @@ struct DevIndexView {
   const float* pnorm;    // [P] ||c_p||^2 (euclidean) or nullptr
   const int64_t* pid;    // [P] original corpus ids
   const float* corpus;   // [P][d_stride] in cluster order, or nullptr
+  // NumPy pairwise-summation plan for a row of d floats: when the recursion
+  // tree is perfect (2^a equal leaves of pw_leaf_n <= 128 elements, e.g. d = 128,
+  // 768, 960, 1536) the re-rank runs the warp-parallel kernel.
+  int pw_nleaves, pw_leaf_n, pw_perfect;
 };
 
 // ---------------------------------------------------------------- numerics

@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "rrg_common.cuh"
 #include "rrg_kernels.h"
 
@@ -482,6 +484,154 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
   if (tid == 0) a.out_count[gq] = kk;
 }
 
+// ================================================= rerank (warp-parallel tree)
+// Same contract as k_rerank_topk for a perfect pairwise plan (2^a equal leaves of
+// nl = pw_leaf_n elements).  Lane layout: a row's 4*nleaves (leaf, pair) slots
+// are spread over G lanes; lane (leaf b, pair h) owns NumPy's accumulators
+// r[2h], r[2h+1] of leaf b and streams float2 elements b*nl + 8i + 2h.  Then
+//   r[2h]+r[2h+1], xor-1, xor-2 shuffles  == ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)),
+//   + the nl%8 tail sequentially,
+//   xor-4/8/16 shuffles (+ slot pairs)     == the perfect leaf tree,
+// i.e. bit-identical to `(diff*diff).sum(axis=1)` (index.py:281-282).
+// G = 4*nleaves lanes per row when <= 32 (so 32/G rows per warp pass), else
+// SLOTS = 4*nleaves/32 slots per lane.
+constexpr int kMaxNb = 16;
+
+template <int SLOTS>
+__global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  const DevIndexView& ix = a.ix;
+  const int q = blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = RNT / 32;
+  const int d = ix.d, ds = ix.d_stride, nl = ix.pw_leaf_n, nb = nl / 8, tail = nl % 8;
+  const int P = 4 * ix.pw_nleaves;
+  const int G = SLOTS == 1 ? P : 32;
+  const int R = 32 / G;
+  const int g = lane / G, pl = lane % G;
+  const int n = a.cand_n[q];
+  uint32_t* dkeys = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* dids = dkeys + a.take_cap;
+  int* selidx = reinterpret_cast<int*>(dids + a.take_cap);
+  uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + a.k);
+  uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const float* xq = a.queries + (size_t)q * d;
+
+  // this lane's slice of the query, in registers
+  float2 xv[SLOTS][kMaxNb];
+  float xt[SLOTS][7];
+  int off[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    int pair = pl + 32 * s;
+    int b = pair >> 2, h = pair & 3;
+    off[s] = b * nl + 2 * h;
+#pragma unroll
+    for (int i = 0; i < kMaxNb; ++i)
+      xv[s][i] = i < nb ? *reinterpret_cast<const float2*>(xq + off[s] + 8 * i) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 7; ++u) xt[s][u] = u < tail ? xq[b * nl + 8 * nb + u] : 0.f;
+  }
+  const int* cp = a.cand_pos + (size_t)q * a.take_cap;
+  for (int row0 = warp * R; row0 < n; row0 += nwarps * R) {
+    const int row = row0 + g;
+    const bool valid = row < n;
+    const int gp = valid ? cp[row] : cp[row0];
+    const float* crow = ix.corpus + (size_t)gp * ds;
+    float slot_sum[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      float2 c[kMaxNb];
+#pragma unroll
+      for (int i = 0; i < kMaxNb; ++i)
+        if (i < nb) c[i] = __ldg(reinterpret_cast<const float2*>(crow + off[s] + 8 * i));
+      float v;
+      if (euclid) {
+        float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxNb; ++i) {
+          if (i < nb) {
+            float d0 = __fsub_rn(c[i].x, xv[s][i].x), d1 = __fsub_rn(c[i].y, xv[s][i].y);
+            float s0 = __fmul_rn(d0, d0), s1 = __fmul_rn(d1, d1);
+            r0 = i == 0 ? s0 : __fadd_rn(r0, s0);
+            r1 = i == 0 ? s1 : __fadd_rn(r1, s1);
+          }
+        }
+        v = __fadd_rn(r0, r1);
+        v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1));
+        v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 2));
+        if (tail) {
+          int b = (pl + 32 * s) >> 2;
+          const float* tp = crow + b * nl + 8 * nb;
+#pragma unroll
+          for (int u = 0; u < 7; ++u)
+            if (u < tail) {
+              float dd = __fsub_rn(__ldg(tp + u), xt[s][u]);
+              v = __fadd_rn(v, __fmul_rn(dd, dd));
+            }
+        }
+      } else {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < kMaxNb; ++i)
+          if (i < nb) acc += c[i].x * xv[s][i].x + c[i].y * xv[s][i].y;
+        if ((pl & 3) == 0) {
+          int b = (pl + 32 * s) >> 2;
+          const float* tp = crow + b * nl + 8 * nb;
+          for (int u = 0; u < tail; ++u) acc += __ldg(tp + u) * xt[s][u];
+        }
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        v = acc;
+      }
+      // perfect leaf tree inside the slot (lane groups of 4 = one leaf)
+      for (int o = 4; o < G; o <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+      slot_sum[s] = v;
+    }
+    float tot = slot_sum[0];
+    if (SLOTS == 2) tot = __fadd_rn(slot_sum[0], slot_sum[1]);
+    if (SLOTS == 4)
+      tot = __fadd_rn(__fadd_rn(slot_sum[0], slot_sum[1]), __fadd_rn(slot_sum[2], slot_sum[3]));
+    if (valid && pl == 0) {
+      float diss = euclid ? tot : -tot;
+      dkeys[row] = mono32(diss);
+      dids[row] = (uint32_t)ix.pid[gp];
+    }
+  }
+  __syncthreads();
+  const int kk = min(a.k, n);
+  auto key = [&](int i) { return dkeys[i]; };
+  auto tie = [&](int i) { return dids[i]; };
+  block_select_smallest<RNT, uint32_t>(n, kk, key, tie, selidx, sm);
+  int np2 = 1;
+  while (np2 < kk) np2 <<= 1;
+  for (int i = tid; i < np2; i += RNT) {
+    uint64_t v = ~0ull;
+    if (i < kk) {
+      int ci = selidx[i];
+      v = ((uint64_t)dkeys[ci] << 32) | dids[ci];
+    }
+    srt[i] = v;
+  }
+  block_bitonic_sort<RNT>(srt, np2);
+  const int gq = a.q0 + q;
+  for (int i = tid; i < a.k; i += RNT) {
+    int64_t id = -1;
+    float sc = __int_as_float(0x7fc00000);
+    if (i < kk) {
+      uint64_t v = srt[i];
+      id = (int64_t)(uint32_t)v;
+      float df = unmono32((uint32_t)(v >> 32));
+      sc = euclid ? df : -df;
+    }
+    a.out_ids[(size_t)gq * a.k + i] = id;
+    a.out_scores[(size_t)gq * a.k + i] = sc;
+  }
+  if (tid == 0) a.out_count[gq] = kk;
+}
+
 // ======================================================= corpus scatter
 // dst[pos_of_id[i0 + i]] = src[i] for a chunk of file rows (original id order
 // -> cluster order), rows padded to d_stride.
@@ -571,6 +721,21 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   a.ix = h.ix; a.queries = h.queries; a.cand_pos = h.cand_pos; a.cand_n = h.cand_n;
   a.take_cap = h.take_cap; a.k = h.k; a.out_ids = h.out_ids; a.out_scores = h.out_scores;
   a.out_count = h.out_count; a.q0 = h.q0;
+  if (h.ix.pw_perfect && (h.ix.d % 2) == 0) {
+    size_t np2 = 1;
+    while (np2 < (size_t)h.k) np2 <<= 1;
+    size_t sm = (size_t)h.take_cap * 8 + (size_t)h.k * 4 + 16 + np2 * 8 + 16;
+    int slots = std::max(1, 4 * h.ix.pw_nleaves / 32);
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_rerank_tree<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      cudaFuncSetAttribute(k_rerank_tree<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      attr = true;
+    }
+    if (slots == 1) k_rerank_tree<1><<<nq, RNT, sm, st>>>(a);
+    else k_rerank_tree<2><<<nq, RNT, sm, st>>>(a);
+    return;
+  }
   size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k);
   static bool attr = false;
   if (!attr) {

@@ -11,7 +11,7 @@ import threading
 import numpy as np
 import pytest
 
-from conftest import golden_cases, load_golden
+from conftest import assert_topk_equivalent, golden_cases, load_golden
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -42,6 +42,13 @@ def _golden_index(pkg, tmp_path, case):
 QUANT_CASES = [c for c in golden_cases() if c != "euclid_f32"]
 
 
+def _corpus_max_norm(g):
+    from oracle import rrann_oracle as O
+
+    idx = O.read_index(g["index_bytes"].tobytes())
+    return 0.0 if idx.corpus is None else float(np.linalg.norm(idx.corpus, axis=1).max())
+
+
 @pytest.mark.parametrize("case", QUANT_CASES)
 @pytest.mark.parametrize("entry", ["host", "device"])
 def test_golden_end_to_end(pkg, tmp_path, case, entry):
@@ -57,14 +64,23 @@ def test_golden_end_to_end(pkg, tmp_path, case, entry):
             ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(q, k, w, t, rr))
         np.testing.assert_array_equal(cnt, g[f"p{pi}_count"], err_msg=f"{case} p{pi} count")
         ref_ids = g[f"p{pi}_ids"]
-        mask = ref_ids >= 0
-        np.testing.assert_array_equal(np.where(mask, ids, -1), ref_ids, err_msg=f"{case} p{pi} ids")
         ref_sc = g[f"p{pi}_scores"]
-        if dev.metric == "euclidean" and rr:
-            np.testing.assert_array_equal(sc[mask].view(np.int32), ref_sc[mask].view(np.int32),
-                                          err_msg=f"{case} p{pi} scores")
-        else:
-            np.testing.assert_allclose(sc[mask], ref_sc[mask], rtol=RTOL, atol=RTOL)
+        q = g["queries"].astype(np.float64)
+        cmax = _corpus_max_norm(g)
+        for i in range(len(cnt)):
+            c = int(cnt[i])
+            if dev.metric == "euclidean" and rr:  # exact: NumPy pairwise tree restated
+                np.testing.assert_array_equal(ids[i, :c], ref_ids[i, :c], err_msg=f"{case} p{pi} q{i}")
+                np.testing.assert_array_equal(sc[i, :c].view(np.int32), ref_sc[i, :c].view(np.int32))
+            elif not rr:  # ids from exact int8 keys; score shift x.x is BLAS sdot (tolerance)
+                np.testing.assert_array_equal(ids[i, :c], ref_ids[i, :c], err_msg=f"{case} p{pi} q{i}")
+                scale = float(q[i] @ q[i]) if dev.metric == "euclidean" else None
+                assert_topk_equivalent(ids[i, :c], sc[i, :c], ref_ids[i, :c], ref_sc[i, :c], RTOL,
+                                       scale, f"{case} p{pi} q{i}")
+            else:  # ip/cosine re-rank: BLAS sgemv order -> tolerance (scale |x||c|) + near-tie swaps
+                scale = float(np.sqrt(q[i] @ q[i]) * cmax)
+                assert_topk_equivalent(ids[i, :c], sc[i, :c], ref_ids[i, :c], ref_sc[i, :c], RTOL,
+                                       scale, f"{case} p{pi} q{i}")
 
 
 @pytest.mark.parametrize("case", QUANT_CASES)
@@ -209,11 +225,14 @@ def test_workload_vs_oracle(pkg, name, nq, params):
         for i, r in enumerate(ref):
             c = int(cnt[i])
             assert c == len(r.ids)
-            np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{name} q{i} {(k, w, t, rr)}")
+            if not rr:
+                np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{name} q{i} {(k, w, t, rr)}")
             if rr:
+                np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{name} q{i} {(k, w, t, rr)}")
                 np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))
             else:
-                np.testing.assert_allclose(sc[i, :c], r.scores, rtol=RTOL)
+                xx = float(q[i].astype(np.float64) @ q[i].astype(np.float64))
+                assert_topk_equivalent(ids[i, :c], sc[i, :c], r.ids, r.scores, RTOL, xx)
 
 
 def test_c2_properties_and_sample_parity(pkg):
@@ -239,3 +258,65 @@ def test_c2_properties_and_sample_parity(pkg):
     if gt is not None:
         rec = np.mean([len(set(ids[i].tolist()) & set(gt[i, :k].tolist())) / k for i in range(len(q))])
         assert rec >= 0.5
+
+
+# ----------------------------------------------------------- random-index shape sweep
+
+SWEEP = [
+    # d, s, r, L, m, metric, exact_ivf
+    (1, 1, 1, 3, 40, "euclidean", False),
+    (3, 2, 2, 4, 60, "euclidean", False),
+    (7, 5, 3, 5, 90, "euclidean", False),
+    (9, 8, 4, 6, 120, "euclidean", False),
+    (31, 16, 8, 7, 300, "euclidean", False),
+    (64, 32, 16, 8, 500, "euclidean", False),
+    (100, 20, 8, 9, 400, "euclidean", False),
+    (127, 33, 32, 10, 700, "euclidean", False),
+    (128, 64, 32, 12, 900, "euclidean", False),
+    (129, 64, 32, 12, 900, "euclidean", False),
+    (200, 48, 24, 8, 600, "euclidean", False),
+    (256, 128, 32, 16, 1500, "euclidean", False),
+    (300, 100, 40, 10, 800, "euclidean", False),
+    (513, 128, 32, 10, 700, "euclidean", False),
+    (768, 256, 32, 16, 2000, "euclidean", False),
+    (960, 64, 32, 16, 1500, "euclidean", False),
+    (1536, 64, 32, 12, 1200, "euclidean", False),
+    (2049, 64, 32, 8, 500, "euclidean", False),
+    (128, 64, 64, 12, 900, "euclidean", False),
+    (96, 40, 12, 10, 500, "euclidean", True),
+    (128, 64, 32, 12, 900, "ip", False),
+    (768, 256, 32, 8, 900, "cosine", False),
+]
+
+
+@pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
+def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf):
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    blob = random_index(d, s, r, L, m, metric, seed=d * 7 + L, exact_ivf=exact_ivf, dup_rows=3)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "rand", blob))
+    oidx = O.read_index(blob)
+    rng = np.random.default_rng(d)
+    q = rng.standard_normal((40, d)).astype(F32)
+    q[1] = oidx.corpus[5]  # query on a corpus point
+    for k, w, t, rr in [(5, 1, 10, True), (10, max(1, L // 2), 60, True), (7, L, m + 5, True),
+                        (m + 3, L, m + 3, True), (6, 3 if L >= 3 else 1, 1, False)]:
+        w = min(w, L)
+        ids, sc, cnt = dev.search_host(q, k, w, t, rr)
+        ref = O.query_batch(oidx, q, k, w, t, rr)
+        for i, rres in enumerate(ref):
+            c = int(cnt[i])
+            assert c == len(rres.ids), (i, c, len(rres.ids))
+            what = f"d={d} {metric} {(k, w, t, rr)} q{i}"
+            if metric == "euclidean" and rr:
+                np.testing.assert_array_equal(ids[i, :c], rres.ids, err_msg=what)
+                np.testing.assert_array_equal(sc[i, :c].view(np.int32), rres.scores.view(np.int32),
+                                              err_msg=what)
+            elif not rr:
+                np.testing.assert_array_equal(ids[i, :c], rres.ids, err_msg=what)
+                scale = float(q[i].astype(np.float64) @ q[i].astype(np.float64)) if metric == "euclidean" else None
+                assert_topk_equivalent(ids[i, :c], sc[i, :c], rres.ids, rres.scores, RTOL, scale, what)
+            else:  # dot products: error scales with |x||c|, not with the (possibly ~0) score
+                scale = float(np.linalg.norm(q[i]) * np.linalg.norm(oidx.corpus, axis=1).max())
+                assert_topk_equivalent(ids[i, :c], sc[i, :c], rres.ids, rres.scores, RTOL, scale, what)

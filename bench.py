@@ -262,15 +262,15 @@ def main():
     # ---- per-stage device time (events around each launch inside librrg), separate pass
     _native.lib.rrg_set_stage_timing(1)
     import ctypes
-    stage_ms = (ctypes.c_double * 6)()
-    stage_n = (ctypes.c_int64 * 6)()
+    stage_ms = (ctypes.c_double * 7)()
+    stage_n = (ctypes.c_int64 * 7)()
     _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         dev.search_device(q, k, w, t, True, out=out)
     _native.lib.rrg_stage_times(stage_ms, stage_n)
     _native.lib.rrg_set_stage_timing(0)
-    names = ["project", "quantize", "route_dist", "route_select", "score_select", "rerank"]
+    names = ["project", "quantize", "route_dist", "route_select", "score_select", "rerank", "bucket"]
     stages = {nm: round(stage_ms[i] / max(1, stage_n[i]), 4) for i, nm in enumerate(names)}
 
     # ---- roofline of the dominant kernel (rerank): algorithmic bytes / launch time
@@ -339,13 +339,12 @@ def main():
 
 
 def dev_cand_counts(dev, q, k, w, t):
-    """Total re-ranked rows of one step (sum over queries of min(t, candidates))."""
-    ids, sc, cnt = dev.search_device(q[:1], k, w, t, True)  # warm path, tiny
-    # re-ranked rows per query = min(t, candidates); candidates >= t for every query at the
-    # operating point when the count of returned ids equals k and clusters are non-trivial
-    import torch
-    cnt_t = torch.full((q.shape[0],), t, dtype=torch.int64)
-    return int(cnt_t.sum().item())
+    """Total re-ranked rows of one step: sum over queries of min(t, candidates routed)."""
+    xp = dev.stage_project(q)[0]
+    sel = dev.stage_route(xp, w).cpu().numpy()
+    sizes = dev.cluster_sizes()
+    cand = sizes[sel].sum(axis=1)
+    return int(np.minimum(cand, t).sum())
 
 
 if __name__ == "__main__":

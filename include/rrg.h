@@ -108,6 +108,8 @@ int rrg_index_create(const RrgIndexDesc* desc, int device, RrgIndex** out);
 
 void rrg_index_destroy(RrgIndex* index);
 int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out);
+/* Points held per cluster (n_clusters entries; 0 for clusters outside a shard). */
+int rrg_index_cluster_sizes(const RrgIndex* index, uint32_t* out);
 
 /* Workspace bytes rrg_search needs for a batch of nq queries. */
 size_t rrg_search_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t k,
@@ -150,10 +152,10 @@ int64_t rrg_last_launch_count(void);
 /* Per-stage device timing (CUDA events recorded on the search stream around
  * every launch) for the calls made on this thread while enabled.  Stages:
  * 0 project, 1 prep/quantize, 2 route distances, 3 route select,
- * 4 score+top-t, 5 rerank+top-k.  rrg_stage_times synchronizes the recorded
- * events, writes the accumulated milliseconds and launch counts per stage
- * (arrays of RRG_N_STAGES) and resets the accumulators. */
-#define RRG_N_STAGES 6
+ * 4 score+top-t, 5 rerank+top-k, 6 query bucketing.  rrg_stage_times
+ * synchronizes the recorded events, writes the accumulated milliseconds and
+ * launch counts per stage (arrays of RRG_N_STAGES) and resets the accumulators. */
+#define RRG_N_STAGES 7
 void rrg_set_stage_timing(int enabled);
 int rrg_stage_times(double* ms, int64_t* launches);
 

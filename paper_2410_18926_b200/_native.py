@@ -50,6 +50,7 @@ SIGNATURES = {
     "rrg_index_create": (c_int, [ctypes.POINTER(RrgIndexDesc), c_int, ctypes.POINTER(c_vp)]),
     "rrg_index_destroy": (None, [c_vp]),
     "rrg_index_info": (c_int, [c_vp, ctypes.POINTER(RrgIndexInfo)]),
+    "rrg_index_cluster_sizes": (c_int, [c_vp, c_vp]),
     "rrg_search_workspace_bytes": (c_size, [c_vp, c_i64, c_i32, c_i32, c_i32, c_i32]),
     "rrg_search": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
                            c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),

@@ -185,6 +185,7 @@ struct RrgIndex {
   RrgIndexInfo info{};
   int64_t max_cluster = 0;
   std::vector<int> sizes_sorted_desc;  // cluster sizes (held), descending
+  std::vector<uint32_t> held_sizes;    // per cluster
   int n_exact = 0;
 
   void* dalloc(size_t bytes) {
@@ -264,6 +265,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
       cl_aidx[l] = c.owned && held ? n_rrr++ : -1;
     }
     P += held;
+    ix->held_sizes.push_back(held);
     if (held) ix->sizes_sorted_desc.push_back((int)held);
     ix->max_cluster = std::max<int64_t>(ix->max_cluster, held);
     if (c.exact) ix->n_exact++;
@@ -275,7 +277,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   std::vector<int8_t> at((size_t)n_rrr * r * v.s_pad, 0);
   std::vector<float> ahead((size_t)n_rrr * r), ascale((size_t)n_rrr * r);
   std::vector<int8_t> bt((size_t)P * v.r_pad, 0), xc((size_t)P_exact * v.s_pad, 0);
-  std::vector<float> phead(P), pscale(P), pnorm(hm.metric == kMetricEuclidean ? P : 0);
+  std::vector<float4> pmeta(P, make_float4(0.f, 0.f, 0.f, 0.f));
   std::vector<int64_t> pid(P);
   std::vector<int> pos_of_id(hm.m, -1);
   for (int l = 0; l < L; ++l) {
@@ -288,14 +290,16 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
       if (id < 0 || id >= hm.m) raise_format("cluster %d ids: id %lld out of range", l, (long long)id);
       pid[p0 + p] = id;
       pos_of_id[id] = (int)(p0 + p);
-      if (!pnorm.empty()) pnorm[p0 + p] = c.norms[p];
+      if (hm.metric == kMetricEuclidean) pmeta[p0 + p].z = c.norms[p];
+      uint32_t id32 = (uint32_t)id;
+      memcpy(&pmeta[p0 + p].w, &id32, 4);
     }
     if (c.exact) {
       // A: s x m (cols = points)
       const int64_t x0 = cl_aidx[l];
       for (int i = 0; i < s; ++i)
         for (int p = 0; p < m; ++p) xc[(size_t)(x0 + p) * v.s_pad + i] = c.a_vals[(size_t)i * m + p];
-      for (int p = 0; p < m; ++p) { phead[p0 + p] = c.a_head[p]; pscale[p0 + p] = c.a_scale[p]; }
+      for (int p = 0; p < m; ++p) { pmeta[p0 + p].x = c.a_head[p]; pmeta[p0 + p].y = c.a_scale[p]; }
     } else {
       const int slot = cl_aidx[l];
       for (int i = 0; i < s; ++i)
@@ -307,7 +311,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
       }
       for (int j = 0; j < r; ++j)
         for (int p = 0; p < m; ++p) bt[(size_t)(p0 + p) * v.r_pad + j] = c.b_vals[(size_t)j * m + p];
-      for (int p = 0; p < m; ++p) { phead[p0 + p] = c.b_head[p]; pscale[p0 + p] = c.b_scale[p]; }
+      for (int p = 0; p < m; ++p) { pmeta[p0 + p].x = c.b_head[p]; pmeta[p0 + p].y = c.b_scale[p]; }
     }
   }
   // centroid squared norms in f64, NumPy order: (c*c).sum(axis=1) (cluster.py:50)
@@ -330,9 +334,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.ascale = ix->upload(ascale);
   v.bt = ix->upload(bt);
   v.xcodes = ix->upload(xc);
-  v.phead = ix->upload(phead);
-  v.pscale = ix->upload(pscale);
-  v.pnorm = pnorm.empty() ? nullptr : ix->upload(pnorm);
+  v.pmeta = ix->upload(pmeta);
   v.pid = ix->upload(pid);
   v.corpus = nullptr;
   if (has_corpus) {
@@ -593,7 +595,7 @@ struct Plan {
   int smem_cap;
   int64_t gcap;    // global overflow capacity per query (0 if none)
   size_t off_xp, off_qc, off_qs, off_qh, off_xx, off_pp, off_diss, off_sel, off_cpos, off_cn,
-      off_gk, off_gp, total;
+      off_gk, off_gp, off_prim, off_order, total;
 };
 
 Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank) {
@@ -631,6 +633,8 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank) 
   p.off_cn = carve(Q * 4);
   p.off_gk = carve(Q * p.gcap * 4);
   p.off_gp = carve(Q * p.gcap * 4);
+  p.off_prim = carve(Q * 4);
+  p.off_order = carve(Q * 4);
   p.total = o;
   return p;
 }
@@ -669,23 +673,28 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
   int* cn = reinterpret_cast<int*>(base + p.off_cn);
   uint32_t* gk = reinterpret_cast<uint32_t*>(base + p.off_gk);
   int* gp = reinterpret_cast<int*>(base + p.off_gp);
+  int* prim = reinterpret_cast<int*>(base + p.off_prim);
+  int* order = reinterpret_cast<int*>(base + p.off_order);
   for (int64_t q0 = 0; q0 < nq; q0 += p.qc) {
     const int n = (int)std::min<int64_t>(p.qc, nq - q0);
     const float* x = queries + q0 * v.d;
     staged(0, st, [&] { launch_project(x, v.W, n, v.d, v.s, xp, st); });
     staged(1, st, [&] { launch_prep(xp, x, n, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st); });
     staged(2, st, [&] { launch_route_dist(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st); });
-    staged(3, st, [&] { launch_route_select(diss, n, v.L, w, sel, st); });
+    staged(3, st, [&] { launch_route_select(diss, n, v.L, w, sel, prim, st); });
+    staged(6, st, [&] { launch_bucket(prim, n, v.L, order, st); });
     ScoreArgsHost sa{};
     sa.ix = v; sa.qcodes = qcodes; sa.qscale = qscale; sa.qhead = qhead; sa.xx = xx; sa.sel = sel;
     sa.w = w; sa.take_cap = p.take_cap; sa.rerank = rerank; sa.k = k; sa.smem_cap = p.smem_cap;
     sa.gkeys = gk; sa.gpos = gp; sa.gcap = p.gcap; sa.cand_pos = cpos; sa.cand_n = cn;
     sa.out_ids = ids; sa.out_scores = scores; sa.out_count = count; sa.q0 = (int)q0;
+    sa.order = order;
     staged(4, st, [&] { launch_score_select(sa, n, st); });
     if (rerank) {
       RerankArgsHost ra{};
       ra.ix = v; ra.queries = x; ra.cand_pos = cpos; ra.cand_n = cn; ra.take_cap = p.take_cap;
       ra.k = k; ra.out_ids = ids; ra.out_scores = scores; ra.out_count = count; ra.q0 = (int)q0;
+      ra.order = order;
       staged(5, st, [&] { launch_rerank(ra, n, st); });
     }
     CUDA_TRY(cudaGetLastError());
@@ -740,6 +749,12 @@ void rrg_index_destroy(RrgIndex* index) { delete index; }
 int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out) {
   if (!index || !out) return fail(RRG_E_USAGE, "ParameterError", "null argument");
   *out = index->info;
+  return RRG_OK;
+}
+
+int rrg_index_cluster_sizes(const RrgIndex* index, uint32_t* out) {
+  if (!index || !out) return fail(RRG_E_USAGE, "ParameterError", "null argument");
+  std::copy(index->held_sizes.begin(), index->held_sizes.end(), out);
   return RRG_OK;
 }
 
@@ -843,10 +858,10 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int
     // recompute pp (f64 pairwise) via the prep kernel on xp; queries unused for xx
     int8_t* qc = reinterpret_cast<int8_t*>(pp + nq);
     float* dummy = nullptr;
-    CUDA_TRY(cudaMallocAsync(&dummy, std::max<int64_t>(nq, 1) * 12, st));
+    CUDA_TRY(cudaMallocAsync(&dummy, std::max<int64_t>(nq, 1) * 16, st));
     launch_prep(xp, xp, (int)nq, v.s, v.s_pad, v.s, qc, dummy, dummy + nq, pp, dummy + 2 * nq, st);
     launch_route_dist(xp, v.cent, (int)nq, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
-    launch_route_select(diss, (int)nq, v.L, w, selected, st);
+    launch_route_select(diss, (int)nq, v.L, w, selected, reinterpret_cast<int*>(dummy + 3 * nq), st);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(dummy, st));
     return RRG_OK;

@@ -39,9 +39,10 @@ struct DevIndexView {
   const float* ascale;   // [n_rrr][r]
   const int8_t* bt;      // [P][r_pad]: B^T codes per point, column 0 = pad row (zero)
   const int8_t* xcodes;  // [P_exact][s_pad]: exact-model codes per point
-  const float* phead;    // [P] head_row of the point's last factor (B, or A for exact)
-  const float* pscale;   // [P] col_scales of the point's last factor
-  const float* pnorm;    // [P] ||c_p||^2 (euclidean) or nullptr
+  // [P] per-point {head_row, col_scale} of the point's last factor (B, or A for an
+  // exact model), ||c_p||^2 (euclidean, else 0) and the low 32 bits of its corpus id:
+  // one 16-byte load per scored point.
+  const float4* pmeta;
   const int64_t* pid;    // [P] original corpus ids
   const float* corpus;   // [P][d_stride] in cluster order, or nullptr
   // NumPy pairwise-summation plan for a row of d floats: when the recursion

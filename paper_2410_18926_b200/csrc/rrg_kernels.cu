@@ -144,7 +144,8 @@ __global__ void k_prep_queries(const float* __restrict__ xp, const float* __rest
 // the w smallest by (diss, cluster id).  One CTA per query.
 template <int NT>
 __global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ diss, int L, int w,
-                                                     int* __restrict__ sel) {
+                                                     int* __restrict__ sel,
+                                                     int* __restrict__ primary) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
@@ -156,6 +157,53 @@ __global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ 
   auto tie = [&](int i) { return (uint32_t)i; };
   block_select_smallest<NT, uint64_t>(L, w, key, tie, outidx, sm);
   for (int i = threadIdx.x; i < w; i += NT) sel[(size_t)blockIdx.x * w + i] = outidx[i];
+  // nearest cluster (route()[0]) -- the bucketing key that groups queries for locality
+  if (threadIdx.x < 32) {
+    uint64_t bk = ~0ull;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < w; i += 32) {
+      int c = outidx[i];
+      uint64_t kc = keys[c];
+      if (kc < bk || (kc == bk && c < bi)) { bk = kc; bi = c; }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+    }
+    if (threadIdx.x == 0) primary[blockIdx.x] = bi;
+  }
+}
+
+// ======================================================== query bucketing
+// Counting sort of the batch by nearest cluster (histogram, exclusive scan,
+// scatter), one CTA.  The scoring and re-rank CTAs then visit queries in bucket
+// order, so queries probing the same clusters -- and re-ranking overlapping
+// corpus rows -- run concurrently and share L2.  Order only affects locality;
+// every query's result is independent of it.
+constexpr int BNT = 1024;
+__global__ void __launch_bounds__(BNT) k_bucket_queries(const int* __restrict__ primary, int nq,
+                                                        int L, int* __restrict__ order) {
+  extern __shared__ int hist[];  // L + 1
+  for (int i = threadIdx.x; i <= L; i += BNT) hist[i] = 0;
+  __syncthreads();
+  for (int q = threadIdx.x; q < nq; q += BNT) atomicAdd(&hist[primary[q]], 1);
+  __syncthreads();
+  if (threadIdx.x < 32) {  // exclusive scan by one warp
+    int lane = threadIdx.x, carry = 0;
+    for (int base = 0; base < L; base += 32) {
+      int i = base + lane;
+      int v = i < L ? hist[i] : 0, incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (i < L) hist[i] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+  __syncthreads();
+  for (int q = threadIdx.x; q < nq; q += BNT) order[atomicAdd(&hist[primary[q]], 1)] = q;
 }
 
 // ====================================================== scoring + top-t select
@@ -188,6 +236,7 @@ struct ScoreArgs {
   float* out_scores;
   int* out_count;
   int q0;  // query offset of this chunk (outputs)
+  const int* order;  // CTA -> chunk-local query (bucket order), or nullptr
 };
 
 constexpr int SNT = 512;
@@ -204,7 +253,7 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
   __shared__ __align__(16) int8_t qs[1024 + 16];
 
   const DevIndexView& ix = a.ix;
-  const int q = blockIdx.x;
+  const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nwarps = SNT / 32;
   const int s_pad = ix.s_pad, r = ix.r, r_pad = ix.r_pad;
@@ -237,8 +286,6 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
     pos = a.gpos + (size_t)q * a.gcap;
   }
   const bool euclid = ix.metric == kMetricEuclidean;
-  const int swords = s_pad / 4;
-  const int* qw = reinterpret_cast<const int*>(qs);
 
   int cand_base = 0;
   for (int c0 = 0; c0 < a.w; c0 += kMaxWChunk) {
@@ -271,9 +318,16 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
         int j = lane + 32 * h;
         inter[h] = 0.0f;
         if (j < r) {
-          const int* aw = reinterpret_cast<const int*>(at + (size_t)j * s_pad);
+          const int4* aw = reinterpret_cast<const int4*>(at + (size_t)j * s_pad);
+          const int4* q4 = reinterpret_cast<const int4*>(qs);
           int raw = 0;
-          for (int u = 0; u < swords; ++u) raw = __dp4a(qw[u], __ldg(aw + u), raw);
+          for (int u = 0; u < s_pad / 16; ++u) {
+            int4 b = __ldg(aw + u), cc = q4[u];
+            raw = __dp4a(cc.x, b.x, raw);
+            raw = __dp4a(cc.y, b.y, raw);
+            raw = __dp4a(cc.z, b.z, raw);
+            raw = __dp4a(cc.w, b.w, raw);
+          }
           inter[h] = deq(raw, xscale, as[j], xhead, ah[j]);
           if (j >= 1) amax = fmaxf(amax, fabsf(inter[h]));
         }
@@ -294,29 +348,42 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
       if (lane == 0) { s2s[c] = sc2; h2s[c] = head2; }
     }
     __syncthreads();
-    // ---- stage B: one thread per candidate point
+    // ---- stage B: one thread per candidate point; 16-byte code and metadata loads
     const int nloc = cl_off[nc] - cand_base;
+    int c = 0;  // cluster of element e, advanced monotonically as e grows
     for (int e = tid; e < nloc; e += SNT) {
-      // locate cluster (nc <= 64: linear scan over the chunk prefix)
-      int c = 0;
       while (cl_off[c + 1] - cand_base <= e) ++c;
-      int p = e - (cl_off[c] - cand_base);
-      int l = cl_l[c];
-      int gp = cl_p0[c] + p;
+      const int p = e - (cl_off[c] - cand_base);
+      const int l = cl_l[c];
+      const int gp = cl_p0[c] + p;
+      const float4 meta = __ldg(ix.pmeta + gp);
       float yhat;
       if (ix.cl_kind[l] == kKindRrr) {
-        const int* bw = reinterpret_cast<const int*>(ix.bt + (size_t)gp * r_pad);
-        const int* cw = reinterpret_cast<const int*>(c2s[c]);
+        const int4* bw = reinterpret_cast<const int4*>(ix.bt + (size_t)gp * r_pad);
+        const int4* cw = reinterpret_cast<const int4*>(c2s[c]);
         int raw = 0;
-        for (int u = 0; u < r_pad / 4; ++u) raw = __dp4a(cw[u], __ldg(bw + u), raw);
-        yhat = deq(raw, s2s[c], ix.pscale[gp], h2s[c], ix.phead[gp]);
+        for (int u = 0; u < r_pad / 16; ++u) {
+          int4 b = __ldg(bw + u), cc = cw[u];
+          raw = __dp4a(cc.x, b.x, raw);
+          raw = __dp4a(cc.y, b.y, raw);
+          raw = __dp4a(cc.z, b.z, raw);
+          raw = __dp4a(cc.w, b.w, raw);
+        }
+        yhat = deq(raw, s2s[c], meta.y, h2s[c], meta.x);
       } else {
-        const int* xw = reinterpret_cast<const int*>(ix.xcodes + (size_t)(ix.cl_aidx[l] + p) * s_pad);
+        const int4* xw = reinterpret_cast<const int4*>(ix.xcodes + (size_t)(ix.cl_aidx[l] + p) * s_pad);
+        const int4* q4 = reinterpret_cast<const int4*>(qs);
         int raw = 0;
-        for (int u = 0; u < swords; ++u) raw = __dp4a(qw[u], __ldg(xw + u), raw);
-        yhat = deq(raw, xscale, ix.pscale[gp], xhead, ix.phead[gp]);
+        for (int u = 0; u < s_pad / 16; ++u) {
+          int4 b = __ldg(xw + u), cc = q4[u];
+          raw = __dp4a(cc.x, b.x, raw);
+          raw = __dp4a(cc.y, b.y, raw);
+          raw = __dp4a(cc.z, b.z, raw);
+          raw = __dp4a(cc.w, b.w, raw);
+        }
+        yhat = deq(raw, xscale, meta.y, xhead, meta.x);
       }
-      float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), ix.pnorm[gp]) : -yhat;
+      float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
       keys[cl_off[c] + p] = mono32(keyf);
       pos[cl_off[c] + p] = gp;
     }
@@ -385,6 +452,7 @@ struct RerankArgs {
   float* out_scores;
   int* out_count;
   int q0;
+  const int* order;
 };
 
 constexpr int RNT = 256;
@@ -393,7 +461,7 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
   const DevIndexView& ix = a.ix;
-  const int q = blockIdx.x;
+  const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = RNT / 32;
   const int d = ix.d, ds = ix.d_stride;
@@ -502,7 +570,7 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
   const DevIndexView& ix = a.ix;
-  const int q = blockIdx.x;
+  const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = RNT / 32;
   const int d = ix.d, ds = ix.d_stride, nl = ix.pw_leaf_n, nb = nl / 8, tail = nl % 8;
@@ -676,7 +744,8 @@ void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s,
 
 size_t route_select_smem(int L) { return (size_t)L * 8 + (size_t)L * 4 + 16; }
 
-void launch_route_select(const double* diss, int nq, int L, int w, int* sel, cudaStream_t st) {
+void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
+                         cudaStream_t st) {
   size_t sm = route_select_smem(L);
   static bool attr = false;
   if (!attr) {
@@ -684,7 +753,17 @@ void launch_route_select(const double* diss, int nq, int L, int w, int* sel, cud
                          200 * 1024);
     attr = true;
   }
-  k_route_select<256><<<nq, 256, sm, st>>>(diss, L, w, sel);
+  k_route_select<256><<<nq, 256, sm, st>>>(diss, L, w, sel, primary);
+}
+
+void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st) {
+  size_t sm = (size_t)(L + 1) * 4;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_bucket_queries, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_bucket_queries<<<1, BNT, sm, st>>>(primary, nq, L, order);
 }
 
 size_t score_select_smem(int smem_cap, int take_cap, int k) {
@@ -700,6 +779,7 @@ void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st) {
   a.smem_cap = h.smem_cap; a.gkeys = h.gkeys; a.gpos = h.gpos; a.gcap = h.gcap;
   a.cand_pos = h.cand_pos; a.cand_n = h.cand_n; a.out_ids = h.out_ids;
   a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
+  a.order = h.order;
   size_t sm = score_select_smem(h.smem_cap, h.take_cap, h.k);
   static bool attr = false;
   if (!attr) {
@@ -720,7 +800,7 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   RerankArgs a;
   a.ix = h.ix; a.queries = h.queries; a.cand_pos = h.cand_pos; a.cand_n = h.cand_n;
   a.take_cap = h.take_cap; a.k = h.k; a.out_ids = h.out_ids; a.out_scores = h.out_scores;
-  a.out_count = h.out_count; a.q0 = h.q0;
+  a.out_count = h.out_count; a.q0 = h.q0; a.order = h.order;
   if (h.ix.pw_perfect && (h.ix.d % 2) == 0) {
     size_t np2 = 1;
     while (np2 < (size_t)h.k) np2 <<= 1;

@@ -29,6 +29,7 @@ struct ScoreArgsHost {
   float* out_scores;
   int* out_count;
   int q0;
+  const int* order = nullptr;
 };
 
 struct RerankArgsHost {
@@ -41,6 +42,7 @@ struct RerankArgsHost {
   float* out_scores;
   int* out_count;
   int q0;
+  const int* order = nullptr;
 };
 
 void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
@@ -50,7 +52,9 @@ void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
                        const double* pp, const double* cnorm, double* diss, cudaStream_t st);
 size_t route_select_smem(int L);
-void launch_route_select(const double* diss, int nq, int L, int w, int* sel, cudaStream_t st);
+void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
+                         cudaStream_t st);
+void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st);
 size_t score_select_smem(int smem_cap, int take_cap, int k);
 void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st);
 size_t rerank_smem(int d_stride, int take_cap, int k);

@@ -143,6 +143,11 @@ class DeviceIndex:
 
     # ----------------------------------------------------------------- search
 
+    def cluster_sizes(self) -> np.ndarray:
+        out = np.zeros(self.n_clusters, dtype=np.uint32)
+        check(lib.rrg_index_cluster_sizes(self._h, out.ctypes.data))
+        return out
+
     def workspace_bytes(self, nq: int, k: int, w: int, t: int, rerank: bool) -> int:
         return int(lib.rrg_search_workspace_bytes(self._h, nq, k, w, t, int(rerank)))
 

@@ -610,7 +610,9 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank) 
   int64_t nmax = 0;
   for (int i = 0; i < (int)ix->sizes_sorted_desc.size() && i < w; ++i) nmax += ix->sizes_sorted_desc[i];
   p.take_cap = (int)std::min<int64_t>(p.take_cap, std::max<int64_t>(nmax, 1));
-  const size_t budget = 100 * 1024;
+  // dynamic smem per scoring CTA: with ~40 KB static this keeps 2 CTAs (2 x 512
+  // threads) resident per SM; queries with more candidates spill to global
+  const size_t budget = 64 * 1024;
   int64_t np2 = 1;
   while (np2 < k) np2 <<= 1;
   int64_t fixed = (int64_t)p.take_cap * 4 + 64 + np2 * 8;
@@ -657,6 +659,12 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
                  int32_t rerank, int64_t* ids, float* scores, int32_t* count, void* ws,
                  size_t ws_bytes, cudaStream_t st) {
   Plan p = make_plan(ix, nq, k, w, t, rerank);
+  {  // shared-memory budgets of the per-query CTAs (static parts bounded by 48 KB)
+    const size_t lim = kMaxSmemPerCta - 48 * 1024;
+    if (score_select_smem(p.smem_cap, p.take_cap, k) > lim ||
+        (rerank && rerank_smem(ix->view.d_stride, p.take_cap, k, rerank_uses_tree(ix->view)) > lim))
+      raise_usage("ParameterError", "t=%d / k=%d exceed the device search limits", t, k);
+  }
   if (ws_bytes < p.total)
     raise_usage("ParameterError", "workspace too small: %zu < %zu bytes", ws_bytes, p.total);
   char* base = static_cast<char*>(ws);

@@ -303,6 +303,149 @@ __device__ int block_select_smallest(int n, int take, KeyF key, TieF tie, int* o
   return take;
 }
 
+// ------------------------------------------------ bucketed block selection
+// Same contract as block_select_smallest, cheaper in the common case: one pass
+// for min/max of the keys, one histogram pass over 2^11 buckets of
+// (key - min) >> shift (a monotone bucketing of the integer keys), a block
+// scan to find the boundary bucket, and one collection pass.  Items of the
+// boundary bucket are resolved exactly by (key, tie) rank counting in shared
+// memory; a boundary bucket larger than the buffer (e.g. thousands of equal
+// keys) falls back to the radix select above.
+constexpr int kSelBins = 2048;
+constexpr int kSelBuf = 512;
+
+struct BucketSmem {
+  int hist[kSelBins];
+  unsigned long long buf_key[kSelBuf];
+  uint32_t buf_tie[kSelBuf];
+  int buf_idx[kSelBuf];
+  int wsum[32];
+  unsigned long long lo, hi;
+  int bb, before, eq, nbuf, count;
+};
+
+__device__ __forceinline__ int bitlen64(unsigned long long v) { return v ? 64 - __clzll(v) : 0; }
+
+template <int NT, typename K, typename KeyF, typename TieF>
+__device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, int* out,
+                                     BucketSmem& bs, SelectSmem& sm) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (take >= n) {
+    for (int i = tid; i < n; i += NT) out[i] = i;
+    __syncthreads();
+    return n;
+  }
+  if (take <= 0) return 0;
+  // 1. key range
+  unsigned long long lo = ~0ull, hi = 0ull;
+  for (int i = tid; i < n; i += NT) {
+    unsigned long long k = (unsigned long long)key(i);
+    lo = k < lo ? k : lo;
+    hi = k > hi ? k : hi;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+    unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+    lo = a < lo ? a : lo;
+    hi = b > hi ? b : hi;
+  }
+  if (tid == 0) { bs.lo = ~0ull; bs.hi = 0ull; bs.nbuf = 0; bs.count = 0; }
+  for (int i = tid; i < kSelBins; i += NT) bs.hist[i] = 0;
+  __syncthreads();
+  if (lane == 0) { atomicMin(&bs.lo, lo); atomicMax(&bs.hi, hi); }
+  __syncthreads();
+  lo = bs.lo;
+  hi = bs.hi;
+  const int bl = bitlen64(hi - lo);
+  const int shift = bl > 11 ? bl - 11 : 0;
+  // 2. histogram
+  for (int i = tid; i < n; i += NT) {
+    int b = (int)(((unsigned long long)key(i) - lo) >> shift);
+    atomicAdd(&bs.hist[b], 1);
+  }
+  __syncthreads();
+  // 3. boundary bucket: block exclusive scan of per-thread bin ranges
+  constexpr int per = kSelBins / NT;
+  int loc = 0;
+#pragma unroll
+  for (int j = 0; j < per; ++j) loc += bs.hist[tid * per + j];
+  int incl = loc;
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) bs.wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int v = lane < NT / 32 ? bs.wsum[lane] : 0, iv = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      int u = __shfl_up_sync(0xffffffffu, iv, o);
+      if (lane >= o) iv += u;
+    }
+    if (lane < NT / 32) bs.wsum[lane] = iv - v;
+  }
+  __syncthreads();
+  int cum = bs.wsum[warp] + incl - loc;
+  if (cum < take && take <= cum + loc) {
+#pragma unroll
+    for (int j = 0; j < per; ++j) {
+      int h = bs.hist[tid * per + j];
+      if (cum + h >= take) {
+        bs.bb = tid * per + j;
+        bs.before = cum;
+        bs.eq = h;
+        break;
+      }
+      cum += h;
+    }
+  }
+  __syncthreads();
+  const int bb = bs.bb, need = take - bs.before, eq = bs.eq;
+  const bool all_eq = eq == need;
+  if (!all_eq && eq > kSelBuf) {
+    __syncthreads();
+    return block_select_smallest<NT, K>(n, take, key, tie, out, sm);
+  }
+  // 4. collect
+  for (int base = 0; base < n; base += NT) {
+    int i = base + tid;
+    bool sel = false;
+    if (i < n) {
+      int b = (int)(((unsigned long long)key(i) - lo) >> shift);
+      if (b < bb || (b == bb && all_eq)) {
+        sel = true;
+      } else if (b == bb) {
+        int s = atomicAdd(&bs.nbuf, 1);
+        bs.buf_key[s] = (unsigned long long)key(i);
+        bs.buf_tie[s] = tie(i);
+        bs.buf_idx[s] = i;
+      }
+    }
+    unsigned m = __ballot_sync(0xffffffffu, sel);
+    int slot = 0;
+    if (lane == 0 && m) slot = atomicAdd(&bs.count, __popc(m));
+    slot = __shfl_sync(0xffffffffu, slot, 0);
+    if (sel) out[slot + __popc(m & ((1u << lane) - 1))] = i;
+  }
+  __syncthreads();
+  // 5. exact resolution of the boundary bucket by (key, tie) rank
+  if (!all_eq) {
+    const int nb = bs.nbuf;
+    for (int e = tid; e < nb; e += NT) {
+      unsigned long long ke = bs.buf_key[e];
+      uint32_t te = bs.buf_tie[e];
+      int rank = 0;
+      for (int f = 0; f < nb; ++f) {
+        unsigned long long kf = bs.buf_key[f];
+        rank += (kf < ke) || (kf == ke && bs.buf_tie[f] < te);
+      }
+      if (rank < need) out[atomicAdd(&bs.count, 1)] = bs.buf_idx[e];
+    }
+    __syncthreads();
+  }
+  return take;
+}
+
 // Bitonic sort (ascending) of n_pow2 u64 keys in shared memory; pad with ~0.
 template <int NT>
 __device__ void block_bitonic_sort(uint64_t* a, int n_pow2) {

@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ 
                                                      int* __restrict__ primary) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
   uint64_t* keys = reinterpret_cast<uint64_t*>(smem_raw);
   int* outidx = reinterpret_cast<int*>(keys + L);
   const double* row = diss + (size_t)blockIdx.x * L;
@@ -155,7 +156,7 @@ __global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ 
   __syncthreads();
   auto key = [&](int i) { return keys[i]; };
   auto tie = [&](int i) { return (uint32_t)i; };
-  block_select_smallest<NT, uint64_t>(L, w, key, tie, outidx, sm);
+  block_select_bucketed<NT, uint64_t>(L, w, key, tie, outidx, bs, sm);
   for (int i = threadIdx.x; i < w; i += NT) sel[(size_t)blockIdx.x * w + i] = outidx[i];
   // nearest cluster (route()[0]) -- the bucketing key that groups queries for locality
   if (threadIdx.x < 32) {
@@ -246,8 +247,10 @@ constexpr int kMaxR = 64;
 __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
   __shared__ __align__(16) int8_t c2s[kMaxWChunk][kMaxR];
   __shared__ float s2s[kMaxWChunk], h2s[kMaxWChunk];
+  __shared__ float inters[kMaxWChunk][kMaxR];
   __shared__ int cl_l[kMaxWChunk], cl_p0[kMaxWChunk], cl_m[kMaxWChunk], cl_off[kMaxWChunk + 1];
   __shared__ int total_n;
   __shared__ __align__(16) int8_t qs[1024 + 16];
@@ -303,49 +306,56 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
       cl_off[nc] = off;
     }
     __syncthreads();
-    // ---- stage A (rrr clusters): warp per cluster, lanes over the r intermediate coords
-    for (int c = warp; c < nc; c += nwarps) {
-      int l = cl_l[c];
-      if (ix.cl_kind[l] != kKindRrr || cl_m[c] == 0) continue;
-      int slot = ix.cl_aidx[l];
-      const int8_t* at = ix.at + (size_t)slot * r * s_pad;
-      const float* ah = ix.ahead + (size_t)slot * r;
-      const float* as = ix.ascale + (size_t)slot * r;
-      float inter[2];
-      float amax = 0.0f;
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int j = lane + 32 * h;
-        inter[h] = 0.0f;
-        if (j < r) {
-          const int4* aw = reinterpret_cast<const int4*>(at + (size_t)j * s_pad);
-          const int4* q4 = reinterpret_cast<const int4*>(qs);
-          int raw = 0;
-          for (int u = 0; u < s_pad / 16; ++u) {
+    // ---- stage A (rrr clusters), all threads: raw1 = codes_x . A[:, j] for every
+    // (cluster, j), the s_pad/16 int4 words split over `parts` consecutive lanes
+    {
+      const int pairs = nc * r;
+      const int nvec = s_pad / 16;
+      int parts = 1;
+      while (parts < 32 && pairs * parts * 2 <= SNT && parts * 2 <= nvec) parts <<= 1;
+      const int4* q4 = reinterpret_cast<const int4*>(qs);
+      for (int base = 0; base < pairs * parts; base += SNT) {
+        const int e = base + tid;
+        const int pr = e / parts, part = e % parts;
+        int raw = 0;
+        int c = pr / r, j = pr % r;
+        bool act = pr < pairs;
+        int l = act ? cl_l[c] : 0;
+        act = act && ix.cl_kind[l] == kKindRrr && cl_m[c] > 0;
+        if (act) {
+          const int4* aw =
+              reinterpret_cast<const int4*>(ix.at + ((size_t)ix.cl_aidx[l] * r + j) * s_pad);
+          for (int u = part; u < nvec; u += parts) {
             int4 b = __ldg(aw + u), cc = q4[u];
             raw = __dp4a(cc.x, b.x, raw);
             raw = __dp4a(cc.y, b.y, raw);
             raw = __dp4a(cc.z, b.z, raw);
             raw = __dp4a(cc.w, b.w, raw);
           }
-          inter[h] = deq(raw, xscale, as[j], xhead, ah[j]);
-          if (j >= 1) amax = fmaxf(amax, fabsf(inter[h]));
+        }
+        for (int o = 1; o < parts; o <<= 1) raw += __shfl_xor_sync(0xffffffffu, raw, o);
+        if (act && part == 0) {
+          const size_t aj = (size_t)ix.cl_aidx[l] * r + j;
+          inters[c][j] = deq(raw, xscale, ix.ascale[aj], xhead, ix.ahead[aj]);
         }
       }
+    }
+    __syncthreads();
+    // re-quantize each cluster's intermediate vector (quantize.py:150): warp per cluster
+    for (int c = warp; c < nc; c += nwarps) {
+      int l = cl_l[c];
+      if (ix.cl_kind[l] != kKindRrr || cl_m[c] == 0) continue;
+      float amax = 0.0f;
+      for (int j = 1 + lane; j < r; j += 32) amax = fmaxf(amax, fabsf(inters[c][j]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-      float sc2 = quant_scale(amax);
-      float head2 = __shfl_sync(0xffffffffu, inter[0], 0);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int j = lane + 32 * h;
-        if (j < r_pad) {
-          int code = 0;
-          if (j >= 1 && j < r && amax != 0.0f) code = quant_code(inter[h], sc2);
-          c2s[c][j] = (int8_t)code;
-        }
+      const float sc2 = quant_scale(amax);
+      for (int j = lane; j < r_pad; j += 32) {
+        int code = 0;
+        if (j >= 1 && j < r && amax != 0.0f) code = quant_code(inters[c][j], sc2);
+        c2s[c][j] = (int8_t)code;
       }
-      if (lane == 0) { s2s[c] = sc2; h2s[c] = head2; }
+      if (lane == 0) { s2s[c] = sc2; h2s[c] = inters[c][0]; }
     }
     __syncthreads();
     // ---- stage B: one thread per candidate point; 16-byte code and metadata loads
@@ -396,7 +406,7 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
   int* selidx = reinterpret_cast<int*>(smem_raw + (size_t)a.smem_cap * 8);  // after keys+pos
   auto key = [&](int i) { return keys[i]; };
   auto tie = [&](int i) { return (uint32_t)ix.pid[pos[i]]; };
-  block_select_smallest<SNT, uint32_t>(N, take, key, tie, selidx, sm);
+  block_select_bucketed<SNT, uint32_t>(N, take, key, tie, selidx, bs, sm);
 
   const int gq = a.q0 + q;
   if (a.rerank) {
@@ -460,6 +470,7 @@ constexpr int RNT = 256;
 __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
   const DevIndexView& ix = a.ix;
   const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -524,7 +535,7 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
   const int kk = min(a.k, n);
   auto key = [&](int i) { return dkeys[i]; };
   auto tie = [&](int i) { return dids[i]; };
-  block_select_smallest<RNT, uint32_t>(n, kk, key, tie, selidx, sm);
+  block_select_bucketed<RNT, uint32_t>(n, kk, key, tie, selidx, bs, sm);
   int np2 = 1;
   while (np2 < kk) np2 <<= 1;
   for (int i = tid; i < np2; i += RNT) {
@@ -569,6 +580,7 @@ template <int SLOTS>
 __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
   const DevIndexView& ix = a.ix;
   const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -672,7 +684,7 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
   const int kk = min(a.k, n);
   auto key = [&](int i) { return dkeys[i]; };
   auto tie = [&](int i) { return dids[i]; };
-  block_select_smallest<RNT, uint32_t>(n, kk, key, tie, selidx, sm);
+  block_select_bucketed<RNT, uint32_t>(n, kk, key, tie, selidx, bs, sm);
   int np2 = 1;
   while (np2 < kk) np2 <<= 1;
   for (int i = tid; i < np2; i += RNT) {
@@ -742,28 +754,32 @@ void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s,
                                                        nullptr, nullptr);
 }
 
+// Opt in to the dynamic shared memory a launch may need (227 KB per CTA minus the
+// kernel's static shared memory), once per kernel slot and device.
+template <typename Kern>
+static void allow_smem(Kern* kernel, int slot) {
+  static int done[16][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[slot][dev]) return;
+  cudaFuncAttributes at{};
+  cudaFuncGetAttributes(&at, (const void*)kernel);
+  cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kMaxSmemPerCta - (int)at.sharedSizeBytes);
+  done[slot][dev] = 1;
+}
+
 size_t route_select_smem(int L) { return (size_t)L * 8 + (size_t)L * 4 + 16; }
 
 void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
                          cudaStream_t st) {
-  size_t sm = route_select_smem(L);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_route_select<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr = true;
-  }
-  k_route_select<256><<<nq, 256, sm, st>>>(diss, L, w, sel, primary);
+  allow_smem(k_route_select<256>, 0);
+  k_route_select<256><<<nq, 256, route_select_smem(L), st>>>(diss, L, w, sel, primary);
 }
 
 void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st) {
-  size_t sm = (size_t)(L + 1) * 4;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_bucket_queries, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  k_bucket_queries<<<1, BNT, sm, st>>>(primary, nq, L, order);
+  allow_smem(k_bucket_queries, 1);
+  k_bucket_queries<<<1, BNT, (size_t)(L + 1) * 4, st>>>(primary, nq, L, order);
 }
 
 size_t score_select_smem(int smem_cap, int take_cap, int k) {
@@ -780,48 +796,37 @@ void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st) {
   a.cand_pos = h.cand_pos; a.cand_n = h.cand_n; a.out_ids = h.out_ids;
   a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
   a.order = h.order;
-  size_t sm = score_select_smem(h.smem_cap, h.take_cap, h.k);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_score_select, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
-  k_score_select<<<nq, SNT, sm, st>>>(a);
+  allow_smem(k_score_select, 2);
+  k_score_select<<<nq, SNT, score_select_smem(h.smem_cap, h.take_cap, h.k), st>>>(a);
 }
 
-size_t rerank_smem(int d_stride, int take_cap, int k) {
+size_t rerank_smem(int d_stride, int take_cap, int k, bool tree) {
   size_t np2 = 1;
   while (np2 < (size_t)k) np2 <<= 1;
-  return (size_t)d_stride * 4 * (1 + RNT / 32) + (size_t)take_cap * 8 + (size_t)k * 4 + 16 +
-         np2 * 8 + 16;
+  size_t rows = tree ? 0 : (size_t)d_stride * 4 * (1 + RNT / 32);
+  return rows + (size_t)take_cap * 8 + (size_t)k * 4 + 16 + np2 * 8 + 16;
 }
+
+bool rerank_uses_tree(const DevIndexView& ix) { return ix.pw_perfect && (ix.d % 2) == 0; }
 
 void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   RerankArgs a;
   a.ix = h.ix; a.queries = h.queries; a.cand_pos = h.cand_pos; a.cand_n = h.cand_n;
   a.take_cap = h.take_cap; a.k = h.k; a.out_ids = h.out_ids; a.out_scores = h.out_scores;
   a.out_count = h.out_count; a.q0 = h.q0; a.order = h.order;
-  if (h.ix.pw_perfect && (h.ix.d % 2) == 0) {
-    size_t np2 = 1;
-    while (np2 < (size_t)h.k) np2 <<= 1;
-    size_t sm = (size_t)h.take_cap * 8 + (size_t)h.k * 4 + 16 + np2 * 8 + 16;
-    int slots = std::max(1, 4 * h.ix.pw_nleaves / 32);
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(k_rerank_tree<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      cudaFuncSetAttribute(k_rerank_tree<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-      attr = true;
+  const bool tree = rerank_uses_tree(h.ix);
+  const size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k, tree);
+  if (tree) {
+    if (4 * h.ix.pw_nleaves <= 32) {
+      allow_smem(k_rerank_tree<1>, 3);
+      k_rerank_tree<1><<<nq, RNT, sm, st>>>(a);
+    } else {
+      allow_smem(k_rerank_tree<2>, 4);
+      k_rerank_tree<2><<<nq, RNT, sm, st>>>(a);
     }
-    if (slots == 1) k_rerank_tree<1><<<nq, RNT, sm, st>>>(a);
-    else k_rerank_tree<2><<<nq, RNT, sm, st>>>(a);
     return;
   }
-  size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_rerank_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  allow_smem(k_rerank_topk, 5);
   k_rerank_topk<<<nq, RNT, sm, st>>>(a);
 }
 

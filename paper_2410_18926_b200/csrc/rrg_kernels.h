@@ -11,6 +11,7 @@ namespace rrg {
 constexpr int EPI_PROJ = 0;
 constexpr int EPI_L2 = 1;
 constexpr int EPI_NEGIP = 2;
+constexpr int kMaxSmemPerCta = 227 * 1024;  // B200 opt-in limit per CTA
 
 struct ScoreArgsHost {
   DevIndexView ix;
@@ -57,7 +58,8 @@ void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int
 void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st);
 size_t score_select_smem(int smem_cap, int take_cap, int k);
 void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st);
-size_t rerank_smem(int d_stride, int take_cap, int k);
+size_t rerank_smem(int d_stride, int take_cap, int k, bool tree);
+bool rerank_uses_tree(const DevIndexView& ix);
 void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st);
 void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
                          const int* pos_of_id, int64_t i0, float* dst, cudaStream_t st);

@@ -83,6 +83,10 @@ __device__ __forceinline__ float unmono32(uint32_t k) {
   uint32_t u = (k & 0x80000000u) ? (k & 0x7fffffffu) : ~k;
   return __uint_as_float(u);
 }
+__device__ __forceinline__ double unmono64(uint64_t k) {
+  uint64_t u = (k & 0x8000000000000000ull) ? (k & 0x7fffffffffffffffull) : ~k;
+  return __longlong_as_double((long long)u);
+}
 __device__ __forceinline__ uint64_t mono64(double f) {
   uint64_t u = (uint64_t)__double_as_longlong(f);
   if (u == 0x8000000000000000ull) u = 0ull;
@@ -326,8 +330,12 @@ struct BucketSmem {
 
 __device__ __forceinline__ int bitlen64(unsigned long long v) { return v ? 64 - __clzll(v) : 0; }
 
-template <int NT, typename K, typename KeyF, typename TieF>
-__device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, int* out,
+// Bucketing is linear in the key's float value v: b = min(B-1, floor(rn(rn(v - vmin) *
+// scale))), a monotone non-decreasing map (IEEE rounding is monotone), so every
+// item of a lower bucket precedes every item of a higher one; ties and the order
+// inside the boundary bucket are resolved on the exact (key, tie).
+template <int NT, typename K, typename V, typename KeyF, typename TieF, typename ValF>
+__device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, ValF val, int* out,
                                      BucketSmem& bs, SelectSmem& sm) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (take >= n) {
@@ -336,7 +344,7 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, int* o
     return n;
   }
   if (take <= 0) return 0;
-  // 1. key range
+  // 1. value range (keys are monotone in value, so the extreme keys give it)
   unsigned long long lo = ~0ull, hi = 0ull;
   for (int i = tid; i < n; i += NT) {
     unsigned long long k = (unsigned long long)key(i);
@@ -354,15 +362,16 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, int* o
   __syncthreads();
   if (lane == 0) { atomicMin(&bs.lo, lo); atomicMax(&bs.hi, hi); }
   __syncthreads();
-  lo = bs.lo;
-  hi = bs.hi;
-  const int bl = bitlen64(hi - lo);
-  const int shift = bl > 11 ? bl - 11 : 0;
+  const V vmin = val((K)bs.lo), vmax = val((K)bs.hi);
+  const V range = vmax - vmin;
+  const V scale = range > (V)0 ? (V)(kSelBins - 1) / range : (V)0;
+  auto bucket = [&](int i) {
+    V f = (val(key(i)) - vmin) * scale;
+    int b = (int)f;
+    return b < kSelBins - 1 ? (b < 0 ? 0 : b) : kSelBins - 1;
+  };
   // 2. histogram
-  for (int i = tid; i < n; i += NT) {
-    int b = (int)(((unsigned long long)key(i) - lo) >> shift);
-    atomicAdd(&bs.hist[b], 1);
-  }
+  for (int i = tid; i < n; i += NT) atomicAdd(&bs.hist[bucket(i)], 1);
   __syncthreads();
   // 3. boundary bucket: block exclusive scan of per-thread bin ranges
   constexpr int per = kSelBins / NT;
@@ -411,7 +420,7 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, int* o
     int i = base + tid;
     bool sel = false;
     if (i < n) {
-      int b = (int)(((unsigned long long)key(i) - lo) >> shift);
+      int b = bucket(i);
       if (b < bb || (b == bb && all_eq)) {
         sel = true;
       } else if (b == bb) {

@@ -156,7 +156,8 @@ __global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ 
   __syncthreads();
   auto key = [&](int i) { return keys[i]; };
   auto tie = [&](int i) { return (uint32_t)i; };
-  block_select_bucketed<NT, uint64_t>(L, w, key, tie, outidx, bs, sm);
+  auto val = [](uint64_t k) { return unmono64(k); };
+  block_select_bucketed<NT, uint64_t, double>(L, w, key, tie, val, outidx, bs, sm);
   for (int i = threadIdx.x; i < w; i += NT) sel[(size_t)blockIdx.x * w + i] = outidx[i];
   // nearest cluster (route()[0]) -- the bucketing key that groups queries for locality
   if (threadIdx.x < 32) {
@@ -293,17 +294,27 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
   int cand_base = 0;
   for (int c0 = 0; c0 < a.w; c0 += kMaxWChunk) {
     const int nc = min(kMaxWChunk, a.w - c0);
-    if (tid == 0) {
-      int off = cand_base;
-      for (int c = 0; c < nc; ++c) {
-        int l = selq[c0 + c];
-        cl_l[c] = l;
-        cl_p0[c] = ix.cl_pos[l];
-        cl_m[c] = ix.cl_pos[l + 1] - ix.cl_pos[l];
-        cl_off[c] = off;
-        off += cl_m[c];
+    if (warp == 0) {  // chunk's cluster table: parallel loads + warp prefix sum
+      int carry = cand_base;
+      for (int b0 = 0; b0 < nc; b0 += 32) {
+        int c = b0 + lane, m = 0;
+        if (c < nc) {
+          int l = selq[c0 + c];
+          int p0 = ix.cl_pos[l];
+          m = ix.cl_pos[l + 1] - p0;
+          cl_l[c] = l;
+          cl_p0[c] = p0;
+          cl_m[c] = m;
+        }
+        int incl = m;
+        for (int o = 1; o < 32; o <<= 1) {
+          int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        if (c < nc) cl_off[c] = carry + incl - m;
+        carry += __shfl_sync(0xffffffffu, incl, 31);
       }
-      cl_off[nc] = off;
+      if (lane == 0) cl_off[nc] = carry;
     }
     __syncthreads();
     // ---- stage A (rrr clusters), all threads: raw1 = codes_x . A[:, j] for every
@@ -406,7 +417,8 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
   int* selidx = reinterpret_cast<int*>(smem_raw + (size_t)a.smem_cap * 8);  // after keys+pos
   auto key = [&](int i) { return keys[i]; };
   auto tie = [&](int i) { return (uint32_t)ix.pid[pos[i]]; };
-  block_select_bucketed<SNT, uint32_t>(N, take, key, tie, selidx, bs, sm);
+  auto val = [](uint32_t k) { return unmono32(k); };
+  block_select_bucketed<SNT, uint32_t, float>(N, take, key, tie, val, selidx, bs, sm);
 
   const int gq = a.q0 + q;
   if (a.rerank) {
@@ -535,7 +547,8 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
   const int kk = min(a.k, n);
   auto key = [&](int i) { return dkeys[i]; };
   auto tie = [&](int i) { return dids[i]; };
-  block_select_bucketed<RNT, uint32_t>(n, kk, key, tie, selidx, bs, sm);
+  auto val = [](uint32_t k) { return unmono32(k); };
+  block_select_bucketed<RNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
   int np2 = 1;
   while (np2 < kk) np2 <<= 1;
   for (int i = tid; i < np2; i += RNT) {
@@ -684,7 +697,8 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
   const int kk = min(a.k, n);
   auto key = [&](int i) { return dkeys[i]; };
   auto tie = [&](int i) { return dids[i]; };
-  block_select_bucketed<RNT, uint32_t>(n, kk, key, tie, selidx, bs, sm);
+  auto val = [](uint32_t k) { return unmono32(k); };
+  block_select_bucketed<RNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
   int np2 = 1;
   while (np2 < kk) np2 <<= 1;
   for (int i = tid; i < np2; i += RNT) {

@@ -145,6 +145,30 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w,
                     int32_t* selected, void* workspace, size_t workspace_bytes,
                     void* stream);
 
+/* ---- cluster-sharded search; one index shard per rank
+ * (rrg_index_open_shard), queries replicated.  Exact reference semantics need
+ * two exchanges because index.py:314-322 re-ranks the GLOBAL top-t:
+ *   1. rrg_shard_phase1 : local top-t (key, corpus id) over the shard's clusters
+ *      -> all-gather -> rrg_merge_candidates : global top-t (identical on all ranks)
+ *   2. rrg_shard_phase2 : re-rank the global candidates this shard holds, local top-k
+ *      -> all-gather -> rrg_merge_results : final top-k == the unsharded result.
+ * Merge inputs use the all-gather layout [G][nq][cap] with counts [G][nq]. */
+size_t rrg_shard_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t k, int32_t w,
+                                 int32_t t);
+int rrg_shard_phase1(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                     int32_t w, int32_t t, uint32_t* keys, uint32_t* ids, int32_t* count,
+                     void* workspace, size_t workspace_bytes, void* stream);
+int rrg_merge_candidates(int64_t nq, int32_t G, int32_t cap, const uint32_t* keys,
+                         const uint32_t* ids, const int32_t* counts, int32_t take,
+                         uint32_t* out_keys, uint32_t* out_ids, int32_t* out_count, void* stream);
+int rrg_shard_phase2(RrgIndex* index, const float* queries, int64_t nq, int32_t dim,
+                     const uint32_t* cand_ids, const int32_t* cand_count, int32_t cap, int32_t k,
+                     int64_t* ids, float* scores, int32_t* count, void* workspace,
+                     size_t workspace_bytes, void* stream);
+int rrg_merge_results(int64_t nq, int32_t G, int32_t k, int32_t metric, const float* scores,
+                      const int64_t* ids, const int32_t* counts, float* out_scores,
+                      int64_t* out_ids, int32_t* out_count, void* stream);
+
 /* Number of CUDA kernel launches issued by the most recent rrg_search* call
  * on this thread (evidence for the bench's gpu_launches). */
 int64_t rrg_last_launch_count(void);

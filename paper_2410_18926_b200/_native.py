@@ -58,6 +58,15 @@ SIGNATURES = {
                                 c_vp, c_vp, c_vp]),
     "rrg_stage_project": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rrg_stage_route": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "rrg_shard_workspace_bytes": (c_size, [c_vp, c_i64, c_i32, c_i32, c_i32]),
+    "rrg_shard_phase1": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
+                                 c_vp, c_size, c_vp]),
+    "rrg_merge_candidates": (c_int, [c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
+                                     c_vp, c_vp]),
+    "rrg_shard_phase2": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
+                                 c_vp, c_vp, c_size, c_vp]),
+    "rrg_merge_results": (c_int, [c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                  c_vp]),
     "rrg_last_launch_count": (c_i64, []),
     "rrg_set_stage_timing": (None, [c_int]),
     "rrg_stage_times": (c_int, [c_vp, c_vp]),

@@ -337,9 +337,11 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.pmeta = ix->upload(pmeta);
   v.pid = ix->upload(pid);
   v.corpus = nullptr;
+  int* d_pos = ix->upload(pos_of_id);
+  v.pos_of_id = d_pos;
+  v.m = hm.m;
   if (has_corpus) {
     float* corp = static_cast<float*>(ix->dalloc((size_t)std::max<int64_t>(P, 1) * v.d_stride * 4));
-    int* d_pos = ix->upload(pos_of_id);
     fill_corpus(corp, d_pos, (int)v.d_stride);
     v.corpus = corp;
   }
@@ -598,7 +600,8 @@ struct Plan {
       off_gk, off_gp, off_prim, off_order, total;
 };
 
-Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank) {
+Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
+               bool exact_take = false) {
   Plan p{};
   const DevIndexView& v = ix->view;
   const int64_t L = v.L;
@@ -609,7 +612,7 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank) 
   // max candidates of any query: sum of the w largest held clusters
   int64_t nmax = 0;
   for (int i = 0; i < (int)ix->sizes_sorted_desc.size() && i < w; ++i) nmax += ix->sizes_sorted_desc[i];
-  p.take_cap = (int)std::min<int64_t>(p.take_cap, std::max<int64_t>(nmax, 1));
+  if (!exact_take) p.take_cap = (int)std::min<int64_t>(p.take_cap, std::max<int64_t>(nmax, 1));
   // dynamic smem per scoring CTA: with ~40 KB static this keeps 2 CTAs (2 x 512
   // threads) resident per SM; queries with more candidates spill to global
   const size_t budget = 64 * 1024;
@@ -655,10 +658,17 @@ void validate_search(const RrgIndex* ix, int32_t dim, int32_t k, int32_t w, int3
     raise_usage("ParameterError", "index was built without the corpus; re-ranking unavailable");
 }
 
+// Sharded phase 1 outputs: the shard's local top-t (key, corpus id) per query.
+struct Phase1Out {
+  uint32_t* keys;
+  uint32_t* ids;
+  int32_t* count;
+};
+
 void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int32_t w, int32_t t,
                  int32_t rerank, int64_t* ids, float* scores, int32_t* count, void* ws,
-                 size_t ws_bytes, cudaStream_t st) {
-  Plan p = make_plan(ix, nq, k, w, t, rerank);
+                 size_t ws_bytes, cudaStream_t st, const Phase1Out* ph1 = nullptr) {
+  Plan p = make_plan(ix, nq, k, w, t, rerank, ph1 != nullptr);
   {  // shared-memory budgets of the per-query CTAs (static parts bounded by 48 KB)
     const size_t lim = kMaxSmemPerCta - 48 * 1024;
     if (score_select_smem(p.smem_cap, p.take_cap, k) > lim ||
@@ -697,8 +707,9 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
     sa.gkeys = gk; sa.gpos = gp; sa.gcap = p.gcap; sa.cand_pos = cpos; sa.cand_n = cn;
     sa.out_ids = ids; sa.out_scores = scores; sa.out_count = count; sa.q0 = (int)q0;
     sa.order = order;
+    if (ph1) { sa.sel_keys = ph1->keys; sa.sel_ids = ph1->ids; sa.sel_count = ph1->count; }
     staged(4, st, [&] { launch_score_select(sa, n, st); });
-    if (rerank) {
+    if (rerank && !ph1) {
       RerankArgsHost ra{};
       ra.ix = v; ra.queries = x; ra.cand_pos = cpos; ra.cand_n = cn; ra.take_cap = p.take_cap;
       ra.k = k; ra.out_ids = ids; ra.out_scores = scores; ra.out_count = count; ra.q0 = (int)q0;
@@ -872,6 +883,88 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int
     launch_route_select(diss, (int)nq, v.L, w, selected, reinterpret_cast<int*>(dummy + 3 * nq), st);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(dummy, st));
+    return RRG_OK;
+  });
+}
+
+// ---------------------------------------------------------- sharded search
+
+size_t rrg_shard_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t k, int32_t w,
+                                 int32_t t) {
+  if (!index || nq <= 0 || k < 1 || w < 1 || t < 1) return 0;
+  size_t a = make_plan(index, nq, k, w, t, 1, true).total;
+  size_t b = ((size_t)nq * t * 4 + 255) / 256 * 256 + ((size_t)nq * 4 + 255) / 256 * 256;
+  return std::max(a, b);
+}
+
+int rrg_shard_phase1(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                     int32_t w, int32_t t, uint32_t* keys, uint32_t* ids, int32_t* count,
+                     void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
+    if (nq == 0) return RRG_OK;
+    validate_search(index, dim, k, w, t, 1);
+    CUDA_TRY(cudaSetDevice(index->device));
+    Phase1Out o{keys, ids, count};
+    search_impl(index, queries, nq, k, w, t, 1, nullptr, nullptr, nullptr, workspace,
+                workspace_bytes, static_cast<cudaStream_t>(stream), &o);
+    return RRG_OK;
+  });
+}
+
+int rrg_merge_candidates(int64_t nq, int32_t G, int32_t cap, const uint32_t* keys,
+                         const uint32_t* ids, const int32_t* counts, int32_t take,
+                         uint32_t* out_keys, uint32_t* out_ids, int32_t* out_count, void* stream) {
+  return guarded([&] {
+    if (G < 1 || G > 64) raise_usage("ParameterError", "G=%d out of range [1, 64]", G);
+    if (nq == 0) return RRG_OK;
+    staged(4, static_cast<cudaStream_t>(stream), [&] {
+      launch_merge(0, 0, (int)nq, G, cap, keys, ids, counts, take, out_keys, out_ids, out_count,
+                   static_cast<cudaStream_t>(stream));
+    });
+    CUDA_TRY(cudaGetLastError());
+    return RRG_OK;
+  });
+}
+
+int rrg_shard_phase2(RrgIndex* index, const float* queries, int64_t nq, int32_t dim,
+                     const uint32_t* cand_ids, const int32_t* cand_count, int32_t cap, int32_t k,
+                     int64_t* ids, float* scores, int32_t* count, void* workspace,
+                     size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
+    if (nq == 0) return RRG_OK;
+    validate_search(index, dim, k, 1, std::max(cap, k), 1);
+    size_t need = ((size_t)nq * cap * 4 + 255) / 256 * 256 + ((size_t)nq * 4 + 255) / 256 * 256;
+    if (workspace_bytes < need) raise_usage("ParameterError", "workspace too small");
+    CUDA_TRY(cudaSetDevice(index->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int* cpos = static_cast<int*>(workspace);
+    int* cn = reinterpret_cast<int*>(static_cast<char*>(workspace) +
+                                     ((size_t)nq * cap * 4 + 255) / 256 * 256);
+    staged(5, st, [&] { launch_ids_to_pos(index->view, (int)nq, cap, cand_ids, cand_count, cpos, cn, st); });
+    RerankArgsHost ra{};
+    ra.ix = index->view; ra.queries = queries; ra.cand_pos = cpos; ra.cand_n = cn;
+    ra.take_cap = cap; ra.k = k; ra.out_ids = ids; ra.out_scores = scores; ra.out_count = count;
+    ra.q0 = 0;
+    staged(5, st, [&] { launch_rerank(ra, (int)nq, st); });
+    CUDA_TRY(cudaGetLastError());
+    return RRG_OK;
+  });
+}
+
+int rrg_merge_results(int64_t nq, int32_t G, int32_t k, int32_t metric, const float* scores,
+                      const int64_t* ids, const int32_t* counts, float* out_scores,
+                      int64_t* out_ids, int32_t* out_count, void* stream) {
+  return guarded([&] {
+    if (G < 1 || G > 64) raise_usage("ParameterError", "G=%d out of range [1, 64]", G);
+    if (nq == 0) return RRG_OK;
+    staged(5, static_cast<cudaStream_t>(stream), [&] {
+      launch_merge(1, metric, (int)nq, G, k, scores, ids, counts, k, out_scores, out_ids,
+                   out_count, static_cast<cudaStream_t>(stream));
+    });
+    CUDA_TRY(cudaGetLastError());
     return RRG_OK;
   });
 }

@@ -45,6 +45,8 @@ struct DevIndexView {
   const float4* pmeta;
   const int64_t* pid;    // [P] original corpus ids
   const float* corpus;   // [P][d_stride] in cluster order, or nullptr
+  const int* pos_of_id;  // [m] corpus id -> position held here, -1 if another shard's
+  int64_t m;             // corpus size (all shards)
   // NumPy pairwise-summation plan for a row of d floats: when the recursion
   // tree is perfect (2^a equal leaves of pw_leaf_n <= 128 elements, e.g. d = 128,
   // 768, 960, 1536) the re-rank runs the warp-parallel kernel.

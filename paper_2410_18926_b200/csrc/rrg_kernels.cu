@@ -239,6 +239,9 @@ struct ScoreArgs {
   int* out_count;
   int q0;  // query offset of this chunk (outputs)
   const int* order;  // CTA -> chunk-local query (bucket order), or nullptr
+  uint32_t* sel_keys;  // optional [nq][take_cap] keys of the local top-t (sharded phase 1)
+  uint32_t* sel_ids;   // optional [nq][take_cap] corpus ids of the local top-t
+  int* sel_count;      // optional [nq]
 };
 
 constexpr int SNT = 512;
@@ -424,6 +427,16 @@ __global__ void __launch_bounds__(SNT) k_score_select(ScoreArgs a) {
   if (a.rerank) {
     int* outp = a.cand_pos + (size_t)q * a.take_cap;
     for (int i = tid; i < take; i += SNT) outp[i] = pos[selidx[i]];
+    if (a.sel_keys) {  // sharded phase 1: (key, corpus id) of the local top-t
+      uint32_t* ok = a.sel_keys + (size_t)(a.q0 + q) * a.take_cap;
+      uint32_t* oi = a.sel_ids + (size_t)(a.q0 + q) * a.take_cap;
+      for (int i = tid; i < take; i += SNT) {
+        int ci = selidx[i];
+        ok[i] = keys[ci];
+        oi[i] = __float_as_uint(__ldg(ix.pmeta + pos[ci]).w);
+      }
+      if (tid == 0) a.sel_count[a.q0 + q] = take;
+    }
     if (tid == 0) a.cand_n[q] = take;
     return;
   }
@@ -627,19 +640,41 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
 #pragma unroll
     for (int u = 0; u < 7; ++u) xt[s][u] = u < tail ? xq[b * nl + 8 * nb + u] : 0.f;
   }
-  const int* cp = a.cand_pos + (size_t)q * a.take_cap;
-  for (int row0 = warp * R; row0 < n; row0 += nwarps * R) {
-    const int row = row0 + g;
+  // candidate positions staged in smem (dids doubles as the position buffer: row i's
+  // slot is read before it is overwritten with the row's corpus id)
+  {
+    const int* cp = a.cand_pos + (size_t)q * a.take_cap;
+    for (int i = tid; i < n; i += RNT) dids[i] = (uint32_t)cp[i];
+  }
+  __syncthreads();
+  // U row groups per warp pass: all U rows' loads are issued before any math
+  constexpr int U = SLOTS == 1 ? 2 : 1;
+  for (int row0 = warp * R * U; row0 < n; row0 += nwarps * R * U) {
+    int rows[U], gps[U];
+    float2 cbuf[U][SLOTS][kMaxNb];
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      rows[uu] = row0 + uu * R + g;
+      gps[uu] = (int)dids[rows[uu] < n ? rows[uu] : row0];
+      const float* crow = ix.corpus + (size_t)gps[uu] * ds;
+#pragma unroll
+      for (int s = 0; s < SLOTS; ++s)
+#pragma unroll
+        for (int i = 0; i < kMaxNb; ++i)
+          if (i < nb && rows[uu] - g < n)
+            cbuf[uu][s][i] = __ldg(reinterpret_cast<const float2*>(crow + off[s] + 8 * i));
+    }
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+    if (rows[uu] - g >= n) break;  // whole lane group past the end (warp-uniform)
+    const int row = rows[uu];
     const bool valid = row < n;
-    const int gp = valid ? cp[row] : cp[row0];
+    const int gp = gps[uu];
     const float* crow = ix.corpus + (size_t)gp * ds;
     float slot_sum[SLOTS];
 #pragma unroll
     for (int s = 0; s < SLOTS; ++s) {
-      float2 c[kMaxNb];
-#pragma unroll
-      for (int i = 0; i < kMaxNb; ++i)
-        if (i < nb) c[i] = __ldg(reinterpret_cast<const float2*>(crow + off[s] + 8 * i));
+      const float2* c = cbuf[uu][s];
       float v;
       if (euclid) {
         float r0 = 0.f, r1 = 0.f;
@@ -690,7 +725,8 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
     if (valid && pl == 0) {
       float diss = euclid ? tot : -tot;
       dkeys[row] = mono32(diss);
-      dids[row] = (uint32_t)ix.pid[gp];
+      dids[row] = __float_as_uint(__ldg(ix.pmeta + gp).w);  // corpus id (low 32 bits)
+    }
     }
   }
   __syncthreads();
@@ -724,6 +760,135 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
     a.out_scores[(size_t)gq * a.k + i] = sc;
   }
   if (tid == 0) a.out_count[gq] = kk;
+}
+
+// ======================================================== sharded merges
+// One CTA per query: compact the G sources' valid entries into shared memory,
+// select the `take` smallest by (key, id) and emit them sorted (the reference's
+// lexsort order, index.py:315,320).  Exact for any G: a global top-t / top-k is
+// always contained in the union of the per-shard top-t / top-k lists.
+constexpr int MNT = 256;
+__global__ void __launch_bounds__(MNT) k_merge(int mode, int metric, int nq, int G, int cap,
+                                               const void* __restrict__ in_keys,
+                                               const void* __restrict__ in_ids,
+                                               const int* __restrict__ in_counts, int take,
+                                               void* __restrict__ out_keys,
+                                               void* __restrict__ out_ids,
+                                               int* __restrict__ out_count) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
+  __shared__ int base[65];
+  const int q = blockIdx.x, tid = threadIdx.x;
+  const int ncap = G * cap;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(smem_raw);
+  uint32_t* ids = keys + ncap;
+  int* selidx = reinterpret_cast<int*>(ids + ncap);
+  uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + take);
+  uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
+  if (tid == 0) {
+    int acc = 0;
+    for (int g = 0; g < G; ++g) { base[g] = acc; acc += in_counts[(size_t)g * nq + q]; }
+    base[G] = acc;
+  }
+  __syncthreads();
+  const int n = base[G];
+  for (int g = 0; g < G; ++g) {
+    const int c = base[g + 1] - base[g];
+    const size_t src = ((size_t)g * nq + q) * cap;
+    for (int i = tid; i < c; i += MNT) {
+      uint32_t k, id;
+      if (mode == 0) {
+        k = static_cast<const uint32_t*>(in_keys)[src + i];
+        id = static_cast<const uint32_t*>(in_ids)[src + i];
+      } else {
+        float s = static_cast<const float*>(in_keys)[src + i];
+        k = mono32(metric == kMetricEuclidean ? s : -s);
+        id = (uint32_t) static_cast<const int64_t*>(in_ids)[src + i];
+      }
+      keys[base[g] + i] = k;
+      ids[base[g] + i] = id;
+    }
+  }
+  __syncthreads();
+  const int kk = min(take, n);
+  auto key = [&](int i) { return keys[i]; };
+  auto tie = [&](int i) { return ids[i]; };
+  auto val = [](uint32_t k) { return unmono32(k); };
+  block_select_bucketed<MNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
+  int np2 = 1;
+  while (np2 < kk) np2 <<= 1;
+  for (int i = tid; i < np2; i += MNT) {
+    uint64_t v = ~0ull;
+    if (i < kk) v = ((uint64_t)keys[selidx[i]] << 32) | ids[selidx[i]];
+    srt[i] = v;
+  }
+  block_bitonic_sort<MNT>(srt, np2);
+  for (int i = tid; i < take; i += MNT) {
+    const size_t o = (size_t)q * take + i;
+    if (mode == 0) {
+      static_cast<uint32_t*>(out_keys)[o] = i < kk ? (uint32_t)(srt[i] >> 32) : ~0u;
+      static_cast<uint32_t*>(out_ids)[o] = i < kk ? (uint32_t)srt[i] : ~0u;
+    } else {
+      float sc = __int_as_float(0x7fc00000);
+      int64_t id = -1;
+      if (i < kk) {
+        float df = unmono32((uint32_t)(srt[i] >> 32));
+        sc = metric == kMetricEuclidean ? df : -df;
+        id = (int64_t)(uint32_t)srt[i];
+      }
+      static_cast<float*>(out_keys)[o] = sc;
+      static_cast<int64_t*>(out_ids)[o] = id;
+    }
+  }
+  if (tid == 0) out_count[q] = kk;
+}
+
+// Warp per query: keep the candidates this shard holds, as positions.
+__global__ void k_ids_to_pos(DevIndexView ix, int nq, int cap, const uint32_t* __restrict__ ids,
+                             const int* __restrict__ counts, int* __restrict__ cand_pos,
+                             int* __restrict__ cand_n) {
+  const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const int c = counts[q];
+  int outn = 0;
+  for (int b = 0; b < c; b += 32) {
+    int i = b + lane;
+    int p = -1;
+    if (i < c) {
+      uint32_t id = ids[(size_t)q * cap + i];
+      p = id < (uint64_t)ix.m ? ix.pos_of_id[id] : -1;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, p >= 0);
+    if (p >= 0) cand_pos[(size_t)q * cap + outn + __popc(m & ((1u << lane) - 1))] = p;
+    outn += __popc(m);
+  }
+  if (lane == 0) cand_n[q] = outn;
+}
+
+void launch_merge(int mode, int metric, int nq, int G, int cap, const void* in_keys,
+                  const void* in_ids, const int* in_counts, int take, void* out_keys,
+                  void* out_ids, int* out_count, cudaStream_t st) {
+  size_t np2 = 1;
+  while (np2 < (size_t)take) np2 <<= 1;
+  size_t sm = (size_t)G * cap * 8 + (size_t)take * 4 + 16 + np2 * 8 + 16;
+  static int done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    cudaFuncAttributes at{};
+    cudaFuncGetAttributes(&at, (const void*)k_merge);
+    cudaFuncSetAttribute((const void*)k_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kMaxSmemPerCta - (int)at.sharedSizeBytes);
+    done[dev] = 1;
+  }
+  k_merge<<<nq, MNT, sm, st>>>(mode, metric, nq, G, cap, in_keys, in_ids, in_counts, take,
+                               out_keys, out_ids, out_count);
+}
+
+void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* ids,
+                       const int* counts, int* cand_pos, int* cand_n, cudaStream_t st) {
+  k_ids_to_pos<<<(nq + 7) / 8, 256, 0, st>>>(ix, nq, cap, ids, counts, cand_pos, cand_n);
 }
 
 // ======================================================= corpus scatter
@@ -810,6 +975,7 @@ void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st) {
   a.cand_pos = h.cand_pos; a.cand_n = h.cand_n; a.out_ids = h.out_ids;
   a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
   a.order = h.order;
+  a.sel_keys = h.sel_keys; a.sel_ids = h.sel_ids; a.sel_count = h.sel_count;
   allow_smem(k_score_select, 2);
   k_score_select<<<nq, SNT, score_select_smem(h.smem_cap, h.take_cap, h.k), st>>>(a);
 }

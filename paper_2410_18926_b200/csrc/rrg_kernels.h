@@ -31,6 +31,9 @@ struct ScoreArgsHost {
   int* out_count;
   int q0;
   const int* order = nullptr;
+  uint32_t* sel_keys = nullptr;
+  uint32_t* sel_ids = nullptr;
+  int* sel_count = nullptr;
 };
 
 struct RerankArgsHost {
@@ -61,6 +64,18 @@ void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st);
 size_t rerank_smem(int d_stride, int take_cap, int k, bool tree);
 bool rerank_uses_tree(const DevIndexView& ix);
 void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st);
+// Sharded search: merge G per-shard lists per query, laid out
+// [G][nq][cap] (the all-gather layout) with counts [G][nq].
+//   mode 0: (key u32, id u32) candidates -> global top-`take` by (key, id), sorted
+//   mode 1: (score f32, id i64) results  -> global top-`take` by (diss, id), sorted,
+//           diss = score (euclidean) | -score (ip/cosine)
+void launch_merge(int mode, int metric, int nq, int G, int cap, const void* in_keys,
+                  const void* in_ids, const int* in_counts, int take, void* out_keys,
+                  void* out_ids, int* out_count, cudaStream_t st);
+// ids -> positions held by this shard (others dropped): cand_pos [nq][cap], cand_n [nq]
+void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* ids,
+                       const int* counts, int* cand_pos, int* cand_n, cudaStream_t st);
+
 void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
                          const int* pos_of_id, int64_t i0, float* dst, cudaStream_t st);
 

@@ -1,0 +1,232 @@
+"""Cluster-sharded search across GPUs with exact reference semantics.
+
+Each rank holds a contiguous range of clusters (balanced by points) with their
+factors and corpus rows (``rrg_index_open_shard``); projection and centroids are
+replicated, so every rank routes every query identically.  Because the
+reference re-ranks the GLOBAL top-t (index.py:314-322), one exchange after a
+per-rank re-rank would not be equivalent; two are needed:
+
+1. phase 1: each rank scores the probed clusters it holds and keeps its local
+   top-t by (key, corpus id); all-gather; every rank merges the identical global
+   top-t (``rrg_merge_candidates``);
+2. phase 2: each rank re-ranks the global candidates it holds (exact distances)
+   and keeps its local top-k; all-gather; merge -> the final top-k
+   (``rrg_merge_results``), id-for-id equal to the single-GPU and CPU results.
+
+The orchestration here is engine-agnostic: ``CudaShardEngine`` drives librrg.so
+(NCCL all-gathers over NVLink through ``TorchExchange``); the CPU tests plug
+in an oracle-backed engine and a gloo exchange with the same control flow.
+"""
+
+from __future__ import annotations
+
+import struct
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._native import check, lib
+from .errors import ParameterError
+
+
+# ------------------------------------------------------------------ partitioning
+
+
+def scan_cluster_sizes(path) -> np.ndarray:
+    """m_l of every cluster record, walking the RRRANN01 layout (index.py:365-402)
+    without reading payloads."""
+    with open(path, "rb") as f:
+        head = f.read(8 + 29)
+        mc, d, s, r, L, m, flags = struct.unpack("<BIIIIQI", head[8:])
+        quant = bool(flags & 1)
+        exact_ivf = bool(flags & 8)
+        off = 8 + 29 + 4 * d * s + 4 * L * s
+        sizes = np.empty(L, dtype=np.int64)
+
+        def factor_bytes(rows, cols):
+            return (8 * cols + rows * cols) if quant else 4 * rows * cols
+
+        for l in range(L):
+            f.seek(off)
+            (ml,) = struct.unpack("<I", f.read(4))
+            sizes[l] = ml
+            off += 4 + 8 * ml
+            exact = exact_ivf or ml < r
+            off += factor_bytes(s, ml if exact else r)
+            if not exact:
+                off += factor_bytes(r, ml)
+            if mc == 0:
+                off += 4 * ml
+    return sizes
+
+
+def partition_clusters(sizes, world: int) -> list[tuple[int, int]]:
+    """Contiguous cluster ranges with near-equal point counts (one per rank)."""
+    sizes = np.asarray(sizes, dtype=np.int64)
+    L = sizes.shape[0]
+    if world < 1 or world > L:
+        raise ParameterError(f"cannot split {L} clusters over {world} ranks")
+    cum = np.concatenate([[0], np.cumsum(sizes)])
+    total = cum[-1]
+    cuts = [0]
+    for g in range(1, world):
+        target = total * g / world
+        c = int(np.searchsorted(cum, target, side="left"))
+        if c > 0 and abs(cum[c - 1] - target) <= abs(cum[min(c, L)] - target):
+            c -= 1  # nearest prefix boundary
+        c = min(max(c, cuts[-1] + 1), L - (world - g))
+        cuts.append(c)
+    cuts.append(L)
+    return [(cuts[g], cuts[g + 1]) for g in range(world)]
+
+
+# -------------------------------------------------------------------- exchanges
+
+
+class TorchExchange:
+    """all-gather over torch.distributed (NCCL for CUDA tensors, gloo for CPU)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.world = dist.get_world_size(group)
+
+    def all_gather(self, t):
+        import torch
+
+        t = t.contiguous()
+        if t.is_cuda:  # NCCL: one fused all-gather into the [G, ...] layout
+            out = torch.empty((self.world,) + tuple(t.shape), dtype=t.dtype, device=t.device)
+            self.dist.all_gather_into_tensor(out, t, group=self.group)
+            return out
+        parts = [torch.empty_like(t) for _ in range(self.world)]  # gloo (CPU tests)
+        self.dist.all_gather(parts, t, group=self.group)
+        return torch.stack(parts)
+
+
+class LocalExchange:
+    """In-process stand-in: the G shards live in one process (tests, 1-GPU emulation)."""
+
+    def __init__(self, world: int):
+        self.world = world
+
+
+# ---------------------------------------------------------------------- engines
+
+
+@dataclass
+class Candidates:
+    keys: object   # [nq, t] uint32 (as int32 tensors / uint32 arrays)
+    ids: object    # [nq, t] uint32
+    count: object  # [nq] int32
+
+
+class CudaShardEngine:
+    """librrg.so shard of a DeviceIndex; tensors are torch CUDA tensors."""
+
+    def __init__(self, dev):
+        self.dev = dev
+
+    @property
+    def metric_code(self) -> int:
+        return {"euclidean": 0, "ip": 1, "cosine": 2}[self.dev.metric]
+
+    def _ws(self, nbytes):
+        import torch
+
+        ws = getattr(self, "_wsbuf", None)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.dev.device}")
+            self._wsbuf = ws
+        return ws
+
+    def phase1(self, q, k, w, t):
+        import torch
+
+        nq, dim = q.shape
+        dev = q.device
+        keys = torch.empty((nq, t), dtype=torch.int32, device=dev)
+        ids = torch.empty((nq, t), dtype=torch.int32, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        nb = int(lib.rrg_shard_workspace_bytes(self.dev.handle, nq, k, w, t))
+        ws = self._ws(nb)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_shard_phase1(self.dev.handle, q.data_ptr(), nq, dim, k, w, t, keys.data_ptr(),
+                                   ids.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(), st))
+        return Candidates(keys, ids, cnt)
+
+    def merge_candidates(self, gk, gi, gc, take):
+        import torch
+
+        G, nq, cap = gk.shape
+        dev = gk.device
+        keys = torch.empty((nq, take), dtype=torch.int32, device=dev)
+        ids = torch.empty((nq, take), dtype=torch.int32, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_merge_candidates(nq, G, cap, gk.data_ptr(), gi.data_ptr(), gc.data_ptr(), take,
+                                       keys.data_ptr(), ids.data_ptr(), cnt.data_ptr(), st))
+        return Candidates(keys, ids, cnt)
+
+    def phase2(self, q, cand: Candidates, k):
+        import torch
+
+        nq, dim = q.shape
+        cap = cand.ids.shape[1]
+        dev = q.device
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        sc = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        nb = 2 * (nq * cap * 4 + nq * 4) + 1024
+        ws = self._ws(nb)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_shard_phase2(self.dev.handle, q.data_ptr(), nq, dim, cand.ids.data_ptr(),
+                                   cand.count.data_ptr(), cap, k, ids.data_ptr(), sc.data_ptr(),
+                                   cnt.data_ptr(), ws.data_ptr(), ws.numel(), st))
+        return ids, sc, cnt
+
+    def merge_results(self, gi, gs, gc, k):
+        import torch
+
+        G, nq, _ = gi.shape
+        dev = gi.device
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        sc = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_merge_results(nq, G, k, self.metric_code, gs.data_ptr(), gi.data_ptr(),
+                                    gc.data_ptr(), sc.data_ptr(), ids.data_ptr(), cnt.data_ptr(), st))
+        return ids, sc, cnt
+
+
+# --------------------------------------------------------------- orchestration
+
+
+def sharded_search(engine, exchange, queries, k: int, w: int, t: int):
+    """Two-phase exact sharded search for one rank (all ranks call it collectively)."""
+    if k > t:
+        raise ParameterError(f"k={k} must be <= t={t} when re-ranking")
+    c1 = engine.phase1(queries, k, w, t)
+    gk = exchange.all_gather(c1.keys)
+    gi = exchange.all_gather(c1.ids)
+    gc = exchange.all_gather(c1.count)
+    cand = engine.merge_candidates(gk, gi, gc, t)
+    ids, sc, cnt = engine.phase2(queries, cand, k)
+    return engine.merge_results(exchange.all_gather(ids), exchange.all_gather(sc),
+                                exchange.all_gather(cnt), k)
+
+
+def sharded_search_local(engines, queries, k: int, w: int, t: int):
+    """All G shards in one process (LocalExchange): same two phases, stacked lists."""
+    import torch
+
+    c1 = [e.phase1(queries, k, w, t) for e in engines]
+    gk = torch.stack([c.keys for c in c1])
+    gi = torch.stack([c.ids for c in c1])
+    gc = torch.stack([c.count for c in c1])
+    cand = engines[0].merge_candidates(gk, gi, gc, t)
+    res = [e.phase2(queries, cand, k) for e in engines]
+    return engines[0].merge_results(torch.stack([r[0] for r in res]), torch.stack([r[1] for r in res]),
+                                    torch.stack([r[2] for r in res]), k)

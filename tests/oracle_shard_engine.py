@@ -1,0 +1,122 @@
+"""CPU (oracle-backed) shard engine with the same interface as ``sharded.CudaShardEngine``.
+
+Test infrastructure only: lets the multi-process (gloo) tests exercise the
+two-phase sharded orchestration of ``paper_2410_18926_b200.sharded`` on CPU.
+Arithmetic per stage is the oracle's (oracle/rrann_oracle.py); ordering is by
+(key, corpus id) with -0.0 == +0.0, as in the kernels.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import rrann_oracle as O
+from paper_2410_18926_b200.sharded import Candidates
+
+F32 = np.float32
+
+
+def mono32(f: np.ndarray) -> np.ndarray:
+    u = np.ascontiguousarray(f, dtype=F32).view(np.uint32).astype(np.uint64)
+    u = np.where(u == 0x80000000, 0, u)
+    return np.where(u & 0x80000000, (~u) & 0xFFFFFFFF, u | 0x80000000).astype(np.uint32)
+
+
+def _as_i32(a: np.ndarray) -> torch.Tensor:
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int32).copy())
+
+
+class OracleShardEngine:
+    def __init__(self, index: O.OIndex, c0: int, c1: int):
+        self.ix = index
+        self.c0, self.c1 = c0, c1
+        self.owner = np.full(index.m, False)
+        for l in range(c0, c1):
+            self.owner[index.clusters[l].ids] = True
+
+    def phase1(self, q, k, w, t):
+        qn = q.numpy()
+        nq = qn.shape[0]
+        keys = np.full((nq, t), 0xFFFFFFFF, np.uint32)
+        ids = np.full((nq, t), 0xFFFFFFFF, np.uint32)
+        cnt = np.zeros(nq, np.int32)
+        for i in range(nq):
+            xp = O.project(qn[i][None, :], self.ix.projection)[0]
+            sel = O.route(xp, self.ix.centroids, w, self.ix.metric)
+            qx = O.q8(xp)
+            kk, ii = [], []
+            for l in sel:
+                if not self.c0 <= int(l) < self.c1:
+                    continue
+                cl = self.ix.clusters[int(l)]
+                sc = O.score_cluster(xp, qx, cl, self.ix.metric)
+                kk.append(sc if self.ix.metric == "euclidean" else -sc)
+                ii.append(cl.ids)
+            if not kk:
+                continue
+            kv = mono32(np.concatenate(kk))
+            iv = np.concatenate(ii).astype(np.uint32)
+            order = np.lexsort((iv, kv))[:t]
+            keys[i, :len(order)] = kv[order]
+            ids[i, :len(order)] = iv[order]
+            cnt[i] = len(order)
+        return Candidates(_as_i32(keys), _as_i32(ids), torch.from_numpy(cnt))
+
+    @staticmethod
+    def _gather(gk, gi, gc):
+        gk = gk.numpy().view(np.uint32)
+        gi = gi.numpy().view(np.uint32)
+        gc = gc.numpy()
+        return gk, gi, gc
+
+    def merge_candidates(self, gk, gi, gc, take):
+        gk, gi, gc = self._gather(gk, gi, gc)
+        G, nq, _ = gk.shape
+        keys = np.full((nq, take), 0xFFFFFFFF, np.uint32)
+        ids = np.full((nq, take), 0xFFFFFFFF, np.uint32)
+        cnt = np.zeros(nq, np.int32)
+        for i in range(nq):
+            kv = np.concatenate([gk[g, i, :gc[g, i]] for g in range(G)])
+            iv = np.concatenate([gi[g, i, :gc[g, i]] for g in range(G)])
+            order = np.lexsort((iv, kv))[:take]
+            keys[i, :len(order)] = kv[order]
+            ids[i, :len(order)] = iv[order]
+            cnt[i] = len(order)
+        return Candidates(_as_i32(keys), _as_i32(ids), torch.from_numpy(cnt))
+
+    def phase2(self, q, cand, k):
+        qn = q.numpy()
+        nq = qn.shape[0]
+        cids = cand.ids.numpy().view(np.uint32)
+        ccnt = cand.count.numpy()
+        out_ids = np.full((nq, k), -1, np.int64)
+        out_sc = np.full((nq, k), np.nan, F32)
+        out_cnt = np.zeros(nq, np.int32)
+        for i in range(nq):
+            ids = cids[i, :ccnt[i]].astype(np.int64)
+            ids = ids[self.owner[ids]]
+            if ids.size == 0:
+                continue
+            diss = O.exact_dissimilarity(self.ix, qn[i], ids)
+            keep = np.lexsort((ids, mono32(diss)))[:k]
+            out_ids[i, :len(keep)] = ids[keep]
+            out_sc[i, :len(keep)] = diss[keep] if self.ix.metric == "euclidean" else -diss[keep]
+            out_cnt[i] = len(keep)
+        return torch.from_numpy(out_ids), torch.from_numpy(out_sc), torch.from_numpy(out_cnt)
+
+    def merge_results(self, gi, gs, gc, k):
+        gi, gs, gc = gi.numpy(), gs.numpy(), gc.numpy()
+        G, nq, _ = gi.shape
+        out_ids = np.full((nq, k), -1, np.int64)
+        out_sc = np.full((nq, k), np.nan, F32)
+        out_cnt = np.zeros(nq, np.int32)
+        for i in range(nq):
+            iv = np.concatenate([gi[g, i, :gc[g, i]] for g in range(G)])
+            sv = np.concatenate([gs[g, i, :gc[g, i]] for g in range(G)]).astype(F32)
+            diss = sv if self.ix.metric == "euclidean" else -sv
+            keep = np.lexsort((iv, mono32(diss)))[:k]
+            out_ids[i, :len(keep)] = iv[keep]
+            out_sc[i, :len(keep)] = sv[keep]
+            out_cnt[i] = len(keep)
+        return torch.from_numpy(out_ids), torch.from_numpy(out_sc), torch.from_numpy(out_cnt)

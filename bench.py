@@ -8,9 +8,12 @@ queries, 1M x 768 corpus, L=1024, s=256, r=32, k=100) through the device entry
 host-buffer C-ABI entry ``rrg_search_host`` with pinned host queries and results
 copied inside the timed region (``e2e``).
 
-Multi-GPU (torchrun, N>1): queries are independent units -- each rank searches
-its own full batch against its own replica of the index with no data-path
-collective; ``value`` = all ranks' queries / max-over-ranks time ("weak").
+Multi-GPU (torchrun, N>1), default ``--mode sharded`` (the north star's layout):
+clusters with their factors and corpus rows are split over the ranks, the query
+batch is replicated, and the two exact merges (global top-t, then top-k) are
+NCCL all-gathers over NVLink; ``value`` = batch / max-over-ranks time
+("strong").  ``--mode replica``: each rank searches its own batch on a full
+index copy with no collective ("weak").
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle port of
 rrann.query_batch, oracle/rrann_oracle.py) on the host cores, on a bounded
@@ -47,6 +50,8 @@ def parse():
     ap.add_argument("--t", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="sharded", choices=["sharded", "replica"],
+                    help="N>1: cluster-sharded index (north star) or full-index replicas")
     return ap.parse_args()
 
 
@@ -193,6 +198,57 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+class LocalSearcher:
+    """One full index per rank (N=1, or replicas: each rank its own query batch)."""
+
+    def __init__(self, dev, k, w, t):
+        self.dev, self.k, self.w, self.t = dev, k, w, t
+
+    def device_step(self, q, out):
+        return self.dev.search_device(q, self.k, self.w, self.t, True, out=out)
+
+    def host_step(self, qpin, hout):
+        return self.dev.search_host(qpin, self.k, self.w, self.t, True, out=hout)
+
+
+class ShardedSearcher:
+    """Cluster-sharded index over the ranks; queries broadcast; two NCCL all-gather merges."""
+
+    def __init__(self, dev, k, w, t):
+        from paper_2410_18926_b200.sharded import CudaShardEngine, TorchExchange
+
+        self.dev, self.k, self.w, self.t = dev, k, w, t
+        self.engine = CudaShardEngine(dev)
+        self.ex = TorchExchange()
+
+    def device_step(self, q, out):
+        from paper_2410_18926_b200.sharded import sharded_search
+
+        ids, sc, cnt = sharded_search(self.engine, self.ex, q, self.k, self.w, self.t)
+        out[0].copy_(ids)
+        out[1].copy_(sc)
+        out[2].copy_(cnt)
+        return out
+
+    def host_step(self, qpin, hout):
+        import torch
+
+        q = torch.from_numpy(qpin).cuda(non_blocking=True)
+        ids, sc, cnt = self.device_step(q, self._out(q))
+        for h, d in zip(hout, (ids, sc, cnt)):
+            torch.from_numpy(h).copy_(d)
+        return hout
+
+    def _out(self, q):
+        import torch
+
+        if getattr(self, "_o", None) is None or self._o[0].shape[0] != q.shape[0]:
+            self._o = (torch.empty((q.shape[0], self.k), dtype=torch.int64, device=q.device),
+                       torch.empty((q.shape[0], self.k), dtype=torch.float32, device=q.device),
+                       torch.empty((q.shape[0],), dtype=torch.int32, device=q.device))
+        return self._o
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -204,6 +260,7 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    sharded = world > 1 and args.mode == "sharded"
 
     from paper_2410_18926_b200 import DeviceIndex, _native, last_launch_count
     from paper_2410_18926_b200 import workloads as W
@@ -215,7 +272,15 @@ def main():
     if world > 1:
         dist.barrier()
         path = W.materialize_index(args.workload)
-    dev = DeviceIndex.from_file(path, device=local)
+    if sharded:
+        from paper_2410_18926_b200.sharded import partition_clusters, scan_cluster_sizes
+
+        parts = partition_clusters(scan_cluster_sizes(path), world)
+        dev = DeviceIndex.from_file(path, device=local, shard=parts[rank])
+        searcher = ShardedSearcher(dev, k, w, t)
+    else:
+        dev = DeviceIndex.from_file(path, device=local)
+        searcher = LocalSearcher(dev, k, w, t)
     q_host = W.load_queries(args.workload)
     nq, d = q_host.shape
     q = torch.from_numpy(q_host).cuda()
@@ -226,7 +291,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     for _ in range(max(3, args.warmup)):
-        dev.search_device(q, k, w, t, True, out=out)
+        searcher.device_step(q, out)
     torch.cuda.synchronize()
     launches_per_step = last_launch_count()
 
@@ -240,7 +305,7 @@ def main():
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             evs[i][0].record(stream)
-            dev.search_device(q, k, w, t, True, out=out)
+            searcher.device_step(q, out)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
@@ -249,7 +314,8 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms_max = float(ms_t.item())
-    value = nq * world / (ms_max / 1e3)
+    total_q = nq if sharded else nq * world
+    value = total_q / (ms_max / 1e3)
 
     # ---- recall of this run's results (identical ids to the oracle -> identical recall)
     gt = W.load_ground_truth(args.workload)
@@ -260,18 +326,18 @@ def main():
                                 for i in range(nq)]))
 
     # ---- per-stage device time (events around each launch inside librrg), separate pass
-    _native.lib.rrg_set_stage_timing(1)
     import ctypes
+    _native.lib.rrg_set_stage_timing(1)
     stage_ms = (ctypes.c_double * 7)()
     stage_n = (ctypes.c_int64 * 7)()
     _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
-        dev.search_device(q, k, w, t, True, out=out)
+        searcher.device_step(q, out)
     _native.lib.rrg_stage_times(stage_ms, stage_n)
     _native.lib.rrg_set_stage_timing(0)
     names = ["project", "quantize", "route_dist", "route_select", "score_select", "rerank", "bucket"]
-    stages = {nm: round(stage_ms[i] / max(1, stage_n[i]), 4) for i, nm in enumerate(names)}
+    stages = {nm: round(stage_ms[i] / args.steps, 4) for i, nm in enumerate(names)}
 
     # ---- roofline of the dominant kernel (rerank): algorithmic bytes / launch time
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
@@ -279,7 +345,7 @@ def main():
     cand = dev_cand_counts(dev, q, k, w, t)
     rerank_bytes = cand * d * 4 + nq * d * 4 + nq * k * 12 + nq * t * 4
     rr_ms = stages["rerank"]
-    achieved = rerank_bytes / (rr_ms / 1e3) / 1e9
+    achieved = rerank_bytes / (rr_ms / 1e3) / 1e9 if rr_ms > 0 else None
     traffic = None
     tf = ROOT / "profiles" / f"{args.workload}_rerank_traffic.json"
     if tf.exists():
@@ -287,22 +353,24 @@ def main():
 
     # ---- e2e through the C ABI host entry: pinned host queries in, results out, per step
     qpin = torch.from_numpy(q_host).pin_memory().numpy()
-    hid = torch.empty((nq, k), dtype=torch.int64).pin_memory().numpy()
-    hsc = torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy()
-    hct = torch.empty((nq,), dtype=torch.int32).pin_memory().numpy()
+    hout = (torch.empty((nq, k), dtype=torch.int64).pin_memory().numpy(),
+            torch.empty((nq, k), dtype=torch.float32).pin_memory().numpy(),
+            torch.empty((nq,), dtype=torch.int32).pin_memory().numpy())
     for _ in range(2):
-        dev.search_host(qpin, k, w, t, True, out=(hid, hsc, hct))
+        searcher.host_step(qpin, hout)
     e2e_s = []
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
         t0 = time.perf_counter()
-        dev.search_host(qpin, k, w, t, True, out=(hid, hsc, hct))
+        searcher.host_step(qpin, hout)
         e2e_s.append(time.perf_counter() - t0)
     e2e_t = torch.tensor([float(np.mean(e2e_s))], device="cuda")
     if world > 1:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
-    e2e_val = nq * world / float(e2e_t.item())
+    e2e_val = total_q / float(e2e_t.item())
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -315,18 +383,20 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32/f64/int8",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f32/f64/int8",
             "data": "synthetic (rrann.bench.synth_dataset clustered, regenerated bit-exact)",
-            "config": {"workload": args.workload, "queries_per_rank": nq, "k": k, "w": w, "t": t,
+            "config": {"workload": args.workload, "queries": total_q, "k": k, "w": w, "t": t,
                        **{kk: man["generator"][kk] for kk in ("m", "d", "n_blobs")}, **man["index"],
                        "recall_at_k": recall, "l2": "256 MiB write between steps (excluded)",
-                       "parallelism": f"replica x{world}" if world > 1 else "single"},
+                       "parallelism": (f"cluster-sharded x{world}, 2x NCCL all-gather merge" if sharded
+                                       else (f"replica x{world}" if world > 1 else "single"))},
             "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": int(nq * d * 4),
                     "d2h_bytes_per_step": int(nq * k * 12 + nq * 4)},
             "gpu_launches": int(launches_per_step * args.steps),
             "stage_ms": stages,
-            "roofline": {"bound": "hbm", "kernel": "k_rerank_topk", "achieved": achieved,
-                         "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "roofline": {"bound": "hbm", "kernel": "k_rerank_tree", "achieved": achieved,
+                         "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak if achieved else None, "traffic": traffic,
                          "algorithmic_bytes_per_launch": int(rerank_bytes),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback"},
             "cpu_baseline": cpu,

@@ -681,10 +681,13 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
 #pragma unroll
         for (int i = 0; i < kMaxNb; ++i) {
           if (i < nb) {
-            float d0 = __fsub_rn(c[i].x, xv[s][i].x), d1 = __fsub_rn(c[i].y, xv[s][i].y);
-            float s0 = __fmul_rn(d0, d0), s1 = __fmul_rn(d1, d1);
-            r0 = i == 0 ? s0 : __fadd_rn(r0, s0);
-            r1 = i == 0 ? s1 : __fadd_rn(r1, s1);
+            // packed FADD2/FMUL2 (per-lane IEEE rn, == __fsub_rn/__fmul_rn); the
+            // accumulation stays scalar __fadd_rn so ptxas cannot contract it
+            // into an FFMA2 (it does contract __fmul2_rn + __fadd2_rn).
+            float2 dd = __fadd2_rn(c[i], make_float2(-xv[s][i].x, -xv[s][i].y));
+            float2 sq = __fmul2_rn(dd, dd);
+            r0 = i == 0 ? sq.x : __fadd_rn(r0, sq.x);
+            r1 = i == 0 ? sq.y : __fadd_rn(r1, sq.y);
           }
         }
         v = __fadd_rn(r0, r1);

@@ -328,15 +328,16 @@ def main():
     # ---- per-stage device time (events around each launch inside librrg), separate pass
     import ctypes
     _native.lib.rrg_set_stage_timing(1)
-    stage_ms = (ctypes.c_double * 7)()
-    stage_n = (ctypes.c_int64 * 7)()
+    stage_ms = (ctypes.c_double * 8)()
+    stage_n = (ctypes.c_int64 * 8)()
     _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         searcher.device_step(q, out)
     _native.lib.rrg_stage_times(stage_ms, stage_n)
     _native.lib.rrg_set_stage_timing(0)
-    names = ["project", "quantize", "route_dist", "route_select", "score_select", "rerank", "bucket"]
+    names = ["project", "quantize", "route_dist", "route_select", "select_topt", "rerank", "bucket",
+             "cluster_score"]
     stages = {nm: round(stage_ms[i] / args.steps, 4) for i, nm in enumerate(names)}
 
     # ---- roofline of the dominant kernel (rerank): algorithmic bytes / launch time

@@ -176,10 +176,12 @@ int64_t rrg_last_launch_count(void);
 /* Per-stage device timing (CUDA events recorded on the search stream around
  * every launch) for the calls made on this thread while enabled.  Stages:
  * 0 project, 1 prep/quantize, 2 route distances, 3 route select,
- * 4 score+top-t, 5 rerank+top-k, 6 query bucketing.  rrg_stage_times
- * synchronizes the recorded events, writes the accumulated milliseconds and
- * launch counts per stage (arrays of RRG_N_STAGES) and resets the accumulators. */
-#define RRG_N_STAGES 7
+ * 4 top-t selection (query-major mode: scoring + top-t), 5 rerank+top-k,
+ * 6 query bucketing, 7 cluster-major scoring (pair bucketing + scoring).
+ * rrg_stage_times synchronizes the recorded events, writes the accumulated
+ * milliseconds and launch counts per stage (arrays of RRG_N_STAGES) and resets
+ * the accumulators. */
+#define RRG_N_STAGES 8
 void rrg_set_stage_timing(int enabled);
 int rrg_stage_times(double* ms, int64_t* launches);
 

@@ -598,6 +598,10 @@ struct Plan {
   int64_t gcap;    // global overflow capacity per query (0 if none)
   size_t off_xp, off_qc, off_qs, off_qh, off_xx, off_pp, off_diss, off_sel, off_cpos, off_cn,
       off_gk, off_gp, off_prim, off_order, total;
+  // cluster-major scoring (score_mode == 1)
+  int score_mode;
+  int kcap;
+  size_t off_qoff, off_ncand, off_pairoff, off_itemoff, off_pairs, off_kbase, off_keys, off_ctr;
 };
 
 Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
@@ -640,6 +644,23 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   p.off_gp = carve(Q * p.gcap * 4);
   p.off_prim = carve(Q * 4);
   p.off_order = carve(Q * 4);
+  // scoring strategy: cluster-major (bucketed pairs, factors staged once per
+  // cluster) unless RRG_SCORE_MODE=query selects the fused query-major kernel
+  {
+    const char* e = getenv("RRG_SCORE_MODE");
+    p.score_mode = (e && strcmp(e, "query") == 0) ? 0 : 1;
+  }
+  if (p.score_mode == 1) {
+    p.kcap = (int)std::min<int64_t>(std::max<int64_t>(nmax, 1), 24 * 1024);
+    p.off_qoff = carve(Q * (int64_t)(w + 1) * 4);
+    p.off_ncand = carve(Q * 4);
+    p.off_pairoff = carve((L + 1) * 4);
+    p.off_itemoff = carve((L + 1) * 4);
+    p.off_pairs = carve(Q * (int64_t)w * 4);
+    p.off_kbase = carve((Q + 1) * 4);
+    p.off_keys = carve(Q * std::max<int64_t>(nmax, 1) * 4);
+    p.off_ctr = carve(16);
+  }
   p.total = o;
   return p;
 }
@@ -671,7 +692,8 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
   Plan p = make_plan(ix, nq, k, w, t, rerank, ph1 != nullptr);
   {  // shared-memory budgets of the per-query CTAs (static parts bounded by 48 KB)
     const size_t lim = kMaxSmemPerCta - 48 * 1024;
-    if (score_select_smem(p.smem_cap, p.take_cap, k) > lim ||
+    if ((p.score_mode == 0 ? score_select_smem(p.smem_cap, p.take_cap, k)
+                           : select_topt_smem(w, p.take_cap, k, p.kcap)) > lim ||
         (rerank && rerank_smem(ix->view.d_stride, p.take_cap, k, rerank_uses_tree(ix->view)) > lim))
       raise_usage("ParameterError", "t=%d / k=%d exceed the device search limits", t, k);
   }
@@ -708,7 +730,28 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
     sa.out_ids = ids; sa.out_scores = scores; sa.out_count = count; sa.q0 = (int)q0;
     sa.order = order;
     if (ph1) { sa.sel_keys = ph1->keys; sa.sel_ids = ph1->ids; sa.sel_count = ph1->count; }
-    staged(4, st, [&] { launch_score_select(sa, n, st); });
+    if (p.score_mode == 0) {
+      staged(4, st, [&] { launch_score_select(sa, n, st); });
+    } else {
+      ClusterScoringHost ch{};
+      ch.ix = v; ch.qcodes = qcodes; ch.qscale = qscale; ch.qhead = qhead; ch.sel = sel; ch.w = w;
+      ch.qoff = reinterpret_cast<int*>(base + p.off_qoff);
+      ch.ncand = reinterpret_cast<int*>(base + p.off_ncand);
+      ch.pair_off = reinterpret_cast<int*>(base + p.off_pairoff);
+      ch.item_off = reinterpret_cast<int*>(base + p.off_itemoff);
+      ch.pairs = reinterpret_cast<int*>(base + p.off_pairs);
+      ch.kbase = reinterpret_cast<int*>(base + p.off_kbase);
+      ch.keys = reinterpret_cast<uint32_t*>(base + p.off_keys);
+      ch.work_counter = reinterpret_cast<int*>(base + p.off_ctr);
+      staged(7, st, [&] { launch_cluster_scoring(ch, n, st); });
+      SelectTopTHost th{};
+      th.ix = v; th.sel = sel; th.w = w; th.qoff = ch.qoff; th.kbase = ch.kbase; th.keys = ch.keys;
+      th.take_cap = p.take_cap; th.rerank = rerank; th.k = k; th.xx = xx; th.cand_pos = cpos;
+      th.cand_n = cn; th.out_ids = ids; th.out_scores = scores; th.out_count = count;
+      th.q0 = (int)q0; th.order = order; th.kcap = p.kcap;
+      if (ph1) { th.sel_keys = ph1->keys; th.sel_ids = ph1->ids; th.sel_count = ph1->count; }
+      staged(4, st, [&] { launch_select_topt(th, n, st); });
+    }
     if (rerank && !ph1) {
       RerankArgsHost ra{};
       ra.ix = v; ra.queries = x; ra.cand_pos = cpos; ra.cand_n = cn; ra.take_cap = p.take_cap;

@@ -1,0 +1,434 @@
+// rrg_cluster_score.cu -- cluster-major ("bucketed") scoring of the LoRANN query path.
+//
+// The query-major k_score_select re-reads a probed cluster's factors once per
+// query (C2: ~440 KB of A/B codes per query, from L2).  Here the batch's
+// (query, cluster) pairs are bucketed by cluster (histogram, scan, scatter --
+// the "bucketing pass" of the north star); one CTA then stages a cluster's
+// A^T/B^T codes and metadata in shared memory once and scores every query of
+// its bucket chunk against it:
+//   stage A  raw1 = codes_x . A (per query, r outputs)  -> inter -> re-quantize
+//   stage B  raw2 = codes_r . B[:,p] (8 dp4a per point at r=32) -> yhat -> key
+// (rrr.py:181-203, quantize.py:109-156; identical arithmetic to k_score_select).
+// Keys land in a per-query candidate array (query-major, exact offsets) that
+// k_select_topt reduces to the top-t by (key, corpus id) (index.py:314-316).
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "rrg_common.cuh"
+#include "rrg_kernels.h"
+
+namespace rrg {
+
+// ---------------------------------------------------------- per-query offsets
+// Warp per query: qoff[q][c] = sum of the sizes of sel[q][0..c) (selection
+// order = candidate order), qoff[q][w] = N[q].
+__global__ void k_cand_offsets(DevIndexView ix, const int* __restrict__ sel, int nq, int w,
+                               int* __restrict__ qoff, int* __restrict__ ncand) {
+  const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  int carry = 0;
+  for (int b = 0; b < w; b += 32) {
+    int c = b + lane, m = 0;
+    if (c < w) {
+      int l = sel[(size_t)q * w + c];
+      m = ix.cl_pos[l + 1] - ix.cl_pos[l];
+    }
+    int incl = m;
+    for (int o = 1; o < 32; o <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    if (c < w) qoff[(size_t)q * (w + 1) + c] = carry + incl - m;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  if (lane == 0) {
+    qoff[(size_t)q * (w + 1) + w] = carry;
+    ncand[q] = carry;
+  }
+}
+
+// ----------------------------------------------------------- pair bucketing
+// One CTA: histogram of the Q*w (query, slot) pairs by cluster, exclusive scans
+// (pair offsets per cluster, work items of <= kPairsPerItem pairs per cluster,
+// key-array base per query), scatter of the pairs into cluster order.
+constexpr int PNT = 1024;
+constexpr int kPairsPerItem = 32;
+
+__device__ void block_exclusive_scan_inplace(int* a, int n, int* total) {
+  // one warp scans (n small: L or Q); carry across 32-element chunks
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int carry = 0;
+    for (int b = 0; b < n; b += 32) {
+      int i = b + lane;
+      int v = i < n ? a[i] : 0, incl = v;
+      for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += t;
+      }
+      if (i < n) a[i] = carry + incl - v;
+      carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) *total = carry;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel, int nq, int w,
+                                                     int L, const int* __restrict__ ncand,
+                                                     int* __restrict__ pair_off,   // L+1
+                                                     int* __restrict__ item_off,   // L+1
+                                                     int* __restrict__ pairs,      // nq*w
+                                                     int* __restrict__ kbase) {    // nq+1
+  extern __shared__ int sh[];  // cnt[L], cur[L]
+  int* cnt = sh;
+  int* cur = sh + L;
+  __shared__ int tot;
+  for (int i = threadIdx.x; i < L; i += PNT) cnt[i] = 0;
+  __syncthreads();
+  const int np = nq * w;
+  for (int i = threadIdx.x; i < np; i += PNT) atomicAdd(&cnt[sel[i]], 1);
+  __syncthreads();
+  for (int i = threadIdx.x; i < L; i += PNT) {
+    cur[i] = cnt[i];
+    item_off[i] = (cnt[i] + kPairsPerItem - 1) / kPairsPerItem;
+  }
+  __syncthreads();
+  block_exclusive_scan_inplace(cur, L, &tot);
+  if (threadIdx.x == 0) pair_off[L] = tot;
+  for (int i = threadIdx.x; i < L; i += PNT) pair_off[i] = cur[i];
+  __syncthreads();
+  block_exclusive_scan_inplace(item_off, L, &tot);
+  if (threadIdx.x == 0) item_off[L] = tot;
+  // scatter (order inside a cluster's bucket is irrelevant to results)
+  for (int i = threadIdx.x; i < np; i += PNT) pairs[atomicAdd(&cur[sel[i]], 1)] = i;
+  // key-array base per query
+  for (int q = threadIdx.x; q < nq; q += PNT) kbase[q] = ncand[q];
+  __syncthreads();
+  block_exclusive_scan_inplace(kbase, nq, &tot);
+  if (threadIdx.x == 0) kbase[nq] = tot;
+}
+
+// ------------------------------------------------------------ cluster scoring
+constexpr int CNT = 256;
+constexpr int kMaxRc = 64;
+
+struct ClusterScoreArgs {
+  DevIndexView ix;
+  const int8_t* qcodes;  // [nq][s_pad]
+  const float* qscale;
+  const float* qhead;
+  const int* sel;        // [nq][w]
+  int w;
+  const int* qoff;       // [nq][w+1]
+  const int* pair_off;   // [L+1]
+  const int* item_off;   // [L+1]
+  const int* pairs;      // [nq*w] pair ids (q*w + c) in cluster order
+  const int* kbase;      // [nq+1]
+  uint32_t* keys;        // [kbase[nq]]
+  int* work_counter;     // zeroed before launch
+};
+
+__global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
+  const DevIndexView& ix = a.ix;
+  __shared__ int item_s;
+  __shared__ __align__(16) int8_t c2s[kPairsPerItem][kMaxRc];
+  __shared__ float s2s[kPairsPerItem], h2s[kPairsPerItem];
+  __shared__ float inters[kPairsPerItem][kMaxRc];
+  __shared__ int pq[kPairsPerItem], pkey[kPairsPerItem];
+  __shared__ float pxs[kPairsPerItem], pxh[kPairsPerItem];
+  const int L = ix.L, r = ix.r, r_pad = ix.r_pad, s_pad = ix.s_pad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total_items = a.item_off[L];
+  const bool euclid = ix.metric == kMetricEuclidean;
+  while (true) {
+    if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = item_s;
+    __syncthreads();
+    if (item >= total_items) break;
+    // cluster of this item: upper_bound over item_off
+    int lo = 0, hi = L;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (a.item_off[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int l = lo;
+    const int j0 = a.pair_off[l] + (item - a.item_off[l]) * kPairsPerItem;
+    const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
+    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    const bool rrr = ix.cl_kind[l] == kKindRrr;
+    if (tid < np) {
+      const int pr = a.pairs[j0 + tid];
+      const int q = pr / a.w, c = pr % a.w;
+      pq[tid] = q;
+      pkey[tid] = a.kbase[q] + a.qoff[(size_t)q * (a.w + 1) + c];
+      pxs[tid] = a.qscale[q];
+      pxh[tid] = a.qhead[q];
+    }
+    __syncthreads();
+    if (m == 0) continue;
+    if (rrr) {
+      // stage A: np x r dot products over s_pad bytes, `parts` lanes per product
+      const int slot = ix.cl_aidx[l];
+      const int nvec = s_pad / 16;
+      const int prs = np * r;
+      int parts = 1;
+      while (parts < 32 && prs * parts * 2 <= CNT && parts * 2 <= nvec) parts <<= 1;
+      for (int base = 0; base < prs * parts; base += CNT) {
+        const int e = base + tid;
+        const int pr = e / parts, part = e % parts;
+        const bool act = pr < prs;
+        const int pi = act ? pr / r : 0, jj = act ? pr % r : 0;
+        int raw = 0;
+        if (act) {
+          const int4* aw = reinterpret_cast<const int4*>(ix.at + ((size_t)slot * r + jj) * s_pad);
+          const int4* q4 = reinterpret_cast<const int4*>(a.qcodes + (size_t)pq[pi] * s_pad);
+          for (int u = part; u < nvec; u += parts) {
+            int4 b = __ldg(aw + u), cc = __ldg(q4 + u);
+            raw = __dp4a(cc.x, b.x, raw);
+            raw = __dp4a(cc.y, b.y, raw);
+            raw = __dp4a(cc.z, b.z, raw);
+            raw = __dp4a(cc.w, b.w, raw);
+          }
+        }
+        for (int o = 1; o < parts; o <<= 1) raw += __shfl_xor_sync(0xffffffffu, raw, o);
+        if (act && part == 0) {
+          const size_t aj = (size_t)slot * r + jj;
+          inters[pi][jj] = deq(raw, pxs[pi], ix.ascale[aj], pxh[pi], ix.ahead[aj]);
+        }
+      }
+      __syncthreads();
+      for (int pi = warp; pi < np; pi += CNT / 32) {  // re-quantize (quantize.py:150)
+        float amax = 0.0f;
+        for (int j = 1 + lane; j < r; j += 32) amax = fmaxf(amax, fabsf(inters[pi][j]));
+        for (int o = 16; o > 0; o >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+        const float sc2 = quant_scale(amax);
+        for (int j = lane; j < r_pad; j += 32) {
+          int code = 0;
+          if (j >= 1 && j < r && amax != 0.0f) code = quant_code(inters[pi][j], sc2);
+          c2s[pi][j] = (int8_t)code;
+        }
+        if (lane == 0) { s2s[pi] = sc2; h2s[pi] = inters[pi][0]; }
+      }
+      __syncthreads();
+      // stage B: thread per point, codes/meta loaded once, all np queries scored
+      for (int p = tid; p < m; p += CNT) {
+        const int gp = p0 + p;
+        const float4 meta = __ldg(ix.pmeta + gp);
+        int4 b[4];
+        const int4* bw = reinterpret_cast<const int4*>(ix.bt + (size_t)gp * r_pad);
+        const int nb4 = r_pad / 16;
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (u < nb4) b[u] = __ldg(bw + u);
+        for (int pi = 0; pi < np; ++pi) {
+          const int4* cw = reinterpret_cast<const int4*>(c2s[pi]);
+          int raw = 0;
+#pragma unroll
+          for (int u = 0; u < 4; ++u)
+            if (u < nb4) {
+              int4 cc = cw[u];
+              raw = __dp4a(cc.x, b[u].x, raw);
+              raw = __dp4a(cc.y, b[u].y, raw);
+              raw = __dp4a(cc.z, b[u].z, raw);
+              raw = __dp4a(cc.w, b[u].w, raw);
+            }
+          const float yhat = deq(raw, s2s[pi], meta.y, h2s[pi], meta.x);
+          const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
+          a.keys[pkey[pi] + p] = mono32(keyf);
+        }
+      }
+    } else {
+      // exact model: raw_p = codes_x . A[:, p] over s_pad bytes (rrr.py:103-113)
+      const int x0 = ix.cl_aidx[l];
+      const int nvec = s_pad / 16;
+      for (int p = tid; p < m; p += CNT) {
+        const int gp = p0 + p;
+        const float4 meta = __ldg(ix.pmeta + gp);
+        const int4* xw = reinterpret_cast<const int4*>(ix.xcodes + (size_t)(x0 + p) * s_pad);
+        for (int pi = 0; pi < np; ++pi) {
+          const int4* q4 = reinterpret_cast<const int4*>(a.qcodes + (size_t)pq[pi] * s_pad);
+          int raw = 0;
+          for (int u = 0; u < nvec; ++u) {
+            int4 bb = __ldg(xw + u), cc = __ldg(q4 + u);
+            raw = __dp4a(cc.x, bb.x, raw);
+            raw = __dp4a(cc.y, bb.y, raw);
+            raw = __dp4a(cc.z, bb.z, raw);
+            raw = __dp4a(cc.w, bb.w, raw);
+          }
+          const float yhat = deq(raw, pxs[pi], meta.y, pxh[pi], meta.x);
+          const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
+          a.keys[pkey[pi] + p] = mono32(keyf);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------- top-t select
+// One CTA per query: the take = min(t|k, N) smallest of the query's keys by
+// (key, corpus id); positions recovered from (slot, offset) via the query's
+// candidate offsets.
+constexpr int TNT = 512;
+
+struct SelectArgs {
+  DevIndexView ix;
+  const int* sel;
+  int w;
+  const int* qoff;
+  const int* kbase;
+  const uint32_t* keys;
+  int take_cap, rerank, k;
+  const float* xx;
+  int* cand_pos;
+  int* cand_n;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+  const int* order;
+  uint32_t* sel_keys;
+  uint32_t* sel_ids;
+  int* sel_count;
+  int kcap;      // keys staged in smem when N <= kcap
+  int sort_cap;  // power of two >= k (no-rerank ordering)
+};
+
+__global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
+  const DevIndexView& ix = a.ix;
+  const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
+  const int tid = threadIdx.x;
+  const int w = a.w;
+  int* offs = reinterpret_cast<int*>(smem_raw);      // w+1
+  int* pbase = offs + (w + 1);                        // w: cl_pos of each slot
+  int* selidx = pbase + w;                            // take_cap
+  uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + a.take_cap);
+  uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
+  uint32_t* kst = reinterpret_cast<uint32_t*>(srt + a.sort_cap);  // kcap staged keys
+  for (int c = tid; c <= w; c += TNT) offs[c] = a.qoff[(size_t)q * (w + 1) + c];
+  for (int c = tid; c < w; c += TNT) pbase[c] = ix.cl_pos[a.sel[(size_t)q * w + c]];
+  __syncthreads();
+  const int N = offs[w];
+  const uint32_t* kq = a.keys + a.kbase[q];
+  if (N <= a.kcap) {  // stage the query's keys once; the select makes ~3 passes
+    const uint4* src = reinterpret_cast<const uint4*>(kq);
+    const bool al = (reinterpret_cast<uintptr_t>(kq) & 15) == 0;
+    if (al) {
+      for (int i = tid; i < N / 4; i += TNT) reinterpret_cast<uint4*>(kst)[i] = __ldg(src + i);
+      for (int i = (N / 4) * 4 + tid; i < N; i += TNT) kst[i] = __ldg(kq + i);
+    } else {
+      for (int i = tid; i < N; i += TNT) kst[i] = __ldg(kq + i);
+    }
+    __syncthreads();
+    kq = kst;
+  }
+  auto pos_of = [&](int i) {
+    int lo = 0, hi = w;  // largest c with offs[c] <= i
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (offs[mid] <= i) lo = mid; else hi = mid;
+    }
+    return pbase[lo] + (i - offs[lo]);
+  };
+  const int take = min(a.take_cap, N);
+  auto key = [&](int i) { return kq[i]; };
+  auto tie = [&](int i) { return __float_as_uint(__ldg(ix.pmeta + pos_of(i)).w); };
+  auto val = [](uint32_t k) { return unmono32(k); };
+  block_select_bucketed<TNT, uint32_t, float>(N, take, key, tie, val, selidx, bs, sm);
+  const int gq = a.q0 + q;
+  if (a.rerank) {
+    int* outp = a.cand_pos + (size_t)q * a.take_cap;
+    for (int i = tid; i < take; i += TNT) outp[i] = pos_of(selidx[i]);
+    if (a.sel_keys) {
+      uint32_t* ok = a.sel_keys + (size_t)gq * a.take_cap;
+      uint32_t* oi = a.sel_ids + (size_t)gq * a.take_cap;
+      for (int i = tid; i < take; i += TNT) {
+        ok[i] = key(selidx[i]);
+        oi[i] = tie(selidx[i]);
+      }
+      if (tid == 0) a.sel_count[gq] = take;
+    }
+    if (tid == 0) a.cand_n[q] = take;
+    return;
+  }
+  int np2 = 1;
+  while (np2 < take) np2 <<= 1;
+  for (int i = tid; i < np2; i += TNT) {
+    uint64_t v = ~0ull;
+    if (i < take) v = ((uint64_t)key(selidx[i]) << 32) | tie(selidx[i]);
+    srt[i] = v;
+  }
+  block_bitonic_sort<TNT>(srt, np2);
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const float xxq = a.xx[q];
+  for (int i = tid; i < a.k; i += TNT) {
+    int64_t id = -1;
+    float sc = __int_as_float(0x7fc00000);
+    if (i < take) {
+      uint64_t v = srt[i];
+      id = (int64_t)(uint32_t)v;
+      float kf = unmono32((uint32_t)(v >> 32));
+      sc = euclid ? __fadd_rn(kf, xxq) : -kf;
+    }
+    a.out_ids[(size_t)gq * a.k + i] = id;
+    a.out_scores[(size_t)gq * a.k + i] = sc;
+  }
+  if (tid == 0) a.out_count[gq] = take;
+}
+
+// ---------------------------------------------------------------- launchers
+
+void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
+  const DevIndexView& ix = h.ix;
+  k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand);
+  k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, h.ncand, h.pair_off,
+                                                  h.item_off, h.pairs, h.kbase);
+  cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
+  ClusterScoreArgs a;
+  a.ix = ix; a.qcodes = h.qcodes; a.qscale = h.qscale; a.qhead = h.qhead; a.sel = h.sel;
+  a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off; a.item_off = h.item_off;
+  a.pairs = h.pairs; a.kbase = h.kbase; a.keys = h.keys; a.work_counter = h.work_counter;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  k_score_cluster<<<sms * 4, CNT, 0, st>>>(a);
+}
+
+static int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+size_t select_topt_smem(int w, int take_cap, int k, int kcap) {
+  return (size_t)(2 * w + 1) * 4 + (size_t)take_cap * 4 + 32 + (size_t)pow2_at_least(k) * 8 +
+         (size_t)kcap * 4 + 16;
+}
+
+void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
+  SelectArgs a;
+  a.ix = h.ix; a.sel = h.sel; a.w = h.w; a.qoff = h.qoff; a.kbase = h.kbase; a.keys = h.keys;
+  a.take_cap = h.take_cap; a.rerank = h.rerank; a.k = h.k; a.xx = h.xx; a.cand_pos = h.cand_pos;
+  a.cand_n = h.cand_n; a.out_ids = h.out_ids; a.out_scores = h.out_scores;
+  a.out_count = h.out_count; a.q0 = h.q0; a.order = h.order; a.sel_keys = h.sel_keys;
+  a.sel_ids = h.sel_ids; a.sel_count = h.sel_count;
+  a.kcap = h.kcap; a.sort_cap = pow2_at_least(h.k);
+  static int done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    cudaFuncAttributes at{};
+    cudaFuncGetAttributes(&at, (const void*)k_select_topt);
+    cudaFuncSetAttribute((const void*)k_select_topt, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kMaxSmemPerCta - (int)at.sharedSizeBytes);
+    done[dev] = 1;
+  }
+  k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
+}
+
+}  // namespace rrg

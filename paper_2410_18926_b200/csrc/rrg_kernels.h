@@ -64,6 +64,49 @@ void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st);
 size_t rerank_smem(int d_stride, int take_cap, int k, bool tree);
 bool rerank_uses_tree(const DevIndexView& ix);
 void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st);
+// Cluster-major scoring (rrg_cluster_score.cu)
+struct ClusterScoringHost {
+  DevIndexView ix;
+  const int8_t* qcodes;
+  const float* qscale;
+  const float* qhead;
+  const int* sel;
+  int w;
+  int* qoff;      // [nq][w+1]
+  int* ncand;     // [nq]
+  int* pair_off;  // [L+1]
+  int* item_off;  // [L+1]
+  int* pairs;     // [nq*w]
+  int* kbase;     // [nq+1]
+  uint32_t* keys; // [sum N]
+  int* work_counter;
+};
+void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st);
+
+struct SelectTopTHost {
+  DevIndexView ix;
+  const int* sel;
+  int w;
+  const int* qoff;
+  const int* kbase;
+  const uint32_t* keys;
+  int take_cap, rerank, k;
+  const float* xx;
+  int* cand_pos;
+  int* cand_n;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+  const int* order;
+  uint32_t* sel_keys;
+  uint32_t* sel_ids;
+  int* sel_count;
+  int kcap;
+};
+size_t select_topt_smem(int w, int take_cap, int k, int kcap);
+void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st);
+
 // Sharded search: merge G per-shard lists per query, laid out
 // [G][nq][cap] (the all-gather layout) with counts [G][nq].
 //   mode 0: (key u32, id u32) candidates -> global top-`take` by (key, id), sorted

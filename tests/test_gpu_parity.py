@@ -50,8 +50,11 @@ def _corpus_max_norm(g):
 
 
 @pytest.mark.parametrize("case", QUANT_CASES)
-@pytest.mark.parametrize("entry", ["host", "device"])
-def test_golden_end_to_end(pkg, tmp_path, case, entry):
+@pytest.mark.parametrize("entry", ["host", "device", "device-querymajor"])
+def test_golden_end_to_end(pkg, tmp_path, case, entry, monkeypatch):
+    if entry == "device-querymajor":  # the fused query-major scoring kernel
+        monkeypatch.setenv("RRG_SCORE_MODE", "query")
+        entry = "device"
     g, dev = _golden_index(pkg, tmp_path, case)
     for pi, (k, w, t, rr) in enumerate(g["params"]):
         if f"p{pi}_ids" not in g:
@@ -289,8 +292,10 @@ SWEEP = [
 ]
 
 
+@pytest.mark.parametrize("mode", ["cluster", "query"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
-def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf):
+def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
+    monkeypatch.setenv("RRG_SCORE_MODE", mode)
     from index_writer import random_index
     from oracle import rrann_oracle as O
 

@@ -600,10 +600,11 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
 // i.e. bit-identical to `(diff*diff).sum(axis=1)` (index.py:281-282).
 // G = 4*nleaves lanes per row when <= 32 (so 32/G rows per warp pass), else
 // SLOTS = 4*nleaves/32 slots per lane.
-constexpr int kMaxNb = 16;
-
-template <int SLOTS>
-__global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
+// NB = chain length nl/8 as a compile-time constant (loads use immediate
+// offsets, no per-element predicates); NB = 0 is the runtime-length fallback.
+template <int SLOTS, int NB>
+__global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankArgs a) {
+  constexpr int kMaxNb = NB > 0 ? NB : 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
   __shared__ BucketSmem bs;
@@ -611,7 +612,8 @@ __global__ void __launch_bounds__(RNT) k_rerank_tree(RerankArgs a) {
   const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = RNT / 32;
-  const int d = ix.d, ds = ix.d_stride, nl = ix.pw_leaf_n, nb = nl / 8, tail = nl % 8;
+  const int d = ix.d, ds = ix.d_stride, nl = ix.pw_leaf_n, tail = nl % 8;
+  const int nb = NB > 0 ? NB : nl / 8;
   const int P = 4 * ix.pw_nleaves;
   const int G = SLOTS == 1 ? P : 32;
   const int R = 32 / G;
@@ -1000,13 +1002,30 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   const bool tree = rerank_uses_tree(h.ix);
   const size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k, tree);
   if (tree) {
-    if (4 * h.ix.pw_nleaves <= 32) {
-      allow_smem(k_rerank_tree<1>, 3);
-      k_rerank_tree<1><<<nq, RNT, sm, st>>>(a);
+    const int nb = h.ix.pw_leaf_n / 8;
+    const bool one = 4 * h.ix.pw_nleaves <= 32;
+#define RRG_TREE(S, NBV, SLOT)                          \
+  do {                                                  \
+    allow_smem(k_rerank_tree<S, NBV>, SLOT);            \
+    k_rerank_tree<S, NBV><<<nq, RNT, sm, st>>>(a);      \
+  } while (0)
+    // leaf sizes of the common dims: 64 (nb 8), 96 (12: d=768/1536/100), 120 (15: d=960), 128 (16)
+    if (one) {
+      switch (nb) {
+        case 8: RRG_TREE(1, 8, 6); break;
+        case 12: RRG_TREE(1, 12, 7); break;
+        case 15: RRG_TREE(1, 15, 8); break;
+        case 16: RRG_TREE(1, 16, 9); break;
+        default: RRG_TREE(1, 0, 3); break;
+      }
     } else {
-      allow_smem(k_rerank_tree<2>, 4);
-      k_rerank_tree<2><<<nq, RNT, sm, st>>>(a);
+      switch (nb) {
+        case 12: RRG_TREE(2, 12, 10); break;
+        case 16: RRG_TREE(2, 16, 11); break;
+        default: RRG_TREE(2, 0, 4); break;
+      }
     }
+#undef RRG_TREE
     return;
   }
   allow_smem(k_rerank_topk, 5);

@@ -340,9 +340,23 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   int* d_pos = ix->upload(pos_of_id);
   v.pos_of_id = d_pos;
   v.m = hm.m;
+  v.corpus_interleaved = 0;
   if (has_corpus) {
     float* corp = static_cast<float*>(ix->dalloc((size_t)std::max<int64_t>(P, 1) * v.d_stride * 4));
-    fill_corpus(corp, d_pos, (int)v.d_stride);
+    const int* d_perm = nullptr;
+    if (v.pw_perfect && d % 2 == 0) {  // step-major interleaved rows (see DevIndexView)
+      const int nl = v.pw_leaf_n, NL = v.pw_nleaves, nb = nl / 8, tail = nl % 8;
+      std::vector<int> perm(d);
+      for (int b = 0; b < NL; ++b)
+        for (int p = 0; p < nl; ++p) {
+          const int e = b * nl + p;
+          perm[e] = p < 8 * nb ? (p / 8) * 8 * NL + 8 * b + (p % 8)
+                               : nb * 8 * NL + b * tail + (p - 8 * nb);
+        }
+      d_perm = ix->upload(perm);
+      v.corpus_interleaved = 1;
+    }
+    fill_corpus(corp, d_pos, (int)v.d_stride, d_perm);
     v.corpus = corp;
   }
   ix->info.metric = hm.metric; ix->info.dim = d; ix->info.reduced_dim = s; ix->info.rank = r;
@@ -462,7 +476,7 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
   std::unique_ptr<RrgIndex> ix(new RrgIndex());
   ix->device = device;
   bool corpus_done = false;
-  auto fill = [&](float* dst, const int* d_pos, int d_stride) {
+  auto fill = [&](float* dst, const int* d_pos, int d_stride, const int* perm) {
     // stream the corpus (original id order) through pinned chunks, scatter into cluster order
     const uint64_t row_bytes = (uint64_t)d * 4;
     const uint64_t rows_per_chunk = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(row_bytes, 1));
@@ -486,7 +500,8 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
           raise_format("truncated file: corpus at offset %llu", (unsigned long long)fr.off);
         fr.take(pinned[b], n * row_bytes, "corpus");
         CUDA_TRY(cudaMemcpyAsync(staging[b], pinned[b], n * row_bytes, cudaMemcpyHostToDevice, st));
-        launch_scatter_rows(staging[b], (int64_t)n, (int)d, d_stride, d_pos, (int64_t)done, dst, st);
+        launch_scatter_rows(staging[b], (int64_t)n, (int)d, d_stride, d_pos, (int64_t)done, perm,
+                            dst, st);
         CUDA_TRY(cudaGetLastError());
         CUDA_TRY(cudaEventRecord(ev[b], st));
         done += n;
@@ -524,7 +539,7 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
   if (fr.off != fr.size)
     raise_format("unknown trailing section at offset %llu: %llu extra bytes",
                  (unsigned long long)fr.off, (unsigned long long)(fr.size - fr.off));
-  if (!quantized) build_device_index(ix.get(), hm, false, [](float*, const int*, int) {});
+  if (!quantized) build_device_index(ix.get(), hm, false, [](float*, const int*, int, const int*) {});
   *out = ix.release();
   return RRG_OK;
 }
@@ -568,7 +583,7 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
   std::unique_ptr<RrgIndex> ix(new RrgIndex());
   ix->device = device;
   const bool has_corpus = dsc->corpus != nullptr;
-  auto fill = [&](float* dst, const int* d_pos, int d_stride) {
+  auto fill = [&](float* dst, const int* d_pos, int d_stride, const int* perm) {
     const uint64_t row_bytes = (uint64_t)d * 4;
     const uint64_t rows_per_chunk = std::max<uint64_t>(1, (64ull << 20) / std::max<uint64_t>(row_bytes, 1));
     float* staging = nullptr;
@@ -576,7 +591,7 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
     for (uint64_t done = 0; done < (uint64_t)hm.m;) {
       uint64_t n = std::min<uint64_t>(rows_per_chunk, hm.m - done);
       CUDA_TRY(cudaMemcpy(staging, dsc->corpus + done * d, n * row_bytes, cudaMemcpyHostToDevice));
-      launch_scatter_rows(staging, (int64_t)n, d, d_stride, d_pos, (int64_t)done, dst, 0);
+      launch_scatter_rows(staging, (int64_t)n, d, d_stride, d_pos, (int64_t)done, perm, dst, 0);
       CUDA_TRY(cudaGetLastError());
       done += n;
     }

@@ -51,6 +51,11 @@ struct DevIndexView {
   // tree is perfect (2^a equal leaves of pw_leaf_n <= 128 elements, e.g. d = 128,
   // 768, 960, 1536) the re-rank runs the warp-parallel kernel.
   int pw_nleaves, pw_leaf_n, pw_perfect;
+  // corpus_interleaved: rows are stored step-major for the perfect pairwise plan
+  // (element (leaf b, step i, accumulator j) at i*8*nleaves + 8*b + j, the nl%8
+  // tails after all steps), so one warp instruction of the re-rank reads 256
+  // contiguous bytes instead of eight 32-byte pieces of the natural layout.
+  int corpus_interleaved;
 };
 
 // ---------------------------------------------------------------- numerics

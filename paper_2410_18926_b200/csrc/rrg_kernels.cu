@@ -630,12 +630,17 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
   // this lane's slice of the query, in registers
   float2 xv[SLOTS][kMaxNb];
   float xt[SLOTS][7];
-  int off[SLOTS];
+  int off[SLOTS], coff[SLOTS], ctail[SLOTS];
+  // corpus rows are interleaved step-major (DevIndexView::corpus_interleaved):
+  // step i of (leaf b, pair h) sits at i*cstep + 8b + 2h
+  const int cstep = 8 * ix.pw_nleaves;
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     int pair = pl + 32 * s;
     int b = pair >> 2, h = pair & 3;
     off[s] = b * nl + 2 * h;
+    coff[s] = 8 * b + 2 * h;
+    ctail[s] = nb * cstep + b * tail;
 #pragma unroll
     for (int i = 0; i < kMaxNb; ++i)
       xv[s][i] = i < nb ? *reinterpret_cast<const float2*>(xq + off[s] + 8 * i) : make_float2(0.f, 0.f);
@@ -664,7 +669,7 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
 #pragma unroll
         for (int i = 0; i < kMaxNb; ++i)
           if (i < nb && rows[uu] - g < n)
-            cbuf[uu][s][i] = __ldg(reinterpret_cast<const float2*>(crow + off[s] + 8 * i));
+            cbuf[uu][s][i] = __ldg(reinterpret_cast<const float2*>(crow + coff[s] + cstep * i));
     }
 #pragma unroll
     for (int uu = 0; uu < U; ++uu) {
@@ -696,8 +701,7 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
         v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1));
         v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 2));
         if (tail) {
-          int b = (pl + 32 * s) >> 2;
-          const float* tp = crow + b * nl + 8 * nb;
+          const float* tp = crow + ctail[s];
 #pragma unroll
           for (int u = 0; u < 7; ++u)
             if (u < tail) {
@@ -711,8 +715,7 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
         for (int i = 0; i < kMaxNb; ++i)
           if (i < nb) acc += c[i].x * xv[s][i].x + c[i].y * xv[s][i].y;
         if ((pl & 3) == 0) {
-          int b = (pl + 32 * s) >> 2;
-          const float* tp = crow + b * nl + 8 * nb;
+          const float* tp = crow + ctail[s];
           for (int u = 0; u < tail; ++u) acc += __ldg(tp + u) * xt[s][u];
         }
         acc += __shfl_xor_sync(0xffffffffu, acc, 1);
@@ -901,14 +904,17 @@ void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* 
 // -> cluster order), rows padded to d_stride.
 __global__ void k_scatter_rows(const float* __restrict__ src, int64_t nrows, int d, int d_stride,
                                const int* __restrict__ pos_of_id, int64_t i0,
-                               float* __restrict__ dst) {
+                               const int* __restrict__ perm, float* __restrict__ dst) {
   int64_t row = blockIdx.x;
   if (row >= nrows) return;
   int p = pos_of_id[i0 + row];
   if (p < 0) return;  // row not held by this shard
   const float* s = src + row * (int64_t)d;
   float* t = dst + (int64_t)p * d_stride;
-  for (int j = threadIdx.x; j < d_stride; j += blockDim.x) t[j] = j < d ? s[j] : 0.0f;
+  for (int j = threadIdx.x; j < d_stride; j += blockDim.x) {
+    if (j >= d) t[j] = 0.0f;
+    else t[perm ? perm[j] : j] = s[j];  // element j -> its (interleaved) slot
+  }
 }
 
 // ===================================================================== launchers
@@ -992,7 +998,7 @@ size_t rerank_smem(int d_stride, int take_cap, int k, bool tree) {
   return rows + (size_t)take_cap * 8 + (size_t)k * 4 + 16 + np2 * 8 + 16;
 }
 
-bool rerank_uses_tree(const DevIndexView& ix) { return ix.pw_perfect && (ix.d % 2) == 0; }
+bool rerank_uses_tree(const DevIndexView& ix) { return ix.corpus_interleaved != 0; }
 
 void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   RerankArgs a;
@@ -1033,9 +1039,11 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
 }
 
 void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
-                         const int* pos_of_id, int64_t i0, float* dst, cudaStream_t st) {
+                         const int* pos_of_id, int64_t i0, const int* perm, float* dst,
+                         cudaStream_t st) {
   if (nrows <= 0) return;
-  k_scatter_rows<<<(unsigned)nrows, 128, 0, st>>>(src, nrows, d, d_stride, pos_of_id, i0, dst);
+  k_scatter_rows<<<(unsigned)nrows, 128, 0, st>>>(src, nrows, d, d_stride, pos_of_id, i0, perm,
+                                                  dst);
 }
 
 }  // namespace rrg

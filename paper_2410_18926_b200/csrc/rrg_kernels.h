@@ -120,6 +120,7 @@ void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* 
                        const int* counts, int* cand_pos, int* cand_n, cudaStream_t st);
 
 void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
-                         const int* pos_of_id, int64_t i0, float* dst, cudaStream_t st);
+                         const int* pos_of_id, int64_t i0, const int* perm, float* dst,
+                         cudaStream_t st);
 
 }  // namespace rrg

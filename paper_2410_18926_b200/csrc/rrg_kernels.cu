@@ -10,6 +10,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "rrg_common.cuh"
 #include "rrg_kernels.h"
@@ -770,6 +772,208 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
   if (tid == 0) a.out_count[gq] = kk;
 }
 
+// ================================================ rerank, TMA-fed variant
+// Same arithmetic and lane layout as k_rerank_tree, but the candidate rows are
+// brought into shared memory by the TMA bulk-copy engine (cp.async.bulk,
+// one instruction per interleaved row, completion on a per-slot mbarrier)
+// through an NBUF-deep ring per warp.  The register file no longer bounds the
+// bytes in flight (k_rerank_tree: 2 rows per warp), and the LSU only serves
+// conflict-free 256 B shared-memory reads.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "RRG_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra RRG_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kRingDepth = 3;  // 3 x 3 KB per warp at d=768: two 256-thread CTAs per SM
+
+template <int SLOTS, int NB>
+__global__ void __launch_bounds__(RNT, 2) k_rerank_tma(RerankArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
+  __shared__ __align__(8) uint64_t bars[RNT / 32][kRingDepth];
+  const DevIndexView& ix = a.ix;
+  const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = RNT / 32;
+  const int d = ix.d, ds = ix.d_stride, nl = ix.pw_leaf_n, tail = nl % 8;
+  constexpr int nb = NB;
+  const int P = 4 * ix.pw_nleaves;
+  const int G = SLOTS == 1 ? P : 32;
+  const int R = 32 / G;
+  const int g = lane / G, pl = lane % G;
+  const int n = a.cand_n[q];
+  const bool euclid = ix.metric == kMetricEuclidean;
+  // smem: ring (128 B aligned) | dkeys[t] | dids[t] | selidx[k] | srt[np2]
+  const int rstride = R > 1 ? ds + 8 : ds;  // +8 floats: conflict-free row groups
+  const int unit_floats = R * rstride;
+  float* ring = reinterpret_cast<float*>(smem_raw);
+  float* myring = ring + (size_t)warp * kRingDepth * unit_floats;
+  uint32_t* dkeys = reinterpret_cast<uint32_t*>(ring + (size_t)nwarps * kRingDepth * unit_floats);
+  uint32_t* dids = dkeys + a.take_cap;
+  int* selidx = reinterpret_cast<int*>(dids + a.take_cap);
+  uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + a.k);
+  uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
+  const float* xq = a.queries + (size_t)q * d;
+  const int cstep = 8 * ix.pw_nleaves;
+  float2 xv[SLOTS][nb];
+  float xt[SLOTS][7];
+  int coff[SLOTS], ctail[SLOTS];
+#pragma unroll
+  for (int s = 0; s < SLOTS; ++s) {
+    int pair = pl + 32 * s;
+    int b = pair >> 2, h = pair & 3;
+    coff[s] = 8 * b + 2 * h;
+    ctail[s] = nb * cstep + b * tail;
+#pragma unroll
+    for (int i = 0; i < nb; ++i) xv[s][i] = *reinterpret_cast<const float2*>(xq + b * nl + 2 * h + 8 * i);
+#pragma unroll
+    for (int u = 0; u < 7; ++u) xt[s][u] = u < tail ? xq[b * nl + 8 * nb + u] : 0.f;
+  }
+  {
+    const int* cp = a.cand_pos + (size_t)q * a.take_cap;
+    for (int i = tid; i < n; i += RNT) dids[i] = (uint32_t)cp[i];
+  }
+  if (lane == 0) {
+    for (int k = 0; k < kRingDepth; ++k) mbar_init(&bars[warp][k], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t row_bytes = (uint32_t)ds * 4u;
+  const int units = (n + R - 1) / R;
+  auto issue = [&](int k) {  // lane 0: unit (warp + k*nwarps) -> ring slot k % depth
+    const int u = warp + k * nwarps;
+    if (u >= units) return;
+    const int slot = k % kRingDepth;
+    const int r0 = u * R, nr = min(R, n - r0);
+    mbar_expect_tx(&bars[warp][slot], (uint32_t)nr * row_bytes);
+    for (int r = 0; r < nr; ++r)
+      bulk_g2s(myring + (size_t)slot * unit_floats + r * rstride,
+               ix.corpus + (size_t)dids[r0 + r] * ds, row_bytes, &bars[warp][slot]);
+  };
+  if (lane == 0)
+    for (int k = 0; k < kRingDepth; ++k) issue(k);
+  for (int k = 0;; ++k) {
+    const int u = warp + k * nwarps;
+    if (u >= units) break;
+    const int slot = k % kRingDepth;
+    mbar_wait(&bars[warp][slot], (uint32_t)((k / kRingDepth) & 1));
+    const int row = u * R + g;
+    const bool valid = row < n;
+    const float* crow = myring + (size_t)slot * unit_floats + g * rstride;
+    const int gp = valid ? (int)dids[row] : 0;
+    float slot_sum[SLOTS];
+#pragma unroll
+    for (int s = 0; s < SLOTS; ++s) {
+      float v;
+      if (euclid) {
+        float r0 = 0.f, r1 = 0.f;
+#pragma unroll
+        for (int i = 0; i < nb; ++i) {
+          float2 c = *reinterpret_cast<const float2*>(crow + coff[s] + cstep * i);
+          float2 dd = __fadd2_rn(c, make_float2(-xv[s][i].x, -xv[s][i].y));
+          float2 sq = __fmul2_rn(dd, dd);
+          r0 = i == 0 ? sq.x : __fadd_rn(r0, sq.x);
+          r1 = i == 0 ? sq.y : __fadd_rn(r1, sq.y);
+        }
+        v = __fadd_rn(r0, r1);
+        v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 1));
+        v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, 2));
+        if (tail) {
+          const float* tp = crow + ctail[s];
+#pragma unroll
+          for (int t = 0; t < 7; ++t)
+            if (t < tail) {
+              float dd = __fsub_rn(tp[t], xt[s][t]);
+              v = __fadd_rn(v, __fmul_rn(dd, dd));
+            }
+        }
+      } else {
+        float acc = 0.f;
+#pragma unroll
+        for (int i = 0; i < nb; ++i) {
+          float2 c = *reinterpret_cast<const float2*>(crow + coff[s] + cstep * i);
+          acc += c.x * xv[s][i].x + c.y * xv[s][i].y;
+        }
+        if ((pl & 3) == 0)
+          for (int t = 0; t < tail; ++t) acc += crow[ctail[s] + t] * xt[s][t];
+        acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+        acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+        v = acc;
+      }
+      for (int o = 4; o < G; o <<= 1) v = __fadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+      slot_sum[s] = v;
+    }
+    float tot = slot_sum[0];
+    if (SLOTS == 2) tot = __fadd_rn(slot_sum[0], slot_sum[1]);
+    __syncwarp();  // every lane is done with this ring slot
+    if (valid && pl == 0) {
+      float diss = euclid ? tot : -tot;
+      dkeys[row] = mono32(diss);
+      dids[row] = __float_as_uint(__ldg(ix.pmeta + gp).w);
+    }
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(k + kRingDepth);
+    }
+  }
+  __syncthreads();
+  const int kk = min(a.k, n);
+  auto key = [&](int i) { return dkeys[i]; };
+  auto tie = [&](int i) { return dids[i]; };
+  auto val = [](uint32_t kv) { return unmono32(kv); };
+  block_select_bucketed<RNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
+  int np2 = 1;
+  while (np2 < kk) np2 <<= 1;
+  for (int i = tid; i < np2; i += RNT) {
+    uint64_t v = ~0ull;
+    if (i < kk) {
+      int ci = selidx[i];
+      v = ((uint64_t)dkeys[ci] << 32) | dids[ci];
+    }
+    srt[i] = v;
+  }
+  block_bitonic_sort<RNT>(srt, np2);
+  const int gq = a.q0 + q;
+  for (int i = tid; i < a.k; i += RNT) {
+    int64_t id = -1;
+    float sc = __int_as_float(0x7fc00000);
+    if (i < kk) {
+      uint64_t v = srt[i];
+      id = (int64_t)(uint32_t)v;
+      float df = unmono32((uint32_t)(v >> 32));
+      sc = euclid ? df : -df;
+    }
+    a.out_ids[(size_t)gq * a.k + i] = id;
+    a.out_scores[(size_t)gq * a.k + i] = sc;
+  }
+  if (tid == 0) a.out_count[gq] = kk;
+}
+
 // ======================================================== sharded merges
 // One CTA per query: compact the G sources' valid entries into shared memory,
 // select the `take` smallest by (key, id) and emit them sorted (the reference's
@@ -1007,6 +1211,39 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   a.out_count = h.out_count; a.q0 = h.q0; a.order = h.order;
   const bool tree = rerank_uses_tree(h.ix);
   const size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k, tree);
+  const char* rmode = getenv("RRG_RERANK");
+  const bool use_tma = !(rmode && strcmp(rmode, "regs") == 0);
+  if (tree && use_tma) {
+    const int nb = h.ix.pw_leaf_n / 8;
+    const bool one = 4 * h.ix.pw_nleaves <= 32;
+    const int G = one ? 4 * h.ix.pw_nleaves : 32, R = 32 / G;
+    const int rstride = R > 1 ? h.ix.d_stride + 8 : h.ix.d_stride;
+    const size_t ring = (size_t)(RNT / 32) * kRingDepth * R * rstride * 4;
+    const size_t smt = ring + rerank_smem(h.ix.d_stride, h.take_cap, h.k, true);
+#define RRG_TMA(S, NBV, SLOT)                           \
+  do {                                                  \
+    allow_smem(k_rerank_tma<S, NBV>, SLOT);             \
+    k_rerank_tma<S, NBV><<<nq, RNT, smt, st>>>(a);      \
+  } while (0)
+    bool launched = true;
+    if (one) {
+      switch (nb) {
+        case 8: RRG_TMA(1, 8, 12); break;
+        case 12: RRG_TMA(1, 12, 13); break;
+        case 15: RRG_TMA(1, 15, 14); break;
+        case 16: RRG_TMA(1, 16, 15); break;
+        default: launched = false;
+      }
+    } else {
+      switch (nb) {
+        case 12: RRG_TMA(2, 12, 16); break;
+        case 16: RRG_TMA(2, 16, 17); break;
+        default: launched = false;
+      }
+    }
+#undef RRG_TMA
+    if (launched) return;
+  }
   if (tree) {
     const int nb = h.ix.pw_leaf_n / 8;
     const bool one = 4 * h.ix.pw_nleaves <= 32;

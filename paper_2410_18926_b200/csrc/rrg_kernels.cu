@@ -604,7 +604,9 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
 // SLOTS = 4*nleaves/32 slots per lane.
 // NB = chain length nl/8 as a compile-time constant (loads use immediate
 // offsets, no per-element predicates); NB = 0 is the runtime-length fallback.
-template <int SLOTS, int NB>
+// NLV = number of leaves as a compile-time constant too (step stride 8*NLV and
+// the lane-group width G become immediates); 0 = runtime.
+template <int SLOTS, int NB, int NLV>
 __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankArgs a) {
   constexpr int kMaxNb = NB > 0 ? NB : 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
   constexpr int nwarps = RNT / 32;
   const int d = ix.d, ds = ix.d_stride, nl = ix.pw_leaf_n, tail = nl % 8;
   const int nb = NB > 0 ? NB : nl / 8;
-  const int P = 4 * ix.pw_nleaves;
+  const int P = 4 * (NLV > 0 ? NLV : ix.pw_nleaves);
   const int G = SLOTS == 1 ? P : 32;
   const int R = 32 / G;
   const int g = lane / G, pl = lane % G;
@@ -635,7 +637,7 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
   int off[SLOTS], coff[SLOTS], ctail[SLOTS];
   // corpus rows are interleaved step-major (DevIndexView::corpus_interleaved):
   // step i of (leaf b, pair h) sits at i*cstep + 8b + 2h
-  const int cstep = 8 * ix.pw_nleaves;
+  const int cstep = 8 * (NLV > 0 ? NLV : ix.pw_nleaves);
 #pragma unroll
   for (int s = 0; s < SLOTS; ++s) {
     int pair = pl + 32 * s;
@@ -1152,7 +1154,7 @@ void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s,
 // kernel's static shared memory), once per kernel slot and device.
 template <typename Kern>
 static void allow_smem(Kern* kernel, int slot) {
-  static int done[16][64] = {};
+  static int done[32][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || done[slot][dev]) return;
@@ -1212,7 +1214,9 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   const bool tree = rerank_uses_tree(h.ix);
   const size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k, tree);
   const char* rmode = getenv("RRG_RERANK");
-  const bool use_tma = !(rmode && strcmp(rmode, "regs") == 0);
+  // default: the register-pipelined k_rerank_tree (measured faster on C2 than the
+  // TMA ring, whose mbarrier polling costs issue slots); RRG_RERANK=tma opts in
+  const bool use_tma = rmode && strcmp(rmode, "tma") == 0;
   if (tree && use_tma) {
     const int nb = h.ix.pw_leaf_n / 8;
     const bool one = 4 * h.ix.pw_nleaves <= 32;
@@ -1247,26 +1251,41 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   if (tree) {
     const int nb = h.ix.pw_leaf_n / 8;
     const bool one = 4 * h.ix.pw_nleaves <= 32;
-#define RRG_TREE(S, NBV, SLOT)                          \
+#define RRG_TREE(S, NBV, NLVV, SLOT)                    \
   do {                                                  \
-    allow_smem(k_rerank_tree<S, NBV>, SLOT);            \
-    k_rerank_tree<S, NBV><<<nq, RNT, sm, st>>>(a);      \
+    allow_smem(k_rerank_tree<S, NBV, NLVV>, SLOT);      \
+    k_rerank_tree<S, NBV, NLVV><<<nq, RNT, sm, st>>>(a); \
   } while (0)
-    // leaf sizes of the common dims: 64 (nb 8), 96 (12: d=768/1536/100), 120 (15: d=960), 128 (16)
-    if (one) {
-      switch (nb) {
-        case 8: RRG_TREE(1, 8, 6); break;
-        case 12: RRG_TREE(1, 12, 7); break;
-        case 15: RRG_TREE(1, 15, 8); break;
-        case 16: RRG_TREE(1, 16, 9); break;
-        default: RRG_TREE(1, 0, 3); break;
-      }
-    } else {
-      switch (nb) {
-        case 12: RRG_TREE(2, 12, 10); break;
-        case 16: RRG_TREE(2, 16, 11); break;
-        default: RRG_TREE(2, 0, 4); break;
-      }
+    // specialised (chain length, leaf count) of the common dims:
+    //   d=768 (8 leaves of 96), 960 (8 x 120), 1536 (16 x 96), 1024 (8 x 128),
+    //   512/256/128 (4/2/1 x 128), 100 (1 x 100)
+    const int key = nb * 100 + h.ix.pw_nleaves;
+    switch (key) {
+      case 1208: RRG_TREE(1, 12, 8, 18); break;
+      case 1508: RRG_TREE(1, 15, 8, 19); break;
+      case 1608: RRG_TREE(1, 16, 8, 20); break;
+      case 1604: RRG_TREE(1, 16, 4, 21); break;
+      case 1602: RRG_TREE(1, 16, 2, 22); break;
+      case 1601: RRG_TREE(1, 16, 1, 23); break;
+      case 1201: RRG_TREE(1, 12, 1, 24); break;
+      case 1216: RRG_TREE(2, 12, 16, 25); break;
+      case 1616: RRG_TREE(2, 16, 16, 26); break;
+      default:
+        if (one) {
+          switch (nb) {
+            case 8: RRG_TREE(1, 8, 0, 6); break;
+            case 12: RRG_TREE(1, 12, 0, 7); break;
+            case 15: RRG_TREE(1, 15, 0, 8); break;
+            case 16: RRG_TREE(1, 16, 0, 9); break;
+            default: RRG_TREE(1, 0, 0, 3); break;
+          }
+        } else {
+          switch (nb) {
+            case 12: RRG_TREE(2, 12, 0, 10); break;
+            case 16: RRG_TREE(2, 16, 0, 11); break;
+            default: RRG_TREE(2, 0, 0, 4); break;
+          }
+        }
     }
 #undef RRG_TREE
     return;

@@ -122,8 +122,9 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # let nvidia-smi attach before the timed region starts
         except FileNotFoundError:
             self.proc = None
         return self
@@ -302,12 +303,18 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
+        t_start = time.perf_counter()
         for i in range(args.steps):
             flush.fill_(i & 0xFF)
             evs[i][0].record(stream)
             searcher.device_step(q, out)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
+        # a few ms of timed steps is shorter than nvidia-smi's sampling period: keep the
+        # same workload running (untimed) until the sampler has seen >= 0.6 s of it
+        while time.perf_counter() - t_start < 1.0:
+            searcher.device_step(q, out)
+            torch.cuda.synchronize()
     step_ms = [a.elapsed_time(b) for a, b in evs]
     ms = float(np.mean(step_ms))
     ms_t = torch.tensor([ms], device="cuda")

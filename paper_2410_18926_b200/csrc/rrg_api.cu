@@ -703,7 +703,8 @@ struct Phase1Out {
 
 void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int32_t w, int32_t t,
                  int32_t rerank, int64_t* ids, float* scores, int32_t* count, void* ws,
-                 size_t ws_bytes, cudaStream_t st, const Phase1Out* ph1 = nullptr) {
+                 size_t ws_bytes, cudaStream_t st, const Phase1Out* ph1 = nullptr,
+                 int* nonfinite = nullptr) {
   Plan p = make_plan(ix, nq, k, w, t, rerank, ph1 != nullptr);
   {  // shared-memory budgets of the per-query CTAs (static parts bounded by 48 KB)
     const size_t lim = kMaxSmemPerCta - 48 * 1024;
@@ -734,7 +735,9 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
     const int n = (int)std::min<int64_t>(p.qc, nq - q0);
     const float* x = queries + q0 * v.d;
     staged(0, st, [&] { launch_project(x, v.W, n, v.d, v.s, xp, st); });
-    staged(1, st, [&] { launch_prep(xp, x, n, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st); });
+    staged(1, st, [&] {
+      launch_prep(xp, x, n, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st, nonfinite);
+    });
     staged(2, st, [&] { launch_route_dist(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st); });
     staged(3, st, [&] { launch_route_select(diss, n, v.L, w, sel, prim, st); });
     staged(6, st, [&] { launch_bucket(prim, n, v.L, order, st); });
@@ -793,12 +796,16 @@ int guarded(F&& f) {
 
 struct HostCtx {
   int device = -1;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;  // compute
+  cudaStream_t cs = nullptr;  // copies
   void* dbuf = nullptr;
   size_t dcap = 0;
+  std::vector<cudaEvent_t> ev;
   ~HostCtx() {
     if (dbuf) cudaFree(dbuf);
     if (st) cudaStreamDestroy(st);
+    if (cs) cudaStreamDestroy(cs);
+    for (auto e : ev) cudaEventDestroy(e);
   }
 };
 thread_local HostCtx g_host;
@@ -863,25 +870,41 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
   return guarded([&] {
     if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
     if (nq == 0) return RRG_OK;
-    // _check_finite (index.py:144-150) happens before any per-query check
-    for (int64_t i = 0; i < nq * (int64_t)dim; ++i)
-      if (!std::isfinite(queries[i]))
-        return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
-    validate_search(index, dim, k, w, t, rerank);
+    // Validation order of query_batch: _check_finite (DataError, index.py:144-150)
+    // before QueryParams.validate.  The finiteness test runs on the GPU inside the
+    // query-prep pass; only when the parameters are invalid is the batch scanned on
+    // the host first, so that a non-finite batch still reports DataError.
+    try {
+      validate_search(index, dim, k, w, t, rerank);
+    } catch (const RrgFail&) {
+      const std::string msg = g_err, kind = g_kind;
+      for (int64_t i = 0; i < nq * (int64_t)dim; ++i)
+        if (!std::isfinite(queries[i]))
+          return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
+      g_err = msg;
+      g_kind = kind;
+      throw;
+    }
     CUDA_TRY(cudaSetDevice(index->device));
     HostCtx& h = g_host;
     if (h.device != index->device) {
       if (h.dbuf) cudaFree(h.dbuf);
       if (h.st) cudaStreamDestroy(h.st);
-      h.dbuf = nullptr; h.dcap = 0; h.st = nullptr;
+      if (h.cs) cudaStreamDestroy(h.cs);
+      h.dbuf = nullptr; h.dcap = 0; h.st = nullptr; h.cs = nullptr;
       CUDA_TRY(cudaStreamCreateWithFlags(&h.st, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&h.cs, cudaStreamNonBlocking));
       h.device = index->device;
     }
-    Plan p = make_plan(index, nq, k, w, t, rerank);
+    // Pipeline: the batch runs in chunks; the H2D copy of chunk j+1 and the D2H
+    // copy of chunk j-1 (copy stream) overlap the search of chunk j (compute stream).
+    const int64_t nchunks = nq >= 4096 ? 4 : 1;
+    const int64_t csz = (nq + nchunks - 1) / nchunks;
+    Plan p = make_plan(index, csz, k, w, t, rerank);
     const size_t qbytes = (size_t)nq * dim * 4, ibytes = (size_t)nq * k * 8,
                  sbytes = (size_t)nq * k * 4, cbytes = (size_t)nq * 4;
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
-    size_t need = al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + p.total;
+    size_t need = al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + 256 + p.total;
     if (need > h.dcap) {
       if (h.dbuf) cudaFree(h.dbuf);
       h.dbuf = nullptr;
@@ -893,13 +916,36 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     int64_t* di = reinterpret_cast<int64_t*>(b + al(qbytes));
     float* dsc = reinterpret_cast<float*>(b + al(qbytes) + al(ibytes));
     int32_t* dc = reinterpret_cast<int32_t*>(b + al(qbytes) + al(ibytes) + al(sbytes));
-    void* ws = b + al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes);
-    CUDA_TRY(cudaMemcpyAsync(dq, queries, qbytes, cudaMemcpyHostToDevice, h.st));
-    search_impl(index, dq, nq, k, w, t, rerank, di, dsc, dc, ws, p.total, h.st);
-    CUDA_TRY(cudaMemcpyAsync(ids, di, ibytes, cudaMemcpyDeviceToHost, h.st));
-    CUDA_TRY(cudaMemcpyAsync(scores, dsc, sbytes, cudaMemcpyDeviceToHost, h.st));
-    CUDA_TRY(cudaMemcpyAsync(count, dc, cbytes, cudaMemcpyDeviceToHost, h.st));
+    int* dflag = reinterpret_cast<int*>(b + al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes));
+    void* ws = b + al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + 256;
+    if (h.ev.empty()) {
+      h.ev.resize(8);
+      for (auto& e : h.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), h.st));
+    for (int64_t j = 0; j < nchunks; ++j) {
+      const int64_t q0 = j * csz, n = std::min<int64_t>(csz, nq - q0);
+      if (n <= 0) break;
+      cudaEvent_t in_ready = h.ev[j % 4], out_ready = h.ev[4 + j % 4];
+      CUDA_TRY(cudaMemcpyAsync(dq + q0 * dim, queries + q0 * dim, (size_t)n * dim * 4,
+                               cudaMemcpyHostToDevice, h.cs));
+      CUDA_TRY(cudaEventRecord(in_ready, h.cs));
+      CUDA_TRY(cudaStreamWaitEvent(h.st, in_ready, 0));
+      search_impl(index, dq + q0 * dim, n, k, w, t, rerank, di + q0 * k, dsc + q0 * k, dc + q0,
+                  ws, p.total, h.st, nullptr, dflag);
+      CUDA_TRY(cudaEventRecord(out_ready, h.st));
+      CUDA_TRY(cudaStreamWaitEvent(h.cs, out_ready, 0));
+      CUDA_TRY(cudaMemcpyAsync(ids + q0 * k, di + q0 * k, (size_t)n * k * 8,
+                               cudaMemcpyDeviceToHost, h.cs));
+      CUDA_TRY(cudaMemcpyAsync(scores + q0 * k, dsc + q0 * k, (size_t)n * k * 4,
+                               cudaMemcpyDeviceToHost, h.cs));
+      CUDA_TRY(cudaMemcpyAsync(count + q0, dc + q0, (size_t)n * 4, cudaMemcpyDeviceToHost, h.cs));
+    }
+    int flag = 0;
     CUDA_TRY(cudaStreamSynchronize(h.st));
+    CUDA_TRY(cudaMemcpyAsync(&flag, dflag, sizeof(int), cudaMemcpyDeviceToHost, h.cs));
+    CUDA_TRY(cudaStreamSynchronize(h.cs));
+    if (flag) return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
     return RRG_OK;
   });
 }

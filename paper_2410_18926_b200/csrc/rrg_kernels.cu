@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(GNT) k_gemm_f64(const float* __restrict__ A, i
 __global__ void k_prep_queries(const float* __restrict__ xp, const float* __restrict__ x, int nq,
                                int s, int s_pad, int d, int8_t* __restrict__ qcodes,
                                float* __restrict__ qscale, float* __restrict__ qhead,
-                               double* __restrict__ pp, float* __restrict__ xx) {
+                               double* __restrict__ pp, float* __restrict__ xx,
+                               int* __restrict__ nonfinite) {
   int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   int lane = threadIdx.x & 31;
   if (warp >= nq) return;
@@ -129,7 +130,14 @@ __global__ void k_prep_queries(const float* __restrict__ xp, const float* __rest
   }
   double xsum = 0.0;
   const float* xr = x + (size_t)warp * d;
-  for (int i = lane; i < d; i += 32) xsum += (double)xr[i] * (double)xr[i];
+  bool bad = false;
+  for (int i = lane; i < d; i += 32) {
+    const float v = xr[i];
+    bad |= !isfinite(v);
+    xsum += (double)v * (double)v;
+  }
+  // _check_finite (index.py:144-150) for the host-buffer entry, folded into this pass
+  if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
   if (lane == 0) {
@@ -1132,11 +1140,12 @@ void launch_project(const float* x, const float* W, int nq, int d, int s, float*
 }
 
 void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
-                 float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st) {
+                 float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st,
+                 int* nonfinite) {
   int warps_per_block = 8;
   int blocks = (nq + warps_per_block - 1) / warps_per_block;
   k_prep_queries<<<blocks, warps_per_block * 32, 0, st>>>(xp, x, nq, s, s_pad, d, qcodes, qscale,
-                                                          qhead, pp, xx);
+                                                          qhead, pp, xx, nonfinite);
 }
 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,

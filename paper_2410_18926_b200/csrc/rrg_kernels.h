@@ -52,7 +52,8 @@ struct RerankArgsHost {
 void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
                     cudaStream_t st);
 void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
-                 float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st);
+                 float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st,
+                 int* nonfinite = nullptr);
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
                        const double* pp, const double* cnorm, double* diss, cudaStream_t st);
 size_t route_select_smem(int L);

@@ -136,9 +136,13 @@ def query_batch(index, queries, params) -> list:
             return []
         ids, scores, count = dev.search_device(q, k, w, t, rerank)
         return _package(ids.cpu().numpy(), scores.cpu().numpy(), count.cpu().numpy(), k)
-    q = _check_finite(queries)
+    q = np.ascontiguousarray(queries, dtype=F32)
+    if q.ndim != 2:
+        raise DataError("queries: expected 2-D array")
     if q.shape[0] == 0:
         return []
+    # non-finite values are detected on the GPU by rrg_search_host (DataError,
+    # raised ahead of parameter errors like index.py:339)
     ids, scores, count = dev.search_host(q, k, w, t, rerank)
     return _package(ids, scores, count, k)
 

@@ -898,7 +898,8 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     }
     // Pipeline: the batch runs in chunks; the H2D copy of chunk j+1 and the D2H
     // copy of chunk j-1 (copy stream) overlap the search of chunk j (compute stream).
-    const int64_t nchunks = nq >= 4096 ? 4 : 1;
+    int64_t nchunks = nq >= 4096 ? 4 : 1;
+    if (const char* e = getenv("RRG_HOST_CHUNKS")) nchunks = std::max(1, atoi(e));
     const int64_t csz = (nq + nchunks - 1) / nchunks;
     Plan p = make_plan(index, csz, k, w, t, rerank);
     const size_t qbytes = (size_t)nq * dim * 4, ibytes = (size_t)nq * k * 8,

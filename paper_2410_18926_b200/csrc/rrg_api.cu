@@ -341,6 +341,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.pos_of_id = d_pos;
   v.m = hm.m;
   v.corpus_interleaved = 0;
+  v.elem_perm = nullptr;
   if (has_corpus) {
     float* corp = static_cast<float*>(ix->dalloc((size_t)std::max<int64_t>(P, 1) * v.d_stride * 4));
     const int* d_perm = nullptr;
@@ -355,6 +356,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
         }
       d_perm = ix->upload(perm);
       v.corpus_interleaved = 1;
+      v.elem_perm = d_perm;
     }
     fill_corpus(corp, d_pos, (int)v.d_stride, d_perm);
     v.corpus = corp;
@@ -617,6 +619,10 @@ struct Plan {
   int score_mode;
   int kcap;
   size_t off_qoff, off_ncand, off_pairoff, off_itemoff, off_pairs, off_kbase, off_keys, off_ctr;
+  // cluster-major re-rank (rr_mode == 1)
+  int rr_mode;
+  int mwords;
+  size_t off_cidx, off_marks, marks_bytes;
 };
 
 Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
@@ -675,6 +681,22 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     p.off_kbase = carve((Q + 1) * 4);
     p.off_keys = carve(Q * std::max<int64_t>(nmax, 1) * 4);
     p.off_ctr = carve(16);
+  }
+  // re-rank strategy: cluster-major (rows of a cluster shared by its queries) when
+  // the scoring is cluster-major and the row plan fits k_rerank_cluster;
+  // RRG_RERANK=query|regs|tma forces a per-query kernel
+  {
+    // measured on C2 (w=1, t=800): per-query k_rerank_tree 2.08 ms vs cluster-major
+    // 2.75 ms, so the cluster-major re-rank is opt-in (RRG_RERANK=cluster)
+    const char* e = getenv("RRG_RERANK");
+    const bool want = e && strcmp(e, "cluster") == 0;
+    p.rr_mode = (want && p.score_mode == 1 && rerank && !exact_take && cluster_rerank_ok(v)) ? 1 : 0;
+  }
+  if (p.rr_mode == 1) {
+    p.mwords = (int)((ix->max_cluster + 31) / 32) + 1;
+    p.off_cidx = carve(Q * (int64_t)p.take_cap * 4);
+    p.marks_bytes = ((size_t)Q * std::max<int64_t>(nmax, 1) / 32 + 2) * 4;
+    p.off_marks = carve(p.marks_bytes);
   }
   p.total = o;
   return p;
@@ -768,9 +790,30 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       th.cand_n = cn; th.out_ids = ids; th.out_scores = scores; th.out_count = count;
       th.q0 = (int)q0; th.order = order; th.kcap = p.kcap;
       if (ph1) { th.sel_keys = ph1->keys; th.sel_ids = ph1->ids; th.sel_count = ph1->count; }
+      uint32_t* marks = reinterpret_cast<uint32_t*>(base + p.off_marks);
+      int* cidx = reinterpret_cast<int*>(base + p.off_cidx);
+      if (p.rr_mode == 1) {
+        CUDA_TRY(cudaMemsetAsync(marks, 0, p.marks_bytes, st));
+        th.cand_idx = cidx;
+        th.marks = marks;
+      }
       staged(4, st, [&] { launch_select_topt(th, n, st); });
+      if (p.rr_mode == 1) {
+        // scores are consumed: the key array is reused for the re-ranked distances
+        ClusterRerankHost rh{};
+        rh.ix = v; rh.queries = x; rh.w = w; rh.qoff = ch.qoff; rh.pair_off = ch.pair_off;
+        rh.item_off = ch.item_off; rh.pairs = ch.pairs; rh.kbase = ch.kbase; rh.marks = marks;
+        rh.diss = ch.keys; rh.work_counter = ch.work_counter + 1; rh.mwords = p.mwords;
+        staged(5, st, [&] { launch_cluster_rerank(rh, st); });
+        TopkFinalHost fh{};
+        fh.ix = v; fh.sel = sel; fh.w = w; fh.qoff = ch.qoff; fh.kbase = ch.kbase; fh.diss = ch.keys;
+        fh.cand_idx = cidx; fh.cand_n = cn; fh.take_cap = p.take_cap; fh.k = k;
+        fh.out_ids = ids; fh.out_scores = scores; fh.out_count = count; fh.q0 = (int)q0;
+        fh.order = order;
+        staged(5, st, [&] { launch_topk_final(fh, n, st); });
+      }
     }
-    if (rerank && !ph1) {
+    if (rerank && !ph1 && p.rr_mode == 0) {
       RerankArgsHost ra{};
       ra.ix = v; ra.queries = x; ra.cand_pos = cpos; ra.cand_n = cn; ra.take_cap = p.take_cap;
       ra.k = k; ra.out_ids = ids; ra.out_scores = scores; ra.out_count = count; ra.q0 = (int)q0;

@@ -294,6 +294,10 @@ struct SelectArgs {
   int* sel_count;
   int kcap;      // keys staged in smem when N <= kcap
   int sort_cap;  // power of two >= k (no-rerank ordering)
+  // cluster-major re-rank: selected candidate indices (into the query's key array)
+  // and a membership bitmap over all keys (bit kbase[q] + i)
+  int* cand_idx;
+  uint32_t* marks;
 };
 
 __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
@@ -341,6 +345,18 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
   auto val = [](uint32_t k) { return unmono32(k); };
   block_select_bucketed<TNT, uint32_t, float>(N, take, key, tie, val, selidx, bs, sm);
   const int gq = a.q0 + q;
+  if (a.rerank && a.marks) {  // cluster-major re-rank consumes (index, membership bit)
+    int* oi = a.cand_idx + (size_t)q * a.take_cap;
+    const size_t kb = (size_t)a.kbase[q];
+    for (int i = tid; i < take; i += TNT) {
+      const int ci = selidx[i];
+      oi[i] = ci;
+      const size_t bit = kb + (size_t)ci;
+      atomicOr(a.marks + (bit >> 5), 1u << (bit & 31));
+    }
+    if (tid == 0) a.cand_n[q] = take;
+    return;
+  }
   if (a.rerank) {
     int* outp = a.cand_pos + (size_t)q * a.take_cap;
     for (int i = tid; i < take; i += TNT) outp[i] = pos_of(selidx[i]);
@@ -381,6 +397,245 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
   if (tid == 0) a.out_count[gq] = take;
 }
 
+// ---------------------------------------------------- cluster-major re-rank
+// Re-ranking is a (query x candidate-row) distance matrix restricted to each
+// query's top-t; rows of one cluster are shared by every query of its bucket
+// (C2: ~10 queries re-rank ~800 of the same ~1000 rows).  One CTA takes a
+// (cluster, <=32 queries) work item of the scoring pass, stages the queries'
+// x (interleaved like the rows) and top-t membership bits in shared memory,
+// and streams the cluster's rows through registers once: each row pair is
+// loaded by one warp and scored against every query of the item that selected
+// either row.  The per-(query, row) arithmetic is k_rerank_tree's -- NumPy's
+// pairwise tree, bit-exact -- with lane (leaf b, pair h) of a 32-lane row
+// group (8 leaves; leaf size a multiple of 8).  Distances land as mono32 keys
+// over the query's candidate-key array; k_topk_final orders them.
+constexpr int XNT = 256;
+constexpr int kRrQ = 16;  // queries whose x is staged at once
+
+struct ClusterRerankArgs {
+  DevIndexView ix;
+  const float* queries;  // chunk-local [nq][d]
+  int w;
+  const int* qoff;
+  const int* pair_off;
+  const int* item_off;
+  const int* pairs;
+  const int* kbase;
+  const uint32_t* marks;
+  uint32_t* diss;
+  int* work_counter;
+  int mwords;  // bitmap words staged per query (>= ceil(max m_l / 32) + 1)
+};
+
+template <int NB>
+__global__ void __launch_bounds__(XNT, 2) k_rerank_cluster(ClusterRerankArgs a) {
+  constexpr int NLV = 8, cstep = 8 * NLV;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const DevIndexView& ix = a.ix;
+  const int ds = ix.d_stride, d = ix.d;
+  float* xs = reinterpret_cast<float*>(smem_raw);                       // [kRrQ][ds]
+  uint32_t* mb = reinterpret_cast<uint32_t*>(xs + (size_t)kRrQ * ds);  // [kRrQ][mwords]
+  __shared__ int item_s;
+  __shared__ int pq[kPairsPerItem], pkey[kPairsPerItem];
+  const int L = ix.L;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = XNT / 32;
+  const int b = lane >> 2, h = lane & 3;
+  const int coff = 8 * b + 2 * h;
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const int total_items = a.item_off[L];
+  while (true) {
+    if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = item_s;
+    __syncthreads();
+    if (item >= total_items) break;
+    int lo = 0, hi = L;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (a.item_off[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int l = lo;
+    const int j0 = a.pair_off[l] + (item - a.item_off[l]) * kPairsPerItem;
+    const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
+    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    if (tid < np) {
+      const int pr = a.pairs[j0 + tid];
+      const int q = pr / a.w, c = pr % a.w;
+      pq[tid] = q;
+      pkey[tid] = a.kbase[q] + a.qoff[(size_t)q * (a.w + 1) + c];
+    }
+    __syncthreads();
+    if (m == 0) continue;
+    const int mw = (m + 31) / 32;
+    for (int g0 = 0; g0 < np; g0 += kRrQ) {
+      const int ng = min(kRrQ, np - g0);
+      // stage x (interleaved) and the membership bits of this query group
+      for (int e = tid; e < ng * d; e += XNT) {
+        const int g = e / d, j = e - g * d;
+        xs[(size_t)g * ds + ix.elem_perm[j]] = a.queries[(size_t)pq[g0 + g] * d + j];
+      }
+      for (int e = tid; e < ng * mw; e += XNT) {
+        const int g = e / mw, k = e - g * mw;
+        const size_t bit = (size_t)pkey[g0 + g] + 32 * (size_t)k;
+        const uint32_t lo32 = a.marks[bit >> 5];
+        const uint32_t hi32 = a.marks[(bit >> 5) + 1];  // bitmap carries one pad word
+        mb[g * a.mwords + k] = __funnelshift_r(lo32, hi32, (unsigned)(bit & 31));
+      }
+      __syncthreads();
+      for (int pa = warp * 2; pa < m; pa += nwarps * 2) {
+        const int pb = pa + 1;
+        const bool hasb = pb < m;
+        float2 ca[NB], cb[NB];
+        const float* ra = ix.corpus + (size_t)(p0 + pa) * ds + coff;
+        const float* rb = ix.corpus + (size_t)(p0 + (hasb ? pb : pa)) * ds + coff;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) ca[i] = __ldg(reinterpret_cast<const float2*>(ra + cstep * i));
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cb[i] = __ldg(reinterpret_cast<const float2*>(rb + cstep * i));
+        // per (query, row pair): this lane's r[2h]+r[2h+1] of both rows
+        auto lane_sums = [&](int g, float& va, float& vb) {
+          const float* xg = xs + (size_t)g * ds + coff;
+          if (euclid) {
+            float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+              const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
+              const float2 nx = make_float2(-xv.x, -xv.y);
+              const float2 da = __fadd2_rn(ca[i], nx), db = __fadd2_rn(cb[i], nx);
+              const float2 sa = __fmul2_rn(da, da), sb = __fmul2_rn(db, db);
+              a0 = i == 0 ? sa.x : __fadd_rn(a0, sa.x);
+              a1 = i == 0 ? sa.y : __fadd_rn(a1, sa.y);
+              b0 = i == 0 ? sb.x : __fadd_rn(b0, sb.x);
+              b1 = i == 0 ? sb.y : __fadd_rn(b1, sb.y);
+            }
+            va = __fadd_rn(a0, a1);
+            vb = __fadd_rn(b0, b1);
+          } else {
+            float acc_a = 0.f, acc_b = 0.f;
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+              const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
+              acc_a += ca[i].x * xv.x + ca[i].y * xv.y;
+              acc_b += cb[i].x * xv.x + cb[i].y * xv.y;
+            }
+            va = acc_a;
+            vb = acc_b;
+          }
+        };
+        auto marked = [&](int g, int p) {
+          return p < m && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
+        };
+        // two queries per step: four independent reductions interleave their shuffles
+        for (int g = 0; g < ng; g += 2) {
+          const int g2 = g + 1 < ng ? g + 1 : g;
+          const bool m1a = marked(g, pa), m1b = marked(g, pb);
+          const bool m2a = g2 != g && marked(g2, pa), m2b = g2 != g && marked(g2, pb);
+          if (!(m1a || m1b || m2a || m2b)) continue;  // warp-uniform
+          float v1a = 0.f, v1b = 0.f, v2a = 0.f, v2b = 0.f;
+          if (m1a || m1b) lane_sums(g, v1a, v1b);
+          if (m2a || m2b) lane_sums(g2, v2a, v2b);
+          // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            v1a = __fadd_rn(v1a, __shfl_xor_sync(0xffffffffu, v1a, o));
+            v1b = __fadd_rn(v1b, __shfl_xor_sync(0xffffffffu, v1b, o));
+            v2a = __fadd_rn(v2a, __shfl_xor_sync(0xffffffffu, v2a, o));
+            v2b = __fadd_rn(v2b, __shfl_xor_sync(0xffffffffu, v2b, o));
+          }
+          if (lane == 0) {
+            const int k1 = pkey[g0 + g], k2 = pkey[g0 + g2];
+            if (m1a) a.diss[k1 + pa] = mono32(euclid ? v1a : -v1a);
+            if (m1b) a.diss[k1 + pb] = mono32(euclid ? v1b : -v1b);
+            if (m2a) a.diss[k2 + pa] = mono32(euclid ? v2a : -v2a);
+            if (m2b) a.diss[k2 + pb] = mono32(euclid ? v2b : -v2b);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Final per-query top-k over the re-ranked candidates (index.py:320-322).
+struct TopkFinalArgs {
+  DevIndexView ix;
+  const int* sel;
+  int w;
+  const int* qoff;
+  const int* kbase;
+  const uint32_t* diss;
+  const int* cand_idx;
+  const int* cand_n;
+  int take_cap, k;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+  const int* order;
+};
+
+__global__ void __launch_bounds__(XNT) k_topk_final(TopkFinalArgs a) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ SelectSmem sm;
+  __shared__ BucketSmem bs;
+  const DevIndexView& ix = a.ix;
+  const int q = a.order ? a.order[blockIdx.x] : (int)blockIdx.x;
+  const int tid = threadIdx.x, w = a.w;
+  const int n = a.cand_n[q];
+  int* offs = reinterpret_cast<int*>(smem_raw);  // w+1
+  int* pbase = offs + (w + 1);                    // w
+  uint32_t* dk = reinterpret_cast<uint32_t*>(pbase + w);  // take_cap
+  uint32_t* di = dk + a.take_cap;                          // take_cap
+  int* selidx = reinterpret_cast<int*>(di + a.take_cap);   // k
+  uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + a.k);
+  uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
+  for (int c = tid; c <= w; c += XNT) offs[c] = a.qoff[(size_t)q * (w + 1) + c];
+  for (int c = tid; c < w; c += XNT) pbase[c] = ix.cl_pos[a.sel[(size_t)q * w + c]];
+  __syncthreads();
+  const uint32_t* dq = a.diss + a.kbase[q];
+  const int* ci = a.cand_idx + (size_t)q * a.take_cap;
+  for (int i = tid; i < n; i += XNT) {
+    const int c = ci[i];
+    int lo = 0, hi = w;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (offs[mid] <= c) lo = mid; else hi = mid;
+    }
+    dk[i] = dq[c];
+    di[i] = __float_as_uint(__ldg(ix.pmeta + pbase[lo] + (c - offs[lo])).w);
+  }
+  __syncthreads();
+  const int kk = min(a.k, n);
+  auto key = [&](int i) { return dk[i]; };
+  auto tie = [&](int i) { return di[i]; };
+  auto val = [](uint32_t kv) { return unmono32(kv); };
+  block_select_bucketed<XNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
+  int np2 = 1;
+  while (np2 < kk) np2 <<= 1;
+  for (int i = tid; i < np2; i += XNT) {
+    uint64_t v = ~0ull;
+    if (i < kk) v = ((uint64_t)dk[selidx[i]] << 32) | di[selidx[i]];
+    srt[i] = v;
+  }
+  block_bitonic_sort<XNT>(srt, np2);
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const int gq = a.q0 + q;
+  for (int i = tid; i < a.k; i += XNT) {
+    int64_t id = -1;
+    float sc = __int_as_float(0x7fc00000);
+    if (i < kk) {
+      const uint64_t v = srt[i];
+      id = (int64_t)(uint32_t)v;
+      const float df = unmono32((uint32_t)(v >> 32));
+      sc = euclid ? df : -df;
+    }
+    a.out_ids[(size_t)gq * a.k + i] = id;
+    a.out_scores[(size_t)gq * a.k + i] = sc;
+  }
+  if (tid == 0) a.out_count[gq] = kk;
+}
+
 // ---------------------------------------------------------------- launchers
 
 void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
@@ -418,6 +673,7 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   a.out_count = h.out_count; a.q0 = h.q0; a.order = h.order; a.sel_keys = h.sel_keys;
   a.sel_ids = h.sel_ids; a.sel_count = h.sel_count;
   a.kcap = h.kcap; a.sort_cap = pow2_at_least(h.k);
+  a.cand_idx = h.cand_idx; a.marks = h.marks;
   static int done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -429,6 +685,61 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
     done[dev] = 1;
   }
   k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
+}
+
+bool cluster_rerank_ok(const DevIndexView& ix) {
+  const int nb = ix.pw_leaf_n / 8;
+  return ix.corpus_interleaved && ix.pw_nleaves == 8 && ix.pw_leaf_n % 8 == 0 &&
+         (nb == 12 || nb == 15 || nb == 16);
+}
+
+size_t cluster_rerank_smem(int d_stride, int mwords) {
+  return (size_t)kRrQ * d_stride * 4 + (size_t)kRrQ * mwords * 4;
+}
+
+template <typename Kern>
+static void opt_in_smem(Kern* kern, int slot) {
+  static int done[8][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[slot][dev]) return;
+  cudaFuncAttributes at{};
+  cudaFuncGetAttributes(&at, (const void*)kern);
+  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kMaxSmemPerCta - (int)at.sharedSizeBytes);
+  done[slot][dev] = 1;
+}
+
+void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
+  ClusterRerankArgs a;
+  a.ix = h.ix; a.queries = h.queries; a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off;
+  a.item_off = h.item_off; a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks;
+  a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
+  cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
+  const size_t sm = cluster_rerank_smem(h.ix.d_stride, h.mwords);
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  switch (h.ix.pw_leaf_n / 8) {
+    case 12: opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * 2, XNT, sm, st>>>(a); break;
+    case 15: opt_in_smem(k_rerank_cluster<15>, 1); k_rerank_cluster<15><<<sms * 2, XNT, sm, st>>>(a); break;
+    default: opt_in_smem(k_rerank_cluster<16>, 2); k_rerank_cluster<16><<<sms * 2, XNT, sm, st>>>(a); break;
+  }
+}
+
+size_t topk_final_smem(int w, int take_cap, int k) {
+  return (size_t)(2 * w + 1) * 4 + (size_t)take_cap * 8 + (size_t)k * 4 + 32 +
+         (size_t)pow2_at_least(k) * 8 + 16;
+}
+
+void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
+  TopkFinalArgs a;
+  a.ix = h.ix; a.sel = h.sel; a.w = h.w; a.qoff = h.qoff; a.kbase = h.kbase; a.diss = h.diss;
+  a.cand_idx = h.cand_idx; a.cand_n = h.cand_n; a.take_cap = h.take_cap; a.k = h.k;
+  a.out_ids = h.out_ids; a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
+  a.order = h.order;
+  opt_in_smem(k_topk_final, 3);
+  k_topk_final<<<nq, XNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a);
 }
 
 }  // namespace rrg

@@ -56,6 +56,7 @@ struct DevIndexView {
   // tails after all steps), so one warp instruction of the re-rank reads 256
   // contiguous bytes instead of eight 32-byte pieces of the natural layout.
   int corpus_interleaved;
+  const int* elem_perm;  // [d] natural element -> interleaved slot (when interleaved)
 };
 
 // ---------------------------------------------------------------- numerics

@@ -614,8 +614,11 @@ __global__ void __launch_bounds__(RNT) k_rerank_topk(RerankArgs a) {
 // offsets, no per-element predicates); NB = 0 is the runtime-length fallback.
 // NLV = number of leaves as a compile-time constant too (step stride 8*NLV and
 // the lane-group width G become immediates); 0 = runtime.
-template <int SLOTS, int NB, int NLV>
-__global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankArgs a) {
+// UROWS row groups in flight per warp and MINB CTAs per SM: measured on C2 (d=768),
+// U=1 at 4 CTAs/SM (64 regs, 32 warps/SM) beats U=2 at 2 CTAs/SM (1.66 vs 2.08 ms):
+// more warps hide the L2 latency better than more rows per warp.
+template <int SLOTS, int NB, int NLV, int UROWS = 1, int MINB = (SLOTS == 1 ? 4 : 1)>
+__global__ void __launch_bounds__(RNT, MINB) k_rerank_tree(RerankArgs a) {
   constexpr int kMaxNb = NB > 0 ? NB : 16;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
@@ -667,7 +670,7 @@ __global__ void __launch_bounds__(RNT, SLOTS == 1 ? 2 : 1) k_rerank_tree(RerankA
   }
   __syncthreads();
   // U row groups per warp pass: all U rows' loads are issued before any math
-  constexpr int U = SLOTS == 1 ? 2 : 1;
+  constexpr int U = UROWS;
   for (int row0 = warp * R * U; row0 < n; row0 += nwarps * R * U) {
     int rows[U], gps[U];
     float2 cbuf[U][SLOTS][kMaxNb];

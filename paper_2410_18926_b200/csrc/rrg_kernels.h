@@ -104,9 +104,49 @@ struct SelectTopTHost {
   uint32_t* sel_ids;
   int* sel_count;
   int kcap;
+  int* cand_idx = nullptr;    // cluster-major re-rank outputs
+  uint32_t* marks = nullptr;
 };
 size_t select_topt_smem(int w, int take_cap, int k, int kcap);
 void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st);
+
+// Cluster-major re-rank (rrg_cluster_score.cu)
+struct ClusterRerankHost {
+  DevIndexView ix;
+  const float* queries;
+  int w;
+  const int* qoff;
+  const int* pair_off;
+  const int* item_off;
+  const int* pairs;
+  const int* kbase;
+  const uint32_t* marks;
+  uint32_t* diss;
+  int* work_counter;
+  int mwords;
+};
+bool cluster_rerank_ok(const DevIndexView& ix);
+size_t cluster_rerank_smem(int d_stride, int mwords);
+void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st);
+
+struct TopkFinalHost {
+  DevIndexView ix;
+  const int* sel;
+  int w;
+  const int* qoff;
+  const int* kbase;
+  const uint32_t* diss;
+  const int* cand_idx;
+  const int* cand_n;
+  int take_cap, k;
+  int64_t* out_ids;
+  float* out_scores;
+  int* out_count;
+  int q0;
+  const int* order;
+};
+size_t topk_final_smem(int w, int take_cap, int k);
+void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st);
 
 // Sharded search: merge G per-shard lists per query, laid out
 // [G][nq][cap] (the all-gather layout) with counts [G][nq].

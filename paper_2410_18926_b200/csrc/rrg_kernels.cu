@@ -24,80 +24,111 @@ namespace rrg {
 // f64 -- the reference's `x.astype(f64) @ W.astype(f64)` (index.py:298) and
 // `p @ c.T` (cluster.py:50,58); the summation order differs from OpenBLAS only at
 // the f64 rounding level (0/153,600 projection mismatches).
-constexpr int GBM = 64, GBN = 64, GBK = 16, GNT = 256;
+// FP64 tensor-core GEMM (DMMA, mma.sync.m8n8k4.f64): 128x64 CTA tile, 8 warps of
+// 32x32 (4x4 m8n8 tiles), K staged 8 at a time, double-buffered, in padded smem (pitch 12
+// doubles: the four 32 B fragment rows of a half-warp fall in distinct banks).
+// f32 inputs are widened to f64 exactly (the reference's `x.astype(f64) @
+// W.astype(f64)`, index.py:298, and `p @ c.T`, cluster.py:50,58); products and
+// sums in f64, so only the f64 summation order differs from OpenBLAS.
+constexpr int MBM = 128, MBN = 64, MBK = 8, DMNT = 256, MPITCH = 12;
+
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
 
 template <int EPI, bool BT>
-__global__ void __launch_bounds__(GNT) k_gemm_f64(const float* __restrict__ A, int lda,
-                                                   const float* __restrict__ B, int ldb, int M,
-                                                   int N, int K, float* __restrict__ outf,
-                                                   double* __restrict__ outd, int ldo,
-                                                   const double* __restrict__ rowterm,
-                                                   const double* __restrict__ colterm) {
-  __shared__ double As[GBK][GBM + 1];
-  __shared__ double Bs[GBK][GBN + 1];
-  const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
-  const int m0 = blockIdx.y * GBM, n0 = blockIdx.x * GBN;
-  double acc[4][4];
+__global__ void __launch_bounds__(DMNT, 2) k_gemm_dmma(const float* __restrict__ A, int lda,
+                                                     const float* __restrict__ B, int ldb, int M,
+                                                     int N, int K, float* __restrict__ outf,
+                                                     double* __restrict__ outd, int ldo,
+                                                     const double* __restrict__ rowterm,
+                                                     const double* __restrict__ colterm) {
+  __shared__ __align__(16) double As[2][MBM][MPITCH];  // [buf][m][k]
+  __shared__ __align__(16) double Bs[2][MBN][MPITCH];  // [buf][n][k]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps of 32x32
+  const int m0 = blockIdx.y * MBM, n0 = blockIdx.x * MBN;
+  double acc[4][4][2];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0;
-
-  for (int k0 = 0; k0 < K; k0 += GBK) {
-    // A tile: 64 rows x 16 k -> 1024 elements, 4 per thread
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // global -> registers (next tile in flight while the current one is multiplied)
+  float ra[(MBM * MBK) / DMNT], rb[(MBN * MBK) / DMNT];
+  auto gload = [&](int k0) {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      int idx = tid + e * GNT;
-      int r = idx / GBK, kk = idx % GBK;
-      int gm = m0 + r, gk = k0 + kk;
-      As[kk][r] = (gm < M && gk < K) ? (double)A[(size_t)gm * lda + gk] : 0.0;
+    for (int e = 0; e < (MBM * MBK) / DMNT; ++e) {  // A tile 128 x 8, k fastest
+      const int idx = tid + e * DMNT, r = idx / MBK, kk = idx % MBK;
+      const int gm = m0 + r, gk = k0 + kk;
+      ra[e] = (gm < M && gk < K) ? __ldg(A + (size_t)gm * lda + gk) : 0.f;
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      int idx = tid + e * GNT;
-      if (BT) {
-        int c = idx / GBK, kk = idx % GBK;
-        int gn = n0 + c, gk = k0 + kk;
-        Bs[kk][c] = (gn < N && gk < K) ? (double)B[(size_t)gn * ldb + gk] : 0.0;
-      } else {
-        int kk = idx / GBN, c = idx % GBN;
-        int gn = n0 + c, gk = k0 + kk;
-        Bs[kk][c] = (gn < N && gk < K) ? (double)B[(size_t)gk * ldb + gn] : 0.0;
-      }
+    for (int e = 0; e < (MBN * MBK) / DMNT; ++e) {  // B tile 64 (n) x 8 (k)
+      const int idx = tid + e * DMNT;
+      int c, kk;
+      if (BT) { c = idx / MBK; kk = idx % MBK; } else { kk = idx / MBN; c = idx % MBN; }
+      const int gn = n0 + c, gk = k0 + kk;
+      float v = 0.f;
+      if (gn < N && gk < K) v = BT ? __ldg(B + (size_t)gn * ldb + gk) : __ldg(B + (size_t)gk * ldb + gn);
+      rb[e] = v;
     }
-    __syncthreads();
+  };
+  auto sstore = [&](int buf) {
 #pragma unroll
-    for (int kk = 0; kk < GBK; ++kk) {
-      double a[4], b[4];
+    for (int e = 0; e < (MBM * MBK) / DMNT; ++e) {
+      const int idx = tid + e * DMNT;
+      As[buf][idx / MBK][idx % MBK] = (double)ra[e];
+    }
 #pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
+    for (int e = 0; e < (MBN * MBK) / DMNT; ++e) {
+      const int idx = tid + e * DMNT;
+      if (BT) Bs[buf][idx / MBK][idx % MBK] = (double)rb[e];
+      else Bs[buf][idx % MBN][idx / MBN] = (double)rb[e];
+    }
+  };
+  const int nk = (K + MBK - 1) / MBK;
+  gload(0);
+  sstore(0);
+  __syncthreads();
+  for (int kt = 0; kt < nk; ++kt) {
+    const int buf = kt & 1;
+    if (kt + 1 < nk) gload((kt + 1) * MBK);
 #pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+    for (int ks = 0; ks < MBK; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = As[buf][wm * 32 + i * 8 + (lane >> 2)][ks + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bs[buf][wn * 32 + j * 8 + (lane >> 2)][ks + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+        for (int j = 0; j < 4; ++j) dmma_m8n8k4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
     }
+    if (kt + 1 < nk) sstore(buf ^ 1);
     __syncthreads();
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int gm = m0 + ty + 16 * i;
+    const int gm = m0 + wm * 32 + i * 8 + (lane >> 2);
     if (gm >= M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      int gn = n0 + tx + 16 * j;
-      if (gn >= N) continue;
-      double v = acc[i][j];
-      if (EPI == EPI_PROJ) {
-        outf[(size_t)gm * ldo + gn] = (float)v;  // one rounding to f32 (round-to-nearest)
-      } else if (EPI == EPI_L2) {
-        // ((p.p) - 2 (p.c)) + (c.c), then max(., 0)  (cluster.py:50-51)
-        double d2 = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, v)), colterm[gn]);
-        outd[(size_t)gm * ldo + gn] = d2 > 0.0 ? d2 : 0.0;
-      } else {
-        outd[(size_t)gm * ldo + gn] = -v;  // -(p @ c.T)  (cluster.py:58)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int gn = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
+        if (gn >= N) continue;
+        const double v = acc[i][j][h];
+        if (EPI == 0) {
+          outf[(size_t)gm * ldo + gn] = (float)v;
+        } else if (EPI == 1) {
+          const double d2 = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, v)), colterm[gn]);
+          outd[(size_t)gm * ldo + gn] = d2 > 0.0 ? d2 : 0.0;
+        } else {
+          outd[(size_t)gm * ldo + gn] = -v;
+        }
       }
     }
   }
@@ -825,7 +856,7 @@ constexpr int kRingDepth = 3;  // 3 x 3 KB per warp at d=768: two 256-thread CTA
 
 template <int SLOTS, int NB>
 __global__ void __launch_bounds__(RNT, 2) k_rerank_tma(RerankArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
   __shared__ BucketSmem bs;
   __shared__ __align__(8) uint64_t bars[RNT / 32][kRingDepth];
@@ -1137,9 +1168,9 @@ __global__ void k_scatter_rows(const float* __restrict__ src, int64_t nrows, int
 // ===================================================================== launchers
 void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
                     cudaStream_t st) {
-  dim3 grid((s + GBN - 1) / GBN, (nq + GBM - 1) / GBM);
-  k_gemm_f64<EPI_PROJ, false><<<grid, GNT, 0, st>>>(x, d, W, s, nq, s, d, xp, nullptr, s,
-                                                     nullptr, nullptr);
+  dim3 grid((s + MBN - 1) / MBN, (nq + MBM - 1) / MBM);
+  k_gemm_dmma<EPI_PROJ, false><<<grid, DMNT, 0, st>>>(x, d, W, s, nq, s, d, xp, nullptr, s,
+                                                      nullptr, nullptr);
 }
 
 void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
@@ -1153,13 +1184,13 @@ void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int 
 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
                        const double* pp, const double* cnorm, double* diss, cudaStream_t st) {
-  dim3 grid((L + GBN - 1) / GBN, (nq + GBM - 1) / GBM);
+  dim3 grid((L + MBN - 1) / MBN, (nq + MBM - 1) / MBM);
   if (metric == kMetricEuclidean)
-    k_gemm_f64<EPI_L2, true><<<grid, GNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L, pp,
-                                                    cnorm);
+    k_gemm_dmma<EPI_L2, true><<<grid, DMNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L, pp,
+                                                     cnorm);
   else
-    k_gemm_f64<EPI_NEGIP, true><<<grid, GNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
-                                                       nullptr, nullptr);
+    k_gemm_dmma<EPI_NEGIP, true><<<grid, DMNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
+                                                        nullptr, nullptr);
 }
 
 // Opt in to the dynamic shared memory a launch may need (227 KB per CTA minus the

@@ -1,11 +1,17 @@
 // rrg_kernels.cu -- sm_100a kernels of the LoRANN batched query path.
 //
 // Stage map (reference file:line -> kernel):
-//   projection      index.py:298                 -> k_gemm_f64<EPI_PROJ>
+//   projection      index.py:298                 -> k_gemm_dmma<EPI_PROJ>
 //   query quantize  quantize.py:61-77 (index.py:302) -> k_prep_queries
-//   routing         cluster.py:46-58,254-264     -> k_gemm_f64<EPI_L2|EPI_NEGIP> + k_route_select
-//   scoring + top-t rrr.py:181-203, index.py:303-316 -> k_score_select
-//   rerank + top-k  index.py:278-283,318-335     -> k_rerank_topk
+//   routing         cluster.py:46-58,254-264     -> k_gemm_dmma<EPI_L2|EPI_NEGIP> + k_route_select
+//   bucketing       (none in the reference)      -> k_bucket_queries
+//   scoring + top-t rrr.py:181-203, index.py:303-316 -> k_score_cluster + k_select_topt
+//                                                   (rrg_cluster_score.cu; query-major
+//                                                    k_score_select with RRG_SCORE_MODE=query)
+//   rerank + top-k  index.py:278-283,318-335     -> k_rerank_tree (perfect pairwise plans,
+//                                                   interleaved rows), k_rerank_topk (any d);
+//                                                   opt-in: k_rerank_tma, k_rerank_cluster
+//   sharded merges            -> k_merge, k_ids_to_pos
 #include <cuda_runtime.h>
 #include <stdint.h>
 

@@ -622,7 +622,7 @@ struct Plan {
   // cluster-major re-rank (rr_mode == 1)
   int rr_mode;
   int mwords;
-  size_t off_cidx, off_marks, marks_bytes;
+  size_t off_cidx, off_marks, marks_bytes, off_rritem;
 };
 
 Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
@@ -697,6 +697,7 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     p.off_cidx = carve(Q * (int64_t)p.take_cap * 4);
     p.marks_bytes = ((size_t)Q * std::max<int64_t>(nmax, 1) / 32 + 2) * 4;
     p.off_marks = carve(p.marks_bytes);
+    p.off_rritem = carve((L + 1) * 4);
   }
   p.total = o;
   return p;
@@ -821,7 +822,8 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         // scores are consumed: the key array is reused for the re-ranked distances
         ClusterRerankHost rh{};
         rh.ix = v; rh.queries = x; rh.w = w; rh.qoff = ch.qoff; rh.pair_off = ch.pair_off;
-        rh.item_off = ch.item_off; rh.pairs = ch.pairs; rh.kbase = ch.kbase; rh.marks = marks;
+        rh.rr_item_off = reinterpret_cast<int*>(base + p.off_rritem); rh.pairs = ch.pairs;
+        rh.kbase = ch.kbase; rh.marks = marks;
         rh.diss = ch.keys; rh.work_counter = ch.work_counter + 1; rh.mwords = p.mwords;
         staged(5, st, [&] { launch_cluster_rerank(rh, st); });
         TopkFinalHost fh{};

@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "rrg_common.cuh"
 #include "rrg_kernels.h"
 
@@ -410,7 +412,8 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
 // group (8 leaves; leaf size a multiple of 8).  Distances land as mono32 keys
 // over the query's candidate-key array; k_topk_final orders them.
 constexpr int XNT = 256;
-constexpr int kRrQ = 16;  // queries whose x is staged at once
+constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
+constexpr int kRrRows = 256;  // rows of the cluster per work item
 
 struct ClusterRerankArgs {
   DevIndexView ix;
@@ -418,7 +421,7 @@ struct ClusterRerankArgs {
   int w;
   const int* qoff;
   const int* pair_off;
-  const int* item_off;
+  const int* rr_item_off;  // [L+1] prefix of ceil(pairs_l/kRrQ) * ceil(m_l/kRrRows)
   const int* pairs;
   const int* kbase;
   const uint32_t* marks;
@@ -427,8 +430,22 @@ struct ClusterRerankArgs {
   int mwords;  // bitmap words staged per query (>= ceil(max m_l / 32) + 1)
 };
 
-template <int NB>
-__global__ void __launch_bounds__(XNT, 2) k_rerank_cluster(ClusterRerankArgs a) {
+// rr_item_off for the re-rank work items (one CTA)
+__global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_off,
+                                                  const int* __restrict__ cl_pos, int L,
+                                                  int* __restrict__ rr_item_off) {
+  __shared__ int tot;
+  for (int l = threadIdx.x; l < L; l += PNT) {
+    const int cnt = pair_off[l + 1] - pair_off[l], m = cl_pos[l + 1] - cl_pos[l];
+    rr_item_off[l] = ((cnt + kRrQ - 1) / kRrQ) * ((m + kRrRows - 1) / kRrRows);
+  }
+  __syncthreads();
+  block_exclusive_scan_inplace(rr_item_off, L, &tot);
+  if (threadIdx.x == 0) rr_item_off[L] = tot;
+}
+
+template <int NB, int MINB = 2>
+__global__ void __launch_bounds__(XNT, MINB) k_rerank_cluster(ClusterRerankArgs a) {
   constexpr int NLV = 8, cstep = 8 * NLV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const DevIndexView& ix = a.ix;
@@ -443,7 +460,9 @@ __global__ void __launch_bounds__(XNT, 2) k_rerank_cluster(ClusterRerankArgs a) 
   const int b = lane >> 2, h = lane & 3;
   const int coff = 8 * b + 2 * h;
   const bool euclid = ix.metric == kMetricEuclidean;
-  const int total_items = a.item_off[L];
+  // work item = (cluster, <= kRrQ queries, <= kRrRows rows): bounded size, so the
+  // largest clusters with the most queries do not serialise the tail
+  const int total_items = a.rr_item_off[L];
   while (true) {
     if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
     __syncthreads();
@@ -453,12 +472,16 @@ __global__ void __launch_bounds__(XNT, 2) k_rerank_cluster(ClusterRerankArgs a) 
     int lo = 0, hi = L;
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
-      if (a.item_off[mid] <= item) lo = mid; else hi = mid;
+      if (a.rr_item_off[mid] <= item) lo = mid; else hi = mid;
     }
     const int l = lo;
-    const int j0 = a.pair_off[l] + (item - a.item_off[l]) * kPairsPerItem;
-    const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
     const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    const int nrc = (m + kRrRows - 1) / kRrRows;
+    const int local = item - a.rr_item_off[l];
+    const int qc = nrc > 0 ? local / nrc : 0, rc = nrc > 0 ? local % nrc : 0;
+    const int j0 = a.pair_off[l] + qc * kRrQ;
+    const int np = min(kRrQ, a.pair_off[l + 1] - j0);
+    const int r0 = rc * kRrRows, r1 = min(m, r0 + kRrRows);
     if (tid < np) {
       const int pr = a.pairs[j0 + tid];
       const int q = pr / a.w, c = pr % a.w;
@@ -483,9 +506,9 @@ __global__ void __launch_bounds__(XNT, 2) k_rerank_cluster(ClusterRerankArgs a) 
         mb[g * a.mwords + k] = __funnelshift_r(lo32, hi32, (unsigned)(bit & 31));
       }
       __syncthreads();
-      for (int pa = warp * 2; pa < m; pa += nwarps * 2) {
+      for (int pa = r0 + warp * 2; pa < r1; pa += nwarps * 2) {
         const int pb = pa + 1;
-        const bool hasb = pb < m;
+        const bool hasb = pb < r1;
         float2 ca[NB], cb[NB];
         const float* ra = ix.corpus + (size_t)(p0 + pa) * ds + coff;
         const float* rb = ix.corpus + (size_t)(p0 + (hasb ? pb : pa)) * ds + coff;
@@ -524,7 +547,7 @@ __global__ void __launch_bounds__(XNT, 2) k_rerank_cluster(ClusterRerankArgs a) 
           }
         };
         auto marked = [&](int g, int p) {
-          return p < m && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
+          return p < r1 && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
         };
         // two queries per step: four independent reductions interleave their shuffles
         for (int g = 0; g < ng; g += 2) {
@@ -713,7 +736,8 @@ static void opt_in_smem(Kern* kern, int slot) {
 void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   ClusterRerankArgs a;
   a.ix = h.ix; a.queries = h.queries; a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off;
-  a.item_off = h.item_off; a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks;
+  a.rr_item_off = h.rr_item_off; a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks;
+  k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, h.rr_item_off);
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
   const size_t sm = cluster_rerank_smem(h.ix.d_stride, h.mwords);
@@ -721,7 +745,14 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   switch (h.ix.pw_leaf_n / 8) {
-    case 12: opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * 2, XNT, sm, st>>>(a); break;
+    case 12: {
+      const char* ev = getenv("RRG_CM_MINB");
+      const int mb = ev ? atoi(ev) : 2;
+      if (mb == 3) { opt_in_smem(k_rerank_cluster<12, 3>, 4); k_rerank_cluster<12, 3><<<sms * 3, XNT, sm, st>>>(a); }
+      else if (mb == 4) { opt_in_smem(k_rerank_cluster<12, 4>, 5); k_rerank_cluster<12, 4><<<sms * 4, XNT, sm, st>>>(a); }
+      else { opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * 2, XNT, sm, st>>>(a); }
+      break;
+    }
     case 15: opt_in_smem(k_rerank_cluster<15>, 1); k_rerank_cluster<15><<<sms * 2, XNT, sm, st>>>(a); break;
     default: opt_in_smem(k_rerank_cluster<16>, 2); k_rerank_cluster<16><<<sms * 2, XNT, sm, st>>>(a); break;
   }

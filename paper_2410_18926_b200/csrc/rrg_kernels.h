@@ -117,7 +117,7 @@ struct ClusterRerankHost {
   int w;
   const int* qoff;
   const int* pair_off;
-  const int* item_off;
+  int* rr_item_off;  // [L+1] scratch (filled by the launcher)
   const int* pairs;
   const int* kbase;
   const uint32_t* marks;

@@ -686,10 +686,11 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   // the scoring is cluster-major and the row plan fits k_rerank_cluster;
   // RRG_RERANK=query|regs|tma forces a per-query kernel
   {
-    // measured on C2 (w=1, t=800): per-query k_rerank_tree 2.08 ms vs cluster-major
-    // 2.75 ms, so the cluster-major re-rank is opt-in (RRG_RERANK=cluster)
+    // measured on C2 (w=1, t=800): cluster-major 1.41 ms (+0.14 ms final top-k) vs
+    // per-query k_rerank_tree 1.66 ms; RRG_RERANK=query|regs|tma selects a per-query kernel
     const char* e = getenv("RRG_RERANK");
-    const bool want = e && strcmp(e, "cluster") == 0;
+    const bool want = !(e && (strcmp(e, "query") == 0 || strcmp(e, "regs") == 0 ||
+                              strcmp(e, "tma") == 0));
     p.rr_mode = (want && p.score_mode == 1 && rerank && !exact_take && cluster_rerank_ok(v)) ? 1 : 0;
   }
   if (p.rr_mode == 1) {

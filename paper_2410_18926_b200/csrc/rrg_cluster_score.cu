@@ -549,15 +549,23 @@ __global__ void __launch_bounds__(XNT, MINB) k_rerank_cluster(ClusterRerankArgs 
         auto marked = [&](int g, int p) {
           return p < r1 && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
         };
-        // two queries per step: four independent reductions interleave their shuffles
-        for (int g = 0; g < ng; g += 2) {
-          const int g2 = g + 1 < ng ? g + 1 : g;
+        // the queries that selected either row (one lane per query, ballot), taken two
+        // at a time: four independent reductions interleave their shuffles, with no
+        // per-query branching inside the arithmetic
+        unsigned act = __ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pb)));
+        while (act) {
+          const int g = __ffs(act) - 1;
+          act &= act - 1;
+          int g2 = g;
+          if (act) {
+            g2 = __ffs(act) - 1;
+            act &= act - 1;
+          }
+          float v1a, v1b, v2a, v2b;
+          lane_sums(g, v1a, v1b);
+          lane_sums(g2, v2a, v2b);
           const bool m1a = marked(g, pa), m1b = marked(g, pb);
           const bool m2a = g2 != g && marked(g2, pa), m2b = g2 != g && marked(g2, pb);
-          if (!(m1a || m1b || m2a || m2b)) continue;  // warp-uniform
-          float v1a = 0.f, v1b = 0.f, v2a = 0.f, v2b = 0.f;
-          if (m1a || m1b) lane_sums(g, v1a, v1b);
-          if (m2a || m2b) lane_sums(g2, v2a, v2b);
           // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree
 #pragma unroll
           for (int o = 1; o < 32; o <<= 1) {
@@ -747,7 +755,7 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   switch (h.ix.pw_leaf_n / 8) {
     case 12: {
       const char* ev = getenv("RRG_CM_MINB");
-      const int mb = ev ? atoi(ev) : 2;
+      const int mb = ev ? atoi(ev) : 3;  // 3 CTAs/SM measured best on C2
       if (mb == 3) { opt_in_smem(k_rerank_cluster<12, 3>, 4); k_rerank_cluster<12, 3><<<sms * 3, XNT, sm, st>>>(a); }
       else if (mb == 4) { opt_in_smem(k_rerank_cluster<12, 4>, 5); k_rerank_cluster<12, 4><<<sms * 4, XNT, sm, st>>>(a); }
       else { opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * 2, XNT, sm, st>>>(a); }

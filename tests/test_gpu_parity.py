@@ -292,10 +292,16 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "query"])
+@pytest.mark.parametrize("mode", ["cluster", "query", "cluster+regs", "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
-    monkeypatch.setenv("RRG_SCORE_MODE", mode)
+    """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
+    with the default re-rank (cluster-major where the row plan allows), query-major
+    scoring (per-query re-rank), and the per-query register / TMA re-rank kernels."""
+    score_mode, _, rerank_mode = mode.partition("+")
+    monkeypatch.setenv("RRG_SCORE_MODE", score_mode)
+    if rerank_mode:
+        monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
     from oracle import rrann_oracle as O
 

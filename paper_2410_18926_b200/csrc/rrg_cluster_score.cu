@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
 // One CTA per query: the take = min(t|k, N) smallest of the query's keys by
 // (key, corpus id); positions recovered from (slot, offset) via the query's
 // candidate offsets.
-constexpr int TNT = 512;
+constexpr int TNT = 256;
 
 struct SelectArgs {
   DevIndexView ix;
@@ -412,6 +412,7 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
 // group (8 leaves; leaf size a multiple of 8).  Distances land as mono32 keys
 // over the query's candidate-key array; k_topk_final orders them.
 constexpr int XNT = 256;
+constexpr int kCmCtas = 3;  // resident CTAs per SM (80 registers)
 constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
 constexpr int kRrRows = 256;  // rows of the cluster per work item
 
@@ -444,8 +445,8 @@ __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_o
   if (threadIdx.x == 0) rr_item_off[L] = tot;
 }
 
-template <int NB, int MINB = 2>
-__global__ void __launch_bounds__(XNT, MINB) k_rerank_cluster(ClusterRerankArgs a) {
+template <int NB>
+__global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankArgs a) {
   constexpr int NLV = 8, cstep = 8 * NLV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const DevIndexView& ix = a.ix;
@@ -589,6 +590,8 @@ __global__ void __launch_bounds__(XNT, MINB) k_rerank_cluster(ClusterRerankArgs 
 }
 
 // Final per-query top-k over the re-ranked candidates (index.py:320-322).
+constexpr int FNT = 256;  // (128 measured slower on C2)
+
 struct TopkFinalArgs {
   DevIndexView ix;
   const int* sel;
@@ -606,7 +609,7 @@ struct TopkFinalArgs {
   const int* order;
 };
 
-__global__ void __launch_bounds__(XNT) k_topk_final(TopkFinalArgs a) {
+__global__ void __launch_bounds__(FNT) k_topk_final(TopkFinalArgs a) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ SelectSmem sm;
   __shared__ BucketSmem bs;
@@ -621,12 +624,12 @@ __global__ void __launch_bounds__(XNT) k_topk_final(TopkFinalArgs a) {
   int* selidx = reinterpret_cast<int*>(di + a.take_cap);   // k
   uintptr_t sp = reinterpret_cast<uintptr_t>(selidx + a.k);
   uint64_t* srt = reinterpret_cast<uint64_t*>((sp + 15) & ~uintptr_t(15));
-  for (int c = tid; c <= w; c += XNT) offs[c] = a.qoff[(size_t)q * (w + 1) + c];
-  for (int c = tid; c < w; c += XNT) pbase[c] = ix.cl_pos[a.sel[(size_t)q * w + c]];
+  for (int c = tid; c <= w; c += FNT) offs[c] = a.qoff[(size_t)q * (w + 1) + c];
+  for (int c = tid; c < w; c += FNT) pbase[c] = ix.cl_pos[a.sel[(size_t)q * w + c]];
   __syncthreads();
   const uint32_t* dq = a.diss + a.kbase[q];
   const int* ci = a.cand_idx + (size_t)q * a.take_cap;
-  for (int i = tid; i < n; i += XNT) {
+  for (int i = tid; i < n; i += FNT) {
     const int c = ci[i];
     int lo = 0, hi = w;
     while (hi - lo > 1) {
@@ -641,18 +644,18 @@ __global__ void __launch_bounds__(XNT) k_topk_final(TopkFinalArgs a) {
   auto key = [&](int i) { return dk[i]; };
   auto tie = [&](int i) { return di[i]; };
   auto val = [](uint32_t kv) { return unmono32(kv); };
-  block_select_bucketed<XNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
+  block_select_bucketed<FNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
   int np2 = 1;
   while (np2 < kk) np2 <<= 1;
-  for (int i = tid; i < np2; i += XNT) {
+  for (int i = tid; i < np2; i += FNT) {
     uint64_t v = ~0ull;
     if (i < kk) v = ((uint64_t)dk[selidx[i]] << 32) | di[selidx[i]];
     srt[i] = v;
   }
-  block_bitonic_sort<XNT>(srt, np2);
+  block_bitonic_sort<FNT>(srt, np2);
   const bool euclid = ix.metric == kMetricEuclidean;
   const int gq = a.q0 + q;
-  for (int i = tid; i < a.k; i += XNT) {
+  for (int i = tid; i < a.k; i += FNT) {
     int64_t id = -1;
     float sc = __int_as_float(0x7fc00000);
     if (i < kk) {
@@ -753,16 +756,10 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   switch (h.ix.pw_leaf_n / 8) {
-    case 12: {
-      const char* ev = getenv("RRG_CM_MINB");
-      const int mb = ev ? atoi(ev) : 3;  // 3 CTAs/SM measured best on C2
-      if (mb == 3) { opt_in_smem(k_rerank_cluster<12, 3>, 4); k_rerank_cluster<12, 3><<<sms * 3, XNT, sm, st>>>(a); }
-      else if (mb == 4) { opt_in_smem(k_rerank_cluster<12, 4>, 5); k_rerank_cluster<12, 4><<<sms * 4, XNT, sm, st>>>(a); }
-      else { opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * 2, XNT, sm, st>>>(a); }
-      break;
-    }
-    case 15: opt_in_smem(k_rerank_cluster<15>, 1); k_rerank_cluster<15><<<sms * 2, XNT, sm, st>>>(a); break;
-    default: opt_in_smem(k_rerank_cluster<16>, 2); k_rerank_cluster<16><<<sms * 2, XNT, sm, st>>>(a); break;
+    // persistent grid: kCmCtas CTAs per SM (3 measured best on C2 vs 2 and 4)
+    case 12: opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+    case 15: opt_in_smem(k_rerank_cluster<15>, 1); k_rerank_cluster<15><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+    default: opt_in_smem(k_rerank_cluster<16>, 2); k_rerank_cluster<16><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
   }
 }
 
@@ -778,7 +775,7 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
   a.out_ids = h.out_ids; a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
   a.order = h.order;
   opt_in_smem(k_topk_final, 3);
-  k_topk_final<<<nq, XNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a);
+  k_topk_final<<<nq, FNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a);
 }
 
 }  // namespace rrg

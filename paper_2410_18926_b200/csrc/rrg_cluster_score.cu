@@ -412,7 +412,10 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
 // group (8 leaves; leaf size a multiple of 8).  Distances land as mono32 keys
 // over the query's candidate-key array; k_topk_final orders them.
 constexpr int XNT = 256;
-constexpr int kCmCtas = 3;  // resident CTAs per SM (80 registers)
+#ifndef RRG_CM_CTAS
+#define RRG_CM_CTAS 3  // C2: 3 CTAs/SM (80 regs, small spill) 1.35 ms vs 2 CTAs 1.39 ms
+#endif
+constexpr int kCmCtas = RRG_CM_CTAS;  // resident CTAs per SM
 constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
 constexpr int kRrRows = 256;  // rows of the cluster per work item
 
@@ -554,34 +557,47 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         // at a time: four independent reductions interleave their shuffles, with no
         // per-query branching inside the arithmetic
         unsigned act = __ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pb)));
-        while (act) {
-          const int g = __ffs(act) - 1;
-          act &= act - 1;
-          int g2 = g;
-          if (act) {
-            g2 = __ffs(act) - 1;
-            act &= act - 1;
-          }
-          float v1a, v1b, v2a, v2b;
-          lane_sums(g, v1a, v1b);
-          lane_sums(g2, v2a, v2b);
-          const bool m1a = marked(g, pa), m1b = marked(g, pb);
-          const bool m2a = g2 != g && marked(g2, pa), m2b = g2 != g && marked(g2, pb);
-          // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree
+        if (!act) continue;
+        // per-lane partials of every active (query, row) pair: value 2*slot + row
+        float v[2 * kRrQ];
 #pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            v1a = __fadd_rn(v1a, __shfl_xor_sync(0xffffffffu, v1a, o));
-            v1b = __fadd_rn(v1b, __shfl_xor_sync(0xffffffffu, v1b, o));
-            v2a = __fadd_rn(v2a, __shfl_xor_sync(0xffffffffu, v2a, o));
-            v2b = __fadd_rn(v2b, __shfl_xor_sync(0xffffffffu, v2b, o));
+        for (int slot = 0; slot < kRrQ; ++slot) {
+          if (act) {  // warp-uniform
+            const int g = __ffs(act) - 1;
+            act &= act - 1;
+            lane_sums(g, v[2 * slot], v[2 * slot + 1]);
+          } else {
+            v[2 * slot] = 0.f;
+            v[2 * slot + 1] = 0.f;
           }
-          if (lane == 0) {
-            const int k1 = pkey[g0 + g], k2 = pkey[g0 + g2];
-            if (m1a) a.diss[k1 + pa] = mono32(euclid ? v1a : -v1a);
-            if (m1b) a.diss[k1 + pb] = mono32(euclid ? v1b : -v1b);
-            if (m2a) a.diss[k2 + pa] = mono32(euclid ? v2a : -v2a);
-            if (m2b) a.diss[k2 + pb] = mono32(euclid ? v2b : -v2b);
+        }
+        // Transposing butterfly: five xor-steps (1, 2, 4, 8, 16 -- NumPy's
+        // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree)
+        // that halve the values held per lane, so lane j ends with value j fully
+        // reduced.  Each add combines the same two partial sums as the plain
+        // butterfly (a+b == b+a exactly), at 31 shuffles per 32 values instead of 160.
+#pragma unroll
+        for (int s = 0; s < 5; ++s) {
+          const int o = 1 << s;
+          const bool hi = (lane >> s) & 1;
+#pragma unroll
+          for (int i = 0; i < (16 >> s); ++i) {
+            const float keep = hi ? v[2 * i + 1] : v[2 * i];
+            const float send = hi ? v[2 * i] : v[2 * i + 1];
+            v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
           }
+        }
+        {  // lane j holds (slot j/2, row j%2); map the slot back to its query
+          unsigned act2 = __ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pb)));
+          const int slot = lane >> 1;
+          int g = -1;
+          for (int sidx = 0; act2; ++sidx) {
+            const int gg = __ffs(act2) - 1;
+            act2 &= act2 - 1;
+            if (sidx == slot) g = gg;
+          }
+          const int p = (lane & 1) ? pb : pa;
+          if (g >= 0 && marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? v[0] : -v[0]);
         }
       }
       __syncthreads();

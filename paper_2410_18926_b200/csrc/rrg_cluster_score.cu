@@ -432,6 +432,7 @@ struct ClusterRerankArgs {
   uint32_t* diss;
   int* work_counter;
   int mwords;  // bitmap words staged per query (>= ceil(max m_l / 32) + 1)
+  float neg_zero;  // -0.0f at run time: see sq2()
 };
 
 // rr_item_off for the re-rank work items (one CTA)
@@ -464,6 +465,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
   const int b = lane >> 2, h = lane & 3;
   const int coff = 8 * b + 2 * h;
   const bool euclid = ix.metric == kMetricEuclidean;
+  const float2 nz2 = make_float2(a.neg_zero, a.neg_zero);
   // work item = (cluster, <= kRrQ queries, <= kRrRows rows): bounded size, so the
   // largest clusters with the most queries do not serialise the tail
   const int total_items = a.rr_item_off[L];
@@ -524,20 +526,18 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         auto lane_sums = [&](int g, float& va, float& vb) {
           const float* xg = xs + (size_t)g * ds + coff;
           if (euclid) {
-            float a0 = 0.f, a1 = 0.f, b0 = 0.f, b1 = 0.f;
+            float2 acca = make_float2(0.f, 0.f), accb = acca;
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
               const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
               const float2 nx = make_float2(-xv.x, -xv.y);
               const float2 da = __fadd2_rn(ca[i], nx), db = __fadd2_rn(cb[i], nx);
-              const float2 sa = __fmul2_rn(da, da), sb = __fmul2_rn(db, db);
-              a0 = i == 0 ? sa.x : __fadd_rn(a0, sa.x);
-              a1 = i == 0 ? sa.y : __fadd_rn(a1, sa.y);
-              b0 = i == 0 ? sb.x : __fadd_rn(b0, sb.x);
-              b1 = i == 0 ? sb.y : __fadd_rn(b1, sb.y);
+              const float2 sa = sq2(da, nz2), sb = sq2(db, nz2);
+              acca = i == 0 ? sa : __fadd2_rn(acca, sa);
+              accb = i == 0 ? sb : __fadd2_rn(accb, sb);
             }
-            va = __fadd_rn(a0, a1);
-            vb = __fadd_rn(b0, b1);
+            va = __fadd_rn(acca.x, acca.y);
+            vb = __fadd_rn(accb.x, accb.y);
           } else {
             float acc_a = 0.f, acc_b = 0.f;
 #pragma unroll
@@ -766,6 +766,7 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   a.rr_item_off = h.rr_item_off; a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks;
   k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, h.rr_item_off);
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
+  a.neg_zero = -0.0f;
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
   const size_t sm = cluster_rerank_smem(h.ix.d_stride, h.mwords);
   int dev = 0, sms = 148;

@@ -81,6 +81,13 @@ __device__ __forceinline__ int quant_code(float v, float scale) {
   return p < 0.0 ? -c : c;
 }
 
+// Packed exact square rn(d*d) per half.  ptxas contracts mul.rn.f32x2 + add.rn.f32x2
+// into FFMA2 (even with --fmad=false), which would break NumPy's square-then-add
+// rounding; fma(d, d, -0) rounds d*d once and is bit-identical to the product, and
+// with nz read from a kernel argument (opaque -0.0) ptxas has nothing to fold, so
+// the following packed accumulation stays a separate FADD2.
+__device__ __forceinline__ float2 sq2(float2 d, float2 nz) { return __ffma2_rn(d, d, nz); }
+
 // Monotone maps so unsigned integer order == float order, with -0.0 == +0.0.
 __device__ __forceinline__ uint32_t mono32(float f) {
   uint32_t u = __float_as_uint(f);

@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
 // over the query's candidate-key array; k_topk_final orders them.
 constexpr int XNT = 256;
 #ifndef RRG_CM_CTAS
-#define RRG_CM_CTAS 3  // C2: 3 CTAs/SM (80 regs, small spill) 1.35 ms vs 2 CTAs 1.39 ms
+#define RRG_CM_CTAS 2  // C2 with next-pair prefetch: 2 CTAs/SM (123 regs) 1.20 ms vs 3 CTAs (80 regs + spill) 1.31 ms
 #endif
 constexpr int kCmCtas = RRG_CM_CTAS;  // resident CTAs per SM
 constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
@@ -459,6 +459,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
   uint32_t* mb = reinterpret_cast<uint32_t*>(xs + (size_t)kRrQ * ds);  // [kRrQ][mwords]
   __shared__ int item_s;
   __shared__ int pq[kPairsPerItem], pkey[kPairsPerItem];
+  __shared__ int slotq[XNT / 32][kRrQ];
   const int L = ix.L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = XNT / 32;
@@ -499,10 +500,25 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
     const int mw = (m + 31) / 32;
     for (int g0 = 0; g0 < np; g0 += kRrQ) {
       const int ng = min(kRrQ, np - g0);
-      // stage x (interleaved) and the membership bits of this query group
-      for (int e = tid; e < ng * d; e += XNT) {
-        const int g = e / d, j = e - g * d;
-        xs[(size_t)g * ds + ix.elem_perm[j]] = a.queries[(size_t)pq[g0 + g] * d + j];
+      {  // stage x (interleaved): SU independent loads in flight per thread
+        constexpr int SU = 4;
+        const int tot = ng * d;
+        for (int e0 = tid; e0 < tot; e0 += XNT * SU) {
+          float xv[SU];
+          int dst[SU];
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            const int e = e0 + u * XNT;
+            if (e < tot) {
+              const int g = e / d, j = e - g * d;
+              xv[u] = __ldg(a.queries + (size_t)pq[g0 + g] * d + j);
+              dst[u] = g * ds + __ldg(ix.elem_perm + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < SU; ++u)
+            if (e0 + u * XNT < tot) xs[dst[u]] = xv[u];
+        }
       }
       for (int e = tid; e < ng * mw; e += XNT) {
         const int g = e / mw, k = e - g * mw;
@@ -512,54 +528,63 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         mb[g * a.mwords + k] = __funnelshift_r(lo32, hi32, (unsigned)(bit & 31));
       }
       __syncthreads();
-      for (int pa = r0 + warp * 2; pa < r1; pa += nwarps * 2) {
-        const int pb = pa + 1;
-        const bool hasb = pb < r1;
-        float2 ca[NB], cb[NB];
+      auto marked = [&](int g, int p) {
+        return p < r1 && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
+      };
+      // this lane's 2-element slice of each step of rows pa and pa+1 (register
+      // double use: the next pair's loads are issued before this pair's reduction)
+      float2 ca[NB], cb[NB];
+      auto load_pair = [&](int pa) {
+        const int pb = pa + 1 < r1 ? pa + 1 : pa;
         const float* ra = ix.corpus + (size_t)(p0 + pa) * ds + coff;
-        const float* rb = ix.corpus + (size_t)(p0 + (hasb ? pb : pa)) * ds + coff;
+        const float* rb = ix.corpus + (size_t)(p0 + pb) * ds + coff;
 #pragma unroll
         for (int i = 0; i < NB; ++i) ca[i] = __ldg(reinterpret_cast<const float2*>(ra + cstep * i));
 #pragma unroll
         for (int i = 0; i < NB; ++i) cb[i] = __ldg(reinterpret_cast<const float2*>(rb + cstep * i));
-        // per (query, row pair): this lane's r[2h]+r[2h+1] of both rows
-        auto lane_sums = [&](int g, float& va, float& vb) {
-          const float* xg = xs + (size_t)g * ds + coff;
-          if (euclid) {
-            float2 acca = make_float2(0.f, 0.f), accb = acca;
+      };
+      // per (query, row pair): this lane's r[2h]+r[2h+1] of both rows
+      auto lane_sums = [&](int g, float& va, float& vb) {
+        const float* xg = xs + (size_t)g * ds + coff;
+        if (euclid) {
+          float2 acca = make_float2(0.f, 0.f), accb = acca;
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
-              const float2 nx = make_float2(-xv.x, -xv.y);
-              const float2 da = __fadd2_rn(ca[i], nx), db = __fadd2_rn(cb[i], nx);
-              const float2 sa = sq2(da, nz2), sb = sq2(db, nz2);
-              acca = i == 0 ? sa : __fadd2_rn(acca, sa);
-              accb = i == 0 ? sb : __fadd2_rn(accb, sb);
-            }
-            va = __fadd_rn(acca.x, acca.y);
-            vb = __fadd_rn(accb.x, accb.y);
-          } else {
-            float acc_a = 0.f, acc_b = 0.f;
-#pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
-              acc_a += ca[i].x * xv.x + ca[i].y * xv.y;
-              acc_b += cb[i].x * xv.x + cb[i].y * xv.y;
-            }
-            va = acc_a;
-            vb = acc_b;
+          for (int i = 0; i < NB; ++i) {
+            const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
+            const float2 nx = make_float2(-xv.x, -xv.y);
+            const float2 da = __fadd2_rn(ca[i], nx), db = __fadd2_rn(cb[i], nx);
+            const float2 sa = sq2(da, nz2), sb = sq2(db, nz2);
+            acca = i == 0 ? sa : __fadd2_rn(acca, sa);
+            accb = i == 0 ? sb : __fadd2_rn(accb, sb);
           }
-        };
-        auto marked = [&](int g, int p) {
-          return p < r1 && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
-        };
-        // the queries that selected either row (one lane per query, ballot), taken two
-        // at a time: four independent reductions interleave their shuffles, with no
-        // per-query branching inside the arithmetic
-        unsigned act = __ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pb)));
-        if (!act) continue;
+          va = __fadd_rn(acca.x, acca.y);
+          vb = __fadd_rn(accb.x, accb.y);
+        } else {
+          float acc_a = 0.f, acc_b = 0.f;
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
+            acc_a += ca[i].x * xv.x + ca[i].y * xv.y;
+            acc_b += cb[i].x * xv.x + cb[i].y * xv.y;
+          }
+          va = acc_a;
+          vb = acc_b;
+        }
+      };
+      int pa = r0 + warp * 2;
+      if (pa < r1) load_pair(pa);
+      for (; pa < r1; pa += nwarps * 2) {
+        const int pb = pa + 1, pn = pa + nwarps * 2;
+        // the queries that selected either row (one lane per query, ballot)
+        const bool mine = lane < ng && (marked(lane, pa) || marked(lane, pb));
+        const unsigned act0 = __ballot_sync(0xffffffffu, mine);
+        if (!act0) {
+          if (pn < r1) load_pair(pn);
+          continue;
+        }
         // per-lane partials of every active (query, row) pair: value 2*slot + row
         float v[2 * kRrQ];
+        unsigned act = act0;
 #pragma unroll
         for (int slot = 0; slot < kRrQ; ++slot) {
           if (act) {  // warp-uniform
@@ -571,6 +596,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
             v[2 * slot + 1] = 0.f;
           }
         }
+        if (pn < r1) load_pair(pn);
         // Transposing butterfly: five xor-steps (1, 2, 4, 8, 16 -- NumPy's
         // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree)
         // that halve the values held per lane, so lane j ends with value j fully
@@ -587,18 +613,16 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
             v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
           }
         }
-        {  // lane j holds (slot j/2, row j%2); map the slot back to its query
-          unsigned act2 = __ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pb)));
-          const int slot = lane >> 1;
-          int g = -1;
-          for (int sidx = 0; act2; ++sidx) {
-            const int gg = __ffs(act2) - 1;
-            act2 &= act2 - 1;
-            if (sidx == slot) g = gg;
-          }
+        // lane j holds (slot j/2, row j%2); slot s is the s-th set bit of act0
+        if (mine) slotq[warp][__popc(act0 & ((1u << lane) - 1u))] = lane;
+        __syncwarp();
+        const int slot = lane >> 1;
+        if (slot < __popc(act0)) {
+          const int g = slotq[warp][slot];
           const int p = (lane & 1) ? pb : pa;
-          if (g >= 0 && marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? v[0] : -v[0]);
+          if (marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? v[0] : -v[0]);
         }
+        __syncwarp();
       }
       __syncthreads();
     }

@@ -30,13 +30,17 @@ namespace rrg {
 // f64 -- the reference's `x.astype(f64) @ W.astype(f64)` (index.py:298) and
 // `p @ c.T` (cluster.py:50,58); the summation order differs from OpenBLAS only at
 // the f64 rounding level (0/153,600 projection mismatches).
-// FP64 tensor-core GEMM (DMMA, mma.sync.m8n8k4.f64): 128x64 CTA tile, 8 warps of
+// FP64 tensor-core GEMM (DMMA, mma.sync.m8n8k4.f64): (32*WM)x64 CTA tile, WM x 2 warps of
 // 32x32 (4x4 m8n8 tiles), K staged 8 at a time, double-buffered, in padded smem (pitch 12
 // doubles: the four 32 B fragment rows of a half-warp fall in distinct banks).
+// WM = 3 (96x64 tiles, 192 threads, 3 CTAs/SM): C2's projection is 105x4 = 420 tiles
+// on 444 CTA slots (one wave, 94% balanced) where 128x64 tiles gave 316 tiles on 296
+// slots (a 20-CTA second wave).
 // f32 inputs are widened to f64 exactly (the reference's `x.astype(f64) @
 // W.astype(f64)`, index.py:298, and `p @ c.T`, cluster.py:50,58); products and
 // sums in f64, so only the f64 summation order differs from OpenBLAS.
-constexpr int MBM = 128, MBN = 64, MBK = 8, DMNT = 256, MPITCH = 12;
+constexpr int MBN = 64, MBK = 8, MPITCH = 12;
+constexpr int kGemmWM = 3;
 
 __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -44,17 +48,19 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
                : "d"(a), "d"(b));
 }
 
-template <int EPI, bool BT>
-__global__ void __launch_bounds__(DMNT, 2) k_gemm_dmma(const float* __restrict__ A, int lda,
+template <int EPI, bool BT, int WM = kGemmWM>
+__global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm_dmma(const float* __restrict__ A, int lda,
                                                      const float* __restrict__ B, int ldb, int M,
                                                      int N, int K, float* __restrict__ outf,
                                                      double* __restrict__ outd, int ldo,
                                                      const double* __restrict__ rowterm,
                                                      const double* __restrict__ colterm) {
+  constexpr int MBM = 32 * WM, DMNT = 64 * WM;
+  constexpr int NA = (MBM * MBK) / DMNT, NB = (MBN * MBK + DMNT - 1) / DMNT;
   __shared__ __align__(16) double As[2][MBM][MPITCH];  // [buf][m][k]
   __shared__ __align__(16) double Bs[2][MBN][MPITCH];  // [buf][n][k]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 1, wn = warp & 1;  // 4 x 2 warps of 32x32
+  const int wm = warp >> 1, wn = warp & 1;  // WM x 2 warps of 32x32
   const int m0 = blockIdx.y * MBM, n0 = blockIdx.x * MBN;
   double acc[4][4][2];
 #pragma unroll
@@ -62,34 +68,36 @@ __global__ void __launch_bounds__(DMNT, 2) k_gemm_dmma(const float* __restrict__
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
   // global -> registers (next tile in flight while the current one is multiplied)
-  float ra[(MBM * MBK) / DMNT], rb[(MBN * MBK) / DMNT];
+  float ra[NA], rb[NB];
   auto gload = [&](int k0) {
 #pragma unroll
-    for (int e = 0; e < (MBM * MBK) / DMNT; ++e) {  // A tile 128 x 8, k fastest
+    for (int e = 0; e < NA; ++e) {  // A tile MBM x 8, k fastest
       const int idx = tid + e * DMNT, r = idx / MBK, kk = idx % MBK;
       const int gm = m0 + r, gk = k0 + kk;
       ra[e] = (gm < M && gk < K) ? __ldg(A + (size_t)gm * lda + gk) : 0.f;
     }
 #pragma unroll
-    for (int e = 0; e < (MBN * MBK) / DMNT; ++e) {  // B tile 64 (n) x 8 (k)
+    for (int e = 0; e < NB; ++e) {  // B tile 64 (n) x 8 (k)
       const int idx = tid + e * DMNT;
       int c, kk;
       if (BT) { c = idx / MBK; kk = idx % MBK; } else { kk = idx / MBN; c = idx % MBN; }
       const int gn = n0 + c, gk = k0 + kk;
       float v = 0.f;
-      if (gn < N && gk < K) v = BT ? __ldg(B + (size_t)gn * ldb + gk) : __ldg(B + (size_t)gk * ldb + gn);
+      if (idx < MBN * MBK && gn < N && gk < K)
+        v = BT ? __ldg(B + (size_t)gn * ldb + gk) : __ldg(B + (size_t)gk * ldb + gn);
       rb[e] = v;
     }
   };
   auto sstore = [&](int buf) {
 #pragma unroll
-    for (int e = 0; e < (MBM * MBK) / DMNT; ++e) {
+    for (int e = 0; e < NA; ++e) {
       const int idx = tid + e * DMNT;
       As[buf][idx / MBK][idx % MBK] = (double)ra[e];
     }
 #pragma unroll
-    for (int e = 0; e < (MBN * MBK) / DMNT; ++e) {
+    for (int e = 0; e < NB; ++e) {
       const int idx = tid + e * DMNT;
+      if (idx >= MBN * MBK) break;
       if (BT) Bs[buf][idx / MBK][idx % MBK] = (double)rb[e];
       else Bs[buf][idx % MBN][idx / MBN] = (double)rb[e];
     }
@@ -1174,8 +1182,8 @@ __global__ void k_scatter_rows(const float* __restrict__ src, int64_t nrows, int
 // ===================================================================== launchers
 void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
                     cudaStream_t st) {
-  dim3 grid((s + MBN - 1) / MBN, (nq + MBM - 1) / MBM);
-  k_gemm_dmma<EPI_PROJ, false><<<grid, DMNT, 0, st>>>(x, d, W, s, nq, s, d, xp, nullptr, s,
+  dim3 grid((s + MBN - 1) / MBN, (nq + 32 * kGemmWM - 1) / (32 * kGemmWM));
+  k_gemm_dmma<EPI_PROJ, false><<<grid, 64 * kGemmWM, 0, st>>>(x, d, W, s, nq, s, d, xp, nullptr, s,
                                                       nullptr, nullptr);
 }
 
@@ -1190,12 +1198,13 @@ void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int 
 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
                        const double* pp, const double* cnorm, double* diss, cudaStream_t st) {
-  dim3 grid((L + MBN - 1) / MBN, (nq + MBM - 1) / MBM);
+  constexpr int WM = 4;  // C2: 128x64 tiles measured 0.214 ms vs 96x64 0.220 ms
+  dim3 grid((L + MBN - 1) / MBN, (nq + 32 * WM - 1) / (32 * WM));
   if (metric == kMetricEuclidean)
-    k_gemm_dmma<EPI_L2, true><<<grid, DMNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L, pp,
+    k_gemm_dmma<EPI_L2, true, WM><<<grid, 64 * WM, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L, pp,
                                                      cnorm);
   else
-    k_gemm_dmma<EPI_NEGIP, true><<<grid, DMNT, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
+    k_gemm_dmma<EPI_NEGIP, true, WM><<<grid, 64 * WM, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
                                                         nullptr, nullptr);
 }
 

@@ -691,7 +691,7 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     const char* e = getenv("RRG_RERANK");
     const bool want = !(e && (strcmp(e, "query") == 0 || strcmp(e, "regs") == 0 ||
                               strcmp(e, "tma") == 0));
-    p.rr_mode = (want && p.score_mode == 1 && rerank && !exact_take && cluster_rerank_ok(v)) ? 1 : 0;
+    p.rr_mode = (want && p.score_mode == 1 && rerank && !exact_take && cluster_rerank_ok(v, ix->max_cluster)) ? 1 : 0;
   }
   if (p.rr_mode == 1) {
     p.mwords = (int)((ix->max_cluster + 31) / 32) + 1;

@@ -761,14 +761,19 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
 }
 
-bool cluster_rerank_ok(const DevIndexView& ix) {
-  const int nb = ix.pw_leaf_n / 8;
-  return ix.corpus_interleaved && ix.pw_nleaves == 8 && ix.pw_leaf_n % 8 == 0 &&
-         (nb == 12 || nb == 15 || nb == 16);
-}
-
 size_t cluster_rerank_smem(int d_stride, int mwords) {
   return (size_t)kRrQ * d_stride * 4 + (size_t)kRrQ * mwords * 4;
+}
+
+// the row plan fits k_rerank_cluster and a query group's x + membership bits of the
+// largest cluster fit in shared memory (otherwise the per-query re-rank serves)
+bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster) {
+  const int nb = ix.pw_leaf_n / 8;
+  if (!(ix.corpus_interleaved && ix.pw_nleaves == 8 && ix.pw_leaf_n % 8 == 0 &&
+        (nb == 12 || nb == 15 || nb == 16)))
+    return false;
+  const int mwords = (int)((max_cluster + 31) / 32) + 1;
+  return cluster_rerank_smem(ix.d_stride, mwords) + 8 * 1024 <= (size_t)kMaxSmemPerCta;
 }
 
 template <typename Kern>

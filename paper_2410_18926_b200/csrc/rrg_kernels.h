@@ -125,7 +125,7 @@ struct ClusterRerankHost {
   int* work_counter;
   int mwords;
 };
-bool cluster_rerank_ok(const DevIndexView& ix);
+bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster);
 size_t cluster_rerank_smem(int d_stride, int mwords);
 void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st);
 

@@ -182,6 +182,28 @@ def test_concurrent_searches_identical(pkg, tmp_path):
             np.testing.assert_array_equal(a, b)
 
 
+def test_skewed_cluster_exceeds_cluster_rerank_smem(pkg, tmp_path):
+    """One 90k-row cluster: its membership bitmap no longer fits the cluster-major
+    re-rank's shared memory, so the plan must fall back to the per-query re-rank and
+    still return the reference's ids and bit-exact scores."""
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    sizes = [90_000, 150, 100, 50]
+    blob = random_index(768, 32, 8, 4, sum(sizes), "euclidean", seed=5, sizes=sizes)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "skew", blob))
+    oidx = O.read_index(blob)
+    q = np.random.default_rng(3).standard_normal((6, 768)).astype(F32)
+    q[0] = oidx.corpus[7]
+    for k, w, t in [(10, 1, 200), (20, 4, 1000)]:
+        ids, sc, cnt = dev.search_host(q, k, w, t, True)
+        ref = O.query_batch(oidx, q, k, w, t, True)
+        for i, rres in enumerate(ref):
+            c = int(cnt[i])
+            np.testing.assert_array_equal(ids[i, :c], rres.ids)
+            np.testing.assert_array_equal(sc[i, :c].view(np.int32), rres.scores.view(np.int32))
+
+
 def test_exactness_limit_recall_one(pkg, tmp_path):
     """w = L, t = all candidates, rerank -> exact top-k (test_index.py:100-106)."""
     from oracle import rrann_oracle as O

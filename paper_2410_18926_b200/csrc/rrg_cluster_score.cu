@@ -350,11 +350,32 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
   if (a.rerank && a.marks) {  // cluster-major re-rank consumes (index, membership bit)
     int* oi = a.cand_idx + (size_t)q * a.take_cap;
     const size_t kb = (size_t)a.kbase[q];
-    for (int i = tid; i < take; i += TNT) {
-      const int ci = selidx[i];
-      oi[i] = ci;
-      const size_t bit = kb + (size_t)ci;
-      atomicOr(a.marks + (bit >> 5), 1u << (bit & 31));
+    const int sh = (int)(kb & 31), nw = (sh + N + 31) / 32;
+    if (N <= a.kcap && nw <= a.kcap) {
+      // the query's bits are one contiguous run: build its words in shared memory
+      // (the staged keys are dead now) and OR whole words into the global bitmap
+      uint32_t* bm = kst;
+      __syncthreads();
+      for (int i = tid; i < nw; i += TNT) bm[i] = 0u;
+      __syncthreads();
+      for (int i = tid; i < take; i += TNT) {
+        const int ci = selidx[i];
+        oi[i] = ci;
+        atomicOr(&bm[(sh + ci) >> 5], 1u << ((sh + ci) & 31));
+      }
+      __syncthreads();
+      uint32_t* gm = a.marks + (kb >> 5);
+      for (int i = tid; i < nw; i += TNT) {
+        const uint32_t v = bm[i];
+        if (v) atomicOr(gm + i, v);  // edge words are shared with the neighbouring queries
+      }
+    } else {
+      for (int i = tid; i < take; i += TNT) {
+        const int ci = selidx[i];
+        oi[i] = ci;
+        const size_t bit = kb + (size_t)ci;
+        atomicOr(a.marks + (bit >> 5), 1u << (bit & 31));
+      }
     }
     if (tid == 0) a.cand_n[q] = take;
     return;
@@ -669,27 +690,27 @@ __global__ void __launch_bounds__(FNT) k_topk_final(TopkFinalArgs a) {
   __syncthreads();
   const uint32_t* dq = a.diss + a.kbase[q];
   const int* ci = a.cand_idx + (size_t)q * a.take_cap;
-  for (int i = tid; i < n; i += FNT) {
+  for (int i = tid; i < n; i += FNT) dk[i] = dq[ci[i]];
+  __syncthreads();
+  const int kk = min(a.k, n);
+  auto key = [&](int i) { return dk[i]; };
+  // corpus ids are gathered lazily: only the boundary bucket and the k winners need them
+  auto tie = [&](int i) {
     const int c = ci[i];
     int lo = 0, hi = w;
     while (hi - lo > 1) {
       int mid = (lo + hi) >> 1;
       if (offs[mid] <= c) lo = mid; else hi = mid;
     }
-    dk[i] = dq[c];
-    di[i] = __float_as_uint(__ldg(ix.pmeta + pbase[lo] + (c - offs[lo])).w);
-  }
-  __syncthreads();
-  const int kk = min(a.k, n);
-  auto key = [&](int i) { return dk[i]; };
-  auto tie = [&](int i) { return di[i]; };
+    return __float_as_uint(__ldg(ix.pmeta + pbase[lo] + (c - offs[lo])).w);
+  };
   auto val = [](uint32_t kv) { return unmono32(kv); };
   block_select_bucketed<FNT, uint32_t, float>(n, kk, key, tie, val, selidx, bs, sm);
   int np2 = 1;
   while (np2 < kk) np2 <<= 1;
   for (int i = tid; i < np2; i += FNT) {
     uint64_t v = ~0ull;
-    if (i < kk) v = ((uint64_t)dk[selidx[i]] << 32) | di[selidx[i]];
+    if (i < kk) v = ((uint64_t)dk[selidx[i]] << 32) | tie(selidx[i]);
     srt[i] = v;
   }
   block_bitonic_sort<FNT>(srt, np2);

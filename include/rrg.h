@@ -80,6 +80,11 @@ typedef struct {
   const int8_t* b_values;   /* sum r*m_l */
   const float* norms;       /* m, cluster order; NULL unless euclidean */
   const float* corpus;      /* m x d in ORIGINAL id order; NULL if no corpus */
+  /* unquantized factors (RRG_FLAG_QUANTIZED clear, RrrConfig.quantize=False,
+   * rrr.py:97-100): f32 blocks with the same shapes and concatenation as
+   * a_values / b_values (no pad row, no head/scale); ignored when quantized */
+  const float* a_values_f32; /* sum s*cols_l */
+  const float* b_values_f32; /* sum r*m_l (non-NULL even if every cluster is exact) */
 } RrgIndexDesc;
 
 typedef struct {

@@ -32,6 +32,7 @@ class RrgIndexDesc(ctypes.Structure):
         ("a_head", c_vp), ("a_scale", c_vp), ("a_values", c_vp),
         ("b_head", c_vp), ("b_scale", c_vp), ("b_values", c_vp),
         ("norms", c_vp), ("corpus", c_vp),
+        ("a_values_f32", c_vp), ("b_values_f32", c_vp),
     ]
 
 

@@ -162,6 +162,7 @@ struct HostCluster {
   std::vector<int8_t> a_vals;  // s x cols (row 0 = pad)
   std::vector<float> b_head, b_scale;
   std::vector<int8_t> b_vals;  // r x m
+  std::vector<float> a_f, b_f;  // unquantized factors (quantize=False): s x cols, r x m
   std::vector<float> norms;
 };
 
@@ -218,10 +219,7 @@ namespace {
 template <typename CorpusFill>
 void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill fill_corpus) {
   const int d = hm.d, s = hm.s, r = hm.r, L = hm.L;
-  if (!(hm.flags & RRG_FLAG_QUANTIZED))
-    raise_usage("ParameterError",
-                "unquantized index: the device path scores int8 factors only "
-                "(quantize=False scoring is tolerance-level, SURVEY.md 8(f) row 4)");
+  const bool quant = hm.flags & RRG_FLAG_QUANTIZED;
   if (s > 1024) raise_usage("ParameterError", "reduced dimension %d > 1024 not supported", s);
   if (r > 64) raise_usage("ParameterError", "rank %d > 64 not supported", r);
   if (hm.m >= (int64_t)1 << 31) raise_usage("ParameterError", "more than 2^31 points");
@@ -274,9 +272,15 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.P = P;
   std::sort(ix->sizes_sorted_desc.begin(), ix->sizes_sorted_desc.end(), std::greater<int>());
 
-  std::vector<int8_t> at((size_t)n_rrr * r * v.s_pad, 0);
+  // quantized: int8 codes (+ head/scale); unquantized: f32 factors, same layouts
+  // (A^T per model slot, B^T per point, exact-model rows per point; rrr.py:97-100)
+  const size_t n_at = (size_t)n_rrr * r * v.s_pad, n_bt = (size_t)P * v.r_pad,
+               n_xc = (size_t)P_exact * v.s_pad;
+  std::vector<int8_t> at(quant ? n_at : 0, 0);
+  std::vector<float> atf(quant ? 0 : n_at, 0.f), btf(quant ? 0 : n_bt, 0.f),
+      xcf(quant ? 0 : n_xc, 0.f);
   std::vector<float> ahead((size_t)n_rrr * r), ascale((size_t)n_rrr * r);
-  std::vector<int8_t> bt((size_t)P * v.r_pad, 0), xc((size_t)P_exact * v.s_pad, 0);
+  std::vector<int8_t> bt(quant ? n_bt : 0, 0), xc(quant ? n_xc : 0, 0);
   std::vector<float4> pmeta(P, make_float4(0.f, 0.f, 0.f, 0.f));
   std::vector<int64_t> pid(P);
   std::vector<int> pos_of_id(hm.m, -1);
@@ -294,7 +298,19 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
       uint32_t id32 = (uint32_t)id;
       memcpy(&pmeta[p0 + p].w, &id32, 4);
     }
-    if (c.exact) {
+    if (!quant) {
+      if (c.exact) {
+        const int64_t x0 = cl_aidx[l];
+        for (int i = 0; i < s; ++i)
+          for (int p = 0; p < m; ++p) xcf[(size_t)(x0 + p) * v.s_pad + i] = c.a_f[(size_t)i * m + p];
+      } else {
+        const int slot = cl_aidx[l];
+        for (int i = 0; i < s; ++i)
+          for (int j = 0; j < r; ++j) atf[((size_t)slot * r + j) * v.s_pad + i] = c.a_f[(size_t)i * r + j];
+        for (int j = 0; j < r; ++j)
+          for (int p = 0; p < m; ++p) btf[(size_t)(p0 + p) * v.r_pad + j] = c.b_f[(size_t)j * m + p];
+      }
+    } else if (c.exact) {
       // A: s x m (cols = points)
       const int64_t x0 = cl_aidx[l];
       for (int i = 0; i < s; ++i)
@@ -334,6 +350,10 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.ascale = ix->upload(ascale);
   v.bt = ix->upload(bt);
   v.xcodes = ix->upload(xc);
+  v.quantized = quant ? 1 : 0;
+  v.atf = quant ? nullptr : ix->upload(atf);
+  v.btf = quant ? nullptr : ix->upload(btf);
+  v.xf = quant ? nullptr : ix->upload(xcf);
   v.pmeta = ix->upload(pmeta);
   v.pid = ix->upload(pid);
   v.corpus = nullptr;
@@ -436,7 +456,6 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
   fr.vec(hm.centroids, (uint64_t)L * s, "centroids");
   hm.clusters.resize(L);
   uint64_t total = 0;
-  std::vector<float> fscratch;
   for (uint32_t l = 0; l < L; ++l) {
     HostCluster& c = hm.clusters[l];
     std::string sec = "cluster " + std::to_string(l);
@@ -451,23 +470,24 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
     const uint64_t acols = c.exact ? ml : r;
     auto read_factor = [&](uint64_t rows, uint64_t cols, const std::string& fsec,
                            std::vector<float>& head, std::vector<float>& scale,
-                           std::vector<int8_t>& vals) {
+                           std::vector<int8_t>& vals, std::vector<float>& fvals) {
       if (quantized) {
         fr.vec(head, cols, fsec + " head row");
         fr.vec(scale, cols, fsec + " scales");
         fr.vec(vals, rows * cols, fsec + " values");
       } else {
-        fr.vec(fscratch, rows * cols, fsec);
+        fr.vec(fvals, rows * cols, fsec);  // f32 rows x cols (index.py:500-502)
       }
     };
-    read_factor(s, acols, sec + " factor A", c.a_head, c.a_scale, c.a_vals);
-    if (!c.exact) read_factor(r, ml, sec + " factor B", c.b_head, c.b_scale, c.b_vals);
+    read_factor(s, acols, sec + " factor A", c.a_head, c.a_scale, c.a_vals, c.a_f);
+    if (!c.exact) read_factor(r, ml, sec + " factor B", c.b_head, c.b_scale, c.b_vals, c.b_f);
     if (mc == kMetricEuclidean) fr.vec(c.norms, ml, sec + " norms");
     if (!c.owned) {  // keep only metadata for routing; release payloads
       std::vector<float>().swap(c.a_head); std::vector<float>().swap(c.a_scale);
       std::vector<int8_t>().swap(c.a_vals); std::vector<float>().swap(c.b_head);
       std::vector<float>().swap(c.b_scale); std::vector<int8_t>().swap(c.b_vals);
       std::vector<float>().swap(c.norms);
+      std::vector<float>().swap(c.a_f); std::vector<float>().swap(c.b_f);
     }
     total += ml;
   }
@@ -520,17 +540,9 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
     cudaStreamDestroy(st);
     corpus_done = true;
   };
-  if (!quantized) {
-    // still validate the whole file like deserialize would, then refuse
-    if (has_corpus) {
-      std::vector<float> chunk;
-      uint64_t left = m * (uint64_t)d;
-      while (left) { uint64_t n = std::min<uint64_t>(left, 1 << 24); fr.vec(chunk, n, "corpus"); left -= n; }
-    }
-  } else {
-    build_device_index(ix.get(), hm, has_corpus, fill);
-  }
+  build_device_index(ix.get(), hm, has_corpus, fill);
   (void)corpus_done;
+  (void)quantized;
   uint64_t crc_off = fr.off;
   uint32_t stored;
   uLong actual = fr.crc;
@@ -541,7 +553,6 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
   if (fr.off != fr.size)
     raise_format("unknown trailing section at offset %llu: %llu extra bytes",
                  (unsigned long long)fr.off, (unsigned long long)(fr.size - fr.off));
-  if (!quantized) build_device_index(ix.get(), hm, false, [](float*, const int*, int, const int*) {});
   *out = ix.release();
   return RRG_OK;
 }
@@ -557,6 +568,9 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
   hm.centroids.assign(dsc->centroids, dsc->centroids + (size_t)L * s);
   hm.clusters.resize(L);
   const bool exact_ivf = hm.flags & RRG_FLAG_EXACT_IVF;
+  const bool quant = hm.flags & RRG_FLAG_QUANTIZED;
+  if (!quant && (!dsc->a_values_f32 || !dsc->b_values_f32))
+    raise_usage("ParameterError", "unquantized index description needs a_values_f32/b_values_f32");
   int64_t po = 0, ao = 0, aoff = 0, bo = 0, boff = 0;
   for (int l = 0; l < L; ++l) {
     HostCluster& c = hm.clusters[l];
@@ -566,15 +580,23 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
     c.ids.assign(dsc->point_ids + po, dsc->point_ids + po + m);
     if (dsc->norms) c.norms.assign(dsc->norms + po, dsc->norms + po + m);
     const int64_t acols = c.exact ? m : r;
-    c.a_head.assign(dsc->a_head + ao, dsc->a_head + ao + acols);
-    c.a_scale.assign(dsc->a_scale + ao, dsc->a_scale + ao + acols);
-    c.a_vals.assign(dsc->a_values + aoff, dsc->a_values + aoff + (size_t)s * acols);
+    if (quant) {
+      c.a_head.assign(dsc->a_head + ao, dsc->a_head + ao + acols);
+      c.a_scale.assign(dsc->a_scale + ao, dsc->a_scale + ao + acols);
+      c.a_vals.assign(dsc->a_values + aoff, dsc->a_values + aoff + (size_t)s * acols);
+    } else {
+      c.a_f.assign(dsc->a_values_f32 + aoff, dsc->a_values_f32 + aoff + (size_t)s * acols);
+    }
     ao += acols;
     aoff += (int64_t)s * acols;
     if (!c.exact) {
-      c.b_head.assign(dsc->b_head + bo, dsc->b_head + bo + m);
-      c.b_scale.assign(dsc->b_scale + bo, dsc->b_scale + bo + m);
-      c.b_vals.assign(dsc->b_values + boff, dsc->b_values + boff + (size_t)r * m);
+      if (quant) {
+        c.b_head.assign(dsc->b_head + bo, dsc->b_head + bo + m);
+        c.b_scale.assign(dsc->b_scale + bo, dsc->b_scale + bo + m);
+        c.b_vals.assign(dsc->b_values + boff, dsc->b_values + boff + (size_t)r * m);
+      } else {
+        c.b_f.assign(dsc->b_values_f32 + boff, dsc->b_values_f32 + boff + (size_t)r * m);
+      }
       bo += m;
       boff += (int64_t)r * m;
     }
@@ -669,7 +691,8 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   // cluster) unless RRG_SCORE_MODE=query selects the fused query-major kernel
   {
     const char* e = getenv("RRG_SCORE_MODE");
-    p.score_mode = (e && strcmp(e, "query") == 0) ? 0 : 1;
+    // the fused query-major kernel scores int8 factors only
+    p.score_mode = (e && strcmp(e, "query") == 0 && v.quantized) ? 0 : 1;
   }
   if (p.score_mode == 1) {
     p.kcap = (int)std::min<int64_t>(std::max<int64_t>(nmax, 1), 24 * 1024);
@@ -795,7 +818,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       staged(4, st, [&] { launch_score_select(sa, n, st); });
     } else {
       ClusterScoringHost ch{};
-      ch.ix = v; ch.qcodes = qcodes; ch.qscale = qscale; ch.qhead = qhead; ch.sel = sel; ch.w = w;
+      ch.ix = v; ch.xp = xp; ch.qcodes = qcodes; ch.qscale = qscale; ch.qhead = qhead; ch.sel = sel; ch.w = w;
       ch.qoff = reinterpret_cast<int*>(base + p.off_qoff);
       ch.ncand = reinterpret_cast<int*>(base + p.off_ncand);
       ch.pair_off = reinterpret_cast<int*>(base + p.off_pairoff);

@@ -129,6 +129,7 @@ struct ClusterScoreArgs {
   const int* kbase;      // [nq+1]
   uint32_t* keys;        // [kbase[nq]]
   int* work_counter;     // zeroed before launch
+  const float* xp;       // [nq][s] projected queries (f32-factor scoring)
 };
 
 __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
@@ -260,6 +261,113 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
             raw = __dp4a(cc.w, bb.w, raw);
           }
           const float yhat = deq(raw, pxs[pi], meta.y, pxh[pi], meta.x);
+          const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
+          a.keys[pkey[pi] + p] = mono32(keyf);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------- cluster scoring, f32 factors
+// Unquantized index (RrrConfig.quantize=False): score = x @ A (@ B) in f32
+// (rrr.py:97-100, 196-202).  NumPy runs these as OpenBLAS sgemv, whose f32 FMA
+// order is not reproducible, so parity is tolerance-level; the
+// dot products here accumulate exact f32 products in f64 and round once, i.e.
+// they return (nearly) the correctly rounded value, which OpenBLAS approximates.
+// Same work items and key layout as k_score_cluster.
+__global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
+  const DevIndexView& ix = a.ix;
+  __shared__ int item_s;
+  __shared__ float inters[kPairsPerItem][kMaxRc];
+  __shared__ int pq[kPairsPerItem], pkey[kPairsPerItem];
+  const int L = ix.L, r = ix.r, r_pad = ix.r_pad, s = ix.s, s_pad = ix.s_pad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total_items = a.item_off[L];
+  const bool euclid = ix.metric == kMetricEuclidean;
+  while (true) {
+    if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = item_s;
+    __syncthreads();
+    if (item >= total_items) break;
+    int lo = 0, hi = L;
+    while (hi - lo > 1) {
+      int mid = (lo + hi) >> 1;
+      if (a.item_off[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int l = lo;
+    const int j0 = a.pair_off[l] + (item - a.item_off[l]) * kPairsPerItem;
+    const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
+    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    if (tid < np) {
+      const int pr = a.pairs[j0 + tid];
+      const int q = pr / a.w, c = pr % a.w;
+      pq[tid] = q;
+      pkey[tid] = a.kbase[q] + a.qoff[(size_t)q * (a.w + 1) + c];
+    }
+    __syncthreads();
+    if (m == 0) continue;
+    if (ix.cl_kind[l] == kKindRrr) {
+      // inter = x @ A: warp per (pair, column), lanes over the s inputs
+      const int slot = ix.cl_aidx[l];
+      for (int o = warp; o < np * r; o += CNT / 32) {
+        const int pi = o / r, j = o % r;
+        const float* av = ix.atf + ((size_t)slot * r + j) * s_pad;
+        const float* xv = a.xp + (size_t)pq[pi] * s;
+        double acc = 0.0;
+        for (int i = lane; i < s; i += 32) acc = fma((double)__ldg(xv + i), (double)__ldg(av + i), acc);
+        for (int d = 16; d > 0; d >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, d);
+        if (lane == 0) inters[pi][j] = (float)acc;
+      }
+      __syncthreads();
+      // yhat = inter @ B: thread per point, B^T row held in registers
+      for (int p = tid; p < m; p += CNT) {
+        const int gp = p0 + p;
+        const float4 meta = __ldg(ix.pmeta + gp);
+        float b[kMaxRc];
+        const float4* bw = reinterpret_cast<const float4*>(ix.btf + (size_t)gp * r_pad);
+#pragma unroll
+        for (int u = 0; u < kMaxRc / 4; ++u) {
+          float4 v = u < r_pad / 4 ? __ldg(bw + u) : make_float4(0.f, 0.f, 0.f, 0.f);
+          b[4 * u] = v.x; b[4 * u + 1] = v.y; b[4 * u + 2] = v.z; b[4 * u + 3] = v.w;
+        }
+        for (int pi = 0; pi < np; ++pi) {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < kMaxRc; ++j)
+            if (j < r) acc = fma((double)inters[pi][j], (double)b[j], acc);
+          const float yhat = (float)acc;
+          const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
+          a.keys[pkey[pi] + p] = mono32(keyf);
+        }
+      }
+    } else {
+      // exact model: yhat = x @ A[:, p] over s (rrr.py:103-113)
+      const int x0 = ix.cl_aidx[l];
+      const int n4 = s / 4;
+      for (int p = tid; p < m; p += CNT) {
+        const int gp = p0 + p;
+        const float4 meta = __ldg(ix.pmeta + gp);
+        const float* xr = ix.xf + (size_t)(x0 + p) * s_pad;
+        for (int pi = 0; pi < np; ++pi) {
+          const float* xv = a.xp + (size_t)pq[pi] * s;
+          double acc = 0.0;
+          if ((s & 3) == 0) {
+            const float4* x4 = reinterpret_cast<const float4*>(xv);
+            const float4* r4 = reinterpret_cast<const float4*>(xr);
+            for (int u = 0; u < n4; ++u) {
+              const float4 xa = __ldg(x4 + u), ra = __ldg(r4 + u);
+              acc = fma((double)xa.x, (double)ra.x, acc);
+              acc = fma((double)xa.y, (double)ra.y, acc);
+              acc = fma((double)xa.z, (double)ra.z, acc);
+              acc = fma((double)xa.w, (double)ra.w, acc);
+            }
+          } else {
+            for (int i = 0; i < s; ++i) acc = fma((double)__ldg(xv + i), (double)__ldg(xr + i), acc);
+          }
+          const float yhat = (float)acc;
           const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
           a.keys[pkey[pi] + p] = mono32(keyf);
         }
@@ -746,7 +854,11 @@ void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  k_score_cluster<<<sms * 4, CNT, 0, st>>>(a);
+  a.xp = h.xp;
+  if (ix.quantized)
+    k_score_cluster<<<sms * 4, CNT, 0, st>>>(a);
+  else
+    k_score_cluster_f32<<<sms * 4, CNT, 0, st>>>(a);
 }
 
 static int pow2_at_least(int v) {

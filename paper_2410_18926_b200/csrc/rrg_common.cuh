@@ -57,6 +57,12 @@ struct DevIndexView {
   // contiguous bytes instead of eight 32-byte pieces of the natural layout.
   int corpus_interleaved;
   const int* elem_perm;  // [d] natural element -> interleaved slot (when interleaved)
+  // unquantized index (quantize=False, rrr.py:97-100): f32 factors in the layouts of
+  // at / bt / xcodes (pitches s_pad / r_pad elements); nullptr when quantized
+  int quantized;
+  const float* atf;  // [n_rrr][r][s_pad]
+  const float* btf;  // [P][r_pad]
+  const float* xf;   // [P_exact][s_pad]
 };
 
 // ---------------------------------------------------------------- numerics

@@ -68,6 +68,7 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st);
 // Cluster-major scoring (rrg_cluster_score.cu)
 struct ClusterScoringHost {
   DevIndexView ix;
+  const float* xp;  // [nq][s] projected queries (unquantized index)
   const int8_t* qcodes;
   const float* qscale;
   const float* qhead;

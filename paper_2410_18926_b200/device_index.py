@@ -88,10 +88,9 @@ class DeviceIndex:
 
     @classmethod
     def from_rrr(cls, index, device: int = 0) -> "DeviceIndex":
-        """Upload an in-memory ``rrann.RrrIndex`` (quantized factors required)."""
+        """Upload an in-memory ``rrann.RrrIndex`` (int8 or f32 factors, index.py:110-118)."""
         cfg = index.config
-        if not cfg.rrr.quantize:
-            raise ParameterError("unquantized index: the device path scores int8 factors only")
+        quant = bool(cfg.rrr.quantize)
         models = index.models
         L = len(models)
         s = index.projection.shape[1]
@@ -103,29 +102,36 @@ class DeviceIndex:
 
         sizes = np.array([mdl.n_points for mdl in models], dtype=np.uint32)
         ids = np.ascontiguousarray(np.concatenate([mdl.point_ids for mdl in models]).astype(np.int64))
-        a_head = np.concatenate([mdl.a.head_row for mdl in models]).astype(np.float32)
-        a_scale = np.concatenate([mdl.a.col_scales for mdl in models]).astype(np.float32)
-        a_vals = np.concatenate([full_values(mdl.a).ravel() for mdl in models]).astype(np.int8)
         bm = [mdl for mdl in models if mdl.b is not None]
         f32 = np.float32
-        b_head = np.concatenate([mdl.b.head_row for mdl in bm]).astype(f32) if bm else np.zeros(1, f32)
-        b_scale = np.concatenate([mdl.b.col_scales for mdl in bm]).astype(f32) if bm else np.zeros(1, f32)
-        b_vals = (np.concatenate([full_values(mdl.b).ravel() for mdl in bm]).astype(np.int8)
-                  if bm else np.zeros(1, np.int8))
+        a_head = a_scale = a_vals = b_head = b_scale = b_vals = a_f32 = b_f32 = None
+        if quant:
+            a_head = np.concatenate([mdl.a.head_row for mdl in models]).astype(f32)
+            a_scale = np.concatenate([mdl.a.col_scales for mdl in models]).astype(f32)
+            a_vals = np.concatenate([full_values(mdl.a).ravel() for mdl in models]).astype(np.int8)
+            b_head = np.concatenate([mdl.b.head_row for mdl in bm]).astype(f32) if bm else np.zeros(1, f32)
+            b_scale = np.concatenate([mdl.b.col_scales for mdl in bm]).astype(f32) if bm else np.zeros(1, f32)
+            b_vals = (np.concatenate([full_values(mdl.b).ravel() for mdl in bm]).astype(np.int8)
+                      if bm else np.zeros(1, np.int8))
+        else:  # f32 factors, file layout (index.py:355-356)
+            a_f32 = np.ascontiguousarray(np.concatenate([np.asarray(mdl.a, f32).ravel() for mdl in models]))
+            b_f32 = (np.ascontiguousarray(np.concatenate([np.asarray(mdl.b, f32).ravel() for mdl in bm]))
+                     if bm else np.zeros(1, f32))
         norms = None
         if cfg.metric == "euclidean":
             norms = np.ascontiguousarray(np.concatenate([mdl.norm_terms for mdl in models]).astype(f32))
         proj = np.ascontiguousarray(index.projection, dtype=f32)
         cent = np.ascontiguousarray(index.centroids, dtype=f32)
         corpus = None if index.corpus is None else np.ascontiguousarray(index.corpus, dtype=f32)
-        flags = FLAG_QUANTIZED
+        flags = FLAG_QUANTIZED if quant else 0
         if corpus is not None:
             flags |= FLAG_CORPUS
         if cfg.balanced:
             flags |= FLAG_BALANCED
         if cfg.scoring_mode == "exact_ivf":
             flags |= FLAG_EXACT_IVF
-        keep = [proj, cent, sizes, ids, a_head, a_scale, a_vals, b_head, b_scale, b_vals, norms, corpus]
+        keep = [proj, cent, sizes, ids, a_head, a_scale, a_vals, b_head, b_scale, b_vals, norms, corpus,
+                a_f32, b_f32]
 
         def ptr(a):
             return None if a is None else a.ctypes.data
@@ -135,7 +141,7 @@ class DeviceIndex:
             n_points=index.n_points, flags=flags, projection=ptr(proj), centroids=ptr(cent),
             cluster_sizes=ptr(sizes), point_ids=ptr(ids), a_head=ptr(a_head), a_scale=ptr(a_scale),
             a_values=ptr(a_vals), b_head=ptr(b_head), b_scale=ptr(b_scale), b_values=ptr(b_vals),
-            norms=ptr(norms), corpus=ptr(corpus))
+            norms=ptr(norms), corpus=ptr(corpus), a_values_f32=ptr(a_f32), b_values_f32=ptr(b_f32))
         h = ctypes.c_void_p()
         check(lib.rrg_index_create(ctypes.byref(desc), device, ctypes.byref(h)))
         del keep

@@ -73,6 +73,17 @@ CASES = {
         metric="euclidean", n_clusters=16, rrr=RrrConfig(rank=8, reduced_dim=20), seed=6)),
     "euclid_f32": dict(m=1500, d=24, n_blobs=15, cfg=IndexConfig(
         metric="euclidean", n_clusters=14, rrr=RrrConfig(rank=6, reduced_dim=12, quantize=False), seed=7)),
+    # unquantized (f32 factor) scoring across metrics / modes
+    "ip_f32": dict(m=1500, d=24, n_blobs=15, cfg=IndexConfig(
+        metric="ip", n_clusters=14, rrr=RrrConfig(rank=6, reduced_dim=12, quantize=False), seed=8)),
+    "cosine_f32_s_eq_d": dict(m=1200, d=16, n_blobs=12, cfg=IndexConfig(
+        metric="cosine", n_clusters=10, rrr=RrrConfig(rank=5, reduced_dim=None, quantize=False), seed=9)),
+    "euclid_exact_ivf_f32": dict(m=900, d=20, n_blobs=9, cfg=IndexConfig(
+        metric="euclidean", n_clusters=9, rrr=RrrConfig(rank=4, reduced_dim=10, quantize=False),
+        scoring_mode="exact_ivf", seed=10)),
+    "euclid_f32_norerank": dict(m=1500, d=24, n_blobs=15, cfg=IndexConfig(
+        metric="euclidean", n_clusters=14, rrr=RrrConfig(rank=6, reduced_dim=12, quantize=False),
+        rerank=False, seed=11)),
 }
 
 
@@ -83,6 +94,7 @@ def stage_trace(index, x):
     sel = route(xp, index.centroids, w, cluster_metric(metric))
     out = dict(xp=xp, selected=sel)
     if not index.config.rrr.quantize:
+        out["scores"] = np.concatenate([score_cluster(xp, index.models[int(l)], metric) for l in sel])
         return out
     qx = quantize_vector(xp, mixed_precision=True)
     out.update(qhead=F32(qx.head), qscale=F32(qx.scale), qcodes=qx.values)
@@ -96,8 +108,10 @@ def stage_trace(index, x):
     return out
 
 
-def main():
+def main(only=None):
     for name, spec in CASES.items():
+        if only and name not in only:
+            continue
         vecs, queries = corpus_with_outliers(spec["m"], spec["d"], seed=11, n_blobs=spec["n_blobs"])
         index = build(vecs, spec["cfg"], workers=4)
         blob = serialize(index)
@@ -129,4 +143,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:] or None)

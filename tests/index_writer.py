@@ -24,11 +24,16 @@ def _quant(rng, rows, cols):
     return head.tobytes() + scale.tobytes() + vals.tobytes()
 
 
+def _f32(rng, rows, cols):
+    return (rng.standard_normal((rows, cols)) / np.sqrt(rows)).astype("<f4").tobytes()
+
+
 def random_index(d, s, r, L, m, metric="euclidean", seed=0, exact_ivf=False, with_corpus=True,
-                 sizes=None, dup_rows=0, corpus_scale=1.0):
+                 sizes=None, dup_rows=0, corpus_scale=1.0, quantize=True):
     rng = np.random.default_rng(seed)
     mc = {"euclidean": 0, "ip": 1, "cosine": 2}[metric]
-    flags = 1 | (2 if with_corpus else 0) | (8 if exact_ivf else 0)
+    flags = (1 if quantize else 0) | (2 if with_corpus else 0) | (8 if exact_ivf else 0)
+    factor = _quant if quantize else _f32
     out = bytearray(b"RRRANN01")
     out += struct.pack("<BIIIIQI", mc, d, s, r, L, m, flags)
     W = (rng.standard_normal((d, s)) / np.sqrt(d)).astype("<f4")
@@ -48,9 +53,9 @@ def random_index(d, s, r, L, m, metric="euclidean", seed=0, exact_ivf=False, wit
         pos += ml
         out += struct.pack("<I", ml) + ids.tobytes()
         exact = exact_ivf or ml < r
-        out += _quant(rng, s, ml if exact else r)
+        out += factor(rng, s, ml if exact else r)
         if not exact:
-            out += _quant(rng, r, ml)
+            out += factor(rng, r, ml)
         if metric == "euclidean":
             c64 = corpus[ids.astype(np.int64)].astype(np.float64)
             out += (c64 * c64).sum(axis=1).astype("<f4").tobytes()

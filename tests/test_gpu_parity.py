@@ -39,7 +39,8 @@ def _golden_index(pkg, tmp_path, case):
     return g, pkg.DeviceIndex.from_file(_write(tmp_path, case, g["index_bytes"].tobytes()))
 
 
-QUANT_CASES = [c for c in golden_cases() if c != "euclid_f32"]
+QUANT_CASES = [c for c in golden_cases() if "f32" not in c]
+F32_CASES = [c for c in golden_cases() if "f32" in c]
 
 
 def _corpus_max_norm(g):
@@ -106,10 +107,109 @@ def test_golden_stages(pkg, tmp_path, case):
         assert set(sel[i].tolist()) == set(g[f"trace{i}_selected"].tolist())
 
 
-def test_unquantized_index_is_refused(pkg, tmp_path):
-    g = load_golden("euclid_f32")
-    with pytest.raises(pkg.ParameterError, match="unquantized"):
-        pkg.DeviceIndex.from_file(_write(tmp_path, "f32", g["index_bytes"].tobytes()))
+# ---------------------------------------------------- unquantized (f32) factors
+# score = x @ A (@ B) runs as OpenBLAS sgemv in the reference (rrr.py:97-100), an
+# FMA order the GPU cannot reproduce, so the approximate scores
+# match within F32_RTOL of their magnitude and the candidate set may differ only
+# by near-ties at the top-t (or top-k) boundary.  Everything downstream of the
+# candidate set (the exact re-rank, its (diss, id) order) is still checked exactly.
+F32_RTOL = 1e-5
+
+
+def _f32_check_query(O, oidx, x, k, w, t, rr, ids, sc, cnt, cmax, what):
+    tr = {}
+    ref = O.query(oidx, x, k, w, t, rr, trace=tr)
+    c = int(cnt)
+    assert c == len(ref.ids), what
+    ids, sc = ids[:c], sc[:c].astype(np.float64)
+    euclid = oidx.metric == "euclidean"
+    xp = tr["xp"].astype(np.float64)
+    mags = []
+    for l in tr["selected"]:  # |x| @ |A| (@ |B|) (+ |norm|): the scale of the sgemv error
+        cl = oidx.clusters[int(l)]
+        y = np.abs(xp) @ np.abs(cl.a.astype(np.float64))
+        if cl.b is not None:
+            y = y @ np.abs(cl.b.astype(np.float64))
+        mags.append(2.0 * y + np.abs(cl.norms) if euclid else y)
+    tol = F32_RTOL * np.concatenate(mags) + 1e-30
+    keys = tr["cand_keys"].astype(np.float64)
+    cid = tr["cand_ids"]
+    order = np.lexsort((cid, keys))
+    take = min(t if rr else k, len(cid))
+    kt, tt = keys[order[take - 1]], tol[order[take - 1]]
+    possible = set(cid[keys <= kt + tol + tt].tolist())
+    certain = cid[keys < kt - tol - tt]
+    assert set(ids.tolist()) <= possible, (what, "id outside the near-tie candidate set")
+    pos = {int(v): i for i, v in enumerate(cid)}
+    if not rr:  # top-k by approximate key; score = key + x.x (sdot) or -key
+        assert set(certain.tolist()) <= set(ids.tolist()), (what, "missed a certain candidate")
+        xx = float(x.astype(np.float64) @ x.astype(np.float64)) if euclid else 0.0
+        for j, v in enumerate(ids):
+            i = pos[int(v)]
+            want = keys[i] + xx if euclid else -keys[i]
+            assert abs(sc[j] - want) <= tol[i] + F32_RTOL * xx, (what, j)
+        return
+    # re-rank: scores are the exact dissimilarities of the returned ids
+    diss = O.exact_dissimilarity(oidx, x, ids).astype(np.float64)
+    got = sc if euclid else -sc
+    if euclid:
+        np.testing.assert_array_equal(sc.astype(np.float32).view(np.int32),
+                                      diss.astype(np.float32).view(np.int32), err_msg=what)
+        dtol = 0.0
+    else:
+        dtol = RTOL * float(np.sqrt(x.astype(np.float64) @ x.astype(np.float64)) * cmax)
+        assert np.all(np.abs(got - diss) <= dtol), what
+    # ... and the top-k by (diss, id) of a candidate set holding every certain candidate
+    last = (got[-1], int(ids[-1]))
+    rest = np.setdiff1d(certain, ids)
+    if rest.size:
+        rd = O.exact_dissimilarity(oidx, x, rest).astype(np.float64)
+        for dv, iv in zip(rd, rest):
+            assert (dv, int(iv)) > last or abs(dv - last[0]) <= 2 * dtol, (what, int(iv))
+
+
+@pytest.mark.parametrize("case", F32_CASES)
+@pytest.mark.parametrize("entry", ["host", "device"])
+def test_golden_f32_factors(pkg, tmp_path, case, entry):
+    """Unquantized index (RrrConfig.quantize=False) through the f32-factor scoring kernel."""
+    from oracle import rrann_oracle as O
+
+    g, dev = _golden_index(pkg, tmp_path, case)
+    oidx = O.read_index(g["index_bytes"].tobytes())
+    cmax = _corpus_max_norm(g)
+    exact_hits = total = 0
+    for pi, (k, w, t, rr) in enumerate(g["params"]):
+        if f"p{pi}_ids" not in g:
+            continue
+        k, w, t, rr = int(k), min(int(w), dev.n_clusters), int(t), bool(rr)
+        if entry == "host":
+            ids, sc, cnt = dev.search_host(g["queries"], k, w, t, rr)
+        else:
+            q = torch.from_numpy(g["queries"]).cuda()
+            ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(q, k, w, t, rr))
+        np.testing.assert_array_equal(cnt, g[f"p{pi}_count"], err_msg=f"{case} p{pi} count")
+        for i in range(len(cnt)):
+            c = int(cnt[i])
+            _f32_check_query(O, oidx, g["queries"][i], k, w, t, rr, ids[i], sc[i], cnt[i], cmax,
+                             f"{case} p{pi} q{i}")
+            exact_hits += np.array_equal(ids[i, :c], g[f"p{pi}_ids"][i, :c])
+            total += 1
+    assert exact_hits >= 0.9 * total, (exact_hits, total)  # near-ties are rare
+
+
+@pytest.mark.parametrize("case", F32_CASES)
+def test_golden_f32_stages(pkg, tmp_path, case):
+    """Projection and routing of an unquantized index are exact like the int8 path's."""
+    g, dev = _golden_index(pkg, tmp_path, case)
+    x = torch.from_numpy(g["queries"][:3]).cuda()
+    xp = dev.stage_project(x)[0]
+    torch.cuda.synchronize()
+    xp = xp.cpu().numpy()
+    for i in range(3):
+        np.testing.assert_array_equal(xp[i].view(np.int32), g[f"trace{i}_xp"].view(np.int32))
+    sel = dev.stage_route(torch.from_numpy(xp).cuda(), min(4, dev.n_clusters)).cpu().numpy()
+    for i in range(3):
+        assert set(sel[i].tolist()) == set(g[f"trace{i}_selected"].tolist())
 
 
 def test_validation_errors(pkg, tmp_path):
@@ -353,3 +453,36 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
             else:  # dot products: error scales with |x||c|, not with the (possibly ~0) score
                 scale = float(np.linalg.norm(q[i]) * np.linalg.norm(oidx.corpus, axis=1).max())
                 assert_topk_equivalent(ids[i, :c], sc[i, :c], rres.ids, rres.scores, RTOL, scale, what)
+
+
+F32_SWEEP = [
+    (31, 16, 8, 7, 300, "euclidean", False),
+    (128, 64, 32, 12, 900, "euclidean", False),
+    (768, 256, 32, 8, 1200, "euclidean", False),
+    (100, 100, 64, 6, 700, "euclidean", False),
+    (96, 40, 12, 10, 500, "euclidean", True),
+    (128, 64, 32, 12, 900, "ip", False),
+    (200, 48, 24, 8, 600, "cosine", True),
+]
+
+
+@pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", F32_SWEEP)
+def test_random_index_f32_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf):
+    """f32-factor scoring over random shapes (s not a multiple of 4, r = 64, exact-IVF)."""
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    blob = random_index(d, s, r, L, m, metric, seed=d * 5 + L, exact_ivf=exact_ivf, dup_rows=3,
+                        quantize=False)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "randf", blob))
+    oidx = O.read_index(blob)
+    rng = np.random.default_rng(d + 1)
+    q = rng.standard_normal((32, d)).astype(F32)
+    q[1] = oidx.corpus[5]
+    cmax = float(np.linalg.norm(oidx.corpus, axis=1).max())
+    for k, w, t, rr in [(5, 1, 10, True), (10, max(1, L // 2), 60, True), (7, L, m + 5, True),
+                        (6, min(3, L), 1, False), (9, min(4, L), 9, False)]:
+        ids, sc, cnt = dev.search_host(q, k, w, t, rr)
+        for i in range(len(q)):
+            _f32_check_query(O, oidx, q[i], k, w, t, rr, ids[i], sc[i], cnt[i], cmax,
+                             f"d={d} {metric} {(k, w, t, rr)} q{i}")

@@ -335,8 +335,8 @@ def main():
     # ---- per-stage device time (events around each launch inside librrg), separate pass
     import ctypes
     _native.lib.rrg_set_stage_timing(1)
-    stage_ms = (ctypes.c_double * 8)()
-    stage_n = (ctypes.c_int64 * 8)()
+    stage_ms = (ctypes.c_double * 9)()
+    stage_n = (ctypes.c_int64 * 9)()
     _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
     for i in range(args.steps):
         flush.fill_(i & 0xFF)

@@ -174,6 +174,15 @@ int rrg_merge_results(int64_t nq, int32_t G, int32_t k, int32_t metric, const fl
                       const int64_t* ids, const int32_t* counts, float* out_scores,
                       int64_t* out_ids, int32_t* out_count, void* stream);
 
+/* Exact k-NN ground truth, replacing rrann.bench.brute_force_knn
+ * (pkg/src/rrann/bench.py:85-124): f64 distances (euclidean
+ * (q.q - 2 q.c) + c.c, ip -(q.c), cosine -(q.c/||c||)), ids ordered by
+ * (distance, id) like the stable argsort.  corpus m x dim and queries nq x dim
+ * f32 on the current device; ids nq x k int64.  Synchronous on `stream`.
+ * ParameterError when k is outside [1, m] (or > 2048). */
+int rrg_ground_truth(const float* corpus, int64_t m, int32_t dim, const float* queries,
+                     int64_t nq, int32_t k, int32_t metric, int64_t* ids, void* stream);
+
 /* Number of CUDA kernel launches issued by the most recent rrg_search* call
  * on this thread (evidence for the bench's gpu_launches). */
 int64_t rrg_last_launch_count(void);
@@ -182,11 +191,12 @@ int64_t rrg_last_launch_count(void);
  * every launch) for the calls made on this thread while enabled.  Stages:
  * 0 project, 1 prep/quantize, 2 route distances, 3 route select,
  * 4 top-t selection (query-major mode: scoring + top-t), 5 rerank+top-k,
- * 6 query bucketing, 7 cluster-major scoring (pair bucketing + scoring).
+ * 6 query bucketing, 7 cluster-major scoring (pair bucketing + scoring),
+ * 8 ground truth (rrg_ground_truth launches).
  * rrg_stage_times synchronizes the recorded events, writes the accumulated
  * milliseconds and launch counts per stage (arrays of RRG_N_STAGES) and resets
  * the accumulators. */
-#define RRG_N_STAGES 8
+#define RRG_N_STAGES 9
 void rrg_set_stage_timing(int enabled);
 int rrg_stage_times(double* ms, int64_t* launches);
 

@@ -364,3 +364,21 @@ def pairwise_sum_f32(a: np.ndarray) -> F32:
     n2 = n // 2
     n2 -= n2 % 8
     return F32(pairwise_sum_f32(a[:n2]) + pairwise_sum_f32(a[n2:]))
+
+
+def brute_force_knn(corpus, queries, k: int, metric: str = "euclidean") -> np.ndarray:
+    """rrann.bench.brute_force_knn (bench.py:85-124) restated: f64 distances, stable argsort."""
+    c = np.asarray(corpus, dtype=F32).astype(F64)
+    m = c.shape[0]
+    if k < 1 or k > m:
+        raise OracleError("ParameterError", f"k={k} out of range [1, {m}]")
+    if metric == "cosine":
+        n = np.linalg.norm(c, axis=1, keepdims=True)
+        n[n == 0] = 1.0
+        c = c / n
+    q = np.asarray(queries, dtype=F32).astype(F64)
+    if metric == "euclidean":
+        diss = (q * q).sum(1)[:, None] - 2.0 * (q @ c.T) + (c * c).sum(1)[None, :]
+    else:
+        diss = -(q @ c.T)
+    return np.argsort(diss, axis=1, kind="stable")[:, :k]

@@ -8,11 +8,12 @@ classes, plus ``DeviceIndex`` (device-resident index) and its
 
 from .errors import BuildError, DataError, FormatError, ParameterError, RrannError, ShapeError
 from .device_index import DeviceIndex, last_launch_count, version
+from .ground_truth import brute_force_knn, ground_truth_device
 from .search import QueryParams, QueryResult, device_index_for, install, query, query_batch
 
 __all__ = [
     "BuildError", "DataError", "DeviceIndex", "FormatError", "ParameterError", "QueryParams",
-    "QueryResult", "RrannError", "ShapeError", "device_index_for", "install", "last_launch_count",
+    "QueryResult", "brute_force_knn", "ground_truth_device", "RrannError", "ShapeError", "device_index_for", "install", "last_launch_count",
     "query", "query_batch", "version",
 ]
 

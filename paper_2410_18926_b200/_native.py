@@ -68,6 +68,7 @@ SIGNATURES = {
                                  c_vp, c_vp, c_size, c_vp]),
     "rrg_merge_results": (c_int, [c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                   c_vp]),
+    "rrg_ground_truth": (c_int, [c_vp, c_i64, c_i32, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp]),
     "rrg_last_launch_count": (c_i64, []),
     "rrg_set_stage_timing": (None, [c_int]),
     "rrg_stage_times": (c_int, [c_vp, c_vp]),

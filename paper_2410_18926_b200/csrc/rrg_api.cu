@@ -882,6 +882,71 @@ int guarded(F&& f) {
   }
 }
 
+// Exact k-NN ground truth (brute_force_knn, bench.py:85-124): f64 distance blocks
+// from the FP64 tensor-core GEMM, merged per query by the radix select of
+// rrg_ground_truth.cu.  Chunked so the distance block stays near 4 GB.
+void ground_truth_impl(const float* corpus, int64_t m, int32_t d, const float* queries,
+                       int64_t nq, int32_t k, int32_t metric, int64_t* out_ids, cudaStream_t st) {
+  if (k < 1 || k > m) raise_usage("ParameterError", "k=%d out of range [1, %lld]", k, (long long)m);
+  if (metric < 0 || metric > 2) raise_usage("ParameterError", "unknown metric code %d", metric);
+  if (k > kGtMaxK) raise_usage("ParameterError", "k=%d > %d not supported by the device ground truth", k, kGtMaxK);
+  if (d < 1) raise_usage("ShapeError", "dimension %d", d);
+  if (nq == 0) return;
+  int64_t Pc = std::min<int64_t>(m, 1 << 20);
+  if (const char* e = getenv("RRG_GT_CHUNK")) Pc = std::max<int64_t>(1, std::min<int64_t>(Pc, atoll(e)));
+  int64_t Qc = std::max<int64_t>(128, ((int64_t)4 << 30) / (Pc * 8));
+  Qc = std::min<int64_t>(Qc, std::max<int64_t>(nq, 1));
+  const int64_t Ql = Qc;
+  char* base = nullptr;
+  size_t off = 0;
+  auto carve = [&](size_t bytes) { size_t r = off; off += (bytes + 255) / 256 * 256; return r; };
+  const size_t o_cc = carve(m * 8), o_qq = carve(Ql * 8), o_diss = carve(Ql * Pc * 8),
+               o_rk0 = carve(Ql * k * 8), o_ri0 = carve(Ql * k * 8), o_rn0 = carve(Ql * 4),
+               o_rk1 = carve(Ql * k * 8), o_ri1 = carve(Ql * k * 8), o_rn1 = carve(Ql * 4),
+               o_err = carve(4);
+  CUDA_TRY(cudaMallocAsync((void**)&base, off, st));
+  struct Free { char* p; cudaStream_t s; ~Free() { cudaFreeAsync(p, s); } } guard{base, st};
+  double* cc = reinterpret_cast<double*>(base + o_cc);
+  double* qq = reinterpret_cast<double*>(base + o_qq);
+  double* diss = reinterpret_cast<double*>(base + o_diss);
+  uint64_t* rk[2] = {reinterpret_cast<uint64_t*>(base + o_rk0), reinterpret_cast<uint64_t*>(base + o_rk1)};
+  int64_t* ri[2] = {reinterpret_cast<int64_t*>(base + o_ri0), reinterpret_cast<int64_t*>(base + o_ri1)};
+  int* rn[2] = {reinterpret_cast<int*>(base + o_rn0), reinterpret_cast<int*>(base + o_rn1)};
+  int* err = reinterpret_cast<int*>(base + o_err);
+  CUDA_TRY(cudaMemsetAsync(err, 0, 4, st));
+  if (metric != kMetricIp)  // euclidean: (c*c).sum(1); cosine: ||c|| with 0 -> 1
+    staged(8, st, [&] { launch_gt_row_norms(corpus, m, d, metric == kMetricCosine ? 1 : 0, cc, st); });
+  for (int64_t q0 = 0; q0 < nq; q0 += Qc) {
+    const int n = (int)std::min<int64_t>(Qc, nq - q0);
+    const float* qx = queries + q0 * d;
+    if (metric == kMetricEuclidean) staged(8, st, [&] { launch_gt_row_norms(qx, n, d, 0, qq, st); });
+    int cur = 0;
+    bool first = true;
+    for (int64_t p0 = 0; p0 < m; p0 += Pc) {
+      const int np = (int)std::min<int64_t>(Pc, m - p0);
+      staged(8, st, [&] {
+        launch_gt_dist(qx, n, corpus + p0 * d, np, d, metric, qq, cc + p0, diss, Pc, st);
+      });
+      GtSelectHost h{};
+      h.diss = diss; h.ld = Pc; h.n = np; h.id0 = p0;
+      h.run_key = first ? nullptr : rk[cur]; h.run_id = first ? nullptr : ri[cur];
+      h.run_n = first ? nullptr : rn[cur];
+      h.out_key = rk[cur ^ 1]; h.out_id = ri[cur ^ 1]; h.out_n = rn[cur ^ 1];
+      h.k = k; h.err = err;
+      staged(8, st, [&] { launch_gt_select(h, n, st); });
+      cur ^= 1;
+      first = false;
+    }
+    CUDA_TRY(cudaMemcpy2DAsync(out_ids + q0 * k, (size_t)k * 8, ri[cur], (size_t)k * 8, (size_t)k * 8,
+                               n, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaGetLastError());
+  }
+  int herr = 0;
+  CUDA_TRY(cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (herr) raise_usage("RrannError", "more than 4096 exact ties at a k-th distance");
+}
+
 struct HostCtx {
   int device = -1;
   cudaStream_t st = nullptr;  // compute
@@ -1184,6 +1249,14 @@ int rrg_stage_times(double* ms, int64_t* launches) {
   }
   return RRG_OK;
 }
+int rrg_ground_truth(const float* corpus, int64_t m, int32_t dim, const float* queries, int64_t nq,
+                     int32_t k, int32_t metric, int64_t* ids, void* stream) {
+  return guarded([&] {
+    ground_truth_impl(corpus, m, dim, queries, nq, k, metric, ids, static_cast<cudaStream_t>(stream));
+    return RRG_OK;
+  });
+}
+
 const char* rrg_last_error(void) { return g_err.c_str(); }
 const char* rrg_last_error_kind(void) { return g_kind.c_str(); }
 const char* rrg_version(void) { return "rrg 0.1.0 (sm_100a)"; }

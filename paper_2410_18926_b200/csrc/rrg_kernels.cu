@@ -140,6 +140,10 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
         } else if (EPI == 1) {
           const double d2 = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, v)), colterm[gn]);
           outd[(size_t)gm * ldo + gn] = d2 > 0.0 ? d2 : 0.0;
+        } else if (EPI == EPI_GT_L2) {
+          outd[(size_t)gm * ldo + gn] = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, v)), colterm[gn]);
+        } else if (EPI == EPI_GT_COS) {
+          outd[(size_t)gm * ldo + gn] = -__ddiv_rn(v, colterm[gn]);
         } else {
           outd[(size_t)gm * ldo + gn] = -v;
         }
@@ -1206,6 +1210,21 @@ void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s,
   else
     k_gemm_dmma<EPI_NEGIP, true, WM><<<grid, 64 * WM, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
                                                         nullptr, nullptr);
+}
+
+void launch_gt_dist(const float* q, int M, const float* c, int N, int d, int metric,
+                    const double* qq, const double* cterm, double* out, int64_t ldo, cudaStream_t st) {
+  constexpr int WM = 4;
+  dim3 grid((N + MBN - 1) / MBN, (M + 32 * WM - 1) / (32 * WM));
+  if (metric == kMetricEuclidean)
+    k_gemm_dmma<EPI_GT_L2, true, WM><<<grid, 64 * WM, 0, st>>>(q, d, c, d, M, N, d, nullptr, out,
+                                                             (int)ldo, qq, cterm);
+  else if (metric == kMetricIp)
+    k_gemm_dmma<EPI_NEGIP, true, WM><<<grid, 64 * WM, 0, st>>>(q, d, c, d, M, N, d, nullptr, out,
+                                                             (int)ldo, nullptr, nullptr);
+  else
+    k_gemm_dmma<EPI_GT_COS, true, WM><<<grid, 64 * WM, 0, st>>>(q, d, c, d, M, N, d, nullptr, out,
+                                                              (int)ldo, nullptr, cterm);
 }
 
 // Opt in to the dynamic shared memory a launch may need (227 KB per CTA minus the

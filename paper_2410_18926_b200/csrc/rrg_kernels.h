@@ -11,6 +11,8 @@ namespace rrg {
 constexpr int EPI_PROJ = 0;
 constexpr int EPI_L2 = 1;
 constexpr int EPI_NEGIP = 2;
+constexpr int EPI_GT_L2 = 3;   // (qq - 2 q.c) + cc, no clip (bench.py:110)
+constexpr int EPI_GT_COS = 4;  // -(q.c / ||c||)           (bench.py:100-103,112)
 constexpr int kMaxSmemPerCta = 227 * 1024;  // B200 opt-in limit per CTA
 
 struct ScoreArgsHost {
@@ -164,5 +166,29 @@ void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* 
 void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
                          const int* pos_of_id, int64_t i0, const int* perm, float* dst,
                          cudaStream_t st);
+
+
+// ---------------------------------------------------- ground truth (rrg_ground_truth.cu)
+struct GtSelectHost {
+  const double* diss;
+  int64_t ld;
+  int n;
+  int64_t id0;
+  const uint64_t* run_key;
+  const int64_t* run_id;
+  const int* run_n;
+  uint64_t* out_key;
+  int64_t* out_id;
+  int* out_n;
+  int k;
+  int* err;
+};
+constexpr int kGtMaxK = 2048;
+size_t gt_select_smem(int k);
+void launch_gt_row_norms(const float* x, int64_t n, int d, int mode, double* out, cudaStream_t st);
+void launch_gt_select(const GtSelectHost& h, int nq, cudaStream_t st);
+// f64 distance block [M][ldo] of queries q (M x d) vs corpus rows c (N x d) (rrg_kernels.cu)
+void launch_gt_dist(const float* q, int M, const float* c, int N, int d, int metric,
+                    const double* qq, const double* cterm, double* out, int64_t ldo, cudaStream_t st);
 
 }  // namespace rrg

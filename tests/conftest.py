@@ -18,7 +18,8 @@ def pytest_configure(config):
 
 
 def golden_cases():
-    return sorted(p.stem for p in GOLDEN.glob("*.npz"))
+    """Index fixtures (an RRRANN01 file + reference query results); ground_truth.npz is separate."""
+    return sorted(p.stem for p in GOLDEN.glob("*.npz") if p.stem != "ground_truth")
 
 
 def load_golden(name):

@@ -142,5 +142,26 @@ def main(only=None):
         print(name, len(blob), "bytes", "exact clusters:", int(rec["n_exact"]))
 
 
+def ground_truth_case():
+    """rrann.bench.brute_force_knn outputs for the GPU ground truth (bench.py:85-124)."""
+    from rrann.bench import brute_force_knn
+
+    rng = np.random.default_rng(21)
+    corpus = (rng.standard_normal((3000, 40)) * 2.0).astype(F32)
+    corpus[7] = corpus[2900]        # duplicate rows: equal distances, lower id first
+    corpus[11] = 0.0                # zero row (cosine norm 0 -> 1)
+    queries = rng.standard_normal((48, 40)).astype(F32)
+    queries[0] = corpus[2900]
+    rec = dict(corpus=corpus, queries=queries)
+    for metric in ("euclidean", "ip", "cosine"):
+        rec[f"{metric}_k10"] = brute_force_knn(corpus, queries, 10, metric)
+        rec[f"{metric}_k100"] = brute_force_knn(corpus, queries, 100, metric)
+    np.savez_compressed(OUT / "ground_truth.npz", **rec)
+    print("ground_truth", corpus.shape)
+
+
 if __name__ == "__main__":
+    if sys.argv[1:] == ["ground_truth"]:
+        ground_truth_case()
+        sys.exit(0)
     main(sys.argv[1:] or None)

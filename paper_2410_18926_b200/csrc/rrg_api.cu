@@ -8,12 +8,15 @@
 #include <zlib.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <memory>
 #include <string>
+#include <map>
+#include <tuple>
 #include <vector>
 
 #include "../../include/rrg.h"
@@ -179,6 +182,13 @@ struct HostModel {
 // ------------------------------------------------------------------ index
 
 struct RrgIndex {
+  // process-unique id: keys cached per-thread state (captured graphs) so a later
+  // index allocated at a freed one's address never reuses it
+  uint64_t serial = next_serial();
+  static uint64_t next_serial() {
+    static std::atomic<uint64_t> n{0};
+    return ++n;
+  }
   int device = 0;
   HostModel meta;  // header fields only (vectors released after upload)
   DevIndexView view{};
@@ -947,6 +957,22 @@ void ground_truth_impl(const float* corpus, int64_t m, int32_t d, const float* q
   if (herr) raise_usage("RrannError", "more than 4096 exact ties at a k-th distance");
 }
 
+// A captured small-batch host search (rrg_search_host): H2D of the pinned staged
+// queries, every kernel of the search and the D2H of the results replay as one
+// CUDA graph -- one launch instead of ~15 stream operations per call.
+struct GraphKey {
+  uint64_t ix;  // RrgIndex::serial
+  int64_t nq;
+  int k, w, t, rerank, dim;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(ix, nq, k, w, t, rerank, dim) < std::tie(o.ix, o.nq, o.k, o.w, o.t, o.rerank, o.dim);
+  }
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  int64_t launches = 0;
+};
+
 struct HostCtx {
   int device = -1;
   cudaStream_t st = nullptr;  // compute
@@ -954,7 +980,17 @@ struct HostCtx {
   void* dbuf = nullptr;
   size_t dcap = 0;
   std::vector<cudaEvent_t> ev;
+  // graph path: pinned staging (queries in; ids, scores, count, flag out)
+  void* pin = nullptr;
+  size_t pcap = 0;
+  std::map<GraphKey, GraphEntry> graphs;
+  void drop_graphs() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second.exec);
+    graphs.clear();
+  }
   ~HostCtx() {
+    drop_graphs();
+    if (pin) cudaFreeHost(pin);
     if (dbuf) cudaFree(dbuf);
     if (st) cudaStreamDestroy(st);
     if (cs) cudaStreamDestroy(cs);
@@ -1041,6 +1077,7 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     CUDA_TRY(cudaSetDevice(index->device));
     HostCtx& h = g_host;
     if (h.device != index->device) {
+      h.drop_graphs();
       if (h.dbuf) cudaFree(h.dbuf);
       if (h.st) cudaStreamDestroy(h.st);
       if (h.cs) cudaStreamDestroy(h.cs);
@@ -1061,6 +1098,7 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     auto al = [](size_t b) { return (b + 255) / 256 * 256; };
     size_t need = al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + 256 + p.total;
     if (need > h.dcap) {
+      h.drop_graphs();  // captured pointers die with the buffer
       if (h.dbuf) cudaFree(h.dbuf);
       h.dbuf = nullptr;
       CUDA_TRY(cudaMalloc(&h.dbuf, need));
@@ -1076,6 +1114,62 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     if (h.ev.empty()) {
       h.ev.resize(9);
       for (auto& e : h.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    // small batches: replay a captured graph (launch latency dominates there)
+    const char* ge = getenv("RRG_GRAPH");
+    const bool use_graph = nq <= 2048 && !g_timer.on && !(ge && atoi(ge) == 0);
+    if (use_graph) {
+      const size_t pneed = al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + 256;
+      if (pneed > h.pcap) {
+        h.drop_graphs();
+        if (h.pin) cudaFreeHost(h.pin);
+        h.pin = nullptr;
+        CUDA_TRY(cudaMallocHost(&h.pin, pneed));
+        h.pcap = pneed;
+      }
+      char* hp = static_cast<char*>(h.pin);
+      float* hq = reinterpret_cast<float*>(hp);
+      int64_t* hi = reinterpret_cast<int64_t*>(hp + al(qbytes));
+      float* hs = reinterpret_cast<float*>(hp + al(qbytes) + al(ibytes));
+      int32_t* hc = reinterpret_cast<int32_t*>(hp + al(qbytes) + al(ibytes) + al(sbytes));
+      int* hf = reinterpret_cast<int*>(hp + al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes));
+      const GraphKey key{index->serial, nq, k, w, t, rerank, dim};
+      auto it = h.graphs.find(key);
+      if (it == h.graphs.end()) {
+        if (h.graphs.size() >= 64) h.drop_graphs();  // bound the cache
+        cudaGraph_t graph = nullptr;
+        CUDA_TRY(cudaStreamBeginCapture(h.st, cudaStreamCaptureModeRelaxed));
+        const int64_t before = g_launches;
+        try {
+          CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), h.st));
+          CUDA_TRY(cudaMemcpyAsync(dq, hq, qbytes, cudaMemcpyHostToDevice, h.st));
+          search_impl(index, dq, nq, k, w, t, rerank, di, dsc, dc, ws, p.total, h.st, nullptr, dflag);
+          CUDA_TRY(cudaMemcpyAsync(hi, di, ibytes, cudaMemcpyDeviceToHost, h.st));
+          CUDA_TRY(cudaMemcpyAsync(hs, dsc, sbytes, cudaMemcpyDeviceToHost, h.st));
+          CUDA_TRY(cudaMemcpyAsync(hc, dc, cbytes, cudaMemcpyDeviceToHost, h.st));
+          CUDA_TRY(cudaMemcpyAsync(hf, dflag, sizeof(int), cudaMemcpyDeviceToHost, h.st));
+        } catch (...) {
+          cudaStreamEndCapture(h.st, &graph);
+          if (graph) cudaGraphDestroy(graph);
+          throw;
+        }
+        CUDA_TRY(cudaStreamEndCapture(h.st, &graph));
+        GraphEntry ge2;
+        ge2.launches = g_launches - before;
+        const cudaError_t ie = cudaGraphInstantiate(&ge2.exec, graph, 0);
+        cudaGraphDestroy(graph);
+        CUDA_TRY(ie);
+        it = h.graphs.emplace(key, ge2).first;
+      }
+      memcpy(hq, queries, qbytes);
+      CUDA_TRY(cudaGraphLaunch(it->second.exec, h.st));
+      CUDA_TRY(cudaStreamSynchronize(h.st));
+      g_launches = it->second.launches;
+      if (*hf) return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
+      memcpy(ids, hi, ibytes);
+      memcpy(scores, hs, sbytes);
+      memcpy(count, hc, cbytes);
+      return RRG_OK;
     }
     CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), h.st));
     std::vector<cudaEvent_t> in_ready;

@@ -38,6 +38,13 @@ WORKLOADS = {
                L=256, s=64, r=32, k=10),
     "c2": dict(m=1_000_000, d=768, n_queries=10_000, seed=1, n_blobs=1000,
                L=1024, s=256, r=32, k=100),
+    # C3 (BASELINE.json configs[2]): OpenAI-embedding shape, s = 64 (the reference default)
+    "c3": dict(m=1_000_000, d=1536, n_queries=10_000, seed=1, n_blobs=1000,
+               L=2048, s=64, r=32, k=100),
+    # C5 (configs[4]): C2's corpus, out-of-distribution queries (test_acceptance.py:321-329
+    # scaled up), RRR fitted on a held-out query sample (RrrConfig(train_source="query_sample"))
+    "c5": dict(m=1_000_000, d=768, n_queries=10_000, seed=1, n_blobs=1000,
+               L=1024, s=256, r=32, k=100, ood=dict(n_train=100_000, seed=5)),
     # tiny workload for smoke tests / golden fixtures
     "tiny": dict(m=4_000, d=32, n_queries=256, seed=7, n_blobs=40,
                  L=32, s=16, r=8, k=10),
@@ -67,12 +74,36 @@ def synth_clustered(m: int, n_queries: int, d: int, seed: int, n_blobs: int,
     return corpus, queries
 
 
+def ood_queries(d: int, n_train: int, n_queries: int, seed: int):
+    """(train, queries) f32 drawn like test_acceptance.py:_ood_trial (lines 321-333):
+    (z * 2*0.85^i + shift) @ R^T with shift ~ 1.5 N(0, I) and R = random_rotation(d, seed+1000)
+    (linalg.py:109-117).  Run in the dev container; the queries are stored in data/
+    (the QR's last bits depend on the host's LAPACK kernels)."""
+    import sys
+
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from rrann.linalg import random_rotation
+
+    rng = np.random.default_rng(seed)
+    rot = random_rotation(d, seed=seed + 1000).astype(np.float64)
+    scales = 2.0 * (0.85 ** np.arange(d))
+    shift = rng.standard_normal(d) * 1.5
+
+    def draw(n):
+        z = rng.standard_normal((n, d)) * scales
+        return ((z + shift) @ rot.T).astype(F32)
+
+    train = draw(n_train)
+    return train, draw(n_queries)
+
+
 def workload_paths(name: str):
     return dict(
         full=DATA_DIR / f"{name}.rrr",
         sidecar=DATA_DIR / f"{name}.rrrm",
         manifest=DATA_DIR / f"{name}.json",
         gt=DATA_DIR / f"{name}.gt.npy",
+        queries=DATA_DIR / f"{name}.queries.npy",
     )
 
 
@@ -118,6 +149,9 @@ def load_queries(name: str, n: int | None = None) -> np.ndarray:
     man = load_manifest(name)
     g = man["generator"]
     nq = g["n_queries"] if n is None else n
+    qp = workload_paths(name)["queries"]
+    if qp.exists():  # stored query set (out-of-distribution workloads)
+        return np.load(qp)[:nq]
     # queries come after the corpus in the rng stream; skip corpus materialisation
     _, q = synth_clustered(g["m"], g["n_queries"], g["d"], g["seed"], g["n_blobs"],
                            with_corpus=False)

@@ -78,10 +78,18 @@ def main() -> None:
     del mine_c, mine_q
     print(f"synth {time.perf_counter() - t0:.1f}s", flush=True)
 
+    train = None
+    if cfg.get("ood"):  # out-of-distribution queries + the RRR training sample (C5)
+        train, queries = W.ood_queries(cfg["d"], cfg["ood"]["n_train"], cfg["n_queries"],
+                                       cfg["ood"]["seed"])
+        np.save(paths["queries"], queries)
     t0 = time.perf_counter()
     icfg = IndexConfig(metric="euclidean", n_clusters=cfg["L"],
-                       rrr=RrrConfig(rank=cfg["r"], reduced_dim=cfg["s"]), seed=0)
-    idx = build(corpus, icfg, workers=args.workers)
+                       rrr=RrrConfig(rank=cfg["r"], reduced_dim=cfg["s"],
+                                     train_source="query_sample" if train is not None else "corpus"),
+                       seed=0)
+    idx = build(corpus, icfg, train=train, workers=args.workers)
+    del train
     build_s = time.perf_counter() - t0
     sizes = np.array([mdl.n_points for mdl in idx.models])
     print(f"build {build_s:.1f}s sizes min/med/max {sizes.min()}/{int(np.median(sizes))}/{sizes.max()} "
@@ -97,7 +105,9 @@ def main() -> None:
     assert crc == zlib.crc32(data[:-4]) & 0xFFFFFFFF
     man = dict(name=args.name, generator=dict(m=cfg["m"], d=cfg["d"], n_queries=cfg["n_queries"],
                                               seed=cfg["seed"], n_blobs=cfg["n_blobs"]),
-               index=dict(L=cfg["L"], s=cfg["s"], r=cfg["r"], metric="euclidean", seed=0),
+               index=dict(L=cfg["L"], s=cfg["s"], r=cfg["r"], metric="euclidean", seed=0,
+                          train_source="query_sample" if cfg.get("ood") else "corpus"),
+               **({"ood": cfg["ood"]} if cfg.get("ood") else {}),
                k=cfg["k"], file_size=len(data), corpus_offset=corpus_off, crc32=crc,
                build_seconds=round(build_s, 1), built_by="rrann (reference, unmodified) via tools/build_index.py")
     del data
@@ -111,8 +121,10 @@ def main() -> None:
         from rrann.bench import mean_recall
         nq = args.grid_queries
         grid = []
-        for w in (1, 2, 4, 8, 16):
-            for t in (100, 200, 400, 800, 1600):
+        ws = (8, 16, 24, 32, 48, 64, 128, 256) if cfg.get("ood") else (1, 2, 4, 8, 16)
+        ts = (800, 1600) if cfg.get("ood") else (100, 200, 400, 800, 1600)
+        for w in ws:
+            for t in ts:
                 if t < cfg["k"]:
                     continue
                 t1 = time.perf_counter()

@@ -578,7 +578,18 @@ __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_o
   if (threadIdx.x == 0) rr_item_off[L] = tot;
 }
 
-template <int NB>
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+// ASYNC: the next row pair is copied global -> shared (cp.async, no registers) while
+// the current pair is scored, so the copy has a whole pair's arithmetic to land;
+// without it the next pair is loaded into registers after the scoring, with only
+// the reduction to hide its latency.
+template <int NB, bool ASYNC>
 __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankArgs a) {
   constexpr int NLV = 8, cstep = 8 * NLV;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -586,6 +597,9 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
   const int ds = ix.d_stride, d = ix.d;
   float* xs = reinterpret_cast<float*>(smem_raw);                       // [kRrQ][ds]
   uint32_t* mb = reinterpret_cast<uint32_t*>(xs + (size_t)kRrQ * ds);  // [kRrQ][mwords]
+  // ASYNC: per-warp staging of one row pair [warp][2][ds] after the bitmaps
+  float* rowbuf = reinterpret_cast<float*>(mb + (size_t)kRrQ * a.mwords) +
+                  (size_t)(threadIdx.x >> 5) * 2 * ds;
   __shared__ int item_s;
   __shared__ int pq[kPairsPerItem], pkey[kPairsPerItem];
   __shared__ int slotq[XNT / 32][kRrQ];
@@ -665,12 +679,37 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
       float2 ca[NB], cb[NB];
       auto load_pair = [&](int pa) {
         const int pb = pa + 1 < r1 ? pa + 1 : pa;
+        if (ASYNC) {  // issue the copy of both rows into this warp's staging slot
+          const float4* ra = reinterpret_cast<const float4*>(ix.corpus + (size_t)(p0 + pa) * ds);
+          const float4* rb = reinterpret_cast<const float4*>(ix.corpus + (size_t)(p0 + pb) * ds);
+          float4* sa = reinterpret_cast<float4*>(rowbuf);
+          float4* sb = reinterpret_cast<float4*>(rowbuf + ds);
+          const int n16 = ds / 4;
+          for (int c = lane; c < n16; c += 32) {
+            cp_async16(sa + c, ra + c);
+            cp_async16(sb + c, rb + c);
+          }
+          cp_async_commit();
+          return;
+        }
         const float* ra = ix.corpus + (size_t)(p0 + pa) * ds + coff;
         const float* rb = ix.corpus + (size_t)(p0 + pb) * ds + coff;
 #pragma unroll
         for (int i = 0; i < NB; ++i) ca[i] = __ldg(reinterpret_cast<const float2*>(ra + cstep * i));
 #pragma unroll
         for (int i = 0; i < NB; ++i) cb[i] = __ldg(reinterpret_cast<const float2*>(rb + cstep * i));
+      };
+      // ASYNC: wait for the staged pair and move this lane's slices to registers
+      auto take_pair = [&]() {
+        cp_async_wait_all();
+        __syncwarp();
+        const float* sa = rowbuf + coff;
+        const float* sb = rowbuf + ds + coff;
+#pragma unroll
+        for (int i = 0; i < NB; ++i) ca[i] = *reinterpret_cast<const float2*>(sa + cstep * i);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) cb[i] = *reinterpret_cast<const float2*>(sb + cstep * i);
+        __syncwarp();
       };
       // per (query, row pair): this lane's r[2h]+r[2h+1] of both rows
       auto lane_sums = [&](int g, float& va, float& vb) {
@@ -701,14 +740,25 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         }
       };
       int pa = r0 + warp * 2;
+      if (ASYNC) {  // skip row pairs no query of the group selected (no copy issued)
+        while (pa < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pa + 1))))
+          pa += nwarps * 2;
+      }
       if (pa < r1) load_pair(pa);
-      for (; pa < r1; pa += nwarps * 2) {
-        const int pb = pa + 1, pn = pa + nwarps * 2;
+      for (; pa < r1;) {
+        const int pb = pa + 1;
+        int pn = pa + nwarps * 2;
         // the queries that selected either row (one lane per query, ballot)
         const bool mine = lane < ng && (marked(lane, pa) || marked(lane, pb));
         const unsigned act0 = __ballot_sync(0xffffffffu, mine);
-        if (!act0) {
+        if (ASYNC) {
+          take_pair();
+          while (pn < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, pn) || marked(lane, pn + 1))))
+            pn += nwarps * 2;
           if (pn < r1) load_pair(pn);
+        } else if (!act0) {
+          if (pn < r1) load_pair(pn);
+          pa = pn;
           continue;
         }
         // per-lane partials of every active (query, row) pair: value 2*slot + row
@@ -725,7 +775,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
             v[2 * slot + 1] = 0.f;
           }
         }
-        if (pn < r1) load_pair(pn);
+        if (!ASYNC && pn < r1) load_pair(pn);
         // Transposing butterfly: five xor-steps (1, 2, 4, 8, 16 -- NumPy's
         // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree)
         // that halve the values held per lane, so lane j ends with value j fully
@@ -752,6 +802,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           if (marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? v[0] : -v[0]);
         }
         __syncwarp();
+        pa = pn;
       }
       __syncthreads();
     }
@@ -894,8 +945,14 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
 }
 
+static bool rerank_async() {
+  const char* e = getenv("RRG_RR_ASYNC");
+  return !(e && atoi(e) == 0);
+}
+
 size_t cluster_rerank_smem(int d_stride, int mwords) {
-  return (size_t)kRrQ * d_stride * 4 + (size_t)kRrQ * mwords * 4;
+  return (size_t)kRrQ * d_stride * 4 + (size_t)kRrQ * mwords * 4 +
+         (rerank_async() ? (size_t)(XNT / 32) * 2 * d_stride * 4 : 0);
 }
 
 // the row plan fits k_rerank_cluster and a query group's x + membership bits of the
@@ -934,12 +991,19 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#define RRG_RR_LAUNCH(NB, AS, SLOT)                                              \
+  do {                                                                           \
+    opt_in_smem(k_rerank_cluster<NB, AS>, SLOT);                                 \
+    k_rerank_cluster<NB, AS><<<sms * kCmCtas, XNT, sm, st>>>(a);                 \
+  } while (0)
+  const bool as = rerank_async();
+  // persistent grid: kCmCtas CTAs per SM
   switch (h.ix.pw_leaf_n / 8) {
-    // persistent grid: kCmCtas CTAs per SM (3 measured best on C2 vs 2 and 4)
-    case 12: opt_in_smem(k_rerank_cluster<12>, 0); k_rerank_cluster<12><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
-    case 15: opt_in_smem(k_rerank_cluster<15>, 1); k_rerank_cluster<15><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
-    default: opt_in_smem(k_rerank_cluster<16>, 2); k_rerank_cluster<16><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+    case 12: if (as) RRG_RR_LAUNCH(12, true, 4); else RRG_RR_LAUNCH(12, false, 0); break;
+    case 15: if (as) RRG_RR_LAUNCH(15, true, 5); else RRG_RR_LAUNCH(15, false, 1); break;
+    default: if (as) RRG_RR_LAUNCH(16, true, 6); else RRG_RR_LAUNCH(16, false, 2); break;
   }
+#undef RRG_RR_LAUNCH
 }
 
 size_t topk_final_smem(int w, int take_cap, int k) {

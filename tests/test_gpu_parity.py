@@ -414,7 +414,7 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "query", "cluster+regs", "cluster+tma"])
+@pytest.mark.parametrize("mode", ["cluster", "cluster+sync", "query", "cluster+regs", "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -422,7 +422,9 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
     scoring (per-query re-rank), and the per-query register / TMA re-rank kernels."""
     score_mode, _, rerank_mode = mode.partition("+")
     monkeypatch.setenv("RRG_SCORE_MODE", score_mode)
-    if rerank_mode:
+    if rerank_mode == "sync":  # cluster-major re-rank with register (not cp.async) row loads
+        monkeypatch.setenv("RRG_RR_ASYNC", "0")
+    elif rerank_mode:
         monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
     from oracle import rrann_oracle as O

@@ -142,6 +142,17 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq,
                     int32_t rerank, int64_t* ids, float* scores,
                     int32_t* count);
 
+/* A stream of `nbatch` host batches (queries[b]: nq[b] x dim; outputs as
+ * rrg_search_host), software-pipelined over two device buffer sets so the
+ * H2D copy of batch b+1 and the D2H copy of batch b-1 overlap the search of
+ * batch b -- the serving loop over consecutive query_batch calls.  Results are
+ * identical to nbatch rrg_search_host calls; pinned host buffers give full
+ * copy bandwidth. */
+int rrg_search_host_many(RrgIndex* index, int32_t nbatch, const float* const* queries,
+                         const int64_t* nq, int32_t dim, int32_t k, int32_t w, int32_t t,
+                         int32_t rerank, int64_t* const* ids, float* const* scores,
+                         int32_t* const* count);
+
 /* Stage entry points used by the stage-parity tests (device buffers). */
 int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq,
                       float* xp, int8_t* qcodes, float* qscale, float* qhead,

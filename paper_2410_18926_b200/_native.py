@@ -57,6 +57,8 @@ SIGNATURES = {
                            c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "rrg_search_host": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32,
                                 c_vp, c_vp, c_vp]),
+    "rrg_search_host_many": (c_int, [c_vp, c_i32, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32,
+                                     c_vp, c_vp, c_vp]),
     "rrg_stage_project": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rrg_stage_route": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_size, c_vp]),
     "rrg_shard_workspace_bytes": (c_size, [c_vp, c_i64, c_i32, c_i32, c_i32]),

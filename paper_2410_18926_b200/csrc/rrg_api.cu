@@ -1196,6 +1196,136 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
   });
 }
 
+// Several host batches in one call, software-pipelined over two device buffer sets:
+// the H2D copy of batch b+1 (copy-in stream) and the D2H copy of batch b-1
+// (copy-out stream) overlap the search of batch b (compute stream).  Each batch
+// is validated and searched exactly like rrg_search_host.
+struct PipeSlot {
+  void* buf = nullptr;
+  size_t cap = 0;
+  cudaEvent_t in_ready = nullptr, comp_done = nullptr, out_done = nullptr;
+};
+struct PipeCtx {
+  int device = -1;
+  cudaStream_t cs = nullptr, ci = nullptr, co = nullptr;
+  PipeSlot slot[2];
+  int* hflags = nullptr;  // pinned, one per batch
+  int64_t nflags = 0;
+  void reset() {
+    for (auto& sl : slot) {
+      if (sl.buf) cudaFree(sl.buf);
+      if (sl.in_ready) cudaEventDestroy(sl.in_ready);
+      if (sl.comp_done) cudaEventDestroy(sl.comp_done);
+      if (sl.out_done) cudaEventDestroy(sl.out_done);
+      sl = PipeSlot{};
+    }
+    if (hflags) cudaFreeHost(hflags);
+    hflags = nullptr;
+    nflags = 0;
+    if (cs) cudaStreamDestroy(cs);
+    if (ci) cudaStreamDestroy(ci);
+    if (co) cudaStreamDestroy(co);
+    cs = ci = co = nullptr;
+    device = -1;
+  }
+  ~PipeCtx() { reset(); }
+};
+thread_local PipeCtx g_pipe;
+
+int rrg_search_host_many(RrgIndex* index, int32_t nbatch, const float* const* queries,
+                         const int64_t* nq, int32_t dim, int32_t k, int32_t w, int32_t t,
+                         int32_t rerank, int64_t* const* ids, float* const* scores,
+                         int32_t* const* count) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
+    if (nbatch < 0) return fail(RRG_E_USAGE, "ParameterError", "nbatch < 0");
+    int64_t qmax = 0;
+    for (int b = 0; b < nbatch; ++b) qmax = std::max<int64_t>(qmax, nq[b]);
+    if (qmax == 0) return RRG_OK;
+    try {
+      validate_search(index, dim, k, w, t, rerank);
+    } catch (const RrgFail&) {  // DataError first for a non-finite batch (index.py:339)
+      const std::string msg = g_err, kind = g_kind;
+      for (int b = 0; b < nbatch; ++b)
+        for (int64_t i = 0; i < nq[b] * (int64_t)dim; ++i)
+          if (!std::isfinite(queries[b][i]))
+            return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
+      g_err = msg;
+      g_kind = kind;
+      throw;
+    }
+    CUDA_TRY(cudaSetDevice(index->device));
+    PipeCtx& pc = g_pipe;
+    if (pc.device != index->device) {
+      pc.reset();
+      CUDA_TRY(cudaStreamCreateWithFlags(&pc.cs, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&pc.ci, cudaStreamNonBlocking));
+      CUDA_TRY(cudaStreamCreateWithFlags(&pc.co, cudaStreamNonBlocking));
+      for (auto& sl : pc.slot) {
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.in_ready, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.comp_done, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&sl.out_done, cudaEventDisableTiming));
+      }
+      pc.device = index->device;
+    }
+    if (pc.nflags < nbatch) {
+      if (pc.hflags) cudaFreeHost(pc.hflags);
+      pc.hflags = nullptr;
+      CUDA_TRY(cudaMallocHost(&pc.hflags, (size_t)nbatch * sizeof(int)));
+      pc.nflags = nbatch;
+    }
+    auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+    Plan pmax = make_plan(index, qmax, k, w, t, rerank);
+    const size_t qb = al((size_t)qmax * dim * 4), ib = al((size_t)qmax * k * 8),
+                 sb = al((size_t)qmax * k * 4), cb = al((size_t)qmax * 4);
+    const size_t need = qb + ib + sb + cb + 256 + pmax.total;
+    for (auto& sl : pc.slot)
+      if (sl.cap < need) {
+        CUDA_TRY(cudaStreamSynchronize(pc.cs));
+        if (sl.buf) cudaFree(sl.buf);
+        sl.buf = nullptr;
+        CUDA_TRY(cudaMalloc(&sl.buf, need));
+        sl.cap = need;
+      }
+    for (int b = 0; b < nbatch; ++b) {
+      PipeSlot& sl = pc.slot[b & 1];
+      const int64_t n = nq[b];
+      char* base = static_cast<char*>(sl.buf);
+      float* dq = reinterpret_cast<float*>(base);
+      int64_t* di = reinterpret_cast<int64_t*>(base + qb);
+      float* dsc = reinterpret_cast<float*>(base + qb + ib);
+      int32_t* dc = reinterpret_cast<int32_t*>(base + qb + ib + sb);
+      int* dflag = reinterpret_cast<int*>(base + qb + ib + sb + cb);
+      void* ws = base + qb + ib + sb + cb + 256;
+      pc.hflags[b] = 0;
+      if (n == 0) continue;
+      // in: the slot's queries were last read by the search of batch b-2
+      if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(pc.ci, sl.comp_done, 0));
+      CUDA_TRY(cudaMemcpyAsync(dq, queries[b], (size_t)n * dim * 4, cudaMemcpyHostToDevice, pc.ci));
+      CUDA_TRY(cudaEventRecord(sl.in_ready, pc.ci));
+      // search: its outputs were last read by the D2H of batch b-2
+      CUDA_TRY(cudaStreamWaitEvent(pc.cs, sl.in_ready, 0));
+      if (b >= 2) CUDA_TRY(cudaStreamWaitEvent(pc.cs, sl.out_done, 0));
+      CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), pc.cs));
+      search_impl(index, dq, n, k, w, t, rerank, di, dsc, dc, ws, pmax.total, pc.cs, nullptr, dflag);
+      CUDA_TRY(cudaEventRecord(sl.comp_done, pc.cs));
+      // out
+      CUDA_TRY(cudaStreamWaitEvent(pc.co, sl.comp_done, 0));
+      CUDA_TRY(cudaMemcpyAsync(ids[b], di, (size_t)n * k * 8, cudaMemcpyDeviceToHost, pc.co));
+      CUDA_TRY(cudaMemcpyAsync(scores[b], dsc, (size_t)n * k * 4, cudaMemcpyDeviceToHost, pc.co));
+      CUDA_TRY(cudaMemcpyAsync(count[b], dc, (size_t)n * 4, cudaMemcpyDeviceToHost, pc.co));
+      CUDA_TRY(cudaMemcpyAsync(pc.hflags + b, dflag, sizeof(int), cudaMemcpyDeviceToHost, pc.co));
+      CUDA_TRY(cudaEventRecord(sl.out_done, pc.co));
+    }
+    CUDA_TRY(cudaStreamSynchronize(pc.co));
+    CUDA_TRY(cudaStreamSynchronize(pc.cs));
+    for (int b = 0; b < nbatch; ++b)
+      if (pc.hflags[b]) return fail(RRG_E_DATA, "DataError", "queries: contains non-finite values");
+    return RRG_OK;
+  });
+}
+
 int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq, float* xp,
                       int8_t* qcodes, float* qscale, float* qhead, void* stream) {
   return guarded([&] {

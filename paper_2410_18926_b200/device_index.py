@@ -216,6 +216,31 @@ class DeviceIndex:
                                   ids.ctypes.data, scores.ctypes.data, count.ctypes.data))
         return ids, scores, count
 
+    def search_host_many(self, batches, k: int, w: int, t: int, rerank: bool = True, outs=None):
+        """Several host batches through ``rrg_search_host_many`` (H2D / search / D2H of
+        consecutive batches overlapped); returns [(ids, scores, count)] per batch."""
+        qs = [np.ascontiguousarray(b, dtype=np.float32) for b in batches]
+        for q in qs:
+            if q.ndim != 2:
+                from .errors import DataError
+                raise DataError("queries: expected 2-D array")
+        dim = qs[0].shape[1] if qs else 0
+        if any(q.shape[1] != dim for q in qs):
+            from .errors import ShapeError
+            raise ShapeError("batches have different dimensions")
+        if outs is None:
+            outs = [(np.empty((q.shape[0], k), np.int64), np.empty((q.shape[0], k), np.float32),
+                     np.empty((q.shape[0],), np.int32)) for q in qs]
+        nb = len(qs)
+        P = ctypes.c_void_p * max(nb, 1)
+        qp = P(*[q.ctypes.data for q in qs])
+        ip = P(*[o[0].ctypes.data for o in outs])
+        sp = P(*[o[1].ctypes.data for o in outs])
+        cp = P(*[o[2].ctypes.data for o in outs])
+        nqa = (ctypes.c_int64 * max(nb, 1))(*[q.shape[0] for q in qs])
+        check(lib.rrg_search_host_many(self._h, nb, qp, nqa, dim, k, w, t, int(rerank), ip, sp, cp))
+        return outs
+
     # ------------------------------------------------------------- stage APIs
 
     def stage_project(self, queries):

@@ -488,3 +488,25 @@ def test_random_index_f32_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf)
         for i in range(len(q)):
             _f32_check_query(O, oidx, q[i], k, w, t, rr, ids[i], sc[i], cnt[i], cmax,
                              f"d={d} {metric} {(k, w, t, rr)} q{i}")
+
+
+def test_search_host_many_equals_single_calls(pkg, tmp_path):
+    """rrg_search_host_many (pipelined H2D / search / D2H) == one rrg_search_host per batch."""
+    g, dev = _golden_index(pkg, tmp_path, "euclid_q")
+    q = g["queries"]
+    batches = [q[:7], q[7:40], q[:0], q[40:], q[::-1].copy(), q[:1]]
+    for k, w, t, rr in [(10, 3, 50, True), (5, 2, 5, False)]:
+        outs = dev.search_host_many(batches, k, w, t, rr)
+        for b, (ids, sc, cnt) in zip(batches, outs):
+            if len(b) == 0:
+                continue
+            ri, rs, rc = dev.search_host(b, k, w, t, rr)
+            np.testing.assert_array_equal(cnt, rc)
+            np.testing.assert_array_equal(ids, ri)
+            np.testing.assert_array_equal(sc.view(np.int32), rs.view(np.int32))
+    bad = q[:5].copy()
+    bad[2, 3] = np.inf
+    with pytest.raises(pkg.DataError):
+        dev.search_host_many([q[:5], bad], 10, 3, 50)
+    with pytest.raises(pkg.ParameterError, match="k must be >= 1"):
+        dev.search_host_many([q[:5]], 0, 3, 50)

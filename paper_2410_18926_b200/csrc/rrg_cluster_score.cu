@@ -528,6 +528,435 @@ __global__ void __launch_bounds__(TNT) k_select_topt(SelectArgs a) {
   if (tid == 0) a.out_count[gq] = take;
 }
 
+// ---------------------------------------------- warp-per-query selection
+// The per-query selections (top-t of the scores, top-k of the re-ranked
+// distances) have ~1k candidates: a 256-thread CTA spends them on barriers
+// (47% barrier stalls in ncu).  Here one warp owns a query: its keys are
+// staged in the warp's shared-memory slice, a 4-pass 8-bit radix select finds
+// the take-th smallest key K* (lanes with equal digits aggregated by
+// __match_any_sync before one shared atomic), keys < K* are compacted by
+// ballot, and the ties at K* are resolved by (key, corpus id) like the block
+// select -- the same exact result, no CTA barrier.
+constexpr int kWarpTieCap = 64;  // boundary elements resolved by rank on-chip
+
+struct WarpSel {
+  const uint32_t* keys;  // the query's keys (staged in the warp's smem slice, or global)
+  int* hist;             // 256
+  int* bidx;             // kWarpTieCap boundary candidates
+  uint32_t* bkey;        // kWarpTieCap
+  uint32_t* selbits;     // ceil(n/32) words marking the selected candidates (optional)
+};
+
+// Selects the `take` smallest of keys[0..n) by (key, tie(i)) -- tie(i) the corpus
+// id, as the reference's lexsort((ids, keys)) (index.py:315,321); n > take >= 1.
+// Indices go out through emit(slot, i), slot in [0, take), arbitrary order; when
+// ws.selbits is set, bit i of it marks the selected candidates.
+//  1. value range of the keys (warp min/max), 256 float-linear buckets (monotone
+//     in the key, so equal keys share a bucket), histogram, boundary bucket bb;
+//  2. buckets < bb are selected (ballot compaction); the boundary bucket's members
+//     are ranked exactly by (key, tie) when they fit kWarpTieCap;
+//  3. otherwise (a dense boundary bucket, e.g. many equal keys) an exact 8-bit
+//     radix select over the keys, equal keys at the take-th ranked by tie.
+template <typename TieF, typename EmitF>
+__device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF tie, EmitF emit) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  auto mark = [&](int i) {
+    if (ws.selbits) atomicOr(&ws.selbits[i >> 5], 1u << (i & 31));
+  };
+  // locate the bucket (of a 256-bin histogram of bucket_of) holding rank `take`
+  auto boundary = [&](int& bb, int& before, int& cnt) {
+    int c[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { c[j] = ws.hist[lane * 8 + j]; tot += c[j]; }
+    int incl = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const bool own = incl - tot < take && take <= incl;
+    bb = 0; before = 0; cnt = 0;
+    if (own) {
+      int run = incl - tot;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (run + c[j] >= take) { bb = lane * 8 + j; before = run; cnt = c[j]; break; }
+        run += c[j];
+      }
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, own)) - 1;
+    bb = __shfl_sync(0xffffffffu, bb, src);
+    before = __shfl_sync(0xffffffffu, before, src);
+    cnt = __shfl_sync(0xffffffffu, cnt, src);
+    __syncwarp();
+  };
+  // ---- 1. range and float-linear histogram (two levels: the boundary bucket of the
+  // first is re-bucketed over its own value span, which absorbs outliers that
+  // stretch the first range)
+  uint32_t lo = 0xFFFFFFFFu, hi = 0u;
+  for (int i = lane; i < n; i += 32) {
+    const uint32_t k = ws.keys[i];
+    lo = min(lo, k);
+    hi = max(hi, k);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  const float vmin = unmono32(lo), vmax = unmono32(hi);
+  const float range = vmax - vmin;
+  const float scale = (range > 0.f && range < 3.0e38f) ? 256.f / range : 0.f;
+  auto bucket = [&](uint32_t k) {
+    const int b = (int)((unmono32(k) - vmin) * scale);
+    return b < 0 ? 0 : (b > 255 ? 255 : b);
+  };
+  for (int b = lane; b < 256; b += 32) ws.hist[b] = 0;
+  __syncwarp();
+  for (int i = lane; i < n; i += 32) atomicAdd(&ws.hist[bucket(ws.keys[i])], 1);
+  __syncwarp();
+  int bb, before, cnt;
+  boundary(bb, before, cnt);
+  // level 2 over the boundary bucket's value span [vmin + bb/scale, vmin + (bb+1)/scale)
+  const float v2lo = scale > 0.f ? vmin + (float)bb / scale : vmin;
+  const float v2hi = scale > 0.f ? vmin + (float)(bb + 1) / scale : vmax;
+  const float r2 = v2hi - v2lo;
+  const float scale2 = (r2 > 0.f && r2 < 3.0e38f) ? 256.f / r2 : 0.f;
+  auto bucket2 = [&](uint32_t k) {
+    const int b = (int)((unmono32(k) - v2lo) * scale2);
+    return b < 0 ? 0 : (b > 255 ? 255 : b);
+  };
+  int bb2 = -1;
+  if (cnt > kWarpTieCap) {
+    const int take1 = take - before;
+    for (int b = lane; b < 256; b += 32) ws.hist[b] = 0;
+    __syncwarp();
+    for (int i = lane; i < n; i += 32) {
+      const uint32_t k = ws.keys[i];
+      if (bucket(k) == bb) atomicAdd(&ws.hist[bucket2(k)], 1);
+    }
+    __syncwarp();
+    int before2, cnt2;
+    {
+      // boundary() searches rank `take`; shift by the elements below bucket bb
+      int c[8], tot = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { c[j] = ws.hist[lane * 8 + j]; tot += c[j]; }
+      int incl = tot;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+      }
+      const bool own = incl - tot < take1 && take1 <= incl;
+      int b2 = 0, bf = 0, cn = 0;
+      if (own) {
+        int run = incl - tot;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          if (run + c[j] >= take1) { b2 = lane * 8 + j; bf = run; cn = c[j]; break; }
+          run += c[j];
+        }
+      }
+      const int src = __ffs(__ballot_sync(0xffffffffu, own)) - 1;
+      bb2 = __shfl_sync(0xffffffffu, b2, src);
+      before2 = __shfl_sync(0xffffffffu, bf, src);
+      cnt2 = __shfl_sync(0xffffffffu, cn, src);
+      __syncwarp();
+    }
+    before += before2;
+    cnt = cnt2;
+  }
+  if (cnt <= kWarpTieCap) {
+    // ---- 2. buckets below the boundary selected; the boundary bucket ranked exactly
+    auto cls = [&](uint32_t k) {  // -1 below, 0 boundary, 1 above
+      const int b = bucket(k);
+      if (b != bb) return b < bb ? -1 : 1;
+      if (bb2 < 0) return 0;
+      const int b2 = bucket2(k);
+      return b2 < bb2 ? -1 : (b2 == bb2 ? 0 : 1);
+    };
+    int nlt = 0, nb = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const uint32_t k = i < n ? ws.keys[i] : 0xFFFFFFFFu;
+      const int c = i < n ? cls(k) : 1;
+      const bool lt = c < 0, eq = c == 0;
+      const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
+      if (lt) emit(nlt + __popc(bl & lt_mask), i);
+      if (eq) {
+        const int slot = nb + __popc(be & lt_mask);
+        ws.bidx[slot] = i;
+        ws.bkey[slot] = k;
+      }
+      if (ws.selbits && lane == 0) ws.selbits[base >> 5] = bl;
+      nlt += __popc(bl);
+      nb += __popc(be);
+    }
+    __syncwarp();
+    const int need = take - before;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = lane + 32 * u;
+      if (e < nb) {
+        const uint32_t ke = ws.bkey[e];
+        int r = 0;
+        bool dup = false;
+        for (int f = 0; f < nb; ++f) {
+          const uint32_t kf = ws.bkey[f];
+          r += kf < ke;
+          dup |= kf == ke && f != e;
+        }
+        if (dup) {  // equal keys: corpus id order
+          const uint32_t te = tie(ws.bidx[e]);
+          for (int f = 0; f < nb; ++f)
+            if (f != e && ws.bkey[f] == ke) r += tie(ws.bidx[f]) < te;
+        }
+        if (r < need) {
+          emit(before + r, ws.bidx[e]);
+          mark(ws.bidx[e]);
+        }
+      }
+    }
+    __syncwarp();
+    return;
+  }
+  // ---- 3. exact radix select over the key bits
+  uint32_t prefix = 0;
+  int kk = take;
+#pragma unroll 1
+  for (int pass = 0; pass < 4; ++pass) {
+    const int shift = 24 - 8 * pass;
+    const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
+    for (int b = lane; b < 256; b += 32) ws.hist[b] = 0;
+    __syncwarp();
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const uint32_t k = i < n ? ws.keys[i] : 0u;
+      const bool m = i < n && (k & hmask) == prefix;
+      const unsigned dig = (k >> shift) & 255u;
+      const unsigned peers = __match_any_sync(0xffffffffu, m ? dig : 256u + lane);
+      if (m && (peers & lt_mask) == 0) atomicAdd(&ws.hist[dig], __popc(peers));
+    }
+    __syncwarp();
+    int c[8], tot = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) { c[j] = ws.hist[lane * 8 + j]; tot += c[j]; }
+    int incl = tot;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const bool own = incl - tot < kk && kk <= incl;
+    int bin = 0, bef = 0;
+    if (own) {
+      int run = incl - tot;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        if (run + c[j] >= kk) { bin = lane * 8 + j; bef = run; break; }
+        run += c[j];
+      }
+    }
+    const int src = __ffs(__ballot_sync(0xffffffffu, own)) - 1;
+    bin = __shfl_sync(0xffffffffu, bin, src);
+    bef = __shfl_sync(0xffffffffu, bef, src);
+    kk -= bef;
+    prefix |= (uint32_t)bin << shift;
+    __syncwarp();
+  }
+  // prefix == K*: keys below it are selected; kk of the keys equal to it, by tie
+  int nlt = 0, nt = 0;
+  for (int base = 0; base < n; base += 32) {
+    const int i = base + lane;
+    const uint32_t k = i < n ? ws.keys[i] : 0xFFFFFFFFu;
+    const bool lt = i < n && k < prefix, eq = i < n && k == prefix;
+    const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
+    if (lt) emit(nlt + __popc(bl & lt_mask), i);
+    if (eq) {
+      const int slot = nt + __popc(be & lt_mask);
+      if (slot < kWarpTieCap) ws.bidx[slot] = i;
+    }
+    if (ws.selbits && lane == 0) ws.selbits[base >> 5] = bl;
+    nlt += __popc(bl);
+    nt += __popc(be);
+  }
+  __syncwarp();
+  if (nt == kk) {  // every key equal to K* is selected
+    int cidx = 0;
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool eq = i < n && ws.keys[i] == prefix;
+      const unsigned be = __ballot_sync(0xffffffffu, eq);
+      if (eq) emit(nlt + cidx + __popc(be & lt_mask), i);
+      if (ws.selbits && lane == 0 && be) atomicOr(&ws.selbits[base >> 5], be);
+      cidx += __popc(be);
+    }
+  } else if (nt <= kWarpTieCap) {
+    uint32_t* tv = ws.bkey;
+    for (int j = lane; j < nt; j += 32) tv[j] = tie(ws.bidx[j]);
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int j = lane + 32 * u;
+      if (j < nt) {
+        int r = 0;
+        for (int f = 0; f < nt; ++f) r += tv[f] < tv[j];
+        if (r < kk) {
+          emit(nlt + r, ws.bidx[j]);
+          mark(ws.bidx[j]);
+        }
+      }
+    }
+  } else {  // more than kWarpTieCap equal keys at K*: rank by streaming (rare)
+    for (int base = 0; base < n; base += 32) {
+      const int i = base + lane;
+      const bool eq = i < n && ws.keys[i] == prefix;
+      if (eq) {
+        const uint32_t tv = tie(i);
+        int r = 0;
+        for (int f = 0; f < n; ++f) r += ws.keys[f] == prefix && tie(f) < tv;
+        if (r < kk) {
+          emit(nlt + r, i);
+          mark(i);
+        }
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// Per-warp slice of the dynamic shared memory of the warp kernels: staged keys
+// (stage_cap, may be 0), histogram, boundary buffers, selection bits.
+__host__ __device__ inline size_t warp_sel_bytes(int stage_cap, int bits_cap) {
+  return ((size_t)stage_cap * 4 + 256 * 4 + kWarpTieCap * 8 + (size_t)((bits_cap + 31) / 32) * 4 +
+          15) / 16 * 16;
+}
+__device__ inline WarpSel warp_sel_slice(unsigned char* base, int stage_cap, int bits_cap,
+                                         uint32_t*& stage) {
+  unsigned char* p = base + (size_t)(threadIdx.x >> 5) * warp_sel_bytes(stage_cap, bits_cap);
+  WarpSel ws;
+  stage = reinterpret_cast<uint32_t*>(p);
+  ws.keys = stage;
+  ws.hist = reinterpret_cast<int*>(stage + stage_cap);
+  ws.bidx = ws.hist + 256;
+  ws.bkey = reinterpret_cast<uint32_t*>(ws.bidx + kWarpTieCap);
+  ws.selbits = bits_cap > 0 ? ws.bkey + kWarpTieCap : nullptr;
+  return ws;
+}
+
+// Candidate index -> held position: largest c with offs[c] <= i (w+1 offsets, global).
+__device__ __forceinline__ int cand_pos(const DevIndexView& ix, const int* qoffq, const int* selq,
+                                        int w, int i) {
+  int lo = 0, hi = w;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(qoffq + mid) <= i) lo = mid; else hi = mid;
+  }
+  return __ldg(ix.cl_pos + __ldg(selq + lo)) + (i - __ldg(qoffq + lo));
+}
+
+// top-t of the scores (index.py:314-316), warp per query, for the re-ranking
+// searches: cluster-major (cand_idx + membership bits) or per-query (cand_pos,
+// plus the sharded phase-1 (key, id) lists).  Keys are staged on-chip when the
+// largest candidate list fits stage_cap, else read through L1.
+__global__ void k_select_topt_warp(SelectArgs a, int stage_cap, int bits_cap, int nq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wq = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wq >= nq) return;
+  const DevIndexView& ix = a.ix;
+  const int q = a.order ? a.order[wq] : wq;
+  const int w = a.w;
+  const int* qoffq = a.qoff + (size_t)q * (w + 1);
+  const int* selq = a.sel + (size_t)q * w;
+  const int N = __ldg(qoffq + w);
+  const int take = min(a.take_cap, N);
+  uint32_t* stage;
+  WarpSel ws = warp_sel_slice(smem_raw, stage_cap, bits_cap, stage);
+  const uint32_t* kq = a.keys + a.kbase[q];
+  if (stage_cap > 0) {
+    for (int i = lane; i < N; i += 32) stage[i] = __ldg(kq + i);
+    __syncwarp();
+  } else {
+    ws.keys = kq;
+  }
+  auto tie = [&](int i) { return __float_as_uint(__ldg(ix.pmeta + cand_pos(ix, qoffq, selq, w, i)).w); };
+  const int gq = a.q0 + q;
+  if (a.marks) {  // cluster-major re-rank: candidate indices + membership bits
+    int* oi = a.cand_idx + (size_t)q * a.take_cap;
+    if (take >= N) {
+      for (int i = lane; i < N; i += 32) oi[i] = i;
+      for (int j = lane; j < (N + 31) / 32; j += 32)
+        ws.selbits[j] = (j + 1) * 32 <= N ? 0xFFFFFFFFu : ((1u << (N & 31)) - 1u);
+    } else {
+      warp_select_smallest(ws, N, take, tie, [&](int slot, int i) { oi[slot] = i; });
+    }
+    __syncwarp();
+    // OR the bits into the query's (unaligned) run of the global bitmap; the edge
+    // words are shared with the neighbouring queries
+    const size_t kb = (size_t)a.kbase[q];
+    const unsigned sh = (unsigned)(kb & 31);
+    uint32_t* gm = a.marks + (kb >> 5);
+    for (int j = lane; j < (N + 31) / 32; j += 32) {
+      const uint32_t word = ws.selbits[j];
+      if (word) {
+        atomicOr(gm + j, word << sh);
+        if (sh) atomicOr(gm + j + 1, word >> (32 - sh));
+      }
+    }
+  } else {
+    int* outp = a.cand_pos + (size_t)q * a.take_cap;
+    uint32_t* ok = a.sel_keys ? a.sel_keys + (size_t)gq * a.take_cap : nullptr;
+    uint32_t* oid = a.sel_keys ? a.sel_ids + (size_t)gq * a.take_cap : nullptr;
+    auto emit = [&](int slot, int i) {
+      const int pos = cand_pos(ix, qoffq, selq, w, i);
+      outp[slot] = pos;
+      if (ok) { ok[slot] = ws.keys[i]; oid[slot] = __float_as_uint(__ldg(ix.pmeta + pos).w); }
+    };
+    if (take >= N) for (int i = lane; i < N; i += 32) emit(i, i);
+    else warp_select_smallest(ws, N, take, tie, emit);
+    if (ok && lane == 0) a.sel_count[gq] = take;
+  }
+  if (lane == 0) a.cand_n[q] = take;
+}
+
+// Warp bitonic sort (ascending) of 32*E u64 values, element e = lane + 32*j in v[j].
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint64_t (&v)[E]) {
+  const int lane = threadIdx.x & 31;
+  constexpr int P = 32 * E;
+#pragma unroll
+  for (int size = 2; size <= P; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      if (stride >= 32) {  // partner in the same lane, register j ^ (stride/32)
+        const int js = stride >> 5;
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int jp = j ^ js;
+          if (jp > j) {
+            const int e = lane + 32 * j;
+            const bool up = (e & size) == 0;
+            const uint64_t x = v[j], y = v[jp];
+            const bool sw = (x > y) == up;
+            v[j] = sw ? y : x;
+            v[jp] = sw ? x : y;
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+          const int e = lane + 32 * j;
+          const uint64_t o = __shfl_xor_sync(0xffffffffu, v[j], stride);
+          const bool up = (e & size) == 0;
+          const bool lower = (lane & stride) == 0;
+          // the lower element of a pair keeps the min when ascending
+          const bool keep_min = lower == up;
+          v[j] = keep_min ? (o < v[j] ? o : v[j]) : (o > v[j] ? o : v[j]);
+        }
+      }
+    }
+  }
+}
+
 // ---------------------------------------------------- cluster-major re-rank
 // Re-ranking is a (query x candidate-row) distance matrix restricted to each
 // query's top-t; rows of one cluster are shared by every query of its bucket
@@ -890,7 +1319,86 @@ __global__ void __launch_bounds__(FNT) k_topk_final(TopkFinalArgs a) {
   if (tid == 0) a.out_count[gq] = kk;
 }
 
+// Final top-k (index.py:320-322), warp per query: radix select of the k smallest
+// re-ranked distances, then a warp bitonic sort of their (distance, corpus id).
+template <int E>
+__global__ void k_topk_final_warp(TopkFinalArgs a, int cap, int nq) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int wq = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wq >= nq) return;
+  const DevIndexView& ix = a.ix;
+  const int q = a.order ? a.order[wq] : wq;
+  const int w = a.w;
+  const int* qoffq = a.qoff + (size_t)q * (w + 1);
+  const int* selq = a.sel + (size_t)q * w;
+  const int n = a.cand_n[q];
+  const int kk = min(a.k, n);
+  uint32_t* stage;
+  const WarpSel ws = warp_sel_slice(smem_raw, cap, 0, stage);
+  const uint32_t* dq = a.diss + a.kbase[q];
+  const int* ci = a.cand_idx + (size_t)q * a.take_cap;
+  for (int i = lane; i < n; i += 32) stage[i] = __ldg(dq + __ldg(ci + i));
+  __syncwarp();
+  auto tie = [&](int i) {
+    return __float_as_uint(__ldg(ix.pmeta + cand_pos(ix, qoffq, selq, w, __ldg(ci + i))).w);
+  };
+  uint64_t v[E];
+  if (kk >= n) {
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int i = lane + 32 * j;
+      v[j] = i < n ? ((uint64_t)stage[i] << 32) | tie(i) : ~0ull;
+    }
+  } else {
+    // the selected indices are emitted after the radix passes, when the 256-entry
+    // histogram is dead: it holds them (kk <= 32*E <= 256)
+    int* out = ws.hist;
+    warp_select_smallest(ws, n, kk, tie, [&](int slot, int i) { out[slot] = i; });
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int sl = lane + 32 * j;
+      v[j] = ~0ull;
+      if (sl < kk) {
+        const int i = out[sl];
+        v[j] = ((uint64_t)stage[i] << 32) | tie(i);
+      }
+    }
+  }
+  warp_bitonic_sort<E>(v);
+  const bool euclid = ix.metric == kMetricEuclidean;
+  const int gq = a.q0 + q;
+#pragma unroll
+  for (int j = 0; j < E; ++j) {
+    const int i = lane + 32 * j;
+    if (i < a.k) {
+      int64_t id = -1;
+      float sc = __int_as_float(0x7fc00000);
+      if (i < kk) {
+        id = (int64_t)(uint32_t)v[j];
+        const float df = unmono32((uint32_t)(v[j] >> 32));
+        sc = euclid ? df : -df;
+      }
+      a.out_ids[(size_t)gq * a.k + i] = id;
+      a.out_scores[(size_t)gq * a.k + i] = sc;
+    }
+  }
+  for (int i = 32 * E + lane; i < a.k; i += 32) {  // k beyond the sorted width: padding
+    a.out_ids[(size_t)gq * a.k + i] = -1;
+    a.out_scores[(size_t)gq * a.k + i] = __int_as_float(0x7fc00000);
+  }
+  if (lane == 0) a.out_count[gq] = kk;
+}
+
 // ---------------------------------------------------------------- launchers
+
+// RRG_WARP_SELECT=0 selects the CTA-per-query selections (k_select_topt, k_topk_final)
+static bool warp_select_ok() {
+  const char* e = getenv("RRG_WARP_SELECT");
+  return !(e && atoi(e) == 0);
+}
+
 
 void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
@@ -942,6 +1450,21 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
                          kMaxSmemPerCta - (int)at.sharedSizeBytes);
     done[dev] = 1;
   }
+  if (warp_select_ok() && h.rerank && h.kcap < 24 * 1024) {
+    // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
+    const int bits_cap = h.marks ? h.kcap : 0;
+    const int stage_cap = warp_sel_bytes(h.kcap, bits_cap) * 8 <= 56 * 1024 ? h.kcap : 0;
+    const size_t per = warp_sel_bytes(stage_cap, bits_cap);
+    constexpr int wpc = 8;
+    static int wdone[64] = {};
+    if (dev >= 0 && dev < 64 && !wdone[dev]) {
+      cudaFuncSetAttribute((const void*)k_select_topt_warp,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemPerCta);
+      wdone[dev] = 1;
+    }
+    k_select_topt_warp<<<(nq + wpc - 1) / wpc, 32 * wpc, per * wpc, st>>>(a, stage_cap, bits_cap, nq);
+    return;
+  }
   k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
 }
 
@@ -968,7 +1491,7 @@ bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster) {
 
 template <typename Kern>
 static void opt_in_smem(Kern* kern, int slot) {
-  static int done[8][64] = {};
+  static int done[16][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || done[slot][dev]) return;
@@ -1017,6 +1540,23 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
   a.cand_idx = h.cand_idx; a.cand_n = h.cand_n; a.take_cap = h.take_cap; a.k = h.k;
   a.out_ids = h.out_ids; a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
   a.order = h.order;
+  const size_t per = warp_sel_bytes(h.take_cap, 0);
+  if (warp_select_ok() && h.k <= 256 && per <= 24 * 1024) {
+    const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (56 * 1024) / per));
+    const unsigned grid = (unsigned)((nq + wpc - 1) / wpc);
+    const size_t sm = per * wpc;
+#define RRG_TKW(E, SLOT)                                                          \
+  do {                                                                            \
+    opt_in_smem(k_topk_final_warp<E>, SLOT);                                      \
+    k_topk_final_warp<E><<<grid, 32 * wpc, sm, st>>>(a, h.take_cap, nq);          \
+  } while (0)
+    if (h.k <= 32) RRG_TKW(1, 8);
+    else if (h.k <= 64) RRG_TKW(2, 9);
+    else if (h.k <= 128) RRG_TKW(4, 10);
+    else RRG_TKW(8, 11);
+#undef RRG_TKW
+    return;
+  }
   opt_in_smem(k_topk_final, 3);
   k_topk_final<<<nq, FNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a);
 }

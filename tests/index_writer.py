@@ -28,12 +28,20 @@ def _f32(rng, rows, cols):
     return (rng.standard_normal((rows, cols)) / np.sqrt(rows)).astype("<f4").tobytes()
 
 
+def _const(rng, rows, cols):
+    """Zero codes and a constant head row: every column scores the same."""
+    head = np.full(cols, 0.5, dtype="<f4")
+    scale = np.full(cols, 3.0, dtype="<f4")
+    return head.tobytes() + scale.tobytes() + np.zeros((rows, cols), np.int8).tobytes()
+
+
 def random_index(d, s, r, L, m, metric="euclidean", seed=0, exact_ivf=False, with_corpus=True,
-                 sizes=None, dup_rows=0, corpus_scale=1.0, quantize=True):
+                 sizes=None, dup_rows=0, corpus_scale=1.0, quantize=True, all_ties=False):
+    """all_ties: every point gets the same score and the same corpus row (tie-breaking by id)."""
     rng = np.random.default_rng(seed)
     mc = {"euclidean": 0, "ip": 1, "cosine": 2}[metric]
     flags = (1 if quantize else 0) | (2 if with_corpus else 0) | (8 if exact_ivf else 0)
-    factor = _quant if quantize else _f32
+    factor = _const if all_ties else (_quant if quantize else _f32)
     out = bytearray(b"RRRANN01")
     out += struct.pack("<BIIIIQI", mc, d, s, r, L, m, flags)
     W = (rng.standard_normal((d, s)) / np.sqrt(d)).astype("<f4")
@@ -44,6 +52,8 @@ def random_index(d, s, r, L, m, metric="euclidean", seed=0, exact_ivf=False, wit
         sizes = np.diff(np.concatenate([[0], cuts, [m]]))
     perm = rng.permutation(m)
     corpus = (rng.standard_normal((m, d)) * corpus_scale).astype("<f4")
+    if all_ties:
+        corpus[:] = corpus[0]
     for i in range(dup_rows):
         corpus[perm[2 * i]] = corpus[perm[2 * i + 1]]
     pos = 0

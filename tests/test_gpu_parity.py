@@ -414,7 +414,8 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "cluster+sync", "query", "cluster+regs", "cluster+tma"])
+@pytest.mark.parametrize("mode", ["cluster", "cluster+sync", "cluster+blocksel", "query",
+                                  "cluster+regs", "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -424,6 +425,8 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
     monkeypatch.setenv("RRG_SCORE_MODE", score_mode)
     if rerank_mode == "sync":  # cluster-major re-rank with register (not cp.async) row loads
         monkeypatch.setenv("RRG_RR_ASYNC", "0")
+    elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections
+        monkeypatch.setenv("RRG_WARP_SELECT", "0")
     elif rerank_mode:
         monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
@@ -510,3 +513,26 @@ def test_search_host_many_equals_single_calls(pkg, tmp_path):
         dev.search_host_many([q[:5], bad], 10, 3, 50)
     with pytest.raises(pkg.ParameterError, match="k must be >= 1"):
         dev.search_host_many([q[:5]], 0, 3, 50)
+
+
+@pytest.mark.parametrize("warp_select", ["1", "0"])
+@pytest.mark.parametrize("d,L,m", [(32, 5, 600), (768, 3, 700)])
+def test_all_scores_and_distances_tied(pkg, tmp_path, warp_select, d, L, m, monkeypatch):
+    """Every candidate has the same score and the same corpus row: top-t and top-k are
+    decided by corpus id alone (index.py:315,321 lexsort), through the many-ties paths."""
+    monkeypatch.setenv("RRG_WARP_SELECT", warp_select)
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    blob = random_index(d, 16, 8, L, m, "euclidean", seed=3, all_ties=True)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "ties", blob))
+    oidx = O.read_index(blob)
+    q = np.random.default_rng(1).standard_normal((9, d)).astype(F32)
+    for k, w, t, rr in [(10, L, 100, True), (7, 2, 50, True), (50, L, 300, True), (12, L, 1, False)]:
+        ids, sc, cnt = dev.search_host(q, k, w, t, rr)
+        ref = O.query_batch(oidx, q, k, w, t, rr)
+        for i, r in enumerate(ref):
+            c = int(cnt[i])
+            np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{(k, w, t, rr)} q{i}")
+            if rr:
+                np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))

@@ -1468,9 +1468,10 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
 }
 
+// measured on C2 (w=1, t=800): register loads 1.134 ms vs cp.async staging 1.249 ms
 static bool rerank_async() {
   const char* e = getenv("RRG_RR_ASYNC");
-  return !(e && atoi(e) == 0);
+  return e && atoi(e) == 1;
 }
 
 size_t cluster_rerank_smem(int d_stride, int mwords) {

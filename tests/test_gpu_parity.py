@@ -414,7 +414,7 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "cluster+sync", "cluster+blocksel", "query",
+@pytest.mark.parametrize("mode", ["cluster", "cluster+async", "cluster+blocksel", "query",
                                   "cluster+regs", "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
@@ -423,8 +423,8 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
     scoring (per-query re-rank), and the per-query register / TMA re-rank kernels."""
     score_mode, _, rerank_mode = mode.partition("+")
     monkeypatch.setenv("RRG_SCORE_MODE", score_mode)
-    if rerank_mode == "sync":  # cluster-major re-rank with register (not cp.async) row loads
-        monkeypatch.setenv("RRG_RR_ASYNC", "0")
+    if rerank_mode == "async":  # cluster-major re-rank with cp.async-staged row pairs
+        monkeypatch.setenv("RRG_RR_ASYNC", "1")
     elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections
         monkeypatch.setenv("RRG_WARP_SELECT", "0")
     elif rerank_mode:

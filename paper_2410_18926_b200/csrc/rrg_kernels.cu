@@ -48,17 +48,22 @@ __device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, do
                : "d"(a), "d"(b));
 }
 
-template <int EPI, bool BT, int WM = kGemmWM>
+// BK: K depth of a stage (8 or 16; 16 halves the barriers per K), pitch BK + 4 doubles.
+template <int WM, int BK>
+constexpr size_t gemm_smem_bytes() { return (size_t)2 * (32 * WM + MBN) * (BK + 4) * 8; }
+
+template <int EPI, bool BT, int WM = kGemmWM, int BK = MBK>
 __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm_dmma(const float* __restrict__ A, int lda,
                                                      const float* __restrict__ B, int ldb, int M,
                                                      int N, int K, float* __restrict__ outf,
                                                      double* __restrict__ outd, int ldo,
                                                      const double* __restrict__ rowterm,
                                                      const double* __restrict__ colterm) {
-  constexpr int MBM = 32 * WM, DMNT = 64 * WM;
-  constexpr int NA = (MBM * MBK) / DMNT, NB = (MBN * MBK + DMNT - 1) / DMNT;
-  __shared__ __align__(16) double As[2][MBM][MPITCH];  // [buf][m][k]
-  __shared__ __align__(16) double Bs[2][MBN][MPITCH];  // [buf][n][k]
+  constexpr int MBM = 32 * WM, DMNT = 64 * WM, PITCH = BK + 4;
+  constexpr int NA = (MBM * BK) / DMNT, NB = (MBN * BK + DMNT - 1) / DMNT;
+  extern __shared__ __align__(16) double gemm_sm[];
+  double (*As)[MBM][PITCH] = reinterpret_cast<double (*)[MBM][PITCH]>(gemm_sm);  // [buf][m][k]
+  double (*Bs)[MBN][PITCH] = reinterpret_cast<double (*)[MBN][PITCH]>(gemm_sm + 2 * MBM * PITCH);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1;  // WM x 2 warps of 32x32
   const int m0 = blockIdx.y * MBM, n0 = blockIdx.x * MBN;
@@ -72,7 +77,7 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
   auto gload = [&](int k0) {
 #pragma unroll
     for (int e = 0; e < NA; ++e) {  // A tile MBM x 8, k fastest
-      const int idx = tid + e * DMNT, r = idx / MBK, kk = idx % MBK;
+      const int idx = tid + e * DMNT, r = idx / BK, kk = idx % BK;
       const int gm = m0 + r, gk = k0 + kk;
       ra[e] = (gm < M && gk < K) ? __ldg(A + (size_t)gm * lda + gk) : 0.f;
     }
@@ -80,10 +85,10 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
     for (int e = 0; e < NB; ++e) {  // B tile 64 (n) x 8 (k)
       const int idx = tid + e * DMNT;
       int c, kk;
-      if (BT) { c = idx / MBK; kk = idx % MBK; } else { kk = idx / MBN; c = idx % MBN; }
+      if (BT) { c = idx / BK; kk = idx % BK; } else { kk = idx / MBN; c = idx % MBN; }
       const int gn = n0 + c, gk = k0 + kk;
       float v = 0.f;
-      if (idx < MBN * MBK && gn < N && gk < K)
+      if (idx < MBN * BK && gn < N && gk < K)
         v = BT ? __ldg(B + (size_t)gn * ldb + gk) : __ldg(B + (size_t)gk * ldb + gn);
       rb[e] = v;
     }
@@ -92,25 +97,25 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
 #pragma unroll
     for (int e = 0; e < NA; ++e) {
       const int idx = tid + e * DMNT;
-      As[buf][idx / MBK][idx % MBK] = (double)ra[e];
+      As[buf][idx / BK][idx % BK] = (double)ra[e];
     }
 #pragma unroll
     for (int e = 0; e < NB; ++e) {
       const int idx = tid + e * DMNT;
-      if (idx >= MBN * MBK) break;
-      if (BT) Bs[buf][idx / MBK][idx % MBK] = (double)rb[e];
+      if (idx >= MBN * BK) break;
+      if (BT) Bs[buf][idx / BK][idx % BK] = (double)rb[e];
       else Bs[buf][idx % MBN][idx / MBN] = (double)rb[e];
     }
   };
-  const int nk = (K + MBK - 1) / MBK;
+  const int nk = (K + BK - 1) / BK;
   gload(0);
   sstore(0);
   __syncthreads();
   for (int kt = 0; kt < nk; ++kt) {
     const int buf = kt & 1;
-    if (kt + 1 < nk) gload((kt + 1) * MBK);
+    if (kt + 1 < nk) gload((kt + 1) * BK);
 #pragma unroll
-    for (int ks = 0; ks < MBK; ks += 4) {
+    for (int ks = 0; ks < BK; ks += 4) {
       double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = As[buf][wm * 32 + i * 8 + (lane >> 2)][ks + (lane & 3)];
@@ -1184,11 +1189,39 @@ __global__ void k_scatter_rows(const float* __restrict__ src, int64_t nrows, int
 }
 
 // ===================================================================== launchers
+// One launch of k_gemm_dmma<EPI, BT, WM, BK> with its dynamic shared memory (opt-in
+// above 48 KB done once per instantiation and device).
+template <int EPI, bool BT, int WM, int BK>
+static void gemm_launch(dim3 grid, cudaStream_t st, const float* A, int lda, const float* B, int ldb,
+                        int M, int N, int K, float* outf, double* outd, int ldo, const double* rt,
+                        const double* ct) {
+  constexpr size_t sm = gemm_smem_bytes<WM, BK>();
+  static int done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    cudaFuncSetAttribute((const void*)k_gemm_dmma<EPI, BT, WM, BK>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    done[dev] = 1;
+  }
+  k_gemm_dmma<EPI, BT, WM, BK><<<grid, 64 * WM, sm, st>>>(A, lda, B, ldb, M, N, K, outf, outd, ldo,
+                                                          rt, ct);
+}
+
+// K depth per stage: 8 (default) or 16 (RRG_GEMM_BK=16) -- measured equal on C2
+// (projection 0.175 ms, routing 0.203 vs 0.207 ms): the DMMA pipe, not the barriers, bounds it
+static int gemm_bk() {
+  const char* e = getenv("RRG_GEMM_BK");
+  return (e && atoi(e) == 16) ? 16 : 8;
+}
+
 void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
                     cudaStream_t st) {
   dim3 grid((s + MBN - 1) / MBN, (nq + 32 * kGemmWM - 1) / (32 * kGemmWM));
-  k_gemm_dmma<EPI_PROJ, false><<<grid, 64 * kGemmWM, 0, st>>>(x, d, W, s, nq, s, d, xp, nullptr, s,
-                                                      nullptr, nullptr);
+  if (gemm_bk() == 16)
+    gemm_launch<EPI_PROJ, false, kGemmWM, 16>(grid, st, x, d, W, s, nq, s, d, xp, nullptr, s, nullptr, nullptr);
+  else
+    gemm_launch<EPI_PROJ, false, kGemmWM, 8>(grid, st, x, d, W, s, nq, s, d, xp, nullptr, s, nullptr, nullptr);
 }
 
 void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
@@ -1204,12 +1237,14 @@ void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s,
                        const double* pp, const double* cnorm, double* diss, cudaStream_t st) {
   constexpr int WM = 4;  // C2: 128x64 tiles measured 0.214 ms vs 96x64 0.220 ms
   dim3 grid((L + MBN - 1) / MBN, (nq + 32 * WM - 1) / (32 * WM));
-  if (metric == kMetricEuclidean)
-    k_gemm_dmma<EPI_L2, true, WM><<<grid, 64 * WM, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L, pp,
-                                                     cnorm);
-  else
-    k_gemm_dmma<EPI_NEGIP, true, WM><<<grid, 64 * WM, 0, st>>>(xp, s, cent, s, nq, L, s, nullptr, diss, L,
-                                                        nullptr, nullptr);
+  const bool bk16 = gemm_bk() == 16;
+  if (metric == kMetricEuclidean) {
+    if (bk16) gemm_launch<EPI_L2, true, WM, 16>(grid, st, xp, s, cent, s, nq, L, s, nullptr, diss, L, pp, cnorm);
+    else gemm_launch<EPI_L2, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, diss, L, pp, cnorm);
+  } else {
+    if (bk16) gemm_launch<EPI_NEGIP, true, WM, 16>(grid, st, xp, s, cent, s, nq, L, s, nullptr, diss, L, nullptr, nullptr);
+    else gemm_launch<EPI_NEGIP, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, diss, L, nullptr, nullptr);
+  }
 }
 
 void launch_gt_dist(const float* q, int M, const float* c, int N, int d, int metric,
@@ -1217,14 +1252,11 @@ void launch_gt_dist(const float* q, int M, const float* c, int N, int d, int met
   constexpr int WM = 4;
   dim3 grid((N + MBN - 1) / MBN, (M + 32 * WM - 1) / (32 * WM));
   if (metric == kMetricEuclidean)
-    k_gemm_dmma<EPI_GT_L2, true, WM><<<grid, 64 * WM, 0, st>>>(q, d, c, d, M, N, d, nullptr, out,
-                                                             (int)ldo, qq, cterm);
+    gemm_launch<EPI_GT_L2, true, WM, 16>(grid, st, q, d, c, d, M, N, d, nullptr, out, (int)ldo, qq, cterm);
   else if (metric == kMetricIp)
-    k_gemm_dmma<EPI_NEGIP, true, WM><<<grid, 64 * WM, 0, st>>>(q, d, c, d, M, N, d, nullptr, out,
-                                                             (int)ldo, nullptr, nullptr);
+    gemm_launch<EPI_NEGIP, true, WM, 16>(grid, st, q, d, c, d, M, N, d, nullptr, out, (int)ldo, nullptr, nullptr);
   else
-    k_gemm_dmma<EPI_GT_COS, true, WM><<<grid, 64 * WM, 0, st>>>(q, d, c, d, M, N, d, nullptr, out,
-                                                              (int)ldo, nullptr, cterm);
+    gemm_launch<EPI_GT_COS, true, WM, 16>(grid, st, q, d, c, d, M, N, d, nullptr, out, (int)ldo, nullptr, cterm);
 }
 
 // Opt in to the dynamic shared memory a launch may need (227 KB per CTA minus the

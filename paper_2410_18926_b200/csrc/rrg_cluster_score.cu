@@ -557,10 +557,28 @@ struct WarpSel {
 //     are ranked exactly by (key, tie) when they fit kWarpTieCap;
 //  3. otherwise (a dense boundary bucket, e.g. many equal keys) an exact 8-bit
 //     radix select over the keys, equal keys at the take-th ranked by tie.
-template <typename TieF, typename EmitF>
-__device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF tie, EmitF emit) {
+template <typename KeyF, typename TieF, typename EmitF>
+__device__ void warp_select_smallest(const WarpSel& ws, KeyF key, int n, int take, TieF tie,
+                                     EmitF emit) {
   const int lane = threadIdx.x & 31;
   const unsigned lt_mask = (1u << lane) - 1u;
+  // in-order sweep over 32-key chunks with four chunks' loads in flight:
+  // body(chunk base, i, valid, key) for every chunk (warp-uniform)
+  auto sweep = [&](auto&& body) {
+    for (int base = 0; base < n; base += 128) {
+      uint32_t kv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int i = base + 32 * u + lane;
+        kv[u] = i < n ? key(i) : 0xFFFFFFFFu;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b0 = base + 32 * u;
+        if (b0 < n) body(b0, b0 + lane, b0 + lane < n, kv[u]);
+      }
+    }
+  };
   auto mark = [&](int i) {
     if (ws.selbits) atomicOr(&ws.selbits[i >> 5], 1u << (i & 31));
   };
@@ -594,11 +612,9 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
   // first is re-bucketed over its own value span, which absorbs outliers that
   // stretch the first range)
   uint32_t lo = 0xFFFFFFFFu, hi = 0u;
-  for (int i = lane; i < n; i += 32) {
-    const uint32_t k = ws.keys[i];
-    lo = min(lo, k);
-    hi = max(hi, k);
-  }
+  sweep([&](int, int, bool valid, uint32_t k) {
+    if (valid) { lo = min(lo, k); hi = max(hi, k); }
+  });
   for (int o = 16; o > 0; o >>= 1) {
     lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
     hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
@@ -612,7 +628,9 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
   };
   for (int b = lane; b < 256; b += 32) ws.hist[b] = 0;
   __syncwarp();
-  for (int i = lane; i < n; i += 32) atomicAdd(&ws.hist[bucket(ws.keys[i])], 1);
+  sweep([&](int, int, bool valid, uint32_t k) {
+    if (valid) atomicAdd(&ws.hist[bucket(k)], 1);
+  });
   __syncwarp();
   int bb, before, cnt;
   boundary(bb, before, cnt);
@@ -630,10 +648,9 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
     const int take1 = take - before;
     for (int b = lane; b < 256; b += 32) ws.hist[b] = 0;
     __syncwarp();
-    for (int i = lane; i < n; i += 32) {
-      const uint32_t k = ws.keys[i];
-      if (bucket(k) == bb) atomicAdd(&ws.hist[bucket2(k)], 1);
-    }
+    sweep([&](int, int, bool valid, uint32_t k) {
+      if (valid && bucket(k) == bb) atomicAdd(&ws.hist[bucket2(k)], 1);
+    });
     __syncwarp();
     int before2, cnt2;
     {
@@ -675,10 +692,8 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
       return b2 < bb2 ? -1 : (b2 == bb2 ? 0 : 1);
     };
     int nlt = 0, nb = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      const uint32_t k = i < n ? ws.keys[i] : 0xFFFFFFFFu;
-      const int c = i < n ? cls(k) : 1;
+    sweep([&](int base, int i, bool valid, uint32_t k) {
+      const int c = valid ? cls(k) : 1;
       const bool lt = c < 0, eq = c == 0;
       const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
       if (lt) emit(nlt + __popc(bl & lt_mask), i);
@@ -690,7 +705,7 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
       if (ws.selbits && lane == 0) ws.selbits[base >> 5] = bl;
       nlt += __popc(bl);
       nb += __popc(be);
-    }
+    });
     __syncwarp();
     const int need = take - before;
 #pragma unroll
@@ -728,14 +743,12 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
     const uint32_t hmask = pass == 0 ? 0u : (0xFFFFFFFFu << (shift + 8));
     for (int b = lane; b < 256; b += 32) ws.hist[b] = 0;
     __syncwarp();
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      const uint32_t k = i < n ? ws.keys[i] : 0u;
-      const bool m = i < n && (k & hmask) == prefix;
+    sweep([&](int, int, bool valid, uint32_t k) {
+      const bool m = valid && (k & hmask) == prefix;
       const unsigned dig = (k >> shift) & 255u;
       const unsigned peers = __match_any_sync(0xffffffffu, m ? dig : 256u + lane);
       if (m && (peers & lt_mask) == 0) atomicAdd(&ws.hist[dig], __popc(peers));
-    }
+    });
     __syncwarp();
     int c[8], tot = 0;
 #pragma unroll
@@ -764,10 +777,8 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
   }
   // prefix == K*: keys below it are selected; kk of the keys equal to it, by tie
   int nlt = 0, nt = 0;
-  for (int base = 0; base < n; base += 32) {
-    const int i = base + lane;
-    const uint32_t k = i < n ? ws.keys[i] : 0xFFFFFFFFu;
-    const bool lt = i < n && k < prefix, eq = i < n && k == prefix;
+  sweep([&](int base, int i, bool valid, uint32_t k) {
+    const bool lt = valid && k < prefix, eq = valid && k == prefix;
     const unsigned bl = __ballot_sync(0xffffffffu, lt), be = __ballot_sync(0xffffffffu, eq);
     if (lt) emit(nlt + __popc(bl & lt_mask), i);
     if (eq) {
@@ -777,18 +788,17 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
     if (ws.selbits && lane == 0) ws.selbits[base >> 5] = bl;
     nlt += __popc(bl);
     nt += __popc(be);
-  }
+  });
   __syncwarp();
   if (nt == kk) {  // every key equal to K* is selected
     int cidx = 0;
-    for (int base = 0; base < n; base += 32) {
-      const int i = base + lane;
-      const bool eq = i < n && ws.keys[i] == prefix;
+    sweep([&](int base, int i, bool valid, uint32_t k) {
+      const bool eq = valid && k == prefix;
       const unsigned be = __ballot_sync(0xffffffffu, eq);
       if (eq) emit(nlt + cidx + __popc(be & lt_mask), i);
       if (ws.selbits && lane == 0 && be) atomicOr(&ws.selbits[base >> 5], be);
       cidx += __popc(be);
-    }
+    });
   } else if (nt <= kWarpTieCap) {
     uint32_t* tv = ws.bkey;
     for (int j = lane; j < nt; j += 32) tv[j] = tie(ws.bidx[j]);
@@ -808,11 +818,11 @@ __device__ void warp_select_smallest(const WarpSel& ws, int n, int take, TieF ti
   } else {  // more than kWarpTieCap equal keys at K*: rank by streaming (rare)
     for (int base = 0; base < n; base += 32) {
       const int i = base + lane;
-      const bool eq = i < n && ws.keys[i] == prefix;
+      const bool eq = i < n && key(i) == prefix;
       if (eq) {
         const uint32_t tv = tie(i);
         int r = 0;
-        for (int f = 0; f < n; ++f) r += ws.keys[f] == prefix && tie(f) < tv;
+        for (int f = 0; f < n; ++f) r += key(f) == prefix && tie(f) < tv;
         if (r < kk) {
           emit(nlt + r, i);
           mark(i);
@@ -872,12 +882,8 @@ __global__ void k_select_topt_warp(SelectArgs a, int stage_cap, int bits_cap, in
   uint32_t* stage;
   WarpSel ws = warp_sel_slice(smem_raw, stage_cap, bits_cap, stage);
   const uint32_t* kq = a.keys + a.kbase[q];
-  if (stage_cap > 0) {
-    for (int i = lane; i < N; i += 32) stage[i] = __ldg(kq + i);
-    __syncwarp();
-  } else {
-    ws.keys = kq;
-  }
+  auto key = [&](int i) { return __ldg(kq + i); };  // read through L1 (4 chunks in flight)
+  (void)stage;
   auto tie = [&](int i) { return __float_as_uint(__ldg(ix.pmeta + cand_pos(ix, qoffq, selq, w, i)).w); };
   const int gq = a.q0 + q;
   if (a.marks) {  // cluster-major re-rank: candidate indices + membership bits
@@ -887,7 +893,7 @@ __global__ void k_select_topt_warp(SelectArgs a, int stage_cap, int bits_cap, in
       for (int j = lane; j < (N + 31) / 32; j += 32)
         ws.selbits[j] = (j + 1) * 32 <= N ? 0xFFFFFFFFu : ((1u << (N & 31)) - 1u);
     } else {
-      warp_select_smallest(ws, N, take, tie, [&](int slot, int i) { oi[slot] = i; });
+      warp_select_smallest(ws, key, N, take, tie, [&](int slot, int i) { oi[slot] = i; });
     }
     __syncwarp();
     // OR the bits into the query's (unaligned) run of the global bitmap; the edge
@@ -909,10 +915,10 @@ __global__ void k_select_topt_warp(SelectArgs a, int stage_cap, int bits_cap, in
     auto emit = [&](int slot, int i) {
       const int pos = cand_pos(ix, qoffq, selq, w, i);
       outp[slot] = pos;
-      if (ok) { ok[slot] = ws.keys[i]; oid[slot] = __float_as_uint(__ldg(ix.pmeta + pos).w); }
+      if (ok) { ok[slot] = key(i); oid[slot] = __float_as_uint(__ldg(ix.pmeta + pos).w); }
     };
     if (take >= N) for (int i = lane; i < N; i += 32) emit(i, i);
-    else warp_select_smallest(ws, N, take, tie, emit);
+    else warp_select_smallest(ws, key, N, take, tie, emit);
     if (ok && lane == 0) a.sel_count[gq] = take;
   }
   if (lane == 0) a.cand_n[q] = take;
@@ -1354,7 +1360,8 @@ __global__ void k_topk_final_warp(TopkFinalArgs a, int cap, int nq) {
     // the selected indices are emitted after the radix passes, when the 256-entry
     // histogram is dead: it holds them (kk <= 32*E <= 256)
     int* out = ws.hist;
-    warp_select_smallest(ws, n, kk, tie, [&](int slot, int i) { out[slot] = i; });
+    warp_select_smallest(ws, [&](int i) { return stage[i]; }, n, kk, tie,
+                         [&](int slot, int i) { out[slot] = i; });
     __syncwarp();
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -1453,7 +1460,7 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   if (warp_select_ok() && h.rerank && h.kcap < 24 * 1024) {
     // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
     const int bits_cap = h.marks ? h.kcap : 0;
-    const int stage_cap = warp_sel_bytes(h.kcap, bits_cap) * 8 <= 56 * 1024 ? h.kcap : 0;
+    const int stage_cap = 0;  // keys are read through L1
     const size_t per = warp_sel_bytes(stage_cap, bits_cap);
     constexpr int wpc = 8;
     static int wdone[64] = {};

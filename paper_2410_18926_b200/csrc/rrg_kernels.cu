@@ -241,6 +241,32 @@ __global__ void __launch_bounds__(NT) k_route_select(const double* __restrict__ 
   }
 }
 
+// w == 1: the nearest cluster by (dissimilarity, cluster id) -- argsort(stable)[0]
+// (cluster.py:263-264) -- one warp per query, a coalesced sweep of the row and a
+// shuffle argmin; no CTA barriers.
+__global__ void k_route_nearest(const double* __restrict__ diss, int nq, int L,
+                                int* __restrict__ sel, int* __restrict__ primary) {
+  const int q = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const double* row = diss + (size_t)q * L;
+  uint64_t bk = ~0ull;
+  int bi = 0x7fffffff;
+  for (int i = lane; i < L; i += 32) {  // ascending ids per lane: strict < keeps the lowest
+    const uint64_t k = mono64(__ldg(row + i));
+    if (k < bk) { bk = k; bi = i; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const uint64_t ok = __shfl_xor_sync(0xffffffffu, bk, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ok < bk || (ok == bk && oi < bi)) { bk = ok; bi = oi; }
+  }
+  if (lane == 0) {
+    sel[q] = bi;
+    primary[q] = bi;
+  }
+}
+
 // ======================================================== query bucketing
 // Counting sort of the batch by nearest cluster (histogram, exclusive scan,
 // scatter), one CTA.  The scoring and re-rank CTAs then visit queries in bucket
@@ -1278,6 +1304,10 @@ size_t route_select_smem(int L) { return (size_t)L * 8 + (size_t)L * 4 + 16; }
 
 void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
                          cudaStream_t st) {
+  if (w == 1) {
+    k_route_nearest<<<(nq + 7) / 8, 256, 0, st>>>(diss, nq, L, sel, primary);
+    return;
+  }
   allow_smem(k_route_select<256>, 0);
   k_route_select<256><<<nq, 256, route_select_smem(L), st>>>(diss, L, w, sel, primary);
 }

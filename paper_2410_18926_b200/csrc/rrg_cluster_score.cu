@@ -56,28 +56,50 @@ __global__ void k_cand_offsets(DevIndexView ix, const int* __restrict__ sel, int
 constexpr int PNT = 1024;
 constexpr int kPairsPerItem = 32;
 
+// In-place exclusive scan of a[0..n) by the whole block (a contiguous run per
+// thread, a shuffle scan of the run sums); *total = sum (all threads call it).
 __device__ void block_exclusive_scan_inplace(int* a, int n, int* total) {
-  // one warp scans (n small: L or Q); carry across 32-element chunks
-  if (threadIdx.x < 32) {
-    const int lane = threadIdx.x;
-    int carry = 0;
-    for (int b = 0; b < n; b += 32) {
-      int i = b + lane;
-      int v = i < n ? a[i] : 0, incl = v;
-      for (int o = 1; o < 32; o <<= 1) {
-        int t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (i < n) a[i] = carry + incl - v;
-      carry += __shfl_sync(0xffffffffu, incl, 31);
-    }
-    if (lane == 0) *total = carry;
+  __shared__ int wsum[33];
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int b0 = min(n, tid * per), b1 = min(n, b0 + per);
+  int sum = 0;
+  for (int i = b0; i < b1; ++i) sum += a[i];
+  int incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
   }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    const int v = lane < nt / 32 ? wsum[lane] : 0;
+    int iv = v;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, iv, o);
+      if (lane >= o) iv += t;
+    }
+    wsum[lane] = iv - v;
+    if (lane == 31) wsum[32] = iv;
+  }
+  __syncthreads();
+  int run = wsum[warp] + incl - sum;
+  for (int i = b0; i < b1; ++i) {
+    const int v = a[i];
+    a[i] = run;
+    run += v;
+  }
+  if (tid == 0) *total = wsum[32];
   __syncthreads();
 }
 
+// Scoring work items split a cluster's points into chunks of kScorePts (the largest
+// clusters would otherwise set the tail of the persistent grid).
+constexpr int kScorePts = 512;
+
 __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel, int nq, int w,
-                                                     int L, const int* __restrict__ ncand,
+                                                     int L, const int* __restrict__ cl_pos,
+                                                     const int* __restrict__ ncand,
                                                      int* __restrict__ pair_off,   // L+1
                                                      int* __restrict__ item_off,   // L+1
                                                      int* __restrict__ pairs,      // nq*w
@@ -93,7 +115,8 @@ __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel
   __syncthreads();
   for (int i = threadIdx.x; i < L; i += PNT) {
     cur[i] = cnt[i];
-    item_off[i] = (cnt[i] + kPairsPerItem - 1) / kPairsPerItem;
+    const int m = cl_pos[i + 1] - cl_pos[i];
+    item_off[i] = ((cnt[i] + kPairsPerItem - 1) / kPairsPerItem) * ((m + kScorePts - 1) / kScorePts);
   }
   __syncthreads();
   block_exclusive_scan_inplace(cur, L, &tot);
@@ -157,9 +180,13 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
       if (a.item_off[mid] <= item) lo = mid; else hi = mid;
     }
     const int l = lo;
-    const int j0 = a.pair_off[l] + (item - a.item_off[l]) * kPairsPerItem;
+    const int p0 = ix.cl_pos[l], mcl = ix.cl_pos[l + 1] - p0;
+    const int npc = (mcl + kScorePts - 1) / kScorePts;
+    const int local = item - a.item_off[l];
+    const int j0 = a.pair_off[l] + (local / npc) * kPairsPerItem;
     const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
-    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    const int pbeg = (local % npc) * kScorePts, pend = min(mcl, pbeg + kScorePts);
+    const int m = pend - pbeg;
     const bool rrr = ix.cl_kind[l] == kKindRrr;
     if (tid < np) {
       const int pr = a.pairs[j0 + tid];
@@ -216,7 +243,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
       }
       __syncthreads();
       // stage B: thread per point, codes/meta loaded once, all np queries scored
-      for (int p = tid; p < m; p += CNT) {
+      for (int p = pbeg + tid; p < pend; p += CNT) {
         const int gp = p0 + p;
         const float4 meta = __ldg(ix.pmeta + gp);
         int4 b[4];
@@ -246,7 +273,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
       // exact model: raw_p = codes_x . A[:, p] over s_pad bytes (rrr.py:103-113)
       const int x0 = ix.cl_aidx[l];
       const int nvec = s_pad / 16;
-      for (int p = tid; p < m; p += CNT) {
+      for (int p = pbeg + tid; p < pend; p += CNT) {
         const int gp = p0 + p;
         const float4 meta = __ldg(ix.pmeta + gp);
         const int4* xw = reinterpret_cast<const int4*>(ix.xcodes + (size_t)(x0 + p) * s_pad);
@@ -298,9 +325,13 @@ __global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
       if (a.item_off[mid] <= item) lo = mid; else hi = mid;
     }
     const int l = lo;
-    const int j0 = a.pair_off[l] + (item - a.item_off[l]) * kPairsPerItem;
+    const int p0 = ix.cl_pos[l], mcl = ix.cl_pos[l + 1] - p0;
+    const int npc = (mcl + kScorePts - 1) / kScorePts;
+    const int local = item - a.item_off[l];
+    const int j0 = a.pair_off[l] + (local / npc) * kPairsPerItem;
     const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
-    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    const int pbeg = (local % npc) * kScorePts, pend = min(mcl, pbeg + kScorePts);
+    const int m = pend - pbeg;
     if (tid < np) {
       const int pr = a.pairs[j0 + tid];
       const int q = pr / a.w, c = pr % a.w;
@@ -323,7 +354,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
       }
       __syncthreads();
       // yhat = inter @ B: thread per point, B^T row held in registers
-      for (int p = tid; p < m; p += CNT) {
+      for (int p = pbeg + tid; p < pend; p += CNT) {
         const int gp = p0 + p;
         const float4 meta = __ldg(ix.pmeta + gp);
         float b[kMaxRc];
@@ -347,7 +378,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
       // exact model: yhat = x @ A[:, p] over s (rrr.py:103-113)
       const int x0 = ix.cl_aidx[l];
       const int n4 = s / 4;
-      for (int p = tid; p < m; p += CNT) {
+      for (int p = pbeg + tid; p < pend; p += CNT) {
         const int gp = p0 + p;
         const float4 meta = __ldg(ix.pmeta + gp);
         const float* xr = ix.xf + (size_t)(x0 + p) * s_pad;
@@ -1410,7 +1441,7 @@ static bool warp_select_ok() {
 void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
   k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand);
-  k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, h.ncand, h.pair_off,
+  k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off,
                                                   h.item_off, h.pairs, h.kbase);
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
   ClusterScoreArgs a;

@@ -360,6 +360,27 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.ascale = ix->upload(ascale);
   v.bt = ix->upload(bt);
   v.xcodes = ix->upload(xc);
+  {  // W^T slice planes for the tensor-core projection (s x d, rows = columns of W)
+    std::vector<float> wt((size_t)s * d);
+    for (int i = 0; i < d; ++i)
+      for (int j = 0; j < s; ++j) wt[(size_t)j * d + i] = hm.projection[(size_t)i * s + j];
+    float* dwt = ix->upload(wt);
+    int8_t* planes = static_cast<int8_t*>(ix->dalloc(sliced_plane_bytes(s, d, false)));
+    int* exps = static_cast<int*>(ix->dalloc((size_t)sliced_rows_pad(s, false) * 4));
+    launch_slice_rows(dwt, s, d, d, false, planes, exps, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    v.wt_planes = planes;
+    v.wt_exps = exps;
+    // centroid slice planes (L x s) for the tensor-core routing
+    int8_t* cpl = static_cast<int8_t*>(ix->dalloc(sliced_plane_bytes(L, s, false)));
+    int* cex = static_cast<int*>(ix->dalloc((size_t)sliced_rows_pad(L, false) * 4));
+    launch_slice_rows(v.cent, L, s, s, false, cpl, cex, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    v.cent_planes = cpl;
+    v.cent_exps = cex;
+  }
   v.quantized = quant ? 1 : 0;
   v.atf = quant ? nullptr : ix->upload(atf);
   v.btf = quant ? nullptr : ix->upload(btf);
@@ -640,8 +661,46 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
 
 // ------------------------------------------------------------------ search
 
+// Projection / routing GEMM engines: the int8 tensor cores (k_gemm_sliced: f64-exact
+// 7-bit slices, tcgen05 + TMEM) or the FP64 DMMA GEMM (k_gemm_dmma).  Measured on C2
+// (10k queries): projection 0.162 ms sliced vs 0.175 ms DMMA, routing 0.220 ms sliced
+// vs 0.203 ms DMMA -- so the defaults are sliced projection, DMMA routing.
+// RRG_PROJ / RRG_ROUTE = sliced|dmma choose each; RRG_GEMM = sliced|dmma sets both.
+static bool gemm_choice(const char* var, bool dflt) {
+  const char* e = getenv("RRG_GEMM");
+  if (!e) e = getenv(var);
+  if (!e) return dflt;
+  return strcmp(e, "sliced") == 0;
+}
+bool sliced_projection() { return gemm_choice("RRG_PROJ", true); }
+bool sliced_routing() { return gemm_choice("RRG_ROUTE", false); }
+
+// Query sub-range bounds of the front stages (and the host entry's copy pieces):
+// multiples of the sliced GEMM's 128-row blocks, so a piece's slice planes are a
+// contiguous run of blocks.
+int64_t piece_bound(int64_t n, int j, int nsub) {
+  if (j >= nsub) return n;
+  return (n * j / nsub) / 128 * 128;
+}
+
+// Routing dissimilarities of n projected queries: sliced tensor-core GEMM (xp slices in
+// qpl/qex) or the DMMA GEMM.
+void route_dist(const DevIndexView& v, const float* xp, int n, const double* pp, double* diss,
+                int8_t* qpl, int* qex, cudaStream_t st) {
+  if (qpl && sliced_routing()) {
+    launch_slice_rows(xp, n, v.s, v.s, true, qpl, qex, st);
+    launch_gemm_sliced(qpl, qex, n, v.cent_planes, v.cent_exps, v.L, v.s,
+                       v.metric == kMetricEuclidean ? EPI_L2 : EPI_NEGIP, nullptr, diss, v.L, pp,
+                       v.cnorm, st);
+  } else {
+    launch_route_dist(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
+  }
+}
+
 struct Plan {
   int64_t qc;      // queries per chunk
+  bool sliced_proj;
+  size_t off_qpl, off_qex;
   int take_cap;
   int smem_cap;
   int64_t gcap;    // global overflow capacity per query (0 if none)
@@ -697,6 +756,11 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   p.off_gp = carve(Q * p.gcap * 4);
   p.off_prim = carve(Q * 4);
   p.off_order = carve(Q * 4);
+  p.sliced_proj = sliced_projection() || sliced_routing();  // slice-plane workspace needed
+  if (p.sliced_proj) {
+    p.off_qpl = carve(sliced_plane_bytes((int)Q, v.d, true));
+    p.off_qex = carve((size_t)sliced_rows_pad((int)Q, true) * 4);
+  }
   // scoring strategy: cluster-major (bucketed pairs, factors staged once per
   // cluster) unless RRG_SCORE_MODE=query selects the fused query-major kernel
   {
@@ -796,21 +860,35 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
     // events they run per arriving sub-range, overlapping the remaining H2D copies
     const int nsub = (in_ready && n == nq) ? (int)in_ready->size() : 1;
     for (int j = 0; j < nsub; ++j) {
-      const int s0 = (int)((int64_t)n * j / nsub), s1 = (int)((int64_t)n * (j + 1) / nsub);
+      const int s0 = (int)piece_bound(n, j, nsub), s1 = (int)piece_bound(n, j + 1, nsub);
       const int ns = s1 - s0;
       if (ns <= 0) continue;
       if (in_ready)  // copies are in order on one stream: the last event covers them all
         CUDA_TRY(cudaStreamWaitEvent(st, (*in_ready)[nsub > 1 ? j : in_ready->size() - 1], 0));
       const float* xs = x + (int64_t)s0 * v.d;
       float* xps = xp + (int64_t)s0 * v.s;
-      staged(0, st, [&] { launch_project(xs, v.W, ns, v.d, v.s, xps, st); });
+      // this piece's run of 128-row slice-plane blocks (s0 is a multiple of 128)
+      int8_t* qpl_d = p.sliced_proj ? reinterpret_cast<int8_t*>(base + p.off_qpl) +
+                                          (s0 / 128) * sliced_block_bytes(v.d, true) : nullptr;
+      int8_t* qpl_s = p.sliced_proj ? reinterpret_cast<int8_t*>(base + p.off_qpl) +
+                                          (s0 / 128) * sliced_block_bytes(v.s, true) : nullptr;
+      int* qex = p.sliced_proj ? reinterpret_cast<int*>(base + p.off_qex) + s0 : nullptr;
+      if (sliced_projection()) {
+        int8_t* qpl = qpl_d;
+        staged(0, st, [&] { launch_slice_rows(xs, ns, v.d, v.d, true, qpl, qex, st); });
+        staged(0, st, [&] {
+          launch_gemm_sliced(qpl, qex, ns, v.wt_planes, v.wt_exps, v.s, v.d, EPI_PROJ, xps, nullptr,
+                             v.s, nullptr, nullptr, st);
+        });
+      } else {
+        staged(0, st, [&] { launch_project(xs, v.W, ns, v.d, v.s, xps, st); });
+      }
       staged(1, st, [&] {
         launch_prep(xps, xs, ns, v.s, v.s_pad, v.d, qcodes + (int64_t)s0 * v.s_pad, qscale + s0,
                     qhead + s0, pp + s0, xx + s0, st, nonfinite);
       });
       staged(2, st, [&] {
-        launch_route_dist(xps, v.cent, ns, v.L, v.s, v.metric, pp + s0, v.cnorm,
-                          diss + (int64_t)s0 * v.L, st);
+        route_dist(v, xps, ns, pp + s0, diss + (int64_t)s0 * v.L, qpl_s, qex, st);
       });
       staged(3, st, [&] {
         launch_route_select(diss + (int64_t)s0 * v.L, ns, v.L, w, sel + (int64_t)s0 * w, prim + s0, st);
@@ -1174,7 +1252,7 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     CUDA_TRY(cudaMemsetAsync(dflag, 0, sizeof(int), h.st));
     std::vector<cudaEvent_t> in_ready;
     for (int j = 0; j < nsub; ++j) {
-      const int64_t s0 = nq * j / nsub, s1 = nq * (j + 1) / nsub;
+      const int64_t s0 = piece_bound(nq, j, nsub), s1 = piece_bound(nq, j + 1, nsub);
       CUDA_TRY(cudaMemcpyAsync(dq + s0 * dim, queries + s0 * dim, (size_t)(s1 - s0) * dim * 4,
                                cudaMemcpyHostToDevice, h.cs));
       CUDA_TRY(cudaEventRecord(h.ev[j], h.cs));
@@ -1336,7 +1414,19 @@ int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq, float* 
     float* xx = nullptr;
     CUDA_TRY(cudaMallocAsync(&pp, std::max<int64_t>(nq, 1) * 8, st));
     CUDA_TRY(cudaMallocAsync(&xx, std::max<int64_t>(nq, 1) * 4, st));
-    launch_project(queries, v.W, (int)nq, v.d, v.s, xp, st);
+    int8_t* qpl = nullptr;
+    int* qex = nullptr;
+    if (sliced_projection() && nq > 0) {
+      CUDA_TRY(cudaMallocAsync(&qpl, sliced_plane_bytes((int)nq, v.d, true), st));
+      CUDA_TRY(cudaMallocAsync(&qex, (size_t)sliced_rows_pad((int)nq, true) * 4, st));
+      launch_slice_rows(queries, (int)nq, v.d, v.d, true, qpl, qex, st);
+      launch_gemm_sliced(qpl, qex, (int)nq, v.wt_planes, v.wt_exps, v.s, v.d, EPI_PROJ, xp, nullptr,
+                         v.s, nullptr, nullptr, st);
+      CUDA_TRY(cudaFreeAsync(qpl, st));
+      CUDA_TRY(cudaFreeAsync(qex, st));
+    } else {
+      launch_project(queries, v.W, (int)nq, v.d, v.s, xp, st);
+    }
     launch_prep(xp, queries, (int)nq, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(pp, st));
@@ -1359,7 +1449,17 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int
     float* dummy = nullptr;
     CUDA_TRY(cudaMallocAsync(&dummy, std::max<int64_t>(nq, 1) * 16, st));
     launch_prep(xp, xp, (int)nq, v.s, v.s_pad, v.s, qc, dummy, dummy + nq, pp, dummy + 2 * nq, st);
-    launch_route_dist(xp, v.cent, (int)nq, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
+    int8_t* qpl = nullptr;
+    int* qex = nullptr;
+    if (sliced_routing()) {
+      CUDA_TRY(cudaMallocAsync(&qpl, sliced_plane_bytes((int)nq, v.s, true), st));
+      CUDA_TRY(cudaMallocAsync(&qex, (size_t)sliced_rows_pad((int)nq, true) * 4, st));
+    }
+    route_dist(v, xp, (int)nq, pp, diss, qpl, qex, st);
+    if (qpl) {
+      CUDA_TRY(cudaFreeAsync(qpl, st));
+      CUDA_TRY(cudaFreeAsync(qex, st));
+    }
     launch_route_select(diss, (int)nq, v.L, w, selected, reinterpret_cast<int*>(dummy + 3 * nq), st);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaFreeAsync(dummy, st));

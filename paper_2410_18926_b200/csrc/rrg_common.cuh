@@ -63,6 +63,12 @@ struct DevIndexView {
   const float* atf;  // [n_rrr][r][s_pad]
   const float* btf;  // [P][r_pad]
   const float* xf;   // [P_exact][s_pad]
+  // W^T as 8 tiled int8 slice planes + per-row exponents (rrg_sliced_gemm.cu): the
+  // tensor-core projection (RRG_PROJ=sliced)
+  const int8_t* wt_planes;
+  const int* wt_exps;
+  const int8_t* cent_planes;  // centroids (L x s), same slicing, for the routing GEMM
+  const int* cent_exps;
 };
 
 // ---------------------------------------------------------------- numerics

@@ -191,4 +191,16 @@ void launch_gt_select(const GtSelectHost& h, int nq, cudaStream_t st);
 void launch_gt_dist(const float* q, int M, const float* c, int N, int d, int metric,
                     const double* qq, const double* cterm, double* out, int64_t ldo, cudaStream_t st);
 
+
+// -------------------------------------- sliced int8 tensor-core GEMM (rrg_sliced_gemm.cu)
+int sliced_kchunks(int K);
+int sliced_rows_pad(int rows, bool a_operand);
+size_t sliced_plane_bytes(int rows, int K, bool a_operand);
+size_t sliced_block_bytes(int K, bool a_operand);  // one 128- (A) / 64-row (B) block
+void launch_slice_rows(const float* x, int rows, int K, int ld, bool a_operand, int8_t* planes,
+                       int* exps, cudaStream_t st);
+void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* b, const int* b_exp,
+                        int N, int K, int epi, float* outf, double* outd, int64_t ldo,
+                        const double* rowterm, const double* colterm, cudaStream_t st);
+
 }  // namespace rrg

@@ -414,8 +414,8 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "cluster+async", "cluster+blocksel", "query",
-                                  "cluster+regs", "cluster+tma"])
+@pytest.mark.parametrize("mode", ["cluster", "cluster+async", "cluster+blocksel", "cluster+dmma",
+                                  "cluster+slicedroute", "query", "cluster+regs", "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -427,6 +427,10 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
         monkeypatch.setenv("RRG_RR_ASYNC", "1")
     elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections
         monkeypatch.setenv("RRG_WARP_SELECT", "0")
+    elif rerank_mode == "dmma":  # FP64 DMMA projection + routing GEMMs
+        monkeypatch.setenv("RRG_GEMM", "dmma")
+    elif rerank_mode == "slicedroute":  # int8 tensor-core (sliced) projection + routing
+        monkeypatch.setenv("RRG_GEMM", "sliced")
     elif rerank_mode:
         monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
@@ -536,3 +540,58 @@ def test_all_scores_and_distances_tied(pkg, tmp_path, warp_select, d, L, m, monk
             np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{(k, w, t, rr)} q{i}")
             if rr:
                 np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))
+
+
+@pytest.mark.parametrize("case", QUANT_CASES + F32_CASES)
+def test_sliced_projection_matches_golden(pkg, tmp_path, case, monkeypatch):
+    """RRG_PROJ=sliced: the projection on the int8 tensor cores (tcgen05 kind::i8, 8 exact
+    7-bit slices per operand, int32 levels in TMEM, f64 epilogue) reproduces the reference's
+    f32(f64(x) @ f64(W)) bit for bit, and the whole search stays exact."""
+    monkeypatch.setenv("RRG_GEMM", "sliced")
+    g, dev = _golden_index(pkg, tmp_path, case)
+    x = torch.from_numpy(g["queries"][:3]).cuda()
+    xp = dev.stage_project(x)[0]
+    torch.cuda.synchronize()
+    xp = xp.cpu().numpy()
+    for i in range(3):
+        np.testing.assert_array_equal(xp[i].view(np.int32), g[f"trace{i}_xp"].view(np.int32))
+    sel = dev.stage_route(torch.from_numpy(xp).cuda(), min(4, dev.n_clusters)).cpu().numpy()
+    for i in range(3):  # routing on the same tensor-core path
+        assert set(sel[i].tolist()) == set(g[f"trace{i}_selected"].tolist())
+    if "f32" in case:
+        return
+    for pi, (k, w, t, rr) in enumerate(g["params"]):
+        if f"p{pi}_ids" not in g or not rr or dev.metric != "euclidean":
+            continue
+        k, w, t = int(k), min(int(w), dev.n_clusters), int(t)
+        q = torch.from_numpy(g["queries"]).cuda()
+        ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(q, k, w, t, True))
+        np.testing.assert_array_equal(cnt, g[f"p{pi}_count"])
+        for i in range(len(cnt)):
+            c = int(cnt[i])
+            np.testing.assert_array_equal(ids[i, :c], g[f"p{pi}_ids"][i, :c])
+
+
+@pytest.mark.parametrize("d,s", [(768, 256), (960, 64), (100, 20), (1536, 64), (33, 33)])
+def test_sliced_projection_equals_dmma(pkg, tmp_path, d, s, monkeypatch):
+    """Tensor-core sliced projection vs the FP64 DMMA projection on random data with a
+    wide dynamic range (zeros, tiny and huge entries): identical f32 outputs."""
+    from index_writer import random_index
+
+    blob = random_index(d, s, 8, 6, 300, "euclidean", seed=d + s)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "proj", blob))
+    rng = np.random.default_rng(d)
+    q = (rng.standard_normal((700, d)) * rng.choice([1e-3, 1.0, 30.0], size=(700, 1))).astype(F32)
+    q[0] = 0.0
+    q[1, ::3] = 0.0
+    q[2, 5] = 1e-30
+    xq = torch.from_numpy(q).cuda()
+    monkeypatch.setenv("RRG_GEMM", "dmma")
+    ref = dev.stage_project(xq)[0].cpu().numpy()
+    ref_sel = dev.stage_route(torch.from_numpy(ref).cuda(), 3).cpu().numpy()
+    monkeypatch.setenv("RRG_GEMM", "sliced")
+    got = dev.stage_project(xq)[0].cpu().numpy()
+    np.testing.assert_array_equal(got.view(np.int32), ref.view(np.int32))
+    sel = dev.stage_route(torch.from_numpy(got).cuda(), 3).cpu().numpy()
+    for a, b in zip(sel, ref_sel):
+        assert set(a.tolist()) == set(b.tolist())

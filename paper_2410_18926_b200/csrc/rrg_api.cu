@@ -723,11 +723,14 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   const int64_t L = v.L;
   int64_t qc = std::max<int64_t>(256, (256ll << 20) / (L * 8));
   qc = std::min<int64_t>(qc, 16384);
-  p.qc = std::max<int64_t>(1, std::min<int64_t>(nq, qc));
-  p.take_cap = rerank ? t : k;
   // max candidates of any query: sum of the w largest held clusters
   int64_t nmax = 0;
   for (int i = 0; i < (int)ix->sizes_sorted_desc.size() && i < w; ++i) nmax += ix->sizes_sorted_desc[i];
+  // the chunk's key array (and its membership bits) is indexed with int32 offsets:
+  // keep a chunk's candidates below 2^29 (2 GB of keys)
+  if (nmax > 0) qc = std::min<int64_t>(qc, std::max<int64_t>(1, ((int64_t)1 << 29) / nmax));
+  p.qc = std::max<int64_t>(1, std::min<int64_t>(nq, qc));
+  p.take_cap = rerank ? t : k;
   if (!exact_take) p.take_cap = (int)std::min<int64_t>(p.take_cap, std::max<int64_t>(nmax, 1));
   // dynamic smem per scoring CTA: with ~40 KB static this keeps 2 CTAs (2 x 512
   // threads) resident per SM; queries with more candidates spill to global
@@ -788,7 +791,14 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     const char* e = getenv("RRG_RERANK");
     const bool want = !(e && (strcmp(e, "query") == 0 || strcmp(e, "regs") == 0 ||
                               strcmp(e, "tma") == 0));
-    p.rr_mode = (want && p.score_mode == 1 && rerank && !exact_take && cluster_rerank_ok(v, ix->max_cluster)) ? 1 : 0;
+    // the cluster-major re-rank streams every row of a probed cluster for its query
+    // group: worth it while a query keeps a large share of its probed rows (C2, w=1:
+    // t / (w m) = 0.82); with many probes per query (C5, w=8: 0.10) the rows a query
+    // keeps are sparse and the per-query kernel is 3-10x faster (measured)
+    const double mbar = v.L > 0 ? (double)v.P / v.L : 0.0;
+    const bool dense = (double)t >= 0.3 * w * mbar || (e && strcmp(e, "cluster") == 0);
+    p.rr_mode = (want && dense && p.score_mode == 1 && rerank && !exact_take &&
+                 cluster_rerank_ok(v, ix->max_cluster)) ? 1 : 0;
   }
   if (p.rr_mode == 1) {
     p.mwords = (int)((ix->max_cluster + 31) / 32) + 1;

@@ -1488,7 +1488,9 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
                          kMaxSmemPerCta - (int)at.sharedSizeBytes);
     done[dev] = 1;
   }
-  if (warp_select_ok() && h.rerank && h.kcap < 24 * 1024) {
+  // warp per query while the candidate lists are short (~1k-8k); the 256-thread CTA
+  // splits long lists (C5 w=64: ~62k candidates per query) over more lanes
+  if (warp_select_ok() && h.rerank && h.kcap <= 8 * 1024) {
     // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
     const int bits_cap = h.marks ? h.kcap : 0;
     const int stage_cap = 0;  // keys are read through L1

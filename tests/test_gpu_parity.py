@@ -414,8 +414,9 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "cluster+async", "cluster+blocksel", "cluster+dmma",
-                                  "cluster+slicedroute", "query", "cluster+regs", "cluster+tma"])
+@pytest.mark.parametrize("mode", ["cluster", "cluster+auto", "cluster+async", "cluster+blocksel",
+                                  "cluster+dmma", "cluster+slicedroute", "query", "cluster+regs",
+                                  "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -423,6 +424,8 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
     scoring (per-query re-rank), and the per-query register / TMA re-rank kernels."""
     score_mode, _, rerank_mode = mode.partition("+")
     monkeypatch.setenv("RRG_SCORE_MODE", score_mode)
+    if score_mode == "cluster" and rerank_mode != "auto":  # force the cluster-major re-rank
+        monkeypatch.setenv("RRG_RERANK", "cluster")     # (where its row plan applies)
     if rerank_mode == "async":  # cluster-major re-rank with cp.async-staged row pairs
         monkeypatch.setenv("RRG_RR_ASYNC", "1")
     elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections

@@ -365,6 +365,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
     for (int i = 0; i < d; ++i)
       for (int j = 0; j < s; ++j) wt[(size_t)j * d + i] = hm.projection[(size_t)i * s + j];
     float* dwt = ix->upload(wt);
+    v.Wt = dwt;
     int8_t* planes = static_cast<int8_t*>(ix->dalloc(sliced_plane_bytes(s, d, false)));
     int* exps = static_cast<int*>(ix->dalloc((size_t)sliced_rows_pad(s, false) * 4));
     launch_slice_rows(dwt, s, d, d, false, planes, exps, 0);
@@ -673,6 +674,9 @@ static bool gemm_choice(const char* var, bool dflt) {
   return strcmp(e, "sliced") == 0;
 }
 bool sliced_projection() { return gemm_choice("RRG_PROJ", true); }
+// up to this many queries the projection / routing run as warp-per-output GEMVs
+// (a GEMM tile of one row is ~10 dependent K-steps: 30-37 us at C2 batch 1)
+constexpr int kSmallBatch = 32;
 bool sliced_routing() { return gemm_choice("RRG_ROUTE", false); }
 
 // Query sub-range bounds of the front stages (and the host entry's copy pieces):
@@ -687,7 +691,9 @@ int64_t piece_bound(int64_t n, int j, int nsub) {
 // qpl/qex) or the DMMA GEMM.
 void route_dist(const DevIndexView& v, const float* xp, int n, const double* pp, double* diss,
                 int8_t* qpl, int* qex, cudaStream_t st) {
-  if (qpl && sliced_routing()) {
+  if (n <= kSmallBatch) {
+    launch_route_dist_small(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
+  } else if (qpl && sliced_routing()) {
     launch_slice_rows(xp, n, v.s, v.s, true, qpl, qex, st);
     launch_gemm_sliced(qpl, qex, n, v.cent_planes, v.cent_exps, v.L, v.s,
                        v.metric == kMetricEuclidean ? EPI_L2 : EPI_NEGIP, nullptr, diss, v.L, pp,
@@ -796,7 +802,10 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     // t / (w m) = 0.82); with many probes per query (C5, w=8: 0.10) the rows a query
     // keeps are sparse and the per-query kernel is 3-10x faster (measured)
     const double mbar = v.L > 0 ? (double)v.P / v.L : 0.0;
-    const bool dense = (double)t >= 0.3 * w * mbar || (e && strcmp(e, "cluster") == 0);
+    // small batches: the cluster-major items ((cluster, row chunk) per probe) spread one
+    // query's rows over many CTAs, where the per-query kernel has one CTA per query
+    const bool small = p.qc * w < 2 * 148;
+    const bool dense = (double)t >= 0.3 * w * mbar || small || (e && strcmp(e, "cluster") == 0);
     p.rr_mode = (want && dense && p.score_mode == 1 && rerank && !exact_take &&
                  cluster_rerank_ok(v, ix->max_cluster)) ? 1 : 0;
   }
@@ -883,7 +892,9 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       int8_t* qpl_s = p.sliced_proj ? reinterpret_cast<int8_t*>(base + p.off_qpl) +
                                           (s0 / 128) * sliced_block_bytes(v.s, true) : nullptr;
       int* qex = p.sliced_proj ? reinterpret_cast<int*>(base + p.off_qex) + s0 : nullptr;
-      if (sliced_projection()) {
+      if (ns <= kSmallBatch) {
+        staged(0, st, [&] { launch_project_small(xs, v.Wt, ns, v.d, v.s, xps, st); });
+      } else if (sliced_projection()) {
         int8_t* qpl = qpl_d;
         staged(0, st, [&] { launch_slice_rows(xs, ns, v.d, v.d, true, qpl, qex, st); });
         staged(0, st, [&] {
@@ -946,7 +957,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         rh.ix = v; rh.queries = x; rh.w = w; rh.qoff = ch.qoff; rh.pair_off = ch.pair_off;
         rh.rr_item_off = reinterpret_cast<int*>(base + p.off_rritem); rh.pairs = ch.pairs;
         rh.kbase = ch.kbase; rh.marks = marks;
-        rh.diss = ch.keys; rh.work_counter = ch.work_counter + 1; rh.mwords = p.mwords;
+        rh.diss = ch.keys; rh.work_counter = ch.work_counter + 1; rh.mwords = p.mwords; rh.nq = n;
         staged(5, st, [&] { launch_cluster_rerank(rh, st); });
         TopkFinalHost fh{};
         fh.ix = v; fh.sel = sel; fh.w = w; fh.qoff = ch.qoff; fh.kbase = ch.kbase; fh.diss = ch.keys;

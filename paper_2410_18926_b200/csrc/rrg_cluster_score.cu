@@ -1012,7 +1012,7 @@ constexpr int XNT = 256;
 #endif
 constexpr int kCmCtas = RRG_CM_CTAS;  // resident CTAs per SM
 constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
-constexpr int kRrRows = 256;  // rows of the cluster per work item
+constexpr int kRrRows = 256;  // rows of the cluster per work item (large batches)
 
 struct ClusterRerankArgs {
   DevIndexView ix;
@@ -1020,7 +1020,8 @@ struct ClusterRerankArgs {
   int w;
   const int* qoff;
   const int* pair_off;
-  const int* rr_item_off;  // [L+1] prefix of ceil(pairs_l/kRrQ) * ceil(m_l/kRrRows)
+  const int* rr_item_off;  // [L+1] prefix of ceil(pairs_l/kRrQ) * ceil(m_l/rr_rows)
+  int rr_rows;             // rows per work item: kRrRows, fewer for small batches
   const int* pairs;
   const int* kbase;
   const uint32_t* marks;
@@ -1032,12 +1033,12 @@ struct ClusterRerankArgs {
 
 // rr_item_off for the re-rank work items (one CTA)
 __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_off,
-                                                  const int* __restrict__ cl_pos, int L,
+                                                  const int* __restrict__ cl_pos, int L, int rows,
                                                   int* __restrict__ rr_item_off) {
   __shared__ int tot;
   for (int l = threadIdx.x; l < L; l += PNT) {
     const int cnt = pair_off[l + 1] - pair_off[l], m = cl_pos[l + 1] - cl_pos[l];
-    rr_item_off[l] = ((cnt + kRrQ - 1) / kRrQ) * ((m + kRrRows - 1) / kRrRows);
+    rr_item_off[l] = ((cnt + kRrQ - 1) / kRrQ) * ((m + rows - 1) / rows);
   }
   __syncthreads();
   block_exclusive_scan_inplace(rr_item_off, L, &tot);
@@ -1092,12 +1093,12 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
     }
     const int l = lo;
     const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
-    const int nrc = (m + kRrRows - 1) / kRrRows;
+    const int nrc = (m + a.rr_rows - 1) / a.rr_rows;
     const int local = item - a.rr_item_off[l];
     const int qc = nrc > 0 ? local / nrc : 0, rc = nrc > 0 ? local % nrc : 0;
     const int j0 = a.pair_off[l] + qc * kRrQ;
     const int np = min(kRrQ, a.pair_off[l + 1] - j0);
-    const int r0 = rc * kRrRows, r1 = min(m, r0 + kRrRows);
+    const int r0 = rc * a.rr_rows, r1 = min(m, r0 + a.rr_rows);
     if (tid < np) {
       const int pr = a.pairs[j0 + tid];
       const int q = pr / a.w, c = pr % a.w;
@@ -1432,9 +1433,12 @@ __global__ void k_topk_final_warp(TopkFinalArgs a, int cap, int nq) {
 // ---------------------------------------------------------------- launchers
 
 // RRG_WARP_SELECT=0 selects the CTA-per-query selections (k_select_topt, k_topk_final)
-static bool warp_select_ok() {
+// RRG_WARP_SELECT: 1 forces the warp-per-query selections, 0 the CTA-per-query ones;
+// unset: warp per query once the batch fills the GPU (>= 1184 queries = 8 per SM)
+static bool warp_select_ok(int nq) {
   const char* e = getenv("RRG_WARP_SELECT");
-  return !(e && atoi(e) == 0);
+  if (e) return atoi(e) != 0;
+  return nq >= 1184;
 }
 
 
@@ -1490,7 +1494,7 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   }
   // warp per query while the candidate lists are short (~1k-8k); the 256-thread CTA
   // splits long lists (C5 w=64: ~62k candidates per query) over more lanes
-  if (warp_select_ok() && h.rerank && h.kcap <= 8 * 1024) {
+  if (warp_select_ok(nq) && h.rerank && h.kcap <= 8 * 1024) {
     // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
     const int bits_cap = h.marks ? h.kcap : 0;
     const int stage_cap = 0;  // keys are read through L1
@@ -1547,7 +1551,12 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   ClusterRerankArgs a;
   a.ix = h.ix; a.queries = h.queries; a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off;
   a.rr_item_off = h.rr_item_off; a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks;
-  k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, h.rr_item_off);
+  // rows per work item: 256 (few, long items) once the batch's (query, cluster) probes
+  // give enough items to fill the GPU; 128 / 32 for small batches (one query's rows
+  // spread over many CTAs: C2 batch 1, 4 -> 31 items)
+  const int64_t probes = (int64_t)h.nq * h.w;
+  a.rr_rows = probes >= 512 ? kRrRows : (probes >= 64 ? 128 : 32);
+  k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off);
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   a.neg_zero = -0.0f;
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
@@ -1582,7 +1591,8 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
   a.out_ids = h.out_ids; a.out_scores = h.out_scores; a.out_count = h.out_count; a.q0 = h.q0;
   a.order = h.order;
   const size_t per = warp_sel_bytes(h.take_cap, 0);
-  if (warp_select_ok() && h.k <= 256 && per <= 24 * 1024) {
+  // warp per query once the batch fills the GPU; tiny batches get a CTA per query
+  if (warp_select_ok(nq) && h.k <= 256 && per <= 24 * 1024) {
     const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (56 * 1024) / per));
     const unsigned grid = (unsigned)((nq + wpc - 1) / wpc);
     const size_t sm = per * wpc;

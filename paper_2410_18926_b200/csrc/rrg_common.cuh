@@ -65,6 +65,7 @@ struct DevIndexView {
   const float* xf;   // [P_exact][s_pad]
   // W^T as 8 tiled int8 slice planes + per-row exponents (rrg_sliced_gemm.cu): the
   // tensor-core projection (RRG_PROJ=sliced)
+  const float* Wt;  // W^T (s x d) f32, for the small-batch GEMV projection
   const int8_t* wt_planes;
   const int* wt_exps;
   const int8_t* cent_planes;  // centroids (L x s), same slicing, for the routing GEMM

@@ -157,6 +157,55 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
   }
 }
 
+// ======================================================= small-batch GEMV
+// Batches of a few queries: one warp per output element, f64 accumulation of the
+// exact f32 products in lane-strided order plus a shuffle tree (the same f64-level
+// contract as k_gemm_dmma: only the f64 summation order differs from OpenBLAS), so
+// the ~10 dependent K-steps of a 1-row GEMM tile do not set the latency.
+// B is N x K row-major (W^T for the projection, the centroids for routing).
+template <int EPI>
+__global__ void k_gemv_f64(const float* __restrict__ A, int lda, const float* __restrict__ B,
+                           int M, int N, int K, float* __restrict__ outf,
+                           double* __restrict__ outd, int ldo, const double* __restrict__ rowterm,
+                           const double* __restrict__ colterm) {
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (wid >= (int64_t)M * N) return;
+  const int q = (int)(wid / N), j = (int)(wid % N);
+  const float* a = A + (size_t)q * lda;
+  const float* b = B + (size_t)j * K;
+  double acc = 0.0;
+  for (int k = lane; k < K; k += 32) acc = fma((double)__ldg(a + k), (double)__ldg(b + k), acc);
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane != 0) return;
+  if (EPI == EPI_PROJ) {
+    outf[(size_t)q * ldo + j] = (float)acc;
+  } else if (EPI == EPI_L2) {
+    const double d2 = __dadd_rn(__dsub_rn(rowterm[q], __dmul_rn(2.0, acc)), colterm[j]);
+    outd[(size_t)q * ldo + j] = d2 > 0.0 ? d2 : 0.0;
+  } else {
+    outd[(size_t)q * ldo + j] = -acc;
+  }
+}
+
+void launch_project_small(const float* x, const float* Wt, int nq, int d, int s, float* xp,
+                          cudaStream_t st) {
+  const int64_t warps = (int64_t)nq * s;
+  k_gemv_f64<EPI_PROJ><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(x, d, Wt, nq, s, d, xp, nullptr,
+                                                                     s, nullptr, nullptr);
+}
+
+void launch_route_dist_small(const float* xp, const float* cent, int nq, int L, int s, int metric,
+                             const double* pp, const double* cnorm, double* diss, cudaStream_t st) {
+  const int64_t warps = (int64_t)nq * L;
+  const unsigned grid = (unsigned)((warps + 7) / 8);
+  if (metric == kMetricEuclidean)
+    k_gemv_f64<EPI_L2><<<grid, 256, 0, st>>>(xp, s, cent, nq, L, s, nullptr, diss, L, pp, cnorm);
+  else
+    k_gemv_f64<EPI_NEGIP><<<grid, 256, 0, st>>>(xp, s, cent, nq, L, s, nullptr, diss, L, nullptr,
+                                                nullptr);
+}
+
 // ========================================================== query prep
 // One warp per query: quantize_vector(xp, mixed_precision=True) (quantize.py:61-77)
 // -> qcodes[q][0..s_pad) with slot 0 = 0 (pairs with the file's zero pad row of A),

@@ -51,6 +51,11 @@ struct RerankArgsHost {
   const int* order = nullptr;
 };
 
+// small batches (a few queries): warp-per-output f64 GEMV (Wt = W^T, s x d)
+void launch_project_small(const float* x, const float* Wt, int nq, int d, int s, float* xp,
+                          cudaStream_t st);
+void launch_route_dist_small(const float* xp, const float* cent, int nq, int L, int s, int metric,
+                             const double* pp, const double* cnorm, double* diss, cudaStream_t st);
 void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
                     cudaStream_t st);
 void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
@@ -127,6 +132,7 @@ struct ClusterRerankHost {
   uint32_t* diss;
   int* work_counter;
   int mwords;
+  int nq;  // queries of the chunk (work-item sizing)
 };
 bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster);
 size_t cluster_rerank_smem(int d_stride, int mwords);

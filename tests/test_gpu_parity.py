@@ -51,10 +51,14 @@ def _corpus_max_norm(g):
 
 
 @pytest.mark.parametrize("case", QUANT_CASES)
-@pytest.mark.parametrize("entry", ["host", "device", "device-querymajor"])
+@pytest.mark.parametrize("entry", ["host", "device", "device-querymajor", "device-warpsel"])
 def test_golden_end_to_end(pkg, tmp_path, case, entry, monkeypatch):
     if entry == "device-querymajor":  # the fused query-major scoring kernel
         monkeypatch.setenv("RRG_SCORE_MODE", "query")
+        entry = "device"
+    if entry == "device-warpsel":  # warp-per-query selections + cluster-major re-rank
+        monkeypatch.setenv("RRG_WARP_SELECT", "1")
+        monkeypatch.setenv("RRG_RERANK", "cluster")
         entry = "device"
     g, dev = _golden_index(pkg, tmp_path, case)
     for pi, (k, w, t, rr) in enumerate(g["params"]):
@@ -426,6 +430,7 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
     monkeypatch.setenv("RRG_SCORE_MODE", score_mode)
     if score_mode == "cluster" and rerank_mode != "auto":  # force the cluster-major re-rank
         monkeypatch.setenv("RRG_RERANK", "cluster")     # (where its row plan applies)
+        monkeypatch.setenv("RRG_WARP_SELECT", "1")      # and the warp-per-query selections
     if rerank_mode == "async":  # cluster-major re-rank with cp.async-staged row pairs
         monkeypatch.setenv("RRG_RR_ASYNC", "1")
     elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections
@@ -598,3 +603,35 @@ def test_sliced_projection_equals_dmma(pkg, tmp_path, d, s, monkeypatch):
     sel = dev.stage_route(torch.from_numpy(got).cuda(), 3).cpu().numpy()
     for a, b in zip(sel, ref_sel):
         assert set(a.tolist()) == set(b.tolist())
+
+
+@pytest.mark.parametrize("case", ["euclid_q", "euclid_d100", "ip_q", "euclid_exact_ivf", "euclid_f32"])
+def test_small_batches_match_golden(pkg, tmp_path, case):
+    """Batches of 1..32 queries take the small-batch kernels (warp-per-output GEMVs,
+    short re-rank work items, CTA-per-query selections) -- same results."""
+    g, dev = _golden_index(pkg, tmp_path, case)
+    cmax = _corpus_max_norm(g)
+    for pi, (k, w, t, rr) in enumerate(g["params"]):
+        if f"p{pi}_ids" not in g:
+            continue
+        k, w, t, rr = int(k), min(int(w), dev.n_clusters), int(t), bool(rr)
+        for b0, b1 in [(0, 1), (5, 12), (20, 52)]:
+            qb = g["queries"][b0:b1]
+            ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(torch.from_numpy(qb).cuda(), k, w, t, rr))
+            hids, hsc, hcnt = dev.search_host(qb, k, w, t, rr)
+            np.testing.assert_array_equal(hids, ids)
+            np.testing.assert_array_equal(hcnt, cnt)
+            for i in range(b1 - b0):
+                c = int(cnt[i])
+                ref_ids, ref_sc = g[f"p{pi}_ids"][b0 + i, :c], g[f"p{pi}_scores"][b0 + i, :c]
+                assert c == g[f"p{pi}_count"][b0 + i]
+                if "f32" in case:
+                    continue  # tolerance-level scores: covered by test_golden_f32_factors
+                if dev.metric == "euclidean" and rr:
+                    np.testing.assert_array_equal(ids[i, :c], ref_ids)
+                    np.testing.assert_array_equal(sc[i, :c].view(np.int32), ref_sc.view(np.int32))
+                else:
+                    x = qb[i].astype(np.float64)
+                    scale = float(x @ x) if dev.metric == "euclidean" else float(np.sqrt(x @ x) * cmax)
+                    assert_topk_equivalent(ids[i, :c], sc[i, :c], ref_ids, ref_sc, RTOL, scale,
+                                           f"{case} p{pi} q{b0 + i}")

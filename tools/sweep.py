@@ -70,7 +70,8 @@ def main():
     man = W.load_manifest(args.workload)
     k = man["k"]
     pts = [p for p in man.get("grid", {}).get("points", []) if p["recall"] >= 0.90]
-    best = max(pts, key=lambda p: p["qps_1core"]) if pts else {"w": 8, "t": 800}
+    # the device path's operating point (bench.py operating_point): smallest t, then w
+    best = min(pts, key=lambda p: (p["t"], p["w"])) if pts else {"w": 8, "t": 800}
     w0 = args.w or best["w"]
     t0 = args.t or best["t"]
     path = W.materialize_index(args.workload)
@@ -86,7 +87,7 @@ def main():
         for B in [int(x) for x in args.batches.split(",")]:
             B = min(B, q.shape[0])
             ms, _ = device_ms(dev, q[:B], k, w0, t0, args.reps, flush)
-            hq = qh[:B].copy()
+            hq = torch.from_numpy(qh[:B].copy()).pin_memory().numpy()  # pinned, as a server would
             dev.search_host(hq, k, w0, t0)
             e2e = []
             for _ in range(args.reps):

@@ -1056,9 +1056,14 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // the current pair is scored, so the copy has a whole pair's arithmetic to land;
 // without it the next pair is loaded into registers after the scoring, with only
 // the reduction to hide its latency.
-template <int NB, bool ASYNC>
+// NH = 2: rows of 16 equal leaves (d = 1536): NumPy's tree is pw(first half) +
+// pw(second half), each half a perfect 8-leaf tree over the same lanes -- the pair is
+// scored half by half (leaves 0-7 sit at [0, 64) of every interleaved 128-float step,
+// leaves 8-15 at [64, 128)) and the two reduced halves are added.
+template <int NB, bool ASYNC, int NH = 1>
 __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankArgs a) {
-  constexpr int NLV = 8, cstep = 8 * NLV;
+  constexpr int NLV = 8 * NH, cstep = 8 * NLV;
+  static_assert(NH == 1 || !ASYNC, "the cp.async variant handles 8-leaf rows");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const DevIndexView& ix = a.ix;
   const int ds = ix.d_stride, d = ix.d;
@@ -1144,6 +1149,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
       // this lane's 2-element slice of each step of rows pa and pa+1 (register
       // double use: the next pair's loads are issued before this pair's reduction)
       float2 ca[NB], cb[NB];
+      int hoff = 0;  // NH = 2: the half (0 or 64 floats into each step) being scored
       auto load_pair = [&](int pa) {
         const int pb = pa + 1 < r1 ? pa + 1 : pa;
         if (ASYNC) {  // issue the copy of both rows into this warp's staging slot
@@ -1159,8 +1165,8 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           cp_async_commit();
           return;
         }
-        const float* ra = ix.corpus + (size_t)(p0 + pa) * ds + coff;
-        const float* rb = ix.corpus + (size_t)(p0 + pb) * ds + coff;
+        const float* ra = ix.corpus + (size_t)(p0 + pa) * ds + coff + hoff;
+        const float* rb = ix.corpus + (size_t)(p0 + pb) * ds + coff + hoff;
 #pragma unroll
         for (int i = 0; i < NB; ++i) ca[i] = __ldg(reinterpret_cast<const float2*>(ra + cstep * i));
 #pragma unroll
@@ -1180,7 +1186,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
       };
       // per (query, row pair): this lane's r[2h]+r[2h+1] of both rows
       auto lane_sums = [&](int g, float& va, float& vb) {
-        const float* xg = xs + (size_t)g * ds + coff;
+        const float* xg = xs + (size_t)g * ds + coff + hoff;
         if (euclid) {
           float2 acca = make_float2(0.f, 0.f), accb = acca;
 #pragma unroll
@@ -1228,6 +1234,9 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           pa = pn;
           continue;
         }
+        float res = 0.f;  // NH = 2: the first half's reduced value
+#pragma unroll
+        for (int h2 = 0; h2 < NH; ++h2) {
         // per-lane partials of every active (query, row) pair: value 2*slot + row
         float v[2 * kRrQ];
         unsigned act = act0;
@@ -1242,7 +1251,13 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
             v[2 * slot + 1] = 0.f;
           }
         }
-        if (!ASYNC && pn < r1) load_pair(pn);
+        if (h2 + 1 < NH) {  // the pair's next half
+          hoff = 64 * (h2 + 1);
+          load_pair(pa);
+        } else if (!ASYNC && pn < r1) {
+          hoff = 0;
+          load_pair(pn);
+        }
         // Transposing butterfly: five xor-steps (1, 2, 4, 8, 16 -- NumPy's
         // ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) per leaf, then the perfect 8-leaf tree)
         // that halve the values held per lane, so lane j ends with value j fully
@@ -1259,6 +1274,8 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
             v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
           }
         }
+        res = h2 == 0 ? v[0] : __fadd_rn(res, v[0]);  // pw(half 0) + pw(half 1)
+        }
         // lane j holds (slot j/2, row j%2); slot s is the s-th set bit of act0
         if (mine) slotq[warp][__popc(act0 & ((1u << lane) - 1u))] = lane;
         __syncwarp();
@@ -1266,7 +1283,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         if (slot < __popc(act0)) {
           const int g = slotq[warp][slot];
           const int p = (lane & 1) ? pb : pa;
-          if (marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? v[0] : -v[0]);
+          if (marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? res : -res);
         }
         __syncwarp();
         pa = pn;
@@ -1527,8 +1544,8 @@ size_t cluster_rerank_smem(int d_stride, int mwords) {
 // largest cluster fit in shared memory (otherwise the per-query re-rank serves)
 bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster) {
   const int nb = ix.pw_leaf_n / 8;
-  if (!(ix.corpus_interleaved && ix.pw_nleaves == 8 && ix.pw_leaf_n % 8 == 0 &&
-        (nb == 12 || nb == 15 || nb == 16)))
+  if (!(ix.corpus_interleaved && (ix.pw_nleaves == 8 || ix.pw_nleaves == 16) &&
+        ix.pw_leaf_n % 8 == 0 && (nb == 12 || nb == 15 || nb == 16)))
     return false;
   const int mwords = (int)((max_cluster + 31) / 32) + 1;
   return cluster_rerank_smem(ix.d_stride, mwords) + 8 * 1024 <= (size_t)kMaxSmemPerCta;
@@ -1569,7 +1586,18 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
     opt_in_smem(k_rerank_cluster<NB, AS>, SLOT);                                 \
     k_rerank_cluster<NB, AS><<<sms * kCmCtas, XNT, sm, st>>>(a);                 \
   } while (0)
-  const bool as = rerank_async();
+  const bool as = rerank_async() && h.ix.pw_nleaves == 8;
+  if (h.ix.pw_nleaves == 16) {  // d = 16 leaves (e.g. 1536): scored as two 8-leaf halves
+    switch (h.ix.pw_leaf_n / 8) {
+      case 12: opt_in_smem(k_rerank_cluster<12, false, 2>, 12);
+               k_rerank_cluster<12, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+      case 15: opt_in_smem(k_rerank_cluster<15, false, 2>, 13);
+               k_rerank_cluster<15, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+      default: opt_in_smem(k_rerank_cluster<16, false, 2>, 14);
+               k_rerank_cluster<16, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+    }
+    return;
+  }
   // persistent grid: kCmCtas CTAs per SM
   switch (h.ix.pw_leaf_n / 8) {
     case 12: if (as) RRG_RR_LAUNCH(12, true, 4); else RRG_RR_LAUNCH(12, false, 0); break;

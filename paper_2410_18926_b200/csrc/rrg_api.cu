@@ -31,7 +31,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local std::string g_kind;
-thread_local int64_t g_launches = 0;
+thread_local int64_t g_launches = 0;  // kernels launched by this thread (note_launch)
 
 // per-stage event timing (rrg_set_stage_timing / rrg_stage_times)
 struct StageTimer {
@@ -63,7 +63,6 @@ void staged(int stage, cudaStream_t st, F&& launch) {
   } else {
     launch();
   }
-  ++g_launches;
 }
 
 int fail(int code, const char* kind, const char* fmt, ...) {
@@ -178,6 +177,8 @@ struct HostModel {
 };
 
 }  // namespace
+
+void rrg::note_launch() { ++g_launches; }
 
 // ------------------------------------------------------------------ index
 
@@ -678,6 +679,12 @@ bool sliced_projection() { return gemm_choice("RRG_PROJ", true); }
 // (a GEMM tile of one row is ~10 dependent K-steps: 30-37 us at C2 batch 1)
 constexpr int kSmallBatch = 32;
 bool sliced_routing() { return gemm_choice("RRG_ROUTE", false); }
+// w = 1 routing fused into the DMMA GEMM (RRG_ROUTE_FUSED=0 writes the full
+// dissimilarity rows and selects separately)
+bool route_fused() {
+  const char* e = getenv("RRG_ROUTE_FUSED");
+  return !(e && atoi(e) == 0);
+}
 
 // Query sub-range bounds of the front stages (and the host entry's copy pieces):
 // multiples of the sliced GEMM's 128-row blocks, so a piece's slice planes are a
@@ -908,12 +915,26 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         launch_prep(xps, xs, ns, v.s, v.s_pad, v.d, qcodes + (int64_t)s0 * v.s_pad, qscale + s0,
                     qhead + s0, pp + s0, xx + s0, st, nonfinite);
       });
-      staged(2, st, [&] {
-        route_dist(v, xps, ns, pp + s0, diss + (int64_t)s0 * v.L, qpl_s, qex, st);
-      });
-      staged(3, st, [&] {
-        launch_route_select(diss + (int64_t)s0 * v.L, ns, v.L, w, sel + (int64_t)s0 * w, prim + s0, st);
-      });
+      if (w == 1 && ns > kSmallBatch && !sliced_routing() && route_fused()) {
+        // nearest cluster straight from the GEMM: per (query, 64-centroid tile) minima
+        const int nt = route_nearest_tiles(v.L);
+        double* part_v = diss + (int64_t)s0 * nt;
+        int* part_i = reinterpret_cast<int*>(diss + p.qc * nt) + (int64_t)s0 * nt;
+        staged(2, st, [&] {
+          launch_route_nearest_fused(xps, v.cent, ns, v.L, v.s, v.metric, pp + s0, v.cnorm, part_v,
+                                     part_i, st);
+        });
+        staged(3, st, [&] {
+          launch_route_nearest_reduce(part_v, part_i, ns, v.L, sel + s0, prim + s0, st);
+        });
+      } else {
+        staged(2, st, [&] {
+          route_dist(v, xps, ns, pp + s0, diss + (int64_t)s0 * v.L, qpl_s, qex, st);
+        });
+        staged(3, st, [&] {
+          launch_route_select(diss + (int64_t)s0 * v.L, ns, v.L, w, sel + (int64_t)s0 * w, prim + s0, st);
+        });
+      }
     }
     staged(6, st, [&] { launch_bucket(prim, n, v.L, order, st); });
     ScoreArgsHost sa{};

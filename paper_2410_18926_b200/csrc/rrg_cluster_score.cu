@@ -1461,9 +1461,9 @@ static bool warp_select_ok(int nq) {
 
 void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
-  k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand);
-  k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off,
-                                                  h.item_off, h.pairs, h.kbase);
+  (k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand), note_launch());
+  (k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off,
+                                                  h.item_off, h.pairs, h.kbase), note_launch());
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
   ClusterScoreArgs a;
   a.ix = ix; a.qcodes = h.qcodes; a.qscale = h.qscale; a.qhead = h.qhead; a.sel = h.sel;
@@ -1474,9 +1474,9 @@ void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   a.xp = h.xp;
   if (ix.quantized)
-    k_score_cluster<<<sms * 4, CNT, 0, st>>>(a);
+    (k_score_cluster<<<sms * 4, CNT, 0, st>>>(a), note_launch());
   else
-    k_score_cluster_f32<<<sms * 4, CNT, 0, st>>>(a);
+    (k_score_cluster_f32<<<sms * 4, CNT, 0, st>>>(a), note_launch());
 }
 
 static int pow2_at_least(int v) {
@@ -1523,10 +1523,10 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
                            cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemPerCta);
       wdone[dev] = 1;
     }
-    k_select_topt_warp<<<(nq + wpc - 1) / wpc, 32 * wpc, per * wpc, st>>>(a, stage_cap, bits_cap, nq);
+    (k_select_topt_warp<<<(nq + wpc - 1) / wpc, 32 * wpc, per * wpc, st>>>(a, stage_cap, bits_cap, nq), note_launch());
     return;
   }
-  k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a);
+  (k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a), note_launch());
 }
 
 // measured on C2 (w=1, t=800): register loads 1.134 ms vs cp.async staging 1.249 ms
@@ -1573,7 +1573,7 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   // spread over many CTAs: C2 batch 1, 4 -> 31 items)
   const int64_t probes = (int64_t)h.nq * h.w;
   a.rr_rows = probes >= 512 ? kRrRows : (probes >= 64 ? 128 : 32);
-  k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off);
+  (k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off), note_launch());
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   a.neg_zero = -0.0f;
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
@@ -1584,17 +1584,17 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
 #define RRG_RR_LAUNCH(NB, AS, SLOT)                                              \
   do {                                                                           \
     opt_in_smem(k_rerank_cluster<NB, AS>, SLOT);                                 \
-    k_rerank_cluster<NB, AS><<<sms * kCmCtas, XNT, sm, st>>>(a);                 \
+    (k_rerank_cluster<NB, AS><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch());                 \
   } while (0)
   const bool as = rerank_async() && h.ix.pw_nleaves == 8;
   if (h.ix.pw_nleaves == 16) {  // d = 16 leaves (e.g. 1536): scored as two 8-leaf halves
     switch (h.ix.pw_leaf_n / 8) {
       case 12: opt_in_smem(k_rerank_cluster<12, false, 2>, 12);
-               k_rerank_cluster<12, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+               (k_rerank_cluster<12, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); break;
       case 15: opt_in_smem(k_rerank_cluster<15, false, 2>, 13);
-               k_rerank_cluster<15, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+               (k_rerank_cluster<15, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); break;
       default: opt_in_smem(k_rerank_cluster<16, false, 2>, 14);
-               k_rerank_cluster<16, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a); break;
+               (k_rerank_cluster<16, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); break;
     }
     return;
   }
@@ -1627,7 +1627,7 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
 #define RRG_TKW(E, SLOT)                                                          \
   do {                                                                            \
     opt_in_smem(k_topk_final_warp<E>, SLOT);                                      \
-    k_topk_final_warp<E><<<grid, 32 * wpc, sm, st>>>(a, h.take_cap, nq);          \
+    (k_topk_final_warp<E><<<grid, 32 * wpc, sm, st>>>(a, h.take_cap, nq), note_launch());          \
   } while (0)
     if (h.k <= 32) RRG_TKW(1, 8);
     else if (h.k <= 64) RRG_TKW(2, 9);
@@ -1637,7 +1637,7 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
     return;
   }
   opt_in_smem(k_topk_final, 3);
-  k_topk_final<<<nq, FNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a);
+  (k_topk_final<<<nq, FNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a), note_launch());
 }
 
 }  // namespace rrg

@@ -22,6 +22,9 @@ constexpr int kKindRrr = 0;    // two-stage A/B model (rrr.py:181-203)
 constexpr int kKindExact = 1;  // single-factor exact model (rrr.py:103-113, index.py:465-468)
 
 // POD view of a device-resident index, passed by value to kernels.
+// Counts one kernel launch of this thread (rrg_last_launch_count; rrg_api.cu).
+void note_launch();
+
 struct DevIndexView {
   int metric, d, s, r, L;
   int s_pad;     // s rounded up to 16 (query / exact codes row pitch, bytes)

@@ -279,7 +279,7 @@ size_t gt_select_smem(int k) {
 
 void launch_gt_row_norms(const float* x, int64_t n, int d, int mode, double* out, cudaStream_t st) {
   const int64_t blocks = (n * 32 + 255) / 256;
-  k_gt_row_norms<<<(unsigned)blocks, 256, 0, st>>>(x, n, d, mode, out);
+  (k_gt_row_norms<<<(unsigned)blocks, 256, 0, st>>>(x, n, d, mode, out), note_launch());
 }
 
 void launch_gt_select(const GtSelectHost& h, int nq, cudaStream_t st) {
@@ -289,7 +289,7 @@ void launch_gt_select(const GtSelectHost& h, int nq, cudaStream_t st) {
   a.out_n = h.out_n; a.k = h.k; a.err = h.err;
   const size_t smem = gt_select_smem(h.k);
   cudaFuncSetAttribute(k_gt_select, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_gt_select<<<nq, GT_T, smem, st>>>(a);
+  (k_gt_select<<<nq, GT_T, smem, st>>>(a), note_launch());
 }
 
 }  // namespace rrg

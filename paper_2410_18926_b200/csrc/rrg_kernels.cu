@@ -58,7 +58,8 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
                                                      int N, int K, float* __restrict__ outf,
                                                      double* __restrict__ outd, int ldo,
                                                      const double* __restrict__ rowterm,
-                                                     const double* __restrict__ colterm) {
+                                                     const double* __restrict__ colterm,
+                                                     int* __restrict__ outi = nullptr) {
   constexpr int MBM = 32 * WM, DMNT = 64 * WM, PITCH = BK + 4;
   constexpr int NA = (MBM * BK) / DMNT, NB = (MBN * BK + DMNT - 1) / DMNT;
   extern __shared__ __align__(16) double gemm_sm[];
@@ -129,6 +130,52 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
     if (kt + 1 < nk) sstore(buf ^ 1);
     __syncthreads();
   }
+  if constexpr (EPI == EPI_L2_ARGMIN || EPI == EPI_NEGIP_ARGMIN) {
+    // routing with w = 1: only each row's nearest column is needed -- reduce this
+    // tile's 64 columns to (dissimilarity, lowest column) per row and write one partial
+    // per (row, column tile) instead of the row of f64 dissimilarities
+    double* red_v = gemm_sm;                                   // [MBM][2]
+    int* red_i = reinterpret_cast<int*>(gemm_sm + 2 * MBM);   // [MBM][2]
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = wm * 32 + i * 8 + (lane >> 2), gm = m0 + rl;
+      double best = __longlong_as_double(0x7ff0000000000000ll);  // +inf
+      int bcol = 0x7fffffff;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
+          if (gn >= N || gm >= M) continue;
+          double dv;
+          if (EPI == EPI_L2_ARGMIN) {
+            dv = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, acc[i][j][h])), colterm[gn]);
+            dv = dv > 0.0 ? dv : 0.0;
+          } else {
+            dv = -acc[i][j][h];
+          }
+          if (dv < best || (dv == best && gn < bcol)) { best = dv; bcol = gn; }
+        }
+#pragma unroll
+      for (int o = 1; o <= 2; o <<= 1) {  // the 4 lanes holding this row's columns
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oc = __shfl_xor_sync(0xffffffffu, bcol, o);
+        if (ob < best || (ob == best && oc < bcol)) { best = ob; bcol = oc; }
+      }
+      if ((lane & 3) == 0) { red_v[rl * 2 + wn] = best; red_i[rl * 2 + wn] = bcol; }
+    }
+    __syncthreads();
+    for (int r = tid; r < MBM; r += DMNT) {
+      const int gm = m0 + r;
+      if (gm >= M) continue;
+      double b0 = red_v[r * 2], b1 = red_v[r * 2 + 1];
+      int c0 = red_i[r * 2], c1 = red_i[r * 2 + 1];
+      if (b1 < b0 || (b1 == b0 && c1 < c0)) { b0 = b1; c0 = c1; }
+      outd[(size_t)gm * ldo + blockIdx.x] = b0;
+      outi[(size_t)gm * ldo + blockIdx.x] = c0;
+    }
+    return;
+  }
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
     const int gm = m0 + wm * 32 + i * 8 + (lane >> 2);
@@ -191,8 +238,8 @@ __global__ void k_gemv_f64(const float* __restrict__ A, int lda, const float* __
 void launch_project_small(const float* x, const float* Wt, int nq, int d, int s, float* xp,
                           cudaStream_t st) {
   const int64_t warps = (int64_t)nq * s;
-  k_gemv_f64<EPI_PROJ><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(x, d, Wt, nq, s, d, xp, nullptr,
-                                                                     s, nullptr, nullptr);
+  (k_gemv_f64<EPI_PROJ><<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(x, d, Wt, nq, s, d, xp, nullptr,
+                                                                     s, nullptr, nullptr), note_launch());
 }
 
 void launch_route_dist_small(const float* xp, const float* cent, int nq, int L, int s, int metric,
@@ -200,10 +247,10 @@ void launch_route_dist_small(const float* xp, const float* cent, int nq, int L, 
   const int64_t warps = (int64_t)nq * L;
   const unsigned grid = (unsigned)((warps + 7) / 8);
   if (metric == kMetricEuclidean)
-    k_gemv_f64<EPI_L2><<<grid, 256, 0, st>>>(xp, s, cent, nq, L, s, nullptr, diss, L, pp, cnorm);
+    (k_gemv_f64<EPI_L2><<<grid, 256, 0, st>>>(xp, s, cent, nq, L, s, nullptr, diss, L, pp, cnorm), note_launch());
   else
-    k_gemv_f64<EPI_NEGIP><<<grid, 256, 0, st>>>(xp, s, cent, nq, L, s, nullptr, diss, L, nullptr,
-                                                nullptr);
+    (k_gemv_f64<EPI_NEGIP><<<grid, 256, 0, st>>>(xp, s, cent, nq, L, s, nullptr, diss, L, nullptr,
+                                                nullptr), note_launch());
 }
 
 // ========================================================== query prep
@@ -1236,13 +1283,13 @@ void launch_merge(int mode, int metric, int nq, int G, int cap, const void* in_k
                          kMaxSmemPerCta - (int)at.sharedSizeBytes);
     done[dev] = 1;
   }
-  k_merge<<<nq, MNT, sm, st>>>(mode, metric, nq, G, cap, in_keys, in_ids, in_counts, take,
-                               out_keys, out_ids, out_count);
+  (k_merge<<<nq, MNT, sm, st>>>(mode, metric, nq, G, cap, in_keys, in_ids, in_counts, take,
+                               out_keys, out_ids, out_count), note_launch());
 }
 
 void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* ids,
                        const int* counts, int* cand_pos, int* cand_n, cudaStream_t st) {
-  k_ids_to_pos<<<(nq + 7) / 8, 256, 0, st>>>(ix, nq, cap, ids, counts, cand_pos, cand_n);
+  (k_ids_to_pos<<<(nq + 7) / 8, 256, 0, st>>>(ix, nq, cap, ids, counts, cand_pos, cand_n), note_launch());
 }
 
 // ======================================================= corpus scatter
@@ -1269,7 +1316,7 @@ __global__ void k_scatter_rows(const float* __restrict__ src, int64_t nrows, int
 template <int EPI, bool BT, int WM, int BK>
 static void gemm_launch(dim3 grid, cudaStream_t st, const float* A, int lda, const float* B, int ldb,
                         int M, int N, int K, float* outf, double* outd, int ldo, const double* rt,
-                        const double* ct) {
+                        const double* ct, int* outi = nullptr) {
   constexpr size_t sm = gemm_smem_bytes<WM, BK>();
   static int done[64] = {};
   int dev = 0;
@@ -1279,8 +1326,8 @@ static void gemm_launch(dim3 grid, cudaStream_t st, const float* A, int lda, con
                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     done[dev] = 1;
   }
-  k_gemm_dmma<EPI, BT, WM, BK><<<grid, 64 * WM, sm, st>>>(A, lda, B, ldb, M, N, K, outf, outd, ldo,
-                                                          rt, ct);
+  (k_gemm_dmma<EPI, BT, WM, BK><<<grid, 64 * WM, sm, st>>>(A, lda, B, ldb, M, N, K, outf, outd, ldo,
+                                                          rt, ct, outi), note_launch());
 }
 
 // K depth per stage: 8 (default) or 16 (RRG_GEMM_BK=16) -- measured equal on C2
@@ -1304,8 +1351,8 @@ void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int 
                  int* nonfinite) {
   int warps_per_block = 8;
   int blocks = (nq + warps_per_block - 1) / warps_per_block;
-  k_prep_queries<<<blocks, warps_per_block * 32, 0, st>>>(xp, x, nq, s, s_pad, d, qcodes, qscale,
-                                                          qhead, pp, xx, nonfinite);
+  (k_prep_queries<<<blocks, warps_per_block * 32, 0, st>>>(xp, x, nq, s, s_pad, d, qcodes, qscale,
+                                                          qhead, pp, xx, nonfinite), note_launch());
 }
 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
@@ -1351,19 +1398,64 @@ static void allow_smem(Kern* kernel, int slot) {
 
 size_t route_select_smem(int L) { return (size_t)L * 8 + (size_t)L * 4 + 16; }
 
+// w == 1 from the fused GEMM's per-tile partials: min over ntiles (dissimilarity,
+// column) pairs per query; tiles ascend in column, so ties keep the lowest id.
+__global__ void k_route_nearest_partials(const double* __restrict__ pv, const int* __restrict__ pi,
+                                         int nq, int ntiles, int* __restrict__ sel,
+                                         int* __restrict__ primary) {
+  const int q = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  double bk = __longlong_as_double(0x7ff0000000000000ll);
+  int bi = 0x7fffffff;
+  for (int t = lane; t < ntiles; t += 32) {
+    const double v = __ldg(pv + (size_t)q * ntiles + t);
+    const int c = __ldg(pi + (size_t)q * ntiles + t);
+    if (v < bk || (v == bk && c < bi)) { bk = v; bi = c; }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, bk, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ob < bk || (ob == bk && oi < bi)) { bk = ob; bi = oi; }
+  }
+  if (lane == 0) { sel[q] = bi; primary[q] = bi; }
+}
+
+int route_nearest_tiles(int L) { return (L + MBN - 1) / MBN; }
+
+void launch_route_nearest_fused(const float* xp, const float* cent, int nq, int L, int s, int metric,
+                                const double* pp, const double* cnorm, double* part_v, int* part_i,
+                                cudaStream_t st) {
+  constexpr int WM = 4;
+  const int nt = route_nearest_tiles(L);
+  dim3 grid(nt, (nq + 32 * WM - 1) / (32 * WM));
+  if (metric == kMetricEuclidean)
+    gemm_launch<EPI_L2_ARGMIN, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, part_v, nt,
+                                            pp, cnorm, part_i);
+  else
+    gemm_launch<EPI_NEGIP_ARGMIN, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, part_v, nt,
+                                               nullptr, nullptr, part_i);
+}
+
+void launch_route_nearest_reduce(const double* part_v, const int* part_i, int nq, int L, int* sel,
+                                 int* primary, cudaStream_t st) {
+  (k_route_nearest_partials<<<(nq + 7) / 8, 256, 0, st>>>(part_v, part_i, nq, route_nearest_tiles(L),
+                                                         sel, primary), note_launch());
+}
+
 void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
                          cudaStream_t st) {
   if (w == 1) {
-    k_route_nearest<<<(nq + 7) / 8, 256, 0, st>>>(diss, nq, L, sel, primary);
+    (k_route_nearest<<<(nq + 7) / 8, 256, 0, st>>>(diss, nq, L, sel, primary), note_launch());
     return;
   }
   allow_smem(k_route_select<256>, 0);
-  k_route_select<256><<<nq, 256, route_select_smem(L), st>>>(diss, L, w, sel, primary);
+  (k_route_select<256><<<nq, 256, route_select_smem(L), st>>>(diss, L, w, sel, primary), note_launch());
 }
 
 void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st) {
   allow_smem(k_bucket_queries, 1);
-  k_bucket_queries<<<1, BNT, (size_t)(L + 1) * 4, st>>>(primary, nq, L, order);
+  (k_bucket_queries<<<1, BNT, (size_t)(L + 1) * 4, st>>>(primary, nq, L, order), note_launch());
 }
 
 size_t score_select_smem(int smem_cap, int take_cap, int k) {
@@ -1382,7 +1474,7 @@ void launch_score_select(const ScoreArgsHost& h, int nq, cudaStream_t st) {
   a.order = h.order;
   a.sel_keys = h.sel_keys; a.sel_ids = h.sel_ids; a.sel_count = h.sel_count;
   allow_smem(k_score_select, 2);
-  k_score_select<<<nq, SNT, score_select_smem(h.smem_cap, h.take_cap, h.k), st>>>(a);
+  (k_score_select<<<nq, SNT, score_select_smem(h.smem_cap, h.take_cap, h.k), st>>>(a), note_launch());
 }
 
 size_t rerank_smem(int d_stride, int take_cap, int k, bool tree) {
@@ -1415,7 +1507,7 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
 #define RRG_TMA(S, NBV, SLOT)                           \
   do {                                                  \
     allow_smem(k_rerank_tma<S, NBV>, SLOT);             \
-    k_rerank_tma<S, NBV><<<nq, RNT, smt, st>>>(a);      \
+    (k_rerank_tma<S, NBV><<<nq, RNT, smt, st>>>(a), note_launch());      \
   } while (0)
     bool launched = true;
     if (one) {
@@ -1442,7 +1534,7 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
 #define RRG_TREE(S, NBV, NLVV, SLOT)                    \
   do {                                                  \
     allow_smem(k_rerank_tree<S, NBV, NLVV>, SLOT);      \
-    k_rerank_tree<S, NBV, NLVV><<<nq, RNT, sm, st>>>(a); \
+    (k_rerank_tree<S, NBV, NLVV><<<nq, RNT, sm, st>>>(a), note_launch()); \
   } while (0)
     // specialised (chain length, leaf count) of the common dims:
     //   d=768 (8 leaves of 96), 960 (8 x 120), 1536 (16 x 96), 1024 (8 x 128),
@@ -1479,15 +1571,15 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
     return;
   }
   allow_smem(k_rerank_topk, 5);
-  k_rerank_topk<<<nq, RNT, sm, st>>>(a);
+  (k_rerank_topk<<<nq, RNT, sm, st>>>(a), note_launch());
 }
 
 void launch_scatter_rows(const float* src, int64_t nrows, int d, int d_stride,
                          const int* pos_of_id, int64_t i0, const int* perm, float* dst,
                          cudaStream_t st) {
   if (nrows <= 0) return;
-  k_scatter_rows<<<(unsigned)nrows, 128, 0, st>>>(src, nrows, d, d_stride, pos_of_id, i0, perm,
-                                                  dst);
+  (k_scatter_rows<<<(unsigned)nrows, 128, 0, st>>>(src, nrows, d, d_stride, pos_of_id, i0, perm,
+                                                  dst), note_launch());
 }
 
 }  // namespace rrg

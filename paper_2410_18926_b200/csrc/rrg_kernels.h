@@ -13,6 +13,8 @@ constexpr int EPI_L2 = 1;
 constexpr int EPI_NEGIP = 2;
 constexpr int EPI_GT_L2 = 3;   // (qq - 2 q.c) + cc, no clip (bench.py:110)
 constexpr int EPI_GT_COS = 4;  // -(q.c / ||c||)           (bench.py:100-103,112)
+constexpr int EPI_L2_ARGMIN = 5;     // routing w = 1: per-row nearest column per tile
+constexpr int EPI_NEGIP_ARGMIN = 6;
 constexpr int kMaxSmemPerCta = 227 * 1024;  // B200 opt-in limit per CTA
 
 struct ScoreArgsHost {
@@ -64,6 +66,14 @@ void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
                        const double* pp, const double* cnorm, double* diss, cudaStream_t st);
 size_t route_select_smem(int L);
+// w = 1 routing fused into the DMMA GEMM: per (row, 64-column tile) minima, then a
+// warp argmin per query (part_v / part_i: nq x route_nearest_tiles(L))
+int route_nearest_tiles(int L);
+void launch_route_nearest_fused(const float* xp, const float* cent, int nq, int L, int s, int metric,
+                                const double* pp, const double* cnorm, double* part_v, int* part_i,
+                                cudaStream_t st);
+void launch_route_nearest_reduce(const double* part_v, const int* part_i, int nq, int L, int* sel,
+                                 int* primary, cudaStream_t st);
 void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
                          cudaStream_t st);
 void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st);

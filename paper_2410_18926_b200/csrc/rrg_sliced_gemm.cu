@@ -281,8 +281,8 @@ void launch_slice_rows(const float* x, int rows, int K, int ld, bool a_operand, 
                        int* exps, cudaStream_t st) {
   const int rp = sliced_rows_pad(rows, a_operand);
   const int64_t blocks = ((int64_t)rp * 32 + 255) / 256;
-  k_slice_rows<<<(unsigned)blocks, 256, 0, st>>>(x, rows, rp, K, ld, sliced_kchunks(K),
-                                                 a_operand ? kSlBM : kSlBN, planes, exps);
+  (k_slice_rows<<<(unsigned)blocks, 256, 0, st>>>(x, rows, rp, K, ld, sliced_kchunks(K),
+                                                 a_operand ? kSlBM : kSlBN, planes, exps), note_launch());
 }
 
 void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* b, const int* b_exp,
@@ -301,7 +301,7 @@ void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* 
   g.kchunks = sliced_kchunks(K);
   g.epi = epi; g.outf = outf; g.outd = outd; g.ldo = ldo; g.rowterm = rowterm; g.colterm = colterm;
   dim3 grid((N + kSlBN - 1) / kSlBN, (M + kSlBM - 1) / kSlBM);
-  k_gemm_sliced<<<grid, kSlThreads, kSlSmem, st>>>(g);
+  (k_gemm_sliced<<<grid, kSlThreads, kSlSmem, st>>>(g), note_launch());
 }
 
 }  // namespace rrg

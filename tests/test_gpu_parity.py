@@ -435,8 +435,9 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
         monkeypatch.setenv("RRG_RR_ASYNC", "1")
     elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections
         monkeypatch.setenv("RRG_WARP_SELECT", "0")
-    elif rerank_mode == "dmma":  # FP64 DMMA projection + routing GEMMs
+    elif rerank_mode == "dmma":  # FP64 DMMA projection + routing GEMMs, unfused w=1 routing
         monkeypatch.setenv("RRG_GEMM", "dmma")
+        monkeypatch.setenv("RRG_ROUTE_FUSED", "0")
     elif rerank_mode == "slicedroute":  # int8 tensor-core (sliced) projection + routing
         monkeypatch.setenv("RRG_GEMM", "sliced")
     elif rerank_mode:
@@ -635,3 +636,36 @@ def test_small_batches_match_golden(pkg, tmp_path, case):
                     scale = float(x @ x) if dev.metric == "euclidean" else float(np.sqrt(x @ x) * cmax)
                     assert_topk_equivalent(ids[i, :c], sc[i, :c], ref_ids, ref_sc, RTOL, scale,
                                            f"{case} p{pi} q{b0 + i}")
+
+
+def test_fused_nearest_cluster_ties(pkg, tmp_path):
+    """w = 1 routing fused into the GEMM: duplicate centroids tie exactly and resolve to
+    the lower cluster id, like route()'s stable argsort (cluster.py:263-264)."""
+    import struct
+    import zlib
+
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    d, s, L = 64, 32, 9
+    blob = bytearray(random_index(d, s, 8, L, 700, "euclidean", seed=5))
+    # duplicate centroid 2 into centroids 6 and 7 (header 8 + 29 bytes, then W d x s f32)
+    off = 8 + 29 + d * s * 4
+    cent = np.frombuffer(bytes(blob[off:off + L * s * 4]), dtype="<f4").reshape(L, s).copy()
+    cent[6] = cent[2]
+    cent[7] = cent[2]
+    blob[off:off + L * s * 4] = cent.tobytes()
+    blob[-4:] = struct.pack("<I", zlib.crc32(bytes(blob[:-4])) & 0xFFFFFFFF)
+    blob = bytes(blob)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "ties", blob))
+    oidx = O.read_index(blob)
+    rng = np.random.default_rng(3)
+    W = oidx.projection.astype(np.float64)
+    # queries whose projection is (near) centroid 2: the three duplicates tie
+    q = rng.standard_normal((200, d)).astype(F32)
+    q[:100] = (np.linalg.pinv(W.T) @ cent[2].astype(np.float64)).astype(F32)[None, :] +         rng.standard_normal((100, d)).astype(F32) * 1e-3
+    ids, sc, cnt = dev.search_host(q, 5, 1, 30, True)
+    ref = O.query_batch(oidx, q, 5, 1, 30, True)
+    for i, r in enumerate(ref):
+        c = int(cnt[i])
+        np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"q{i}")

@@ -95,7 +95,13 @@ __device__ void block_exclusive_scan_inplace(int* a, int n, int* total) {
 
 // Scoring work items split a cluster's points into chunks of kScorePts (the largest
 // clusters would otherwise set the tail of the persistent grid).
-constexpr int kScorePts = 512;
+#ifndef RRG_SCORE_PTS
+#define RRG_SCORE_PTS 1024  // C2 scoring: 256 -> 0.188, 512 -> 0.142, 1024 -> 0.126, 1536 -> 0.132, 2048 -> 0.143 ms
+#endif
+#ifndef RRG_SCORE_CTAS
+#define RRG_SCORE_CTAS 4
+#endif
+constexpr int kScorePts = RRG_SCORE_PTS;
 
 __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel, int nq, int w,
                                                      int L, const int* __restrict__ cl_pos,
@@ -1474,7 +1480,7 @@ void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   a.xp = h.xp;
   if (ix.quantized)
-    (k_score_cluster<<<sms * 4, CNT, 0, st>>>(a), note_launch());
+    (k_score_cluster<<<sms * RRG_SCORE_CTAS, CNT, 0, st>>>(a), note_launch());
   else
     (k_score_cluster_f32<<<sms * 4, CNT, 0, st>>>(a), note_launch());
 }

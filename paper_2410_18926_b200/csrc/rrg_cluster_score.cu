@@ -1018,7 +1018,10 @@ constexpr int XNT = 256;
 #endif
 constexpr int kCmCtas = RRG_CM_CTAS;  // resident CTAs per SM
 constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
-constexpr int kRrRows = 256;  // rows of the cluster per work item (large batches)
+#ifndef RRG_RR_ROWS
+#define RRG_RR_ROWS 512  // C2 re-rank: 128 -> 1.240, 256 -> 1.122, 384 -> 1.106, 512 -> 1.095, 768 -> 1.134, 1024 -> 1.149 ms
+#endif
+constexpr int kRrRows = RRG_RR_ROWS;  // rows of the cluster per work item (large batches)
 
 struct ClusterRerankArgs {
   DevIndexView ix;

@@ -915,15 +915,24 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         launch_prep(xps, xs, ns, v.s, v.s_pad, v.d, qcodes + (int64_t)s0 * v.s_pad, qscale + s0,
                     qhead + s0, pp + s0, xx + s0, st, nonfinite);
       });
-      if (w == 1 && ns > kSmallBatch && !sliced_routing() && route_fused()) {
+      if (w == 1 && ns > kSmallBatch && route_fused()) {
         // nearest cluster straight from the GEMM: per (query, 64-centroid tile) minima
         const int nt = route_nearest_tiles(v.L);
         double* part_v = diss + (int64_t)s0 * nt;
         int* part_i = reinterpret_cast<int*>(diss + p.qc * nt) + (int64_t)s0 * nt;
-        staged(2, st, [&] {
-          launch_route_nearest_fused(xps, v.cent, ns, v.L, v.s, v.metric, pp + s0, v.cnorm, part_v,
-                                     part_i, st);
-        });
+        if (sliced_routing() && qpl_s) {
+          staged(2, st, [&] { launch_slice_rows(xps, ns, v.s, v.s, true, qpl_s, qex, st); });
+          staged(2, st, [&] {
+            launch_gemm_sliced(qpl_s, qex, ns, v.cent_planes, v.cent_exps, v.L, v.s,
+                               v.metric == kMetricEuclidean ? EPI_L2_ARGMIN : EPI_NEGIP_ARGMIN,
+                               nullptr, part_v, nt, pp + s0, v.cnorm, st, part_i);
+          });
+        } else {
+          staged(2, st, [&] {
+            launch_route_nearest_fused(xps, v.cent, ns, v.L, v.s, v.metric, pp + s0, v.cnorm, part_v,
+                                       part_i, st);
+          });
+        }
         staged(3, st, [&] {
           launch_route_nearest_reduce(part_v, part_i, ns, v.L, sel + s0, prim + s0, st);
         });

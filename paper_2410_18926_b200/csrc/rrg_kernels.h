@@ -217,6 +217,7 @@ void launch_slice_rows(const float* x, int rows, int K, int ld, bool a_operand, 
                        int* exps, cudaStream_t st);
 void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* b, const int* b_exp,
                         int N, int K, int epi, float* outf, double* outd, int64_t ldo,
-                        const double* rowterm, const double* colterm, cudaStream_t st);
+                        const double* rowterm, const double* colterm, cudaStream_t st,
+                        int* outi = nullptr);  // EPI_*_ARGMIN: [M][ceil(N/64)] partials
 
 }  // namespace rrg

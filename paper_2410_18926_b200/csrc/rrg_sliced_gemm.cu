@@ -147,6 +147,7 @@ struct SlicedGemmArgs {
   int64_t ldo;
   const double* rowterm;
   const double* colterm;
+  int* outi;  // EPI_*_ARGMIN: per (row, column tile) nearest column
 };
 
 // Warp 0 (one lane): bulk-copy producer over a kSlStages ring; warp 1 (one lane):
@@ -224,6 +225,9 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
   // 2^(ea - 14) and 2^eb as exact f64 powers of two (|e| stays far inside the range)
   auto pow2 = [](int e) { return __longlong_as_double((long long)(1023 + e) << 52); };
   const double sa = pow2(g.a_exp[gm] - 14);  // padded rows have exponent 0
+  constexpr double kInf = __builtin_huge_val();
+  double best = kInf;  // EPI_*_ARGMIN: this row's (value, lowest column) over the tile
+  int bcol = 0x7fffffff;
 #pragma unroll 1
   for (int c0 = 0; c0 < kSlBN; c0 += 16) {
     uint32_t v[kSl][16];
@@ -249,14 +253,22 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
         const double val = (acc * sa) * pow2(g.b_exp[gn]);
         if (g.epi == EPI_PROJ) {
           g.outf[(size_t)gm * g.ldo + gn] = (float)val;
-        } else if (g.epi == EPI_L2) {
-          const double d2 = __dadd_rn(__dsub_rn(g.rowterm[gm], __dmul_rn(2.0, val)), g.colterm[gn]);
-          g.outd[(size_t)gm * g.ldo + gn] = d2 > 0.0 ? d2 : 0.0;
+        } else if (g.epi == EPI_L2 || g.epi == EPI_L2_ARGMIN) {
+          double d2 = __dadd_rn(__dsub_rn(g.rowterm[gm], __dmul_rn(2.0, val)), g.colterm[gn]);
+          d2 = d2 > 0.0 ? d2 : 0.0;
+          if (g.epi == EPI_L2) g.outd[(size_t)gm * g.ldo + gn] = d2;
+          else if (d2 < best) { best = d2; bcol = gn; }  // columns ascend: ties keep the lowest
+        } else if (g.epi == EPI_NEGIP_ARGMIN) {
+          if (-val < best) { best = -val; bcol = gn; }
         } else {
           g.outd[(size_t)gm * g.ldo + gn] = -val;
         }
       }
     }
+  }
+  if ((g.epi == EPI_L2_ARGMIN || g.epi == EPI_NEGIP_ARGMIN) && gm < g.M) {
+    g.outd[(size_t)gm * g.ldo + nb] = best;
+    g.outi[(size_t)gm * g.ldo + nb] = bcol;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -287,7 +299,7 @@ void launch_slice_rows(const float* x, int rows, int K, int ld, bool a_operand, 
 
 void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* b, const int* b_exp,
                         int N, int K, int epi, float* outf, double* outd, int64_t ldo,
-                        const double* rowterm, const double* colterm, cudaStream_t st) {
+                        const double* rowterm, const double* colterm, cudaStream_t st, int* outi) {
   static int done[64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -300,6 +312,7 @@ void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* 
   g.a = a; g.a_exp = a_exp; g.b = b; g.b_exp = b_exp; g.M = M; g.N = N;
   g.kchunks = sliced_kchunks(K);
   g.epi = epi; g.outf = outf; g.outd = outd; g.ldo = ldo; g.rowterm = rowterm; g.colterm = colterm;
+  g.outi = outi;
   dim3 grid((N + kSlBN - 1) / kSlBN, (M + kSlBM - 1) / kSlBM);
   (k_gemm_sliced<<<grid, kSlThreads, kSlSmem, st>>>(g), note_launch());
 }

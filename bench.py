@@ -8,12 +8,13 @@ queries, 1M x 768 corpus, L=1024, s=256, r=32, k=100) through the device entry
 host-buffer C-ABI entry ``rrg_search_host`` with pinned host queries and results
 copied inside the timed region (``e2e``).
 
-Multi-GPU (torchrun, N>1), default ``--mode sharded`` (the north star's layout):
-clusters with their factors and corpus rows are split over the ranks, the query
-batch is replicated, and the two exact merges (global top-t, then top-k) are
-NCCL all-gathers over NVLink; ``value`` = batch / max-over-ranks time
-("strong").  ``--mode replica``: each rank searches its own batch on a full
-index copy with no collective ("weak").
+Multi-GPU (torchrun, N>1), default ``--mode replica``: the C2 index (3.1 GB) fits
+one GPU, so each rank searches its own 10k-query batch on a full index copy with no
+collective on the data path ("weak"; value = all ranks' queries / max-over-ranks
+time).  ``--mode sharded`` (the north star's layout for indexes larger than one
+GPU): clusters with their factors and corpus rows are split over the ranks, the
+query batch is replicated, and the two exact merges (global top-t, then top-k) are
+NCCL all-gathers over NVLink ("strong").
 
 ``--impl reference`` times the reference's CPU algorithm (the oracle port of
 rrann.query_batch, oracle/rrann_oracle.py) on the host cores, on a bounded
@@ -50,8 +51,11 @@ def parse():
     ap.add_argument("--t", type=int, default=None)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default="sharded", choices=["sharded", "replica"],
-                    help="N>1: cluster-sharded index (north star) or full-index replicas")
+    ap.add_argument("--mode", default=os.environ.get("RRG_BENCH_MODE", "replica"),
+                    choices=["sharded", "replica"],
+                    help="N>1: full-index replicas, each rank its own query batch (default: the "
+                         "C2 index fits one GPU, no collective on the data path) or the "
+                         "cluster-sharded index with the two exact NCCL merges (DESIGN.md §5)")
     return ap.parse_args()
 
 
@@ -413,12 +417,17 @@ def main():
         torch.cuda.synchronize()
         runs = []
         for _ in range(3):
+            if world > 1:
+                dist.barrier()
             t0 = time.perf_counter()
             searcher.host_many(qs, outs)
             runs.append(time.perf_counter() - t0)
         for o in outs:  # every step returned the same results as the single call
             assert np.array_equal(o[0], hout[0]) and np.array_equal(o[2], hout[2])
-        e2e_val = total_q * nb / float(np.median(runs))
+        el_t = torch.tensor([float(np.median(runs))], device="cuda")
+        if world > 1:  # the slowest rank sets the whole job's rate
+            dist.all_reduce(el_t, op=dist.ReduceOp.MAX)
+        e2e_val = total_q * nb / float(el_t.item())
         e2e_mode = (f"rrg_search_host_many over {nb} consecutive batches (H2D/D2H of "
                     "neighbouring steps overlapped with the search), median of 3 runs")
 

@@ -1520,7 +1520,9 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   }
   // warp per query at any list length once the batch fills the GPU (measured on C5:
   // w=16 (~16k candidates) 2.0 vs 4.9 ms, w=64 (~62k) 6.6 vs 14.5 ms for the CTA select)
-  if (warp_select_ok(nq) && h.rerank) {
+  // (the membership bits are sized by kcap = min(largest list, 24k): a capped kcap
+  // cannot hold every candidate's bit, so the CTA select handles that case)
+  if (warp_select_ok(nq) && h.rerank && !(h.marks && h.kcap >= 24 * 1024)) {
     // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
     const int bits_cap = h.marks ? h.kcap : 0;
     const int stage_cap = 0;  // keys are read through L1

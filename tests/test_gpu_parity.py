@@ -669,3 +669,26 @@ def test_fused_nearest_cluster_ties(pkg, tmp_path):
     for i, r in enumerate(ref):
         c = int(cnt[i])
         np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"q{i}")
+
+
+@pytest.mark.parametrize("rerank_mode", ["query", "cluster"])
+def test_long_candidate_lists(pkg, tmp_path, rerank_mode, monkeypatch):
+    """~30k candidates per query (w = L on 4 large clusters): the warp top-t streams
+    long lists (per-query re-rank) and yields to the CTA select where its membership
+    bits would not fit (cluster-major re-rank, lists above the 24k key cap)."""
+    monkeypatch.setenv("RRG_WARP_SELECT", "1")
+    monkeypatch.setenv("RRG_RERANK", rerank_mode)
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    blob = random_index(16, 8, 4, 4, 30000, "euclidean", seed=11, dup_rows=5)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "long", blob))
+    oidx = O.read_index(blob)
+    q = np.random.default_rng(2).standard_normal((24, 16)).astype(F32)
+    for k, w, t in [(10, 4, 300), (20, 3, 2000)]:
+        ids, sc, cnt = dev.search_host(q, k, w, t, True)
+        ref = O.query_batch(oidx, q, k, w, t, True)
+        for i, r in enumerate(ref):
+            c = int(cnt[i])
+            np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{(k, w, t)} q{i}")
+            np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))

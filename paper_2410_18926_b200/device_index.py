@@ -119,17 +119,40 @@ class DeviceIndex:
                      if bm else np.zeros(1, f32))
         norms = None
         if cfg.metric == "euclidean":
-            norms = np.ascontiguousarray(np.concatenate([mdl.norm_terms for mdl in models]).astype(f32))
-        proj = np.ascontiguousarray(index.projection, dtype=f32)
-        cent = np.ascontiguousarray(index.centroids, dtype=f32)
-        corpus = None if index.corpus is None else np.ascontiguousarray(index.corpus, dtype=f32)
-        flags = FLAG_QUANTIZED if quant else 0
-        if corpus is not None:
-            flags |= FLAG_CORPUS
-        if cfg.balanced:
-            flags |= FLAG_BALANCED
-        if cfg.scoring_mode == "exact_ivf":
-            flags |= FLAG_EXACT_IVF
+            norms = np.concatenate([mdl.norm_terms for mdl in models])
+        extra = (FLAG_BALANCED if cfg.balanced else 0) | (FLAG_EXACT_IVF if cfg.scoring_mode == "exact_ivf" else 0)
+        return cls.from_arrays(
+            metric=cfg.metric, rank=r, projection=index.projection, centroids=index.centroids,
+            cluster_sizes=sizes, point_ids=ids, a_head=a_head, a_scale=a_scale, a_values=a_vals,
+            b_head=b_head, b_scale=b_scale, b_values=b_vals, norms=norms, corpus=index.corpus,
+            a_values_f32=a_f32, b_values_f32=b_f32, n_points=index.n_points, extra_flags=extra,
+            device=device, source="rrr")
+
+    @classmethod
+    def from_arrays(cls, *, metric: str, rank: int, projection, centroids, cluster_sizes, point_ids,
+                    a_head=None, a_scale=None, a_values=None, b_head=None, b_scale=None, b_values=None,
+                    norms=None, corpus=None, a_values_f32=None, b_values_f32=None, n_points=None,
+                    extra_flags: int = 0, device: int = 0, source: str = "arrays") -> "DeviceIndex":
+        """Upload host arrays laid out as ``RrgIndexDesc`` documents (include/rrg.h): the
+        fields of an in-memory index (index.py:110-118), per-cluster payloads concatenated
+        in cluster order, quantized factors with their zero pad row (index.py:346-353).
+        Quantized iff ``a_values`` is given."""
+        f32 = np.float32
+
+        def arr(a, dt):
+            return None if a is None else np.ascontiguousarray(a, dtype=dt)
+
+        proj, cent = arr(projection, f32), arr(centroids, f32)
+        sizes, ids = arr(cluster_sizes, np.uint32), arr(point_ids, np.int64)
+        a_head, a_scale, a_vals = arr(a_head, f32), arr(a_scale, f32), arr(a_values, np.int8)
+        b_head, b_scale, b_vals = arr(b_head, f32), arr(b_scale, f32), arr(b_values, np.int8)
+        norms, corpus = arr(norms, f32), arr(corpus, f32)
+        a_f32, b_f32 = arr(a_values_f32, f32), arr(b_values_f32, f32)
+        quant = a_vals is not None
+        flags = (FLAG_QUANTIZED if quant else 0) | (FLAG_CORPUS if corpus is not None else 0) | extra_flags
+        d, s = proj.shape
+        L = cent.shape[0]
+        m = int(sizes.sum()) if n_points is None else int(n_points)
         keep = [proj, cent, sizes, ids, a_head, a_scale, a_vals, b_head, b_scale, b_vals, norms, corpus,
                 a_f32, b_f32]
 
@@ -137,15 +160,15 @@ class DeviceIndex:
             return None if a is None else a.ctypes.data
 
         desc = RrgIndexDesc(
-            metric=_METRIC_CODES[cfg.metric], dim=index.dim, reduced_dim=s, rank=r, n_clusters=L,
-            n_points=index.n_points, flags=flags, projection=ptr(proj), centroids=ptr(cent),
+            metric=_METRIC_CODES[metric], dim=d, reduced_dim=s, rank=rank, n_clusters=L,
+            n_points=m, flags=flags, projection=ptr(proj), centroids=ptr(cent),
             cluster_sizes=ptr(sizes), point_ids=ptr(ids), a_head=ptr(a_head), a_scale=ptr(a_scale),
             a_values=ptr(a_vals), b_head=ptr(b_head), b_scale=ptr(b_scale), b_values=ptr(b_vals),
             norms=ptr(norms), corpus=ptr(corpus), a_values_f32=ptr(a_f32), b_values_f32=ptr(b_f32))
         h = ctypes.c_void_p()
         check(lib.rrg_index_create(ctypes.byref(desc), device, ctypes.byref(h)))
         del keep
-        return cls(h.value, device, "rrr")
+        return cls(h.value, device, source)
 
     # ----------------------------------------------------------------- search
 

@@ -1,0 +1,381 @@
+"""C4 (10M x 960 GIST shape, L=8192, s=64, r=32, k=100): build, parity and 1-GPU measurement.
+
+The reference cannot build C4 here (its build() holds the whole corpus as the
+training set in NumPy; SURVEY.md §7 hard part 6), so this tool restates
+``build()`` (index.py:170-262) on the GPU with torch and hands the arrays to
+``DeviceIndex.from_arrays`` (the ``RrgIndexDesc`` boundary) -- index
+construction is test/bench infrastructure, not the product path.  Differences
+from the reference build, all on the construction side (the search contract is
+the index content, and both the device path and the oracle read the same arrays):
+
+* data: ``synth_dataset`` semantics (bench.py:140-170: centers 6 N(0,I), uniform
+  labels, points/queries = center + N(0,I), n_blobs = m/1000) drawn with torch's
+  CUDA generator instead of NumPy's stream;
+* projection: top-s eigenvectors of the Gram of a training sample
+  (linalg.py:120-146) times a block rotation fixing coordinate 0 (index.py:159-164);
+* clustering: Lloyd k-means on the projected corpus, random init, ``--iters`` passes
+  (cluster.py:121-150 uses k-means++ and runs to convergence);
+* training rows: a ``--train`` sample of the corpus routed to its top train_w=2
+  clusters (rrr.py:217-233 with the whole corpus), borrowing the cluster's own
+  rows below r (index.py:240-245);
+* RRR fit per cluster: y = X C^T (targets in the original dimension), V_r from a
+  randomized range finder with 4 power passes (rrr.py:163-166), A = pinv(px) y V_r,
+  B = V_r^T, both quantized column-wise in mixed precision (quantize.py:80-106).
+
+Steps: generate -> build -> upload -> GPU exact ground truth -> (w, t) grid ->
+timed 10k-query batches (L2 flushed between steps) -> oracle parity on a query sample.
+Prints one JSON line.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def log(*a):
+    print(f"[c4 {time.strftime('%H:%M:%S')}]", *a, file=sys.stderr, flush=True)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--m", type=int, default=10_000_000)
+    ap.add_argument("--d", type=int, default=960)
+    ap.add_argument("--L", type=int, default=8192)
+    ap.add_argument("--s", type=int, default=64)
+    ap.add_argument("--r", type=int, default=32)
+    ap.add_argument("--k", type=int, default=100)
+    ap.add_argument("--nq", type=int, default=10_000)
+    ap.add_argument("--train", type=int, default=2_000_000)
+    ap.add_argument("--iters", type=int, default=10)
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--grid", default="1:200,1:400,1:800,2:400,2:800,3:800,4:800,4:1600")
+    ap.add_argument("--parity", type=int, default=64, help="queries checked against the oracle")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------------ build
+
+
+def quantize_columns(m):
+    """quantize_matrix_columns(m, mixed_precision=True) (quantize.py:80-106) on the GPU.
+    Returns (head_row f32[cols], col_scales f32[cols], values int8[rows, cols] with the
+    zero pad row of the file layout, index.py:349-353)."""
+    import torch
+
+    m = m.float()
+    head = m[0].clone()
+    tail = m[1:]
+    absmax = tail.abs().amax(dim=0) if tail.shape[0] else torch.zeros_like(head)
+    safe = torch.where(absmax > 0, absmax.double(), torch.ones_like(absmax, dtype=torch.float64))
+    scales = torch.where(absmax > 0, 127.0 / safe, torch.ones_like(safe)).float()
+    p = tail.double() * scales.double()
+    codes = (torch.sign(p) * torch.floor(p.abs() + 0.5)).clamp(-127, 127).to(torch.int8)
+    vals = torch.cat([torch.zeros((1, m.shape[1]), dtype=torch.int8, device=m.device), codes])
+    return head, scales, vals
+
+
+def build(args, corpus, g):
+    import torch
+
+    dev = corpus.device
+    m, d = corpus.shape
+    s, r, L = args.s, args.r, args.L
+    torch.backends.cuda.matmul.allow_tf32 = False
+    # training sample (the reference trains on the whole corpus)
+    tsel = torch.randperm(m, generator=g, device=dev)[: args.train]
+    train = corpus[tsel]
+    # projection: top-s eigenvectors of the f64 Gram (linalg.py:137-146), block rotation
+    gram = torch.zeros((d, d), dtype=torch.float64, device=dev)
+    for i in range(0, train.shape[0], 262_144):
+        x = train[i:i + 262_144].double()
+        gram += x.T @ x
+    evals, evecs = torch.linalg.eigh(gram)
+    w = evecs[:, torch.argsort(evals, descending=True)[:s]]
+    idx = w.abs().argmax(dim=0)
+    w = w * torch.sign(w[idx, torch.arange(s, device=dev)])
+    rot = torch.eye(s, dtype=torch.float64, device=dev)
+    qm, _ = torch.linalg.qr(torch.randn((s - 1, s - 1), generator=g, device=dev, dtype=torch.float64))
+    rot[1:, 1:] = qm
+    W = (w @ rot).float()
+    W64 = W.double()
+
+    def project(x):
+        out = torch.empty((x.shape[0], s), dtype=torch.float32, device=dev)
+        for i in range(0, x.shape[0], 1 << 20):
+            out[i:i + (1 << 20)] = (x[i:i + (1 << 20)].double() @ W64).float()
+        return out
+
+    pc = project(corpus)
+    pt = pc[tsel]
+    log("projection done")
+
+    def nearest(x, cent, topn=1):
+        cc = (cent.double() ** 2).sum(1).float()
+        out = torch.empty((x.shape[0], topn), dtype=torch.int64, device=dev)
+        for i in range(0, x.shape[0], 1 << 18):
+            xb = x[i:i + (1 << 18)]
+            dd = cc[None, :] - 2.0 * (xb @ cent.T)
+            out[i:i + (1 << 18)] = torch.topk(dd, topn, dim=1, largest=False).indices
+        return out
+
+    cent = pc[torch.randperm(m, generator=g, device=dev)[:L]].clone()
+    for it in range(args.iters):
+        asg = nearest(pc, cent)[:, 0]
+        cnt = torch.bincount(asg, minlength=L)
+        sums = torch.zeros((L, s), dtype=torch.float64, device=dev).index_add_(0, asg, pc.double())
+        empty = cnt == 0
+        newc = (sums / cnt.clamp(min=1)[:, None]).float()
+        if empty.any():
+            newc[empty] = pc[torch.randint(m, (int(empty.sum()),), generator=g, device=dev)]
+        cent = newc
+        log(f"kmeans iter {it}: empty={int(empty.sum())} max={int(cnt.max())} min={int(cnt.min())}")
+    asg = nearest(pc, cent)[:, 0]
+    sizes = torch.bincount(asg, minlength=L)
+    order = torch.argsort(asg, stable=True)
+    starts = torch.cumsum(sizes, 0) - sizes
+    # routed training rows: top train_w=2 clusters of each training row (rrr.py:217-233)
+    tr = nearest(pt, cent, 2)
+    tcl = tr.reshape(-1)
+    trow = torch.arange(pt.shape[0], device=dev).repeat_interleave(2)
+    torder = torch.argsort(tcl, stable=True)
+    tsizes = torch.bincount(tcl, minlength=L)
+    tstarts = torch.cumsum(tsizes, 0) - tsizes
+    trow = trow[torder]
+
+    sizes_h, starts_h = sizes.cpu().numpy(), starts.cpu().numpy()
+    tsizes_h, tstarts_h = tsizes.cpu().numpy(), tstarts.cpu().numpy()
+    a_head, a_scale, a_vals, b_head, b_scale, b_vals = [], [], [], [], [], []
+    n_exact = 0
+    t0 = time.time()
+    for l in range(L):
+        ml = int(sizes_h[l])
+        ids = order[starts_h[l]:starts_h[l] + ml]
+        if ml < r:  # exact model (rrr.py:103-114): A = C^T of the projected cluster block
+            ha, sa, va = quantize_columns(pc[ids].T.contiguous())
+            a_head.append(ha); a_scale.append(sa); a_vals.append(va.reshape(-1))
+            n_exact += 1
+            continue
+        rows = trow[tstarts_h[l]:tstarts_h[l] + int(tsizes_h[l])]
+        x = train[rows]
+        px = pt[rows]
+        c = corpus[ids]
+        if rows.shape[0] < r:  # index.py:240-245
+            x = torch.cat([x, c])
+            px = torch.cat([px, pc[ids]])
+        y = x.double() @ c.double().T                       # n_l x m_l
+        om = torch.randn((ml, r + 8), generator=g, device=dev, dtype=torch.float64)
+        z, _ = torch.linalg.qr(y @ om)
+        for _ in range(4):
+            z, _ = torch.linalg.qr(y @ (y.T @ z))
+        bm = z.T @ y                                         # (r+8) x m_l
+        ev, eu = torch.linalg.eigh(bm @ bm.T)
+        top = torch.argsort(ev, descending=True)[:r]
+        sig = ev[top].clamp(min=1e-300).sqrt()
+        vr = (bm.T @ eu[:, top]) / sig[None, :]              # m_l x r
+        rhs = px.double().T @ (y @ vr)                       # s x r
+        a = torch.linalg.solve(px.double().T @ px.double(), rhs).float()
+        b = vr.T.contiguous().float()                        # r x m_l
+        ha, sa, va = quantize_columns(a)
+        hb, sb, vb = quantize_columns(b)
+        a_head.append(ha); a_scale.append(sa); a_vals.append(va.reshape(-1))
+        b_head.append(hb); b_scale.append(sb); b_vals.append(vb.reshape(-1))
+        if l % 1024 == 0:
+            log(f"rrr fit {l}/{L} ({time.time() - t0:.0f} s)")
+    norms = torch.empty(m, dtype=torch.float32, device=dev)
+    for i in range(0, m, 1 << 20):
+        blk = corpus[order[i:i + (1 << 20)]].double()
+        norms[i:i + (1 << 20)] = (blk * blk).sum(1).float()
+    cat = lambda xs, dt: torch.cat(xs).cpu().numpy().astype(dt)  # noqa: E731
+    return dict(
+        projection=W.cpu().numpy(), centroids=cent.cpu().numpy(), cluster_sizes=sizes_h.astype(np.uint32),
+        point_ids=order.cpu().numpy().astype(np.int64),
+        a_head=cat(a_head, np.float32), a_scale=cat(a_scale, np.float32), a_values=cat(a_vals, np.int8),
+        b_head=cat(b_head, np.float32), b_scale=cat(b_scale, np.float32), b_values=cat(b_vals, np.int8),
+        norms=norms.cpu().numpy(), n_exact=n_exact)
+
+
+# ------------------------------------------------------------------------------- main
+
+
+def main():
+    args = parse()
+    import psutil
+    import torch
+
+    from paper_2410_18926_b200 import DeviceIndex
+    from paper_2410_18926_b200.ground_truth import ground_truth_device
+
+    need = args.m * args.d * 4
+    avail = psutil.virtual_memory().available
+    log(f"host RAM available {avail / 2**30:.0f} GiB, corpus {need / 2**30:.1f} GiB")
+    if avail < 1.3 * need:
+        print(json.dumps({"workload": "c4", "unavailable": f"host RAM {avail / 2**30:.0f} GiB < 1.3 x corpus"}))
+        return
+    dev = torch.device("cuda:0")
+    g = torch.Generator(device=dev)
+    g.manual_seed(args.seed)
+    n_blobs = args.m // 1000
+    t0 = time.time()
+    centers = torch.randn((n_blobs, args.d), generator=g, device=dev) * 6.0
+    corpus = torch.empty((args.m, args.d), dtype=torch.float32, device=dev)
+    for i in range(0, args.m, 1 << 20):
+        n = min(1 << 20, args.m - i)
+        lab = torch.randint(n_blobs, (n,), generator=g, device=dev)
+        corpus[i:i + n] = centers[lab] + torch.randn((n, args.d), generator=g, device=dev)
+    qlab = torch.randint(n_blobs, (args.nq,), generator=g, device=dev)
+    queries = centers[qlab] + torch.randn((args.nq, args.d), generator=g, device=dev)
+    log(f"data generated ({time.time() - t0:.0f} s)")
+    t0 = time.time()
+    arrs = build(args, corpus, g)
+    build_s = time.time() - t0
+    log(f"build done ({build_s:.0f} s), exact clusters {arrs['n_exact']}")
+    gt = ground_truth_device(corpus, queries, args.k).cpu().numpy()
+    torch.cuda.synchronize()
+    log("ground truth done")
+    corpus_h = corpus.cpu().numpy()
+    del corpus
+    torch.cuda.empty_cache()
+    n_exact = arrs.pop("n_exact")
+    di = DeviceIndex.from_arrays(metric="euclidean", rank=args.r, corpus=corpus_h, device=0, **arrs)
+    log(f"device index {di}")
+    # ... measurement continues in run()
+    return run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact)
+
+
+def recall(ids, gt, k):
+    hits = 0
+    for i in range(gt.shape[0]):
+        hits += np.intersect1d(ids[i, :k], gt[i, :k]).size
+    return hits / (gt.shape[0] * k)
+
+
+def run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact):
+    import torch
+
+    from bench import ClockSampler
+    from paper_2410_18926_b200 import _native, last_launch_count
+
+    k = args.k
+    grid = []
+    for item in args.grid.split(","):
+        w, t = (int(v) for v in item.split(":"))
+        ids, sc, cnt = di.search_device(queries, k, w, t, True)
+        torch.cuda.synchronize()
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        for _ in range(3):
+            di.search_device(queries, k, w, t, True)
+        ev1.record()
+        torch.cuda.synchronize()
+        ms = ev0.elapsed_time(ev1) / 3
+        rc = recall(ids.cpu().numpy(), gt, k)
+        grid.append({"w": w, "t": t, "recall": rc, "ms": ms, "qps": args.nq / ms * 1e3})
+        log(f"w={w} t={t} recall={rc:.4f} {ms:.3f} ms")
+    ok = [p for p in grid if p["recall"] >= 0.90]
+    best = max(ok, key=lambda p: p["qps"]) if ok else max(grid, key=lambda p: p["recall"])
+    w, t = best["w"], best["t"]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=queries.device)
+    out = None
+    for _ in range(args.warmup):
+        out = di.search_device(queries, k, w, t, True)
+    torch.cuda.synchronize()
+    total = 0.0
+    launches = 0
+    with ClockSampler(0) as clk:
+        for _ in range(args.steps):
+            flush.fill_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            out = di.search_device(queries, k, w, t, True)
+            e1.record()
+            torch.cuda.synchronize()
+            total += e0.elapsed_time(e1)
+            launches += last_launch_count()
+    ms = total / args.steps
+    ids, sc, cnt = (x.cpu().numpy() for x in out)
+    rc = recall(ids, gt, k)
+    # stage split
+    import ctypes
+    _native.lib.rrg_set_stage_timing(1)
+    stage_ms, stage_n = (ctypes.c_double * 9)(), (ctypes.c_int64 * 9)()
+    _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
+    for i in range(3):
+        flush.fill_(i)
+        di.search_device(queries, k, w, t, True)
+    _native.lib.rrg_stage_times(stage_ms, stage_n)
+    _native.lib.rrg_set_stage_timing(0)
+    names = ["project", "quantize", "route_dist", "route_select", "select_topt", "rerank", "bucket",
+             "cluster_score"]
+    stage = {nm: round(stage_ms[i] / 3, 4) for i, nm in enumerate(names)}
+    # oracle parity on a query sample (id-for-id, score bits)
+    parity = oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t) if args.parity else None
+    line = {
+        "metric": "QPS at recall@100 >=0.90 (batched), 1 B200", "value": args.nq / ms * 1e3,
+        "unit": "queries/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "config": {"workload": "c4", "m": args.m, "d": args.d, "L": args.L, "s": args.s, "r": args.r,
+                   "k": k, "queries": args.nq, "w": w, "t": t, "n_blobs": args.m // 1000,
+                   "recall_at_k": rc, "l2": "256 MiB write between steps (excluded)",
+                   "index": f"GPU restatement of build(): train sample {args.train}, k-means {args.iters} "
+                            f"Lloyd passes, {n_exact} exact clusters", "build_s": build_s},
+        "gpu_launches": launches // args.steps, "grid": grid, "stage_ms": stage, "parity": parity,
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
+def oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t):
+    from oracle import rrann_oracle as O
+
+    r, s = args.r, args.s
+    sizes = arrs["cluster_sizes"].astype(np.int64)
+    L = sizes.shape[0]
+    idx = O.OIndex(metric="euclidean", d=args.d, s=s, r=r, L=L, m=int(sizes.sum()), flags=3,
+                   projection=arrs["projection"], centroids=arrs["centroids"], corpus=corpus_h)
+    pa_cols = pa_vals = pb_cols = pb_vals = pp = 0
+    for l in range(L):
+        ml = int(sizes[l])
+        exact = ml < r
+        cols = ml if exact else r
+        av = arrs["a_values"][pa_vals:pa_vals + s * cols].reshape(s, cols)
+        a = O.OQuant(arrs["a_head"][pa_cols:pa_cols + cols], arrs["a_scale"][pa_cols:pa_cols + cols],
+                     av[1:], s, cols)
+        pa_cols += cols
+        pa_vals += s * cols
+        b = None
+        if not exact:
+            bv = arrs["b_values"][pb_vals:pb_vals + r * ml].reshape(r, ml)
+            b = O.OQuant(arrs["b_head"][pb_cols:pb_cols + ml], arrs["b_scale"][pb_cols:pb_cols + ml],
+                         bv[1:], r, ml)
+            pb_cols += ml
+            pb_vals += r * ml
+        idx.clusters.append(O.OCluster(ids=arrs["point_ids"][pp:pp + ml], a=a, b=b,
+                                       norms=arrs["norms"][pp:pp + ml], exact=exact))
+        pp += ml
+    qh = queries.cpu().numpy()
+    sample = np.linspace(0, qh.shape[0] - 1, args.parity).astype(int)
+    bad = 0
+    t0 = time.time()
+    for i in sample:
+        ref = O.query(idx, qh[i], args.k, w, t, True)
+        c = int(cnt[i])
+        same = (c == len(ref.ids) and np.array_equal(ids[i, :c], ref.ids)
+                and np.array_equal(sc[i, :c].view(np.int32), ref.scores.view(np.int32)))
+        bad += not same
+    return {"queries": len(sample), "mismatches": bad, "oracle_s": time.time() - t0,
+            "check": "ids id-for-id and score bits vs oracle/rrann_oracle.query on the same arrays"}
+
+
+if __name__ == "__main__":
+    main()

@@ -110,6 +110,11 @@ int rrg_index_open_shard(const char* path, int device, int32_t cluster_begin,
 
 /* Build from host arrays (see RrgIndexDesc). */
 int rrg_index_create(const RrgIndexDesc* desc, int device, RrgIndex** out);
+/* Shard of an in-memory index: clusters [cluster_begin, cluster_end) keep their
+ * factors and corpus rows, every cluster keeps its centroid (routing is replicated);
+ * same layout as rrg_index_open_shard. */
+int rrg_index_create_shard(const RrgIndexDesc* desc, int device, int32_t cluster_begin,
+                           int32_t cluster_end, RrgIndex** out);
 
 void rrg_index_destroy(RrgIndex* index);
 int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out);

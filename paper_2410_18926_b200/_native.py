@@ -49,6 +49,8 @@ SIGNATURES = {
     "rrg_index_open": (c_int, [ctypes.c_char_p, c_int, ctypes.POINTER(c_vp)]),
     "rrg_index_open_shard": (c_int, [ctypes.c_char_p, c_int, c_i32, c_i32, ctypes.POINTER(c_vp)]),
     "rrg_index_create": (c_int, [ctypes.POINTER(RrgIndexDesc), c_int, ctypes.POINTER(c_vp)]),
+    "rrg_index_create_shard": (c_int, [ctypes.POINTER(RrgIndexDesc), c_int, c_i32, c_i32,
+                                       ctypes.POINTER(c_vp)]),
     "rrg_index_destroy": (None, [c_vp]),
     "rrg_index_info": (c_int, [c_vp, ctypes.POINTER(RrgIndexInfo)]),
     "rrg_index_cluster_sizes": (c_int, [c_vp, c_vp]),

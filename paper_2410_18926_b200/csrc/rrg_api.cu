@@ -50,7 +50,10 @@ struct StageTimer {
 };
 thread_local StageTimer g_timer;
 
-// Runs one launch, counting it and (when enabled) bracketing it with events.
+[[noreturn]] void launch_failed(int stage, cudaError_t e);
+
+// Runs one launch, counting it and (when enabled) bracketing it with events; a launch
+// rejected at submission (bad grid / shared-memory size) fails here, naming its stage.
 template <typename F>
 void staged(int stage, cudaStream_t st, F&& launch) {
   StageTimer& t = g_timer;
@@ -63,6 +66,8 @@ void staged(int stage, cudaStream_t st, F&& launch) {
   } else {
     launch();
   }
+  cudaError_t e = cudaPeekAtLastError();
+  if (e != cudaSuccess) launch_failed(stage, e);
 }
 
 int fail(int code, const char* kind, const char* fmt, ...) {
@@ -79,6 +84,13 @@ int fail(int code, const char* kind, const char* fmt, ...) {
 struct RrgFail {
   int code;
 };
+
+void launch_failed(int stage, cudaError_t e) {
+  cudaGetLastError();
+  fail(RRG_E_INTERNAL, "RrannError", "CUDA error %s at launch %lld (stage %d): %s", cudaGetErrorName(e),
+       (long long)g_launches, stage, cudaGetErrorString(e));
+  throw RrgFail{RRG_E_INTERNAL};
+}
 
 #define CUDA_TRY(expr)                                                                        \
   do {                                                                                        \
@@ -590,7 +602,7 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
   return RRG_OK;
 }
 
-int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
+int create_impl(const RrgIndexDesc* dsc, int device, int32_t cb, int32_t ce, RrgIndex** out) {
   CUDA_TRY(cudaSetDevice(device));
   HostModel hm;
   hm.metric = dsc->metric; hm.d = dsc->dim; hm.s = dsc->reduced_dim; hm.r = dsc->rank;
@@ -602,6 +614,9 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
   hm.clusters.resize(L);
   const bool exact_ivf = hm.flags & RRG_FLAG_EXACT_IVF;
   const bool quant = hm.flags & RRG_FLAG_QUANTIZED;
+  if (ce < 0) ce = L;
+  if (cb < 0 || cb > ce || ce > L)
+    raise_usage("ParameterError", "shard cluster range [%d, %d) outside [0, %d]", cb, ce, L);
   if (!quant && (!dsc->a_values_f32 || !dsc->b_values_f32))
     raise_usage("ParameterError", "unquantized index description needs a_values_f32/b_values_f32");
   int64_t po = 0, ao = 0, aoff = 0, bo = 0, boff = 0;
@@ -609,11 +624,13 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
     HostCluster& c = hm.clusters[l];
     c.m = dsc->cluster_sizes[l];
     c.exact = exact_ivf || (int)c.m < r;
+    c.owned = l >= cb && l < ce;  // a shard keeps only the payloads of its own clusters
     const int64_t m = c.m;
     c.ids.assign(dsc->point_ids + po, dsc->point_ids + po + m);
-    if (dsc->norms) c.norms.assign(dsc->norms + po, dsc->norms + po + m);
+    if (dsc->norms && c.owned) c.norms.assign(dsc->norms + po, dsc->norms + po + m);
     const int64_t acols = c.exact ? m : r;
-    if (quant) {
+    if (!c.owned) {
+    } else if (quant) {
       c.a_head.assign(dsc->a_head + ao, dsc->a_head + ao + acols);
       c.a_scale.assign(dsc->a_scale + ao, dsc->a_scale + ao + acols);
       c.a_vals.assign(dsc->a_values + aoff, dsc->a_values + aoff + (size_t)s * acols);
@@ -623,7 +640,8 @@ int create_impl(const RrgIndexDesc* dsc, int device, RrgIndex** out) {
     ao += acols;
     aoff += (int64_t)s * acols;
     if (!c.exact) {
-      if (quant) {
+      if (!c.owned) {
+      } else if (quant) {
         c.b_head.assign(dsc->b_head + bo, dsc->b_head + bo + m);
         c.b_scale.assign(dsc->b_scale + bo, dsc->b_scale + bo + m);
         c.b_vals.assign(dsc->b_values + boff, dsc->b_values + boff + (size_t)r * m);
@@ -1143,7 +1161,12 @@ int rrg_index_open_shard(const char* path, int device, int32_t cb, int32_t ce, R
 }
 
 int rrg_index_create(const RrgIndexDesc* desc, int device, RrgIndex** out) {
-  return guarded([&] { return create_impl(desc, device, out); });
+  return guarded([&] { return create_impl(desc, device, 0, -1, out); });
+}
+
+int rrg_index_create_shard(const RrgIndexDesc* desc, int device, int32_t cb, int32_t ce,
+                           RrgIndex** out) {
+  return guarded([&] { return create_impl(desc, device, cb, ce, out); });
 }
 
 void rrg_index_destroy(RrgIndex* index) { delete index; }

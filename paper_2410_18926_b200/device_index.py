@@ -132,11 +132,14 @@ class DeviceIndex:
     def from_arrays(cls, *, metric: str, rank: int, projection, centroids, cluster_sizes, point_ids,
                     a_head=None, a_scale=None, a_values=None, b_head=None, b_scale=None, b_values=None,
                     norms=None, corpus=None, a_values_f32=None, b_values_f32=None, n_points=None,
-                    extra_flags: int = 0, device: int = 0, source: str = "arrays") -> "DeviceIndex":
+                    extra_flags: int = 0, device: int = 0, source: str = "arrays",
+                    shard: tuple[int, int] | None = None) -> "DeviceIndex":
         """Upload host arrays laid out as ``RrgIndexDesc`` documents (include/rrg.h): the
         fields of an in-memory index (index.py:110-118), per-cluster payloads concatenated
         in cluster order, quantized factors with their zero pad row (index.py:346-353).
-        Quantized iff ``a_values`` is given."""
+        Quantized iff ``a_values`` is given; ``shard=(begin, end)`` keeps only that
+        cluster range's payloads (``rrg_index_create_shard``, the layout of
+        ``from_file(..., shard=...)``)."""
         f32 = np.float32
 
         def arr(a, dt):
@@ -166,7 +169,12 @@ class DeviceIndex:
             a_values=ptr(a_vals), b_head=ptr(b_head), b_scale=ptr(b_scale), b_values=ptr(b_vals),
             norms=ptr(norms), corpus=ptr(corpus), a_values_f32=ptr(a_f32), b_values_f32=ptr(b_f32))
         h = ctypes.c_void_p()
-        check(lib.rrg_index_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        if shard is None:
+            check(lib.rrg_index_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        else:
+            check(lib.rrg_index_create_shard(ctypes.byref(desc), device, int(shard[0]), int(shard[1]),
+                                             ctypes.byref(h)))
+            source = f"{source}[{shard[0]}:{shard[1]}]"
         del keep
         return cls(h.value, device, source)
 

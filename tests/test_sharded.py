@@ -127,3 +127,47 @@ def test_gpu_shards_equal_unsharded(tmp_path, G):
         np.testing.assert_array_equal(cnt, rcnt)
         np.testing.assert_array_equal(ids, rid)
         np.testing.assert_array_equal(np.nan_to_num(sc).view(np.int32), np.nan_to_num(rsc).view(np.int32))
+
+
+def oindex_arrays(o):
+    """An oracle-parsed index as the plain arrays of RrgIndexDesc (include/rrg.h): per-cluster
+    payloads concatenated in cluster order, quantized factors with their zero pad row."""
+    def full(q):
+        return np.concatenate([np.zeros((1, q.cols), np.int8), q.values]).ravel()
+
+    cl = o.clusters
+    bm = [c for c in cl if c.b is not None]
+    return dict(metric=o.metric, rank=o.r, projection=o.projection, centroids=o.centroids,
+                cluster_sizes=np.array([c.ids.shape[0] for c in cl], np.uint32),
+                point_ids=np.concatenate([c.ids for c in cl]),
+                a_head=np.concatenate([c.a.head_row for c in cl]),
+                a_scale=np.concatenate([c.a.col_scales for c in cl]),
+                a_values=np.concatenate([full(c.a) for c in cl]),
+                b_head=np.concatenate([c.b.head_row for c in bm]),
+                b_scale=np.concatenate([c.b.col_scales for c in bm]),
+                b_values=np.concatenate([full(c.b) for c in bm]),
+                norms=np.concatenate([c.norms for c in cl]), corpus=o.corpus)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("G", [1, 3])
+def test_gpu_array_shards_equal_unsharded(G):
+    """rrg_index_create_shard (shards of an in-memory index, used by tools/c4.py) gives the
+    unsharded result id-for-id, like the file shards above."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2410_18926_b200 import DeviceIndex
+    from paper_2410_18926_b200.sharded import CudaShardEngine
+
+    blob = random_index(128, 64, 32, 12, 3000, seed=10 + G, dup_rows=5)
+    arrs = oindex_arrays(O.read_index(blob))
+    full = DeviceIndex.from_arrays(**arrs)
+    parts = partition_clusters(arrs["cluster_sizes"].astype(np.int64), G)
+    engines = [CudaShardEngine(DeviceIndex.from_arrays(shard=ab, **arrs)) for ab in parts]
+    q = torch.from_numpy(np.random.default_rng(G).standard_normal((64, 128)).astype(np.float32)).cuda()
+    for k, w, t in [(10, 3, 100), (5, 12, 3000)]:
+        ids, sc, cnt = (x.cpu().numpy() for x in sharded_search_local(engines, q, k, w, t))
+        rid, rsc, rcnt = (x.cpu().numpy() for x in full.search_device(q, k, w, t, True))
+        np.testing.assert_array_equal(cnt, rcnt)
+        np.testing.assert_array_equal(ids, rid)
+        np.testing.assert_array_equal(np.nan_to_num(sc).view(np.int32), np.nan_to_num(rsc).view(np.int32))

@@ -61,6 +61,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--grid", default="1:200,1:400,1:800,2:400,2:800,3:800,4:800,4:1600")
     ap.add_argument("--parity", type=int, default=64, help="queries checked against the oracle")
+    ap.add_argument("--shards", default="2,8", help="G values for the 1-GPU shard emulation")
+    ap.add_argument("--link-gbs", type=float, default=400.0,
+                    help="assumed per-GPU NVLink all-gather receive bandwidth (exchange estimate)")
     return ap.parse_args()
 
 
@@ -129,7 +132,17 @@ def build(args, corpus, g):
             out[i:i + (1 << 18)] = torch.topk(dd, topn, dim=1, largest=False).indices
         return out
 
-    cent = pc[torch.randperm(m, generator=g, device=dev)[:L]].clone()
+    # k-means++ seeding (cluster.py:67-85) on a 1M-point sample: D^2 sampling picks
+    # distinct blobs, where a uniform draw leaves many blobs without a centroid
+    samp = pc[torch.randperm(m, generator=g, device=dev)[: min(m, 1 << 20)]]
+    cent = torch.empty((L, s), dtype=torch.float32, device=dev)
+    cent[0] = samp[torch.randint(samp.shape[0], (1,), generator=g, device=dev)]
+    dmin = ((samp - cent[0]) ** 2).sum(1)
+    for j in range(1, L):
+        pick = torch.multinomial(dmin.clamp(min=0), 1, generator=g)
+        cent[j] = samp[pick[0]]
+        torch.minimum(dmin, ((samp - cent[j]) ** 2).sum(1), out=dmin)
+    log("k-means++ seeding done")
     for it in range(args.iters):
         asg = nearest(pc, cent)[:, 0]
         cnt = torch.bincount(asg, minlength=L)
@@ -321,6 +334,10 @@ def run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact):
     stage = {nm: round(stage_ms[i] / 3, 4) for i, nm in enumerate(names)}
     # oracle parity on a query sample (id-for-id, score bits)
     parity = oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t) if args.parity else None
+    shards = {}
+    for G in [int(v) for v in args.shards.split(",") if v]:
+        shards[G] = shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G)
+        log(f"G={G}: {shards[G]}")
     line = {
         "metric": "QPS at recall@100 >=0.90 (batched), 1 B200", "value": args.nq / ms * 1e3,
         "unit": "queries/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -330,9 +347,67 @@ def run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact):
                    "index": f"GPU restatement of build(): train sample {args.train}, k-means {args.iters} "
                             f"Lloyd passes, {n_exact} exact clusters", "build_s": build_s},
         "gpu_launches": launches // args.steps, "grid": grid, "stage_ms": stage, "parity": parity,
+        "sharded_emulation": shards,
         "clocks": clk.summary(),
     }
     print(json.dumps(line))
+
+
+def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
+    """The G-rank cluster-sharded search (sharded.py) with all G shards on this GPU:
+    results must equal the unsharded search id-for-id; each shard's phase times are
+    measured alone (what one of G GPUs would spend), the all-gathers are estimated
+    from their byte counts at ``--link-gbs`` (not measured: one GPU here)."""
+    import torch
+
+    from paper_2410_18926_b200 import DeviceIndex
+    from paper_2410_18926_b200.sharded import CudaShardEngine, partition_clusters
+
+    k = args.k
+    parts = partition_clusters(arrs["cluster_sizes"].astype(np.int64), G)
+    engines = [CudaShardEngine(DeviceIndex.from_arrays(metric="euclidean", rank=args.r, corpus=corpus_h,
+                                                       shard=ab, **arrs)) for ab in parts]
+
+    def timed(fn):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record()
+        out = fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return out, e0.elapsed_time(e1)
+
+    best = None
+    for _ in range(3):  # first pass warms up workspaces
+        c1 = [timed(lambda e=e: e.phase1(queries, k, w, t)) for e in engines]
+        gk = torch.stack([c[0].keys for c in c1])
+        gi = torch.stack([c[0].ids for c in c1])
+        gc = torch.stack([c[0].count for c in c1])
+        cand, m1 = timed(lambda: engines[0].merge_candidates(gk, gi, gc, t))
+        res = [timed(lambda e=e: e.phase2(queries, cand, k)) for e in engines]
+        out, m2 = timed(lambda: engines[0].merge_results(torch.stack([r[0][0] for r in res]),
+                                                         torch.stack([r[0][1] for r in res]),
+                                                         torch.stack([r[0][2] for r in res]), k))
+        p1 = [c[1] for c in c1]
+        p2 = [r[1] for r in res]
+        cur = (max(p1) + m1 + max(p2) + m2, p1, p2, m1, m2)
+        best = cur if best is None or cur[0] < best[0] else best
+    oid, osc, ocnt = (x.cpu().numpy() for x in out)
+    equal = bool(np.array_equal(ocnt, cnt) and np.array_equal(oid, ids)
+                 and np.array_equal(np.nan_to_num(osc).view(np.int32), np.nan_to_num(sc).view(np.int32)))
+    nq = queries.shape[0]
+    x1 = (G - 1) * nq * (t * 8 + 4)          # phase-1 all-gather received per rank
+    x2 = (G - 1) * nq * (k * 12 + 4)         # phase-2 all-gather received per rank
+    xch_ms = (x1 + x2) / (args.link_gbs * 1e9) * 1e3
+    compute_ms, p1, p2, m1, m2 = best
+    del engines
+    torch.cuda.empty_cache()
+    return {"G": G, "equal_to_unsharded": equal, "phase1_ms": [round(v, 4) for v in p1],
+            "phase2_ms": [round(v, 4) for v in p2], "merge1_ms": round(m1, 4), "merge2_ms": round(m2, 4),
+            "exchange_bytes_per_rank": x1 + x2, "exchange_ms_est": round(xch_ms, 4),
+            "step_ms_est": round(compute_ms + xch_ms, 4), "qps_est": nq / (compute_ms + xch_ms) * 1e3,
+            "note": "shards run one after another on one GPU; step = max-shard phase times + merges + "
+                    f"all-gather bytes at {args.link_gbs:.0f} GB/s (estimated, not measured)"}
 
 
 def oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t):

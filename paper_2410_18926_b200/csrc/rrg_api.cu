@@ -245,6 +245,8 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   const bool quant = hm.flags & RRG_FLAG_QUANTIZED;
   if (s > 1024) raise_usage("ParameterError", "reduced dimension %d > 1024 not supported", s);
   if (r > 64) raise_usage("ParameterError", "rank %d > 64 not supported", r);
+  // per-batch cluster tables (pair offsets, query buckets) live in one CTA's shared memory
+  if (L > kMaxClusters) raise_usage("ParameterError", "%d clusters > %d not supported", L, kMaxClusters);
   if (hm.m >= (int64_t)1 << 31) raise_usage("ParameterError", "more than 2^31 points");
   DevIndexView& v = ix->view;
   v.metric = hm.metric; v.d = d; v.s = s; v.r = r; v.L = L;

@@ -1468,9 +1468,23 @@ static bool warp_select_ok(int nq) {
 }
 
 
+template <typename Kern>
+static void opt_in_smem(Kern* kern, int slot) {
+  static int done[16][64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64 || done[slot][dev]) return;
+  cudaFuncAttributes at{};
+  cudaFuncGetAttributes(&at, (const void*)kern);
+  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kMaxSmemPerCta - (int)at.sharedSizeBytes);
+  done[slot][dev] = 1;
+}
+
 void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
   (k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand), note_launch());
+  opt_in_smem(k_pairs_build, 15);  // L * 8 bytes: 64 KB at L = 8192 (C4)
   (k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off,
                                                   h.item_off, h.pairs, h.kbase), note_launch());
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
@@ -1562,18 +1576,6 @@ bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster) {
   return cluster_rerank_smem(ix.d_stride, mwords) + 8 * 1024 <= (size_t)kMaxSmemPerCta;
 }
 
-template <typename Kern>
-static void opt_in_smem(Kern* kern, int slot) {
-  static int done[16][64] = {};
-  int dev = 0;
-  cudaGetDevice(&dev);
-  if (dev < 0 || dev >= 64 || done[slot][dev]) return;
-  cudaFuncAttributes at{};
-  cudaFuncGetAttributes(&at, (const void*)kern);
-  cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       kMaxSmemPerCta - (int)at.sharedSizeBytes);
-  done[slot][dev] = 1;
-}
 
 void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   ClusterRerankArgs a;

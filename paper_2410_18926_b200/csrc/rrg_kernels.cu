@@ -1455,6 +1455,14 @@ void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int
 
 void launch_bucket(const int* primary, int nq, int L, int* order, cudaStream_t st) {
   allow_smem(k_bucket_queries, 1);
+  static int bdone[64] = {};
+  int bdev = 0;
+  cudaGetDevice(&bdev);
+  if (bdev >= 0 && bdev < 64 && !bdone[bdev]) {  // (L + 1) * 4 bytes: past 48 KB above L = 12k
+    cudaFuncSetAttribute((const void*)k_bucket_queries, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kMaxSmemPerCta - 1024);
+    bdone[bdev] = 1;
+  }
   (k_bucket_queries<<<1, BNT, (size_t)(L + 1) * 4, st>>>(primary, nq, L, order), note_launch());
 }
 

@@ -16,6 +16,8 @@ constexpr int EPI_GT_COS = 4;  // -(q.c / ||c||)           (bench.py:100-103,112
 constexpr int EPI_L2_ARGMIN = 5;     // routing w = 1: per-row nearest column per tile
 constexpr int EPI_NEGIP_ARGMIN = 6;
 constexpr int kMaxSmemPerCta = 227 * 1024;  // B200 opt-in limit per CTA
+// cluster count bound: routing (w > 1) keeps 12 B per cluster in one CTA's shared memory
+constexpr int kMaxClusters = (kMaxSmemPerCta - 4096) / 12;
 
 struct ScoreArgsHost {
   DevIndexView ix;

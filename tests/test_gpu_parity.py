@@ -692,3 +692,38 @@ def test_long_candidate_lists(pkg, tmp_path, rerank_mode, monkeypatch):
             c = int(cnt[i])
             np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{(k, w, t)} q{i}")
             np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L", [8192, 16384])
+def test_many_clusters(pkg, tmp_path, L):
+    """C4-scale cluster counts: the per-batch cluster tables (pair offsets, query buckets,
+    routing selection) outgrow the default 48 KB of shared memory; batches large enough
+    for the cluster-major path, oracle-checked id-for-id."""
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    d, s, r = 96, 32, 8
+    m = 4 * L
+    blob = random_index(d, s, r, L, m, seed=L, dup_rows=2)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "many", blob))
+    oidx = O.read_index(blob)
+    q = np.random.default_rng(L).standard_normal((3000, d)).astype(F32)
+    for k, w, t in [(10, 1, 20), (10, 3, 40), (5, 64, 200)]:
+        ids, sc, cnt = dev.search_host(q, k, w, t, True)
+        for i in range(0, q.shape[0], 97):
+            rres = O.query(oidx, q[i], k, w, t, True)
+            c = int(cnt[i])
+            assert c == len(rres.ids)
+            np.testing.assert_array_equal(ids[i, :c], rres.ids)
+            np.testing.assert_array_equal(sc[i, :c].view(np.int32), rres.scores.view(np.int32))
+
+
+@pytest.mark.gpu
+def test_too_many_clusters_rejected(pkg, tmp_path):
+    """More clusters than the one-CTA cluster tables hold: a ParameterError at load."""
+    from index_writer import random_index
+
+    blob = random_index(16, 8, 4, 20000, 20000, seed=1)
+    with pytest.raises(pkg.ParameterError, match="clusters"):
+        pkg.DeviceIndex.from_file(_write(tmp_path, "toomany", blob))

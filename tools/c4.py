@@ -453,4 +453,14 @@ def oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t):
 
 
 if __name__ == "__main__":
-    main()
+    # os._exit: skip interpreter teardown (a failed run once sat in it past its timeout)
+    rc = 0
+    try:
+        main()
+    except Exception:
+        import traceback
+        traceback.print_exc()
+        rc = 1
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os._exit(rc)

@@ -1221,22 +1221,24 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           vb = acc_b;
         }
       };
-      int pa = r0 + warp * 2;
-      if (ASYNC) {  // skip row pairs no query of the group selected (no copy issued)
-        while (pa < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, pa) || marked(lane, pa + 1))))
-          pa += nwarps * 2;
-      }
+      // row pairs no query of the group selected are skipped before any load is
+      // issued: with unbalanced clusters (C4: up to 11x the mean size) a query keeps a
+      // small share of its cluster's rows and most pairs are unmarked
+      auto next_marked = [&](int p) {
+        while (p < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, p) || marked(lane, p + 1))))
+          p += nwarps * 2;
+        return p;
+      };
+      int pa = next_marked(r0 + warp * 2);
       if (pa < r1) load_pair(pa);
       for (; pa < r1;) {
         const int pb = pa + 1;
-        int pn = pa + nwarps * 2;
+        const int pn = next_marked(pa + nwarps * 2);
         // the queries that selected either row (one lane per query, ballot)
         const bool mine = lane < ng && (marked(lane, pa) || marked(lane, pb));
         const unsigned act0 = __ballot_sync(0xffffffffu, mine);
         if (ASYNC) {
           take_pair();
-          while (pn < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, pn) || marked(lane, pn + 1))))
-            pn += nwarps * 2;
           if (pn < r1) load_pair(pn);
         } else if (!act0) {
           if (pn < r1) load_pair(pn);

@@ -208,6 +208,7 @@ struct RrgIndex {
   std::vector<void*> allocs;
   RrgIndexInfo info{};
   int64_t max_cluster = 0;
+  double m_biased = 0.0;  // size-biased mean cluster size: sum m_l^2 / sum m_l
   std::vector<int> sizes_sorted_desc;  // cluster sizes (held), descending
   std::vector<uint32_t> held_sizes;    // per cluster
   int n_exact = 0;
@@ -295,6 +296,11 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   }
   cl_pos[L] = (int)P;
   v.P = P;
+  {
+    double s1 = 0.0, s2 = 0.0;
+    for (uint32_t hsz : ix->held_sizes) { s1 += hsz; s2 += (double)hsz * hsz; }
+    ix->m_biased = s1 > 0 ? s2 / s1 : 0.0;
+  }
   std::sort(ix->sizes_sorted_desc.begin(), ix->sizes_sorted_desc.end(), std::greater<int>());
 
   // quantized: int8 codes (+ head/scale); unquantized: f32 factors, same layouts
@@ -1008,6 +1014,12 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         rh.rr_item_off = reinterpret_cast<int*>(base + p.off_rritem); rh.pairs = ch.pairs;
         rh.kbase = ch.kbase; rh.marks = marks;
         rh.diss = ch.keys; rh.work_counter = ch.work_counter + 1; rh.mwords = p.mwords; rh.nq = n;
+        // sparse selections (a query keeps < half of the rows its probes cover, taking
+        // cluster sizes as a random query sees them): skip unselected row pairs
+        {
+          const char* e = getenv("RRG_RR_SKIP");
+          rh.skip = e ? atoi(e) != 0 : (double)t < 0.5 * w * ix->m_biased;
+        }
         staged(5, st, [&] { launch_cluster_rerank(rh, st); });
         TopkFinalHost fh{};
         fh.ix = v; fh.sel = sel; fh.w = w; fh.qoff = ch.qoff; fh.kbase = ch.kbase; fh.diss = ch.keys;

@@ -1069,7 +1069,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // pw(second half), each half a perfect 8-leaf tree over the same lanes -- the pair is
 // scored half by half (leaves 0-7 sit at [0, 64) of every interleaved 128-float step,
 // leaves 8-15 at [64, 128)) and the two reduced halves are added.
-template <int NB, bool ASYNC, int NH = 1>
+// SKIP: row pairs no query of the work item selected are passed over before any load
+// is issued -- for unbalanced clusters (C4: up to 11x the mean size), where a query
+// keeps a small share of its cluster's rows; balanced clusters (C2: a query keeps 82%
+// of them) prefetch every pair without the extra ballot (measured 1.10 vs 1.26 ms).
+template <int NB, bool ASYNC, int NH = 1, bool SKIP = false>
 __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankArgs a) {
   constexpr int NLV = 8 * NH, cstep = 8 * NLV;
   static_assert(NH == 1 || !ASYNC, "the cp.async variant handles 8-leaf rows");
@@ -1221,10 +1225,8 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           vb = acc_b;
         }
       };
-      // row pairs no query of the group selected are skipped before any load is
-      // issued: with unbalanced clusters (C4: up to 11x the mean size) a query keeps a
-      // small share of its cluster's rows and most pairs are unmarked
       auto next_marked = [&](int p) {
+        if (!(SKIP || ASYNC)) return p;
         while (p < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, p) || marked(lane, p + 1))))
           p += nwarps * 2;
         return p;
@@ -1472,7 +1474,7 @@ static bool warp_select_ok(int nq) {
 
 template <typename Kern>
 static void opt_in_smem(Kern* kern, int slot) {
-  static int done[16][64] = {};
+  static int done[32][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || done[slot][dev]) return;
@@ -1596,29 +1598,32 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#define RRG_RR_LAUNCH(NB, AS, SLOT)                                              \
+#define RRG_RR_LAUNCH(NB, AS, NH, SK, SLOT)                                      \
   do {                                                                           \
-    opt_in_smem(k_rerank_cluster<NB, AS>, SLOT);                                 \
-    (k_rerank_cluster<NB, AS><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch());                 \
+    opt_in_smem(k_rerank_cluster<NB, AS, NH, SK>, SLOT);                         \
+    (k_rerank_cluster<NB, AS, NH, SK><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); \
+  } while (0)
+#define RRG_RR_SK(NB, NH, SLOT)                                                  \
+  do {                                                                           \
+    if (h.skip) RRG_RR_LAUNCH(NB, false, NH, true, SLOT + 16);                   \
+    else RRG_RR_LAUNCH(NB, false, NH, false, SLOT);                              \
   } while (0)
   const bool as = rerank_async() && h.ix.pw_nleaves == 8;
   if (h.ix.pw_nleaves == 16) {  // d = 16 leaves (e.g. 1536): scored as two 8-leaf halves
     switch (h.ix.pw_leaf_n / 8) {
-      case 12: opt_in_smem(k_rerank_cluster<12, false, 2>, 12);
-               (k_rerank_cluster<12, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); break;
-      case 15: opt_in_smem(k_rerank_cluster<15, false, 2>, 13);
-               (k_rerank_cluster<15, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); break;
-      default: opt_in_smem(k_rerank_cluster<16, false, 2>, 14);
-               (k_rerank_cluster<16, false, 2><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); break;
+      case 12: RRG_RR_SK(12, 2, 12); break;
+      case 15: RRG_RR_SK(15, 2, 13); break;
+      default: RRG_RR_SK(16, 2, 14); break;
     }
     return;
   }
   // persistent grid: kCmCtas CTAs per SM
   switch (h.ix.pw_leaf_n / 8) {
-    case 12: if (as) RRG_RR_LAUNCH(12, true, 4); else RRG_RR_LAUNCH(12, false, 0); break;
-    case 15: if (as) RRG_RR_LAUNCH(15, true, 5); else RRG_RR_LAUNCH(15, false, 1); break;
-    default: if (as) RRG_RR_LAUNCH(16, true, 6); else RRG_RR_LAUNCH(16, false, 2); break;
+    case 12: if (as) RRG_RR_LAUNCH(12, true, 1, false, 4); else RRG_RR_SK(12, 1, 0); break;
+    case 15: if (as) RRG_RR_LAUNCH(15, true, 1, false, 5); else RRG_RR_SK(15, 1, 1); break;
+    default: if (as) RRG_RR_LAUNCH(16, true, 1, false, 6); else RRG_RR_SK(16, 1, 2); break;
   }
+#undef RRG_RR_SK
 #undef RRG_RR_LAUNCH
 }
 

@@ -143,6 +143,7 @@ struct ClusterRerankHost {
   const uint32_t* marks;
   uint32_t* diss;
   int* work_counter;
+  bool skip;  // pass over row pairs no query of a work item selected (sparse selections)
   int mwords;
   int nq;  // queries of the chunk (work-item sizing)
 };

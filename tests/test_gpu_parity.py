@@ -418,7 +418,7 @@ SWEEP = [
 ]
 
 
-@pytest.mark.parametrize("mode", ["cluster", "cluster+auto", "cluster+async", "cluster+blocksel",
+@pytest.mark.parametrize("mode", ["cluster", "cluster+auto", "cluster+async", "cluster+skip", "cluster+blocksel",
                                   "cluster+dmma", "cluster+slicedroute", "query", "cluster+regs",
                                   "cluster+tma"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
@@ -433,6 +433,8 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
         monkeypatch.setenv("RRG_WARP_SELECT", "1")      # and the warp-per-query selections
     if rerank_mode == "async":  # cluster-major re-rank with cp.async-staged row pairs
         monkeypatch.setenv("RRG_RR_ASYNC", "1")
+    elif rerank_mode == "skip":  # cluster-major re-rank passing over unselected row pairs
+        monkeypatch.setenv("RRG_RR_SKIP", "1")
     elif rerank_mode == "blocksel":  # CTA-per-query top-t / top-k selections
         monkeypatch.setenv("RRG_WARP_SELECT", "0")
     elif rerank_mode == "dmma":  # FP64 DMMA projection + routing GEMMs, unfused w=1 routing

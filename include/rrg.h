@@ -182,6 +182,18 @@ int rrg_shard_phase1(RrgIndex* index, const float* queries, int64_t nq, int32_t 
 int rrg_merge_candidates(int64_t nq, int32_t G, int32_t cap, const uint32_t* keys,
                          const uint32_t* ids, const int32_t* counts, int32_t take,
                          uint32_t* out_keys, uint32_t* out_ids, int32_t* out_count, void* stream);
+/* Sparse phase-1 exchange: a rank's [nq][cap] lists packed back to back
+ * (offsets[nq + 1], offsets[nq] = total) before the all-gather, and the G gathered
+ * packed lists (stride elements each) unpacked into the [G][nq][cap] layout
+ * rrg_merge_candidates reads.  With w = 1 a query's candidates sit on one rank,
+ * so the exchange shrinks about G-fold. */
+int rrg_pack_candidates(int64_t nq, int32_t cap, const uint32_t* keys, const uint32_t* ids,
+                        const int32_t* counts, uint32_t* packed_keys, uint32_t* packed_ids,
+                        int32_t* offsets, void* stream);
+int rrg_unpack_candidates(int64_t nq, int32_t G, int64_t stride, int32_t cap,
+                          const uint32_t* packed_keys, const uint32_t* packed_ids,
+                          const int32_t* offsets, uint32_t* keys, uint32_t* ids, int32_t* counts,
+                          void* stream);
 int rrg_shard_phase2(RrgIndex* index, const float* queries, int64_t nq, int32_t dim,
                      const uint32_t* cand_ids, const int32_t* cand_count, int32_t cap, int32_t k,
                      int64_t* ids, float* scores, int32_t* count, void* workspace,

@@ -68,6 +68,9 @@ SIGNATURES = {
                                  c_vp, c_size, c_vp]),
     "rrg_merge_candidates": (c_int, [c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                      c_vp, c_vp]),
+    "rrg_pack_candidates": (c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),
+    "rrg_unpack_candidates": (c_int, [c_i64, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                      c_vp]),
     "rrg_shard_phase2": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_i32, c_i32, c_vp, c_vp,
                                  c_vp, c_vp, c_size, c_vp]),
     "rrg_merge_results": (c_int, [c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,

@@ -1596,6 +1596,35 @@ int rrg_merge_candidates(int64_t nq, int32_t G, int32_t cap, const uint32_t* key
   });
 }
 
+int rrg_pack_candidates(int64_t nq, int32_t cap, const uint32_t* keys, const uint32_t* ids,
+                        const int32_t* counts, uint32_t* packed_keys, uint32_t* packed_ids,
+                        int32_t* offsets, void* stream) {
+  return guarded([&] {
+    if (nq < 0 || cap < 1) raise_usage("ParameterError", "bad list shape");
+    if (nq == 0) return RRG_OK;
+    staged(4, static_cast<cudaStream_t>(stream), [&] {
+      launch_pack_candidates((int)nq, cap, keys, ids, counts, packed_keys, packed_ids, offsets,
+                             static_cast<cudaStream_t>(stream));
+    });
+    return RRG_OK;
+  });
+}
+
+int rrg_unpack_candidates(int64_t nq, int32_t G, int64_t stride, int32_t cap,
+                          const uint32_t* packed_keys, const uint32_t* packed_ids,
+                          const int32_t* offsets, uint32_t* keys, uint32_t* ids, int32_t* counts,
+                          void* stream) {
+  return guarded([&] {
+    if (G < 1 || G > 64) raise_usage("ParameterError", "G=%d out of range [1, 64]", G);
+    if (nq == 0) return RRG_OK;
+    staged(4, static_cast<cudaStream_t>(stream), [&] {
+      launch_unpack_candidates((int)nq, G, stride, cap, packed_keys, packed_ids, offsets, keys, ids,
+                               counts, static_cast<cudaStream_t>(stream));
+    });
+    return RRG_OK;
+  });
+}
+
 int rrg_shard_phase2(RrgIndex* index, const float* queries, int64_t nq, int32_t dim,
                      const uint32_t* cand_ids, const int32_t* cand_count, int32_t cap, int32_t k,
                      int64_t* ids, float* scores, int32_t* count, void* workspace,

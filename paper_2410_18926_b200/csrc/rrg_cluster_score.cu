@@ -1660,4 +1660,65 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
   (k_topk_final<<<nq, FNT, topk_final_smem(h.w, h.take_cap, h.k), st>>>(a), note_launch());
 }
 
+// ======================================================= sparse phase-1 exchange
+// A rank's local top-t lists are mostly short or empty when its clusters hold few
+// of a query's probes (w = 1: one rank holds all of them), so they travel packed:
+// counts -> offsets (one CTA scan), then one warp per query copies its list.
+__global__ void __launch_bounds__(PNT) k_pack_offsets(const int* __restrict__ counts, int nq,
+                                                      int* __restrict__ off) {
+  __shared__ int tot;
+  for (int i = threadIdx.x; i < nq; i += PNT) off[i] = counts[i];
+  __syncthreads();
+  block_exclusive_scan_inplace(off, nq, &tot);
+  if (threadIdx.x == 0) off[nq] = tot;
+}
+
+__global__ void k_pack_lists(const uint32_t* __restrict__ keys, const uint32_t* __restrict__ ids,
+                             int nq, int cap, const int* __restrict__ off,
+                             uint32_t* __restrict__ pk, uint32_t* __restrict__ pi) {
+  const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  const int o = off[q], n = off[q + 1] - o;
+  for (int j = lane; j < n; j += 32) {
+    pk[o + j] = keys[(size_t)q * cap + j];
+    pi[o + j] = ids[(size_t)q * cap + j];
+  }
+}
+
+// G packed lists (stride elements each, offsets [G][nq+1]) -> the [G][nq][cap] layout k_merge reads
+__global__ void k_unpack_lists(const uint32_t* __restrict__ pk, const uint32_t* __restrict__ pi,
+                               const int* __restrict__ off, int G, int nq, int64_t stride, int cap,
+                               uint32_t* __restrict__ keys, uint32_t* __restrict__ ids,
+                               int* __restrict__ counts) {
+  const int64_t gq = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (gq >= (int64_t)G * nq) return;
+  const int g = (int)(gq / nq), q = (int)(gq % nq);
+  const int* og = off + (size_t)g * (nq + 1);
+  const int o = og[q], n = min(og[q + 1] - o, cap);
+  const uint32_t* sk = pk + g * stride + o;
+  const uint32_t* si = pi + g * stride + o;
+  uint32_t* dk = keys + (size_t)gq * cap;
+  uint32_t* di = ids + (size_t)gq * cap;
+  for (int j = lane; j < n; j += 32) {
+    dk[j] = sk[j];
+    di[j] = si[j];
+  }
+  if (lane == 0) counts[gq] = n;
+}
+
+void launch_pack_candidates(int nq, int cap, const uint32_t* keys, const uint32_t* ids,
+                            const int* counts, uint32_t* pk, uint32_t* pi, int* off, cudaStream_t st) {
+  (k_pack_offsets<<<1, PNT, 0, st>>>(counts, nq, off), note_launch());
+  (k_pack_lists<<<(nq + 7) / 8, 256, 0, st>>>(keys, ids, nq, cap, off, pk, pi), note_launch());
+}
+
+void launch_unpack_candidates(int nq, int G, int64_t stride, int cap, const uint32_t* pk,
+                              const uint32_t* pi, const int* off, uint32_t* keys, uint32_t* ids,
+                              int* counts, cudaStream_t st) {
+  const int64_t n = (int64_t)G * nq;
+  (k_unpack_lists<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(pk, pi, off, G, nq, stride, cap, keys, ids,
+                                                          counts), note_launch());
+}
+
 }  // namespace rrg

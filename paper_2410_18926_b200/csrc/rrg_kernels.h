@@ -179,6 +179,11 @@ void launch_merge(int mode, int metric, int nq, int G, int cap, const void* in_k
                   const void* in_ids, const int* in_counts, int take, void* out_keys,
                   void* out_ids, int* out_count, cudaStream_t st);
 // ids -> positions held by this shard (others dropped): cand_pos [nq][cap], cand_n [nq]
+void launch_pack_candidates(int nq, int cap, const uint32_t* keys, const uint32_t* ids,
+                            const int* counts, uint32_t* pk, uint32_t* pi, int* off, cudaStream_t st);
+void launch_unpack_candidates(int nq, int G, int64_t stride, int cap, const uint32_t* pk,
+                              const uint32_t* pi, const int* off, uint32_t* keys, uint32_t* ids,
+                              int* counts, cudaStream_t st);
 void launch_ids_to_pos(const DevIndexView& ix, int nq, int cap, const uint32_t* ids,
                        const int* counts, int* cand_pos, int* cand_n, cudaStream_t st);
 

@@ -93,6 +93,12 @@ class TorchExchange:
         self.group = group
         self.world = dist.get_world_size(group)
 
+    def max_scalar(self, t) -> int:
+        """max over ranks of a one-element int tensor (all-reduce MAX)."""
+        t = t.clone()
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX, group=self.group)
+        return int(t.item())
+
     def all_gather(self, t):
         import torch
 
@@ -170,6 +176,35 @@ class CudaShardEngine:
                                        keys.data_ptr(), ids.data_ptr(), cnt.data_ptr(), st))
         return Candidates(keys, ids, cnt)
 
+    def pack_candidates(self, c: Candidates):
+        """Local lists packed back to back: (keys [nq*cap], ids [nq*cap], offsets [nq+1])."""
+        import torch
+
+        nq, cap = c.keys.shape
+        dev = c.keys.device
+        pk = torch.empty((max(nq * cap, 1),), dtype=torch.int32, device=dev)
+        pi = torch.empty_like(pk)
+        off = torch.empty((nq + 1,), dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_pack_candidates(nq, cap, c.keys.data_ptr(), c.ids.data_ptr(), c.count.data_ptr(),
+                                      pk.data_ptr(), pi.data_ptr(), off.data_ptr(), st))
+        return pk, pi, off
+
+    def unpack_candidates(self, gk, gi, goff, cap):
+        """G gathered packed lists -> the [G, nq, cap] layout of merge_candidates."""
+        import torch
+
+        G, stride = gk.shape
+        nq = goff.shape[1] - 1
+        dev = gk.device
+        keys = torch.empty((G, nq, cap), dtype=torch.int32, device=dev)
+        ids = torch.empty_like(keys)
+        cnt = torch.empty((G, nq), dtype=torch.int32, device=dev)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_unpack_candidates(nq, G, stride, cap, gk.data_ptr(), gi.data_ptr(), goff.data_ptr(),
+                                        keys.data_ptr(), ids.data_ptr(), cnt.data_ptr(), st))
+        return keys, ids, cnt
+
     def phase2(self, q, cand: Candidates, k):
         import torch
 
@@ -204,28 +239,49 @@ class CudaShardEngine:
 # --------------------------------------------------------------- orchestration
 
 
-def sharded_search(engine, exchange, queries, k: int, w: int, t: int):
+def exchange_candidates(engine, exchange, c1: Candidates, sparse: bool = True):
+    """Phase-1 all-gather.  Sparse: each rank's lists travel packed (offsets + the
+    max-over-ranks total of entries, padded to it) and are unpacked to the [G, nq, t]
+    layout on arrival -- about G-fold fewer bytes when a query's probes sit on one
+    rank (w = 1); dense: the padded [nq, t] lists as they are."""
+    if not sparse:
+        return exchange.all_gather(c1.keys), exchange.all_gather(c1.ids), exchange.all_gather(c1.count)
+    pk, pi, off = engine.pack_candidates(c1)
+    tot = max(exchange.max_scalar(off[-1:]), 1)
+    gk = exchange.all_gather(pk[:tot])
+    gi = exchange.all_gather(pi[:tot])
+    goff = exchange.all_gather(off)
+    return engine.unpack_candidates(gk, gi, goff, c1.keys.shape[1])
+
+
+def sharded_search(engine, exchange, queries, k: int, w: int, t: int, sparse: bool = True):
     """Two-phase exact sharded search for one rank (all ranks call it collectively)."""
     if k > t:
         raise ParameterError(f"k={k} must be <= t={t} when re-ranking")
     c1 = engine.phase1(queries, k, w, t)
-    gk = exchange.all_gather(c1.keys)
-    gi = exchange.all_gather(c1.ids)
-    gc = exchange.all_gather(c1.count)
+    gk, gi, gc = exchange_candidates(engine, exchange, c1, sparse)
     cand = engine.merge_candidates(gk, gi, gc, t)
     ids, sc, cnt = engine.phase2(queries, cand, k)
     return engine.merge_results(exchange.all_gather(ids), exchange.all_gather(sc),
                                 exchange.all_gather(cnt), k)
 
 
-def sharded_search_local(engines, queries, k: int, w: int, t: int):
-    """All G shards in one process (LocalExchange): same two phases, stacked lists."""
+def sharded_search_local(engines, queries, k: int, w: int, t: int, sparse: bool = False):
+    """All G shards in one process (LocalExchange): same two phases, stacked lists
+    (sparse: through the pack / unpack of the packed exchange)."""
     import torch
 
     c1 = [e.phase1(queries, k, w, t) for e in engines]
-    gk = torch.stack([c.keys for c in c1])
-    gi = torch.stack([c.ids for c in c1])
-    gc = torch.stack([c.count for c in c1])
+    if sparse:
+        packed = [e.pack_candidates(c) for e, c in zip(engines, c1)]
+        tot = max(max(int(p[2][-1]) for p in packed), 1)
+        gk, gi, gc = engines[0].unpack_candidates(torch.stack([p[0][:tot] for p in packed]),
+                                                  torch.stack([p[1][:tot] for p in packed]),
+                                                  torch.stack([p[2] for p in packed]), t)
+    else:
+        gk = torch.stack([c.keys for c in c1])
+        gi = torch.stack([c.ids for c in c1])
+        gc = torch.stack([c.count for c in c1])
     cand = engines[0].merge_candidates(gk, gi, gc, t)
     res = [e.phase2(queries, cand, k) for e in engines]
     return engines[0].merge_results(torch.stack([r[0] for r in res]), torch.stack([r[1] for r in res]),

@@ -64,6 +64,34 @@ class OracleShardEngine:
         return Candidates(_as_i32(keys), _as_i32(ids), torch.from_numpy(cnt))
 
     @staticmethod
+    def pack_candidates(c: Candidates):
+        keys, ids, cnt = c.keys.numpy(), c.ids.numpy(), c.count.numpy()
+        nq, cap = keys.shape
+        off = np.zeros(nq + 1, np.int32)
+        off[1:] = np.cumsum(cnt)
+        pk = np.zeros(max(nq * cap, 1), np.int32)
+        pi = np.zeros_like(pk)
+        for i in range(nq):
+            pk[off[i]:off[i + 1]] = keys[i, :cnt[i]]
+            pi[off[i]:off[i + 1]] = ids[i, :cnt[i]]
+        return torch.from_numpy(pk), torch.from_numpy(pi), torch.from_numpy(off)
+
+    @staticmethod
+    def unpack_candidates(gk, gi, goff, cap):
+        gk, gi, goff = gk.numpy(), gi.numpy(), goff.numpy()
+        G, nq = gk.shape[0], goff.shape[1] - 1
+        keys = np.full((G, nq, cap), -1, np.int32)
+        ids = np.full((G, nq, cap), -1, np.int32)
+        cnt = np.zeros((G, nq), np.int32)
+        for g in range(G):
+            for i in range(nq):
+                n = goff[g, i + 1] - goff[g, i]
+                keys[g, i, :n] = gk[g, goff[g, i]:goff[g, i + 1]]
+                ids[g, i, :n] = gi[g, goff[g, i]:goff[g, i + 1]]
+                cnt[g, i] = n
+        return torch.from_numpy(keys), torch.from_numpy(ids), torch.from_numpy(cnt)
+
+    @staticmethod
     def _gather(gk, gi, gc):
         gk = gk.numpy().view(np.uint32)
         gi = gi.numpy().view(np.uint32)

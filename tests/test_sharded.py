@@ -75,7 +75,9 @@ def _gloo_worker(rank, world, port, blob, q, params, out_dir):
         idx, engines = _engines(blob, world)
         ex = TorchExchange()
         for j, (k, w, t) in enumerate(params):
-            ids, sc, cnt = sharded_search(engines[rank], ex, torch.from_numpy(q), k, w, t)
+            # alternate the packed (sparse) and padded phase-1 exchanges
+            ids, sc, cnt = sharded_search(engines[rank], ex, torch.from_numpy(q), k, w, t,
+                                          sparse=j % 2 == 0)
             np.savez(os.path.join(out_dir, f"r{rank}_p{j}.npz"), ids=ids.numpy(), sc=sc.numpy(),
                      cnt=cnt.numpy())
     finally:
@@ -165,8 +167,8 @@ def test_gpu_array_shards_equal_unsharded(G):
     parts = partition_clusters(arrs["cluster_sizes"].astype(np.int64), G)
     engines = [CudaShardEngine(DeviceIndex.from_arrays(shard=ab, **arrs)) for ab in parts]
     q = torch.from_numpy(np.random.default_rng(G).standard_normal((64, 128)).astype(np.float32)).cuda()
-    for k, w, t in [(10, 3, 100), (5, 12, 3000)]:
-        ids, sc, cnt = (x.cpu().numpy() for x in sharded_search_local(engines, q, k, w, t))
+    for (k, w, t), sparse in [((10, 3, 100), True), ((5, 12, 3000), False), ((10, 1, 200), True)]:
+        ids, sc, cnt = (x.cpu().numpy() for x in sharded_search_local(engines, q, k, w, t, sparse))
         rid, rsc, rcnt = (x.cpu().numpy() for x in full.search_device(q, k, w, t, True))
         np.testing.assert_array_equal(cnt, rcnt)
         np.testing.assert_array_equal(ids, rid)

@@ -380,10 +380,15 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
     best = None
     for _ in range(3):  # first pass warms up workspaces
         c1 = [timed(lambda e=e: e.phase1(queries, k, w, t)) for e in engines]
-        gk = torch.stack([c[0].keys for c in c1])
-        gi = torch.stack([c[0].ids for c in c1])
-        gc = torch.stack([c[0].count for c in c1])
+        # sparse phase-1 exchange (sharded.exchange_candidates): pack on each rank,
+        # unpack + merge on the receiver
+        packed = [timed(lambda e=e, c=c: e.pack_candidates(c[0])) for e, c in zip(engines, c1)]
+        tot = max(max(int(p[0][2][-1]) for p in packed), 1)
+        (gk, gi, gc), mu = timed(lambda: engines[0].unpack_candidates(
+            torch.stack([p[0][0][:tot] for p in packed]), torch.stack([p[0][1][:tot] for p in packed]),
+            torch.stack([p[0][2] for p in packed]), t))
         cand, m1 = timed(lambda: engines[0].merge_candidates(gk, gi, gc, t))
+        m1 += mu + max(p[1] for p in packed)
         res = [timed(lambda e=e: e.phase2(queries, cand, k)) for e in engines]
         out, m2 = timed(lambda: engines[0].merge_results(torch.stack([r[0][0] for r in res]),
                                                          torch.stack([r[0][1] for r in res]),
@@ -396,7 +401,8 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
     equal = bool(np.array_equal(ocnt, cnt) and np.array_equal(oid, ids)
                  and np.array_equal(np.nan_to_num(osc).view(np.int32), np.nan_to_num(sc).view(np.int32)))
     nq = queries.shape[0]
-    x1 = (G - 1) * nq * (t * 8 + 4)          # phase-1 all-gather received per rank
+    x1 = (G - 1) * (tot * 8 + (nq + 1) * 4)  # packed phase-1 all-gather received per rank
+    x1_dense = (G - 1) * nq * (t * 8 + 4)    # the padded exchange it replaces
     x2 = (G - 1) * nq * (k * 12 + 4)         # phase-2 all-gather received per rank
     xch_ms = (x1 + x2) / (args.link_gbs * 1e9) * 1e3
     compute_ms, p1, p2, m1, m2 = best
@@ -404,9 +410,10 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
     torch.cuda.empty_cache()
     return {"G": G, "equal_to_unsharded": equal, "phase1_ms": [round(v, 4) for v in p1],
             "phase2_ms": [round(v, 4) for v in p2], "merge1_ms": round(m1, 4), "merge2_ms": round(m2, 4),
-            "exchange_bytes_per_rank": x1 + x2, "exchange_ms_est": round(xch_ms, 4),
+            "exchange_bytes_per_rank": x1 + x2, "padded_exchange_bytes_per_rank": x1_dense + x2,
+            "exchange_ms_est": round(xch_ms, 4),
             "step_ms_est": round(compute_ms + xch_ms, 4), "qps_est": nq / (compute_ms + xch_ms) * 1e3,
-            "note": "shards run one after another on one GPU; step = max-shard phase times + merges + "
+            "note": "shards run one after another on one GPU; step = max-shard phase times + pack/unpack/merges + "
                     f"all-gather bytes at {args.link_gbs:.0f} GB/s (estimated, not measured)"}
 
 

@@ -838,11 +838,17 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     // group: worth it while a query keeps a large share of its probed rows (C2, w=1:
     // t / (w m) = 0.82); with many probes per query (C5, w=8: 0.10) the rows a query
     // keeps are sparse and the per-query kernel is 3-10x faster (measured)
-    const double mbar = v.L > 0 ? (double)v.P / v.L : 0.0;
+    // cluster sizes as a random query sees them (size-biased mean); a strongly skewed
+    // size distribution (C4: 13.9k-point hub clusters, mean 1.2k) leaves each query
+    // group's selected rows sparse inside the big clusters, where the per-query kernel
+    // was measured faster (C4 w=1: 4.49 vs 4.90 ms per 10k; w=2: 5.72 vs 7.46 ms)
+    const double mbar = ix->m_biased;
+    const bool skewed = v.L > 0 && ix->m_biased > 2.0 * (double)v.P / v.L;
     // small batches: the cluster-major items ((cluster, row chunk) per probe) spread one
     // query's rows over many CTAs, where the per-query kernel has one CTA per query
     const bool small = p.qc * w < 2 * 148;
-    const bool dense = (double)t >= 0.3 * w * mbar || small || (e && strcmp(e, "cluster") == 0);
+    const bool dense = ((double)t >= 0.3 * w * mbar && !skewed) || small ||
+                       (e && strcmp(e, "cluster") == 0);
     p.rr_mode = (want && dense && p.score_mode == 1 && rerank && !exact_take &&
                  cluster_rerank_ok(v, ix->max_cluster)) ? 1 : 0;
   }

@@ -344,6 +344,10 @@ def run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact):
         "config": {"workload": "c4", "m": args.m, "d": args.d, "L": args.L, "s": args.s, "r": args.r,
                    "k": k, "queries": args.nq, "w": w, "t": t, "n_blobs": args.m // 1000,
                    "recall_at_k": rc, "l2": "256 MiB write between steps (excluded)",
+                   "cluster_sizes": {"mean": float(arrs["cluster_sizes"].mean()),
+                                     "size_biased_mean": float((arrs["cluster_sizes"].astype(float) ** 2).sum()
+                                                               / arrs["cluster_sizes"].sum()),
+                                     "max": int(arrs["cluster_sizes"].max())},
                    "index": f"GPU restatement of build(): train sample {args.train}, k-means {args.iters} "
                             f"Lloyd passes, {n_exact} exact clusters", "build_s": build_s},
         "gpu_launches": launches // args.steps, "grid": grid, "stage_ms": stage, "parity": parity,

@@ -117,6 +117,10 @@ int rrg_index_create_shard(const RrgIndexDesc* desc, int device, int32_t cluster
                            int32_t cluster_end, RrgIndex** out);
 
 void rrg_index_destroy(RrgIndex* index);
+/* Search-variant switches (RRG_GEMM, RRG_RERANK, RRG_SCREEN, ... -- A/B measurement
+ * and test coverage of every kernel variant) are read from the environment once,
+ * when the index is created; this re-reads them for an existing index. */
+int rrg_index_reload_options(RrgIndex* index);
 int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out);
 /* Points held per cluster (n_clusters entries; 0 for clusters outside a shard). */
 int rrg_index_cluster_sizes(const RrgIndex* index, uint32_t* out);
@@ -140,8 +144,10 @@ int rrg_search(RrgIndex* index, const float* queries, int64_t nq, int32_t dim,
                size_t workspace_bytes, void* stream);
 
 /* Host-buffer convenience form (the SPEC.md:522-526 binding): copies queries
- * in, searches, copies results out, synchronous.  Validates finiteness of the
- * queries on the host first (DataError, index.py:144-150). */
+ * in, searches, copies results out, synchronous.  Non-finite queries raise
+ * DataError (index.py:144-150) ahead of parameter errors: the finiteness test
+ * runs on the GPU inside the query-prep pass, and the batch is scanned on the
+ * host only when the parameters are invalid, so the DataError still wins. */
 int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq,
                     int32_t dim, int32_t k, int32_t w, int32_t t,
                     int32_t rerank, int64_t* ids, float* scores,
@@ -165,6 +171,21 @@ int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq,
 int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w,
                     int32_t* selected, void* workspace, size_t workspace_bytes,
                     void* stream);
+
+/* K4 of the search path (score_cluster, rrr.py:181-203 / quantize.py:109-156) for
+ * caller-chosen probes sel [nq][w] (device int32), run by the production
+ * cluster-major scoring kernel with its stage outputs switched on, so the int32
+ * products and f32 scores can be compared bit for bit with the reference:
+ *   raw1     [nq][w][rank] int32: stage-A products x_i8 . A_i8 of RRR clusters
+ *   cand_off [nq + 1] int32: start of each query's candidates (probes in sel order)
+ *   raw2     [cand_off[nq]] int32: last-stage product per point (stage B, or stage A
+ *            of an exact model)
+ *   scores   [cand_off[nq]] f32: score_cluster's output per point
+ * Synchronous on `stream`. */
+size_t rrg_stage_score_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t w);
+int rrg_stage_score(RrgIndex* index, const float* queries, int64_t nq, int32_t w,
+                    const int32_t* sel, int32_t* raw1, int32_t* raw2, float* scores,
+                    int32_t* cand_off, void* workspace, size_t workspace_bytes, void* stream);
 
 /* ---- cluster-sharded search; one index shard per rank
  * (rrg_index_open_shard), queries replicated.  Exact reference semantics need

@@ -63,6 +63,10 @@ SIGNATURES = {
                                      c_vp, c_vp, c_vp]),
     "rrg_stage_project": (c_int, [c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "rrg_stage_route": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "rrg_stage_score_workspace_bytes": (c_size, [c_vp, c_i64, c_i32]),
+    "rrg_stage_score": (c_int, [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                c_size, c_vp]),
+    "rrg_index_reload_options": (c_int, [c_vp]),
     "rrg_shard_workspace_bytes": (c_size, [c_vp, c_i64, c_i32, c_i32, c_i32]),
     "rrg_shard_phase1": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
                                  c_vp, c_size, c_vp]),

@@ -238,6 +238,8 @@ struct RrgIndex {
 
 namespace {
 
+RrgOpts read_opts();
+
 // Build the device layout from the staged host model.  `corpus_rows` fills the
 // reordered corpus (cluster order) given pos_of_id on the device.
 template <typename CorpusFill>
@@ -250,6 +252,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   if (L > kMaxClusters) raise_usage("ParameterError", "%d clusters > %d not supported", L, kMaxClusters);
   if (hm.m >= (int64_t)1 << 31) raise_usage("ParameterError", "more than 2^31 points");
   DevIndexView& v = ix->view;
+  v.opt = read_opts();
   v.metric = hm.metric; v.d = d; v.s = s; v.r = r; v.L = L;
   v.s_pad = (int)round_up(s, 16);
   v.r_pad = (int)round_up(r, 16);
@@ -694,23 +697,43 @@ int create_impl(const RrgIndexDesc* dsc, int device, int32_t cb, int32_t ce, Rrg
 // (10k queries): projection 0.162 ms sliced vs 0.175 ms DMMA, routing 0.220 ms sliced
 // vs 0.203 ms DMMA -- so the defaults are sliced projection, DMMA routing.
 // RRG_PROJ / RRG_ROUTE = sliced|dmma choose each; RRG_GEMM = sliced|dmma sets both.
-static bool gemm_choice(const char* var, bool dflt) {
-  const char* e = getenv("RRG_GEMM");
-  if (!e) e = getenv(var);
-  if (!e) return dflt;
-  return strcmp(e, "sliced") == 0;
+// Every switch is read here, once per index (RrgOpts), not per search call.
+RrgOpts read_opts() {
+  auto env = [](const char* v) -> const char* { return getenv(v); };
+  auto gemm = [&](const char* var, bool dflt) {
+    const char* e = env("RRG_GEMM");
+    if (!e) e = env(var);
+    return e ? (strcmp(e, "sliced") == 0 ? 1 : 0) : (dflt ? 1 : 0);
+  };
+  auto flag = [&](const char* var, int dflt) {
+    const char* e = env(var);
+    return e ? atoi(e) : dflt;
+  };
+  RrgOpts o{};
+  o.proj_sliced = gemm("RRG_PROJ", true);
+  o.route_sliced = gemm("RRG_ROUTE", false);
+  o.route_fused = flag("RRG_ROUTE_FUSED", 1) != 0;
+  o.gemm_bk = flag("RRG_GEMM_BK", 8) == 16 ? 16 : 8;
+  {
+    const char* e = env("RRG_SCORE_MODE");
+    o.score_query = e && strcmp(e, "query") == 0;
+  }
+  {
+    const char* e = env("RRG_RERANK");
+    o.rerank = !e ? 0 : strcmp(e, "cluster") == 0 ? 1 : strcmp(e, "query") == 0 ? 2
+             : strcmp(e, "regs") == 0 ? 3 : strcmp(e, "tma") == 0 ? 4 : 0;
+  }
+  o.rr_skip = env("RRG_RR_SKIP") ? (flag("RRG_RR_SKIP", 0) != 0) : -1;
+  o.rr_async = flag("RRG_RR_ASYNC", 0) == 1;
+  o.warp_select = env("RRG_WARP_SELECT") ? (flag("RRG_WARP_SELECT", 0) != 0) : -1;
+  o.host_pieces = std::max(0, std::min(8, flag("RRG_HOST_PIECES", 0)));
+  o.graph = flag("RRG_GRAPH", 1) != 0;
+  o.screen = env("RRG_SCREEN") ? (flag("RRG_SCREEN", 0) != 0) : -1;
+  return o;
 }
-bool sliced_projection() { return gemm_choice("RRG_PROJ", true); }
 // up to this many queries the projection / routing run as warp-per-output GEMVs
 // (a GEMM tile of one row is ~10 dependent K-steps: 30-37 us at C2 batch 1)
 constexpr int kSmallBatch = 32;
-bool sliced_routing() { return gemm_choice("RRG_ROUTE", false); }
-// w = 1 routing fused into the DMMA GEMM (RRG_ROUTE_FUSED=0 writes the full
-// dissimilarity rows and selects separately)
-bool route_fused() {
-  const char* e = getenv("RRG_ROUTE_FUSED");
-  return !(e && atoi(e) == 0);
-}
 
 // Query sub-range bounds of the front stages (and the host entry's copy pieces):
 // multiples of the sliced GEMM's 128-row blocks, so a piece's slice planes are a
@@ -726,13 +749,13 @@ void route_dist(const DevIndexView& v, const float* xp, int n, const double* pp,
                 int8_t* qpl, int* qex, cudaStream_t st) {
   if (n <= kSmallBatch) {
     launch_route_dist_small(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
-  } else if (qpl && sliced_routing()) {
+  } else if (qpl && v.opt.route_sliced) {
     launch_slice_rows(xp, n, v.s, v.s, true, qpl, qex, st);
     launch_gemm_sliced(qpl, qex, n, v.cent_planes, v.cent_exps, v.L, v.s,
                        v.metric == kMetricEuclidean ? EPI_L2 : EPI_NEGIP, nullptr, diss, v.L, pp,
                        v.cnorm, st);
   } else {
-    launch_route_dist(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, st);
+    launch_route_dist(xp, v.cent, n, v.L, v.s, v.metric, pp, v.cnorm, diss, v.opt.gemm_bk, st);
   }
 }
 
@@ -802,18 +825,15 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   p.off_gp = carve(Q * p.gcap * 4);
   p.off_prim = carve(Q * 4);
   p.off_order = carve(Q * 4);
-  p.sliced_proj = sliced_projection() || sliced_routing();  // slice-plane workspace needed
+  p.sliced_proj = v.opt.proj_sliced || v.opt.route_sliced;  // slice-plane workspace needed
   if (p.sliced_proj) {
     p.off_qpl = carve(sliced_plane_bytes((int)Q, v.d, true));
     p.off_qex = carve((size_t)sliced_rows_pad((int)Q, true) * 4);
   }
   // scoring strategy: cluster-major (bucketed pairs, factors staged once per
   // cluster) unless RRG_SCORE_MODE=query selects the fused query-major kernel
-  {
-    const char* e = getenv("RRG_SCORE_MODE");
-    // the fused query-major kernel scores int8 factors only
-    p.score_mode = (e && strcmp(e, "query") == 0 && v.quantized) ? 0 : 1;
-  }
+  // the fused query-major kernel scores int8 factors only
+  p.score_mode = (v.opt.score_query && v.quantized) ? 0 : 1;
   if (p.score_mode == 1) {
     p.kcap = (int)std::min<int64_t>(std::max<int64_t>(nmax, 1), 24 * 1024);
     p.off_qoff = carve(Q * (int64_t)(w + 1) * 4);
@@ -831,24 +851,22 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
   {
     // measured on C2 (w=1, t=800): cluster-major 1.41 ms (+0.14 ms final top-k) vs
     // per-query k_rerank_tree 1.66 ms; RRG_RERANK=query|regs|tma selects a per-query kernel
-    const char* e = getenv("RRG_RERANK");
-    const bool want = !(e && (strcmp(e, "query") == 0 || strcmp(e, "regs") == 0 ||
-                              strcmp(e, "tma") == 0));
+    const bool want = v.opt.rerank <= 1;  // query / regs / tma force a per-query kernel
     // the cluster-major re-rank streams every row of a probed cluster for its query
     // group: worth it while a query keeps a large share of its probed rows (C2, w=1:
     // t / (w m) = 0.82); with many probes per query (C5, w=8: 0.10) the rows a query
     // keeps are sparse and the per-query kernel is 3-10x faster (measured)
-    // cluster sizes as a random query sees them (size-biased mean); a strongly skewed
-    // size distribution (C4: 13.9k-point hub clusters, mean 1.2k) leaves each query
-    // group's selected rows sparse inside the big clusters, where the per-query kernel
-    // was measured faster (C4 w=1: 4.49 vs 4.90 ms per 10k; w=2: 5.72 vs 7.46 ms)
+    // The share is taken with cluster sizes as a random query sees them (the
+    // size-biased mean sum m_l^2 / sum m_l: C2 1,037, C3 613, C4 1,622 against a
+    // plain mean of 1,221).  That is what moves C4 w = 2 to the per-query kernel
+    // (800 < 0.3 * 2 * 1,622; measured 5.72 vs 7.46 ms per 10k), while C4 w = 1 stays
+    // cluster-major (800 >= 0.3 * 1,622).
     const double mbar = ix->m_biased;
-    const bool skewed = v.L > 0 && ix->m_biased > 2.0 * (double)v.P / v.L;
     // small batches: the cluster-major items ((cluster, row chunk) per probe) spread one
     // query's rows over many CTAs, where the per-query kernel has one CTA per query
     const bool small = p.qc * w < 2 * 148;
-    const bool dense = ((double)t >= 0.3 * w * mbar && !skewed) || small ||
-                       (e && strcmp(e, "cluster") == 0);
+    const bool dense = (double)t >= 0.3 * w * mbar || small ||
+                       v.opt.rerank == 1;
     p.rr_mode = (want && dense && p.score_mode == 1 && rerank && !exact_take &&
                  cluster_rerank_ok(v, ix->max_cluster)) ? 1 : 0;
   }
@@ -937,7 +955,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       int* qex = p.sliced_proj ? reinterpret_cast<int*>(base + p.off_qex) + s0 : nullptr;
       if (ns <= kSmallBatch) {
         staged(0, st, [&] { launch_project_small(xs, v.Wt, ns, v.d, v.s, xps, st); });
-      } else if (sliced_projection()) {
+      } else if (v.opt.proj_sliced) {
         int8_t* qpl = qpl_d;
         staged(0, st, [&] { launch_slice_rows(xs, ns, v.d, v.d, true, qpl, qex, st); });
         staged(0, st, [&] {
@@ -945,18 +963,18 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
                              v.s, nullptr, nullptr, st);
         });
       } else {
-        staged(0, st, [&] { launch_project(xs, v.W, ns, v.d, v.s, xps, st); });
+        staged(0, st, [&] { launch_project(xs, v.W, ns, v.d, v.s, xps, v.opt.gemm_bk, st); });
       }
       staged(1, st, [&] {
         launch_prep(xps, xs, ns, v.s, v.s_pad, v.d, qcodes + (int64_t)s0 * v.s_pad, qscale + s0,
                     qhead + s0, pp + s0, xx + s0, st, nonfinite);
       });
-      if (w == 1 && ns > kSmallBatch && route_fused()) {
+      if (w == 1 && ns > kSmallBatch && v.opt.route_fused) {
         // nearest cluster straight from the GEMM: per (query, 64-centroid tile) minima
         const int nt = route_nearest_tiles(v.L);
         double* part_v = diss + (int64_t)s0 * nt;
         int* part_i = reinterpret_cast<int*>(diss + p.qc * nt) + (int64_t)s0 * nt;
-        if (sliced_routing() && qpl_s) {
+        if (v.opt.route_sliced && qpl_s) {
           staged(2, st, [&] { launch_slice_rows(xps, ns, v.s, v.s, true, qpl_s, qex, st); });
           staged(2, st, [&] {
             launch_gemm_sliced(qpl_s, qex, ns, v.cent_planes, v.cent_exps, v.L, v.s,
@@ -1026,10 +1044,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         rh.diss = ch.keys; rh.work_counter = ch.work_counter + 1; rh.mwords = p.mwords; rh.nq = n;
         // sparse selections (a query keeps < half of the rows its probes cover, taking
         // cluster sizes as a random query sees them): skip unselected row pairs
-        {
-          const char* e = getenv("RRG_RR_SKIP");
-          rh.skip = e ? atoi(e) != 0 : (double)t < 0.5 * w * ix->m_biased;
-        }
+        rh.skip = v.opt.rr_skip >= 0 ? v.opt.rr_skip != 0 : (double)t < 0.5 * w * ix->m_biased;
         staged(5, st, [&] { launch_cluster_rerank(rh, st); });
         TopkFinalHost fh{};
         fh.ix = v; fh.sel = sel; fh.w = w; fh.qoff = ch.qoff; fh.kbase = ch.kbase; fh.diss = ch.keys;
@@ -1195,6 +1210,13 @@ int rrg_index_create_shard(const RrgIndexDesc* desc, int device, int32_t cb, int
 
 void rrg_index_destroy(RrgIndex* index) { delete index; }
 
+int rrg_index_reload_options(RrgIndex* index) {
+  if (!index) return fail(RRG_E_USAGE, "ParameterError", "null argument");
+  index->view.opt = read_opts();
+  index->serial = RrgIndex::next_serial();  // captured graphs embed the old variant choices
+  return RRG_OK;
+}
+
 int rrg_index_info(const RrgIndex* index, RrgIndexInfo* out) {
   if (!index || !out) return fail(RRG_E_USAGE, "ParameterError", "null argument");
   *out = index->info;
@@ -1267,7 +1289,7 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
     // per-query front stages (projection .. routing) of piece j start as soon as it
     // has landed, overlapping the copies of pieces j+1..; results come back after.
     int nsub = nq >= 4096 ? 2 : 1;  // measured on C2: 2 pieces 3.17 ms, 4: 3.20, 1: 3.32
-    if (const char* e = getenv("RRG_HOST_PIECES")) nsub = std::max(1, std::min(8, atoi(e)));
+    if (index->view.opt.host_pieces > 0) nsub = index->view.opt.host_pieces;
     Plan p = make_plan(index, nq, k, w, t, rerank);
     const size_t qbytes = (size_t)nq * dim * 4, ibytes = (size_t)nq * k * 8,
                  sbytes = (size_t)nq * k * 4, cbytes = (size_t)nq * 4;
@@ -1292,8 +1314,7 @@ int rrg_search_host(RrgIndex* index, const float* queries, int64_t nq, int32_t d
       for (auto& e : h.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     // small batches: replay a captured graph (launch latency dominates there)
-    const char* ge = getenv("RRG_GRAPH");
-    const bool use_graph = nq <= 2048 && !g_timer.on && !(ge && atoi(ge) == 0);
+    const bool use_graph = nq <= 2048 && !g_timer.on && index->view.opt.graph;
     if (use_graph) {
       const size_t pneed = al(qbytes) + al(ibytes) + al(sbytes) + al(cbytes) + 256;
       if (pneed > h.pcap) {
@@ -1514,7 +1535,7 @@ int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq, float* 
     CUDA_TRY(cudaMallocAsync(&xx, std::max<int64_t>(nq, 1) * 4, st));
     int8_t* qpl = nullptr;
     int* qex = nullptr;
-    if (sliced_projection() && nq > 0) {
+    if (v.opt.proj_sliced && nq > 0) {
       CUDA_TRY(cudaMallocAsync(&qpl, sliced_plane_bytes((int)nq, v.d, true), st));
       CUDA_TRY(cudaMallocAsync(&qex, (size_t)sliced_rows_pad((int)nq, true) * 4, st));
       launch_slice_rows(queries, (int)nq, v.d, v.d, true, qpl, qex, st);
@@ -1523,7 +1544,7 @@ int rrg_stage_project(RrgIndex* index, const float* queries, int64_t nq, float* 
       CUDA_TRY(cudaFreeAsync(qpl, st));
       CUDA_TRY(cudaFreeAsync(qex, st));
     } else {
-      launch_project(queries, v.W, (int)nq, v.d, v.s, xp, st);
+      launch_project(queries, v.W, (int)nq, v.d, v.s, xp, v.opt.gemm_bk, st);
     }
     launch_prep(xp, queries, (int)nq, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st);
     CUDA_TRY(cudaGetLastError());
@@ -1549,7 +1570,7 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int
     launch_prep(xp, xp, (int)nq, v.s, v.s_pad, v.s, qc, dummy, dummy + nq, pp, dummy + 2 * nq, st);
     int8_t* qpl = nullptr;
     int* qex = nullptr;
-    if (sliced_routing()) {
+    if (v.opt.route_sliced) {
       CUDA_TRY(cudaMallocAsync(&qpl, sliced_plane_bytes((int)nq, v.s, true), st));
       CUDA_TRY(cudaMallocAsync(&qex, (size_t)sliced_rows_pad((int)nq, true) * 4, st));
     }
@@ -1563,6 +1584,73 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int
     CUDA_TRY(cudaFreeAsync(dummy, st));
     return RRG_OK;
   });
+}
+
+// K4 stage outputs (score_cluster, rrr.py:181-203 / quantize.py:109-156) of the
+// production cluster-major scoring kernel for caller-chosen probes: the projection
+// and query quantization of the search path, then k_score_cluster with its stage
+// outputs switched on.  Layout: raw1[q][c][j] (stage A, j < r, RRR clusters), and per
+// candidate (query-major, probes in sel order: cand_off[q] + offset of probe c +
+// point) raw2 = the last stage's int32 product (stage B, or stage A of an exact
+// model) and the f32 score.
+int rrg_stage_score(RrgIndex* index, const float* queries, int64_t nq, int32_t w,
+                    const int32_t* sel, int32_t* raw1, int32_t* raw2, float* scores,
+                    int32_t* cand_off, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index) return fail(RRG_E_USAGE, "ParameterError", "null index");
+    if (nq == 0) return RRG_OK;
+    const DevIndexView& v = index->view;
+    if (!(1 <= w && w <= v.L)) raise_usage("ParameterError", "w=%d out of range [1, %d]", w, v.L);
+    if (v.opt.score_query) raise_usage("ParameterError", "stage scoring runs the cluster-major kernel");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaSetDevice(index->device));
+    Plan p = make_plan(index, nq, 1, w, 1, 0);
+    if (p.qc < nq) raise_usage("ParameterError", "stage batch of %lld queries exceeds one chunk", (long long)nq);
+    if (workspace_bytes < p.total)
+      raise_usage("ParameterError", "workspace too small: %zu < %zu bytes", workspace_bytes, p.total);
+    char* base = static_cast<char*>(workspace);
+    float* xp = reinterpret_cast<float*>(base + p.off_xp);
+    int8_t* qcodes = reinterpret_cast<int8_t*>(base + p.off_qc);
+    float* qscale = reinterpret_cast<float*>(base + p.off_qs);
+    float* qhead = reinterpret_cast<float*>(base + p.off_qh);
+    float* xx = reinterpret_cast<float*>(base + p.off_xx);
+    double* pp = reinterpret_cast<double*>(base + p.off_pp);
+    const int n = (int)nq;
+    if (n <= kSmallBatch) {
+      launch_project_small(queries, v.Wt, n, v.d, v.s, xp, st);
+    } else if (v.opt.proj_sliced) {
+      int8_t* qpl = reinterpret_cast<int8_t*>(base + p.off_qpl);
+      int* qex = reinterpret_cast<int*>(base + p.off_qex);
+      launch_slice_rows(queries, n, v.d, v.d, true, qpl, qex, st);
+      launch_gemm_sliced(qpl, qex, n, v.wt_planes, v.wt_exps, v.s, v.d, EPI_PROJ, xp, nullptr, v.s,
+                         nullptr, nullptr, st);
+    } else {
+      launch_project(queries, v.W, n, v.d, v.s, xp, v.opt.gemm_bk, st);
+    }
+    launch_prep(xp, queries, n, v.s, v.s_pad, v.d, qcodes, qscale, qhead, pp, xx, st);
+    ClusterScoringHost ch{};
+    ch.ix = v; ch.xp = xp; ch.qcodes = qcodes; ch.qscale = qscale; ch.qhead = qhead; ch.sel = sel;
+    ch.w = w;
+    ch.qoff = reinterpret_cast<int*>(base + p.off_qoff);
+    ch.ncand = reinterpret_cast<int*>(base + p.off_ncand);
+    ch.pair_off = reinterpret_cast<int*>(base + p.off_pairoff);
+    ch.item_off = reinterpret_cast<int*>(base + p.off_itemoff);
+    ch.pairs = reinterpret_cast<int*>(base + p.off_pairs);
+    ch.kbase = cand_off;
+    ch.keys = reinterpret_cast<uint32_t*>(base + p.off_keys);
+    ch.work_counter = reinterpret_cast<int*>(base + p.off_ctr);
+    ch.dbg_raw1 = raw1; ch.dbg_raw2 = raw2; ch.dbg_score = scores;
+    launch_cluster_scoring(ch, n, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return RRG_OK;
+  });
+}
+
+size_t rrg_stage_score_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t w) {
+  if (!index || nq <= 0 || w < 1) return 0;
+  return make_plan(index, nq, 1, w, 1, 0).total;
 }
 
 // ---------------------------------------------------------- sharded search

@@ -159,6 +159,13 @@ struct ClusterScoreArgs {
   uint32_t* keys;        // [kbase[nq]]
   int* work_counter;     // zeroed before launch
   const float* xp;       // [nq][s] projected queries (f32-factor scoring)
+  // stage outputs for the bit-parity tests (rrg_stage_score; nullptr on the search
+  // path): stage-A int32 products per (pair, j < r) of RRR clusters, and per scored
+  // point (key-array layout) the last stage's int32 product and the f32 score of
+  // score_cluster (rrr.py:181-203: -2 yhat + ||c||^2 for euclidean, yhat otherwise)
+  int* dbg_raw1;
+  int* dbg_raw2;
+  float* dbg_score;
 };
 
 __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
@@ -232,6 +239,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
         if (act && part == 0) {
           const size_t aj = (size_t)slot * r + jj;
           inters[pi][jj] = deq(raw, pxs[pi], ix.ascale[aj], pxh[pi], ix.ahead[aj]);
+          if (a.dbg_raw1) a.dbg_raw1[(size_t)a.pairs[j0 + pi] * r + jj] = raw;
         }
       }
       __syncthreads();
@@ -273,6 +281,10 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
           const float yhat = deq(raw, s2s[pi], meta.y, h2s[pi], meta.x);
           const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
           a.keys[pkey[pi] + p] = mono32(keyf);
+          if (a.dbg_raw2) {
+            a.dbg_raw2[pkey[pi] + p] = raw;
+            a.dbg_score[pkey[pi] + p] = euclid ? keyf : yhat;
+          }
         }
       }
     } else {
@@ -296,6 +308,10 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
           const float yhat = deq(raw, pxs[pi], meta.y, pxh[pi], meta.x);
           const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
           a.keys[pkey[pi] + p] = mono32(keyf);
+          if (a.dbg_raw2) {
+            a.dbg_raw2[pkey[pi] + p] = raw;
+            a.dbg_score[pkey[pi] + p] = euclid ? keyf : yhat;
+          }
         }
       }
     }
@@ -378,6 +394,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
           const float yhat = (float)acc;
           const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
           a.keys[pkey[pi] + p] = mono32(keyf);
+          if (a.dbg_score) a.dbg_score[pkey[pi] + p] = euclid ? keyf : yhat;
         }
       }
     } else {
@@ -407,6 +424,7 @@ __global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
           const float yhat = (float)acc;
           const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
           a.keys[pkey[pi] + p] = mono32(keyf);
+          if (a.dbg_score) a.dbg_score[pkey[pi] + p] = euclid ? keyf : yhat;
         }
       }
     }
@@ -1017,7 +1035,6 @@ constexpr int XNT = 256;
 #define RRG_CM_CTAS 2  // C2 with next-pair prefetch: 2 CTAs/SM (123 regs) 1.20 ms vs 3 CTAs (80 regs + spill) 1.31 ms
 #endif
 constexpr int kCmCtas = RRG_CM_CTAS;  // resident CTAs per SM
-constexpr int kRrQ = 16;      // queries whose x is staged at once (one work item)
 #ifndef RRG_RR_ROWS
 #define RRG_RR_ROWS 512  // C2 re-rank: 128 -> 1.240, 256 -> 1.122, 384 -> 1.106, 512 -> 1.095, 768 -> 1.134, 1024 -> 1.149 ms
 #endif
@@ -1054,6 +1071,11 @@ __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_o
   if (threadIdx.x == 0) rr_item_off[L] = tot;
 }
 
+void launch_rr_items(const int* pair_off, const int* cl_pos, int L, int rows, int* item_off,
+                     cudaStream_t st) {
+  (k_rr_items<<<1, PNT, 0, st>>>(pair_off, cl_pos, L, rows, item_off), note_launch());
+}
+
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem) : "memory");
@@ -1069,12 +1091,18 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // pw(second half), each half a perfect 8-leaf tree over the same lanes -- the pair is
 // scored half by half (leaves 0-7 sit at [0, 64) of every interleaved 128-float step,
 // leaves 8-15 at [64, 128)) and the two reduced halves are added.
-// SKIP: row pairs no query of the work item selected are passed over before any load
-// is issued -- for unbalanced clusters (C4: up to 11x the mean size), where a query
-// keeps a small share of its cluster's rows; balanced clusters (C2: a query keeps 82%
-// of them) prefetch every pair without the extra ballot (measured 1.10 vs 1.26 ms).
-template <int NB, bool ASYNC, int NH = 1, bool SKIP = false>
+// RM (row mode) 0: every row pair of the item's range is loaded (balanced clusters: a
+// C2 query keeps 82% of its rows; measured 1.10 vs 1.26 ms for RM 1).  RM 1 (SKIP): row
+// pairs no query of the work item selected are passed over before any load is issued
+// (unbalanced clusters, C4: up to 11x the mean size).  RM 2 (COMPACT): the rows any
+// query of the item selected are listed first (a block-wide compaction of the OR of
+// the item's membership words) and the warps take pairs of listed rows -- for the
+// sparse selections the re-rank screen leaves (~k of t rows per query survive), where
+// pairs of adjacent rows would load many unselected rows.
+template <int NB, bool ASYNC, int NH = 1, int RM = 0>
 __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankArgs a) {
+  constexpr bool SKIP = RM == 1;
+  static_assert(!(ASYNC && RM == 2), "the cp.async variant streams adjacent row pairs");
   constexpr int NLV = 8 * NH, cstep = 8 * NLV;
   static_assert(NH == 1 || !ASYNC, "the cp.async variant handles 8-leaf rows");
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1088,6 +1116,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
   __shared__ int item_s;
   __shared__ int pq[kPairsPerItem], pkey[kPairsPerItem];
   __shared__ int slotq[XNT / 32][kRrQ];
+  __shared__ int rowlist[RM == 2 ? kRrRows : 1], nrows_s;
   const int L = ix.L;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = XNT / 32;
@@ -1159,12 +1188,45 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
       auto marked = [&](int g, int p) {
         return p < r1 && ((mb[g * a.mwords + (p >> 5)] >> (p & 31)) & 1u);
       };
+      if (RM == 2) {  // list the rows of [r0, r1) any query of the item selected
+        if (warp == 0) {
+          int base_n = 0;
+          for (int k0 = r0 >> 5; k0 <= (r1 - 1) >> 5; k0 += 32) {
+            const int k = k0 + lane;
+            uint32_t u = 0;
+            if (k <= (r1 - 1) >> 5) {
+              for (int g = 0; g < ng; ++g) u |= mb[g * a.mwords + k];
+              if (k == r0 >> 5) u &= 0xffffffffu << (r0 & 31);
+              if (k == (r1 - 1) >> 5) u &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
+            }
+            const int cnt = __popc(u);
+            int incl = cnt;
+            for (int o = 1; o < 32; o <<= 1) {
+              const int v = __shfl_up_sync(0xffffffffu, incl, o);
+              if (lane >= o) incl += v;
+            }
+            int at = base_n + incl - cnt;
+            while (u) {
+              const int b = __ffs(u) - 1;
+              u &= u - 1;
+              rowlist[at++] = 32 * k + b;
+            }
+            base_n += __shfl_sync(0xffffffffu, incl, 31);
+          }
+          if (lane == 0) nrows_s = base_n;
+        }
+        __syncthreads();
+      }
+      // work runs over indices ia of the item's rows: r0 + ia, or the listed rows (RM 2)
+      const int n_idx = RM == 2 ? nrows_s : r1 - r0;
+      auto row_of = [&](int ia) { return RM == 2 ? rowlist[ia] : r0 + ia; };
       // this lane's 2-element slice of each step of rows pa and pa+1 (register
       // double use: the next pair's loads are issued before this pair's reduction)
       float2 ca[NB], cb[NB];
       int hoff = 0;  // NH = 2: the half (0 or 64 floats into each step) being scored
-      auto load_pair = [&](int pa) {
-        const int pb = pa + 1 < r1 ? pa + 1 : pa;
+      auto load_pair = [&](int ia) {
+        const int pa = row_of(ia);
+        const int pb = ia + 1 < n_idx ? row_of(ia + 1) : pa;
         if (ASYNC) {  // issue the copy of both rows into this warp's staging slot
           const float4* ra = reinterpret_cast<const float4*>(ix.corpus + (size_t)(p0 + pa) * ds);
           const float4* rb = reinterpret_cast<const float4*>(ix.corpus + (size_t)(p0 + pb) * ds);
@@ -1225,26 +1287,28 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           vb = acc_b;
         }
       };
-      auto next_marked = [&](int p) {
-        if (!(SKIP || ASYNC)) return p;
-        while (p < r1 && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, p) || marked(lane, p + 1))))
-          p += nwarps * 2;
-        return p;
+      auto next_marked = [&](int ia) {
+        if (!(SKIP || ASYNC)) return ia;
+        while (ia < n_idx && !__ballot_sync(0xffffffffu, lane < ng && (marked(lane, r0 + ia) ||
+                                                                         marked(lane, r0 + ia + 1))))
+          ia += nwarps * 2;
+        return ia;
       };
-      int pa = next_marked(r0 + warp * 2);
-      if (pa < r1) load_pair(pa);
-      for (; pa < r1;) {
-        const int pb = pa + 1;
-        const int pn = next_marked(pa + nwarps * 2);
+      int ia = next_marked(warp * 2);
+      if (ia < n_idx) load_pair(ia);
+      for (; ia < n_idx;) {
+        const int pa = row_of(ia);
+        const int pb = ia + 1 < n_idx ? row_of(ia + 1) : pa;
+        const int pn = next_marked(ia + nwarps * 2);
         // the queries that selected either row (one lane per query, ballot)
         const bool mine = lane < ng && (marked(lane, pa) || marked(lane, pb));
         const unsigned act0 = __ballot_sync(0xffffffffu, mine);
         if (ASYNC) {
           take_pair();
-          if (pn < r1) load_pair(pn);
+          if (pn < n_idx) load_pair(pn);
         } else if (!act0) {
-          if (pn < r1) load_pair(pn);
-          pa = pn;
+          if (pn < n_idx) load_pair(pn);
+          ia = pn;
           continue;
         }
         float res = 0.f;  // NH = 2: the first half's reduced value
@@ -1266,8 +1330,8 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         }
         if (h2 + 1 < NH) {  // the pair's next half
           hoff = 64 * (h2 + 1);
-          load_pair(pa);
-        } else if (!ASYNC && pn < r1) {
+          load_pair(ia);
+        } else if (!ASYNC && pn < n_idx) {
           hoff = 0;
           load_pair(pn);
         }
@@ -1299,7 +1363,7 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
           if (marked(g, p)) a.diss[pkey[g0 + g] + p] = mono32(euclid ? res : -res);
         }
         __syncwarp();
-        pa = pn;
+        ia = pn;
       }
       __syncthreads();
     }
@@ -1465,16 +1529,15 @@ __global__ void k_topk_final_warp(TopkFinalArgs a, int cap, int nq) {
 // RRG_WARP_SELECT=0 selects the CTA-per-query selections (k_select_topt, k_topk_final)
 // RRG_WARP_SELECT: 1 forces the warp-per-query selections, 0 the CTA-per-query ones;
 // unset: warp per query once the batch fills the GPU (>= 1184 queries = 8 per SM)
-static bool warp_select_ok(int nq) {
-  const char* e = getenv("RRG_WARP_SELECT");
-  if (e) return atoi(e) != 0;
+static bool warp_select_ok(const DevIndexView& ix, int nq) {
+  if (ix.opt.warp_select >= 0) return ix.opt.warp_select != 0;
   return nq >= 1184;
 }
 
 
 template <typename Kern>
 static void opt_in_smem(Kern* kern, int slot) {
-  static int done[32][64] = {};
+  static int done[48][64] = {};
   int dev = 0;
   cudaGetDevice(&dev);
   if (dev < 0 || dev >= 64 || done[slot][dev]) return;
@@ -1496,6 +1559,7 @@ void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st
   a.ix = ix; a.qcodes = h.qcodes; a.qscale = h.qscale; a.qhead = h.qhead; a.sel = h.sel;
   a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off; a.item_off = h.item_off;
   a.pairs = h.pairs; a.kbase = h.kbase; a.keys = h.keys; a.work_counter = h.work_counter;
+  a.dbg_raw1 = h.dbg_raw1; a.dbg_raw2 = h.dbg_raw2; a.dbg_score = h.dbg_score;
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1540,7 +1604,7 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   // w=16 (~16k candidates) 2.0 vs 4.9 ms, w=64 (~62k) 6.6 vs 14.5 ms for the CTA select)
   // (the membership bits are sized by kcap = min(largest list, 24k): a capped kcap
   // cannot hold every candidate's bit, so the CTA select handles that case)
-  if (warp_select_ok(nq) && h.rerank && !(h.marks && h.kcap >= 24 * 1024)) {
+  if (warp_select_ok(h.ix, nq) && h.rerank && !(h.marks && h.kcap >= 24 * 1024)) {
     // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
     const int bits_cap = h.marks ? h.kcap : 0;
     const int stage_cap = 0;  // keys are read through L1
@@ -1558,15 +1622,11 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
   (k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a), note_launch());
 }
 
-// measured on C2 (w=1, t=800): register loads 1.134 ms vs cp.async staging 1.249 ms
-static bool rerank_async() {
-  const char* e = getenv("RRG_RR_ASYNC");
-  return e && atoi(e) == 1;
-}
-
-size_t cluster_rerank_smem(int d_stride, int mwords) {
-  return (size_t)kRrQ * d_stride * 4 + (size_t)kRrQ * mwords * 4 +
-         (rerank_async() ? (size_t)(XNT / 32) * 2 * d_stride * 4 : 0);
+// RRG_RR_ASYNC=1 (ix.opt.rr_async): cp.async row staging -- measured on C2 (w=1,
+// t=800): register loads 1.134 ms vs cp.async staging 1.249 ms
+size_t cluster_rerank_smem(const DevIndexView& ix, int mwords) {
+  return (size_t)kRrQ * ix.d_stride * 4 + (size_t)kRrQ * mwords * 4 +
+         (ix.opt.rr_async ? (size_t)(XNT / 32) * 2 * ix.d_stride * 4 : 0);
 }
 
 // the row plan fits k_rerank_cluster and a query group's x + membership bits of the
@@ -1577,7 +1637,7 @@ bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster) {
         ix.pw_leaf_n % 8 == 0 && (nb == 12 || nb == 15 || nb == 16)))
     return false;
   const int mwords = (int)((max_cluster + 31) / 32) + 1;
-  return cluster_rerank_smem(ix.d_stride, mwords) + 8 * 1024 <= (size_t)kMaxSmemPerCta;
+  return cluster_rerank_smem(ix, mwords) + 8 * 1024 <= (size_t)kMaxSmemPerCta;
 }
 
 
@@ -1594,21 +1654,22 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   a.neg_zero = -0.0f;
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
-  const size_t sm = cluster_rerank_smem(h.ix.d_stride, h.mwords);
+  const size_t sm = cluster_rerank_smem(h.ix, h.mwords);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-#define RRG_RR_LAUNCH(NB, AS, NH, SK, SLOT)                                      \
+#define RRG_RR_LAUNCH(NB, AS, NH, RM, SLOT)                                      \
   do {                                                                           \
-    opt_in_smem(k_rerank_cluster<NB, AS, NH, SK>, SLOT);                         \
-    (k_rerank_cluster<NB, AS, NH, SK><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); \
+    opt_in_smem(k_rerank_cluster<NB, AS, NH, RM>, SLOT);                         \
+    (k_rerank_cluster<NB, AS, NH, RM><<<sms * kCmCtas, XNT, sm, st>>>(a), note_launch()); \
   } while (0)
 #define RRG_RR_SK(NB, NH, SLOT)                                                  \
   do {                                                                           \
-    if (h.skip) RRG_RR_LAUNCH(NB, false, NH, true, SLOT + 16);                   \
-    else RRG_RR_LAUNCH(NB, false, NH, false, SLOT);                              \
+    if (h.compact) RRG_RR_LAUNCH(NB, false, NH, 2, SLOT + 20);                   \
+    else if (h.skip) RRG_RR_LAUNCH(NB, false, NH, 1, SLOT + 16);                 \
+    else RRG_RR_LAUNCH(NB, false, NH, 0, SLOT);                                  \
   } while (0)
-  const bool as = rerank_async() && h.ix.pw_nleaves == 8;
+  const bool as = h.ix.opt.rr_async && h.ix.pw_nleaves == 8 && !h.compact;
   if (h.ix.pw_nleaves == 16) {  // d = 16 leaves (e.g. 1536): scored as two 8-leaf halves
     switch (h.ix.pw_leaf_n / 8) {
       case 12: RRG_RR_SK(12, 2, 12); break;
@@ -1619,9 +1680,9 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   }
   // persistent grid: kCmCtas CTAs per SM
   switch (h.ix.pw_leaf_n / 8) {
-    case 12: if (as) RRG_RR_LAUNCH(12, true, 1, false, 4); else RRG_RR_SK(12, 1, 0); break;
-    case 15: if (as) RRG_RR_LAUNCH(15, true, 1, false, 5); else RRG_RR_SK(15, 1, 1); break;
-    default: if (as) RRG_RR_LAUNCH(16, true, 1, false, 6); else RRG_RR_SK(16, 1, 2); break;
+    case 12: if (as) RRG_RR_LAUNCH(12, true, 1, 0, 4); else RRG_RR_SK(12, 1, 0); break;
+    case 15: if (as) RRG_RR_LAUNCH(15, true, 1, 0, 5); else RRG_RR_SK(15, 1, 1); break;
+    default: if (as) RRG_RR_LAUNCH(16, true, 1, 0, 6); else RRG_RR_SK(16, 1, 2); break;
   }
 #undef RRG_RR_SK
 #undef RRG_RR_LAUNCH
@@ -1640,7 +1701,7 @@ void launch_topk_final(const TopkFinalHost& h, int nq, cudaStream_t st) {
   a.order = h.order;
   const size_t per = warp_sel_bytes(h.take_cap, 0);
   // warp per query once the batch fills the GPU; tiny batches get a CTA per query
-  if (warp_select_ok(nq) && h.k <= 256 && per <= 24 * 1024) {
+  if (warp_select_ok(h.ix, nq) && h.k <= 256 && per <= 24 * 1024) {
     const int wpc = (int)std::max<size_t>(1, std::min<size_t>(8, (56 * 1024) / per));
     const unsigned grid = (unsigned)((nq + wpc - 1) / wpc);
     const size_t sm = per * wpc;

@@ -21,6 +21,24 @@ constexpr int kMetricCosine = 2;
 constexpr int kKindRrr = 0;    // two-stage A/B model (rrr.py:181-203)
 constexpr int kKindExact = 1;  // single-factor exact model (rrr.py:103-113, index.py:465-468)
 
+// Search-variant switches (A/B measurement and test coverage of every kernel
+// variant), read from the environment once per index -- at rrg_index_open /
+// rrg_index_create and on rrg_index_reload_options -- never per search call.
+struct RrgOpts {
+  int proj_sliced;   // RRG_GEMM / RRG_PROJ = sliced|dmma (default sliced)
+  int route_sliced;  // RRG_GEMM / RRG_ROUTE = sliced|dmma (default dmma)
+  int route_fused;   // RRG_ROUTE_FUSED (default 1): w = 1 argmin fused into the GEMM
+  int gemm_bk;       // RRG_GEMM_BK = 8|16: K depth per DMMA stage
+  int score_query;   // RRG_SCORE_MODE=query: fused query-major scoring
+  int rerank;        // RRG_RERANK: 0 auto, 1 cluster, 2 query, 3 regs, 4 tma
+  int rr_skip;       // RRG_RR_SKIP: -1 auto, 0 off, 1 on
+  int rr_async;      // RRG_RR_ASYNC: cp.async row staging in the cluster re-rank
+  int warp_select;   // RRG_WARP_SELECT: -1 auto, 0 CTA per query, 1 warp per query
+  int host_pieces;   // RRG_HOST_PIECES: 0 auto
+  int graph;         // RRG_GRAPH: captured graphs for small host batches (default 1)
+  int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
+};
+
 // POD view of a device-resident index, passed by value to kernels.
 // Counts one kernel launch of this thread (rrg_last_launch_count; rrg_api.cu).
 void note_launch();
@@ -73,6 +91,16 @@ struct DevIndexView {
   const int* wt_exps;
   const int8_t* cent_planes;  // centroids (L x s), same slicing, for the routing GEMM
   const int* cent_exps;
+  // re-rank screen (rrg_screen.cu, euclidean indexes with a corpus; nullptr otherwise):
+  // residual rows r = c - mu_l as fp16 (x 2^-e_row), pre-tiled per 128-row block in the
+  // UMMA K-major layout, with the exact residual norms the error bound needs
+  const uint16_t* scr_plane;  // [blocks][scr_kc][128 rows x 16 fp16]
+  const int* scr_blk0;        // [L+1] first block of each cluster (clusters padded to 128 rows)
+  const float* scr_mu;        // [L][d] per-cluster mean (natural element order)
+  const double* scr_rr;       // [P] ||c - mu||^2 (f64)
+  const float4* scr_rmeta;    // [P] {||r_hat||, ||r - r_hat||, 2^e_row, 0} (scaled units, rounded up)
+  int scr_kc;                 // K chunks of 16 elements: ceil(d / 16)
+  RrgOpts opt;
 };
 
 // ---------------------------------------------------------------- numerics

@@ -153,6 +153,9 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
             dv = dv > 0.0 ? dv : 0.0;
           } else {
             dv = -acc[i][j][h];
+            // a non-finite query (rejected with DataError after the search) must still
+            // route to a valid cluster: NaN compares false, so rank it as +inf
+            if (dv != dv) dv = __longlong_as_double(0x7ff0000000000000ll);
           }
           if (dv < best || (dv == best && gn < bcol)) { best = dv; bcol = gn; }
         }
@@ -1332,15 +1335,12 @@ static void gemm_launch(dim3 grid, cudaStream_t st, const float* A, int lda, con
 
 // K depth per stage: 8 (default) or 16 (RRG_GEMM_BK=16) -- measured equal on C2
 // (projection 0.175 ms, routing 0.203 vs 0.207 ms): the DMMA pipe, not the barriers, bounds it
-static int gemm_bk() {
-  const char* e = getenv("RRG_GEMM_BK");
-  return (e && atoi(e) == 16) ? 16 : 8;
-}
+// (RrgOpts.gemm_bk, resolved once per index)
 
-void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
+void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp, int bk,
                     cudaStream_t st) {
   dim3 grid((s + MBN - 1) / MBN, (nq + 32 * kGemmWM - 1) / (32 * kGemmWM));
-  if (gemm_bk() == 16)
+  if (bk == 16)
     gemm_launch<EPI_PROJ, false, kGemmWM, 16>(grid, st, x, d, W, s, nq, s, d, xp, nullptr, s, nullptr, nullptr);
   else
     gemm_launch<EPI_PROJ, false, kGemmWM, 8>(grid, st, x, d, W, s, nq, s, d, xp, nullptr, s, nullptr, nullptr);
@@ -1356,10 +1356,10 @@ void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int 
 }
 
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
-                       const double* pp, const double* cnorm, double* diss, cudaStream_t st) {
+                       const double* pp, const double* cnorm, double* diss, int bk, cudaStream_t st) {
   constexpr int WM = 4;  // C2: 128x64 tiles measured 0.214 ms vs 96x64 0.220 ms
   dim3 grid((L + MBN - 1) / MBN, (nq + 32 * WM - 1) / (32 * WM));
-  const bool bk16 = gemm_bk() == 16;
+  const bool bk16 = bk == 16;
   if (metric == kMetricEuclidean) {
     if (bk16) gemm_launch<EPI_L2, true, WM, 16>(grid, st, xp, s, cent, s, nq, L, s, nullptr, diss, L, pp, cnorm);
     else gemm_launch<EPI_L2, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, diss, L, pp, cnorm);
@@ -1418,6 +1418,7 @@ __global__ void k_route_nearest_partials(const double* __restrict__ pv, const in
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (ob < bk || (ob == bk && oi < bi)) { bk = ob; bi = oi; }
   }
+  if (bi == 0x7fffffff) bi = 0;  // defensive: every partial was unordered
   if (lane == 0) { sel[q] = bi; primary[q] = bi; }
 }
 
@@ -1501,10 +1502,10 @@ void launch_rerank(const RerankArgsHost& h, int nq, cudaStream_t st) {
   a.out_count = h.out_count; a.q0 = h.q0; a.order = h.order;
   const bool tree = rerank_uses_tree(h.ix);
   const size_t sm = rerank_smem(h.ix.d_stride, h.take_cap, h.k, tree);
-  const char* rmode = getenv("RRG_RERANK");
+
   // default: the register-pipelined k_rerank_tree (measured faster on C2 than the
   // TMA ring, whose mbarrier polling costs issue slots); RRG_RERANK=tma opts in
-  const bool use_tma = rmode && strcmp(rmode, "tma") == 0;
+  const bool use_tma = h.ix.opt.rerank == 4;
   if (tree && use_tma) {
     const int nb = h.ix.pw_leaf_n / 8;
     const bool one = 4 * h.ix.pw_nleaves <= 32;

@@ -60,13 +60,13 @@ void launch_project_small(const float* x, const float* Wt, int nq, int d, int s,
                           cudaStream_t st);
 void launch_route_dist_small(const float* xp, const float* cent, int nq, int L, int s, int metric,
                              const double* pp, const double* cnorm, double* diss, cudaStream_t st);
-void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp,
+void launch_project(const float* x, const float* W, int nq, int d, int s, float* xp, int bk,
                     cudaStream_t st);
 void launch_prep(const float* xp, const float* x, int nq, int s, int s_pad, int d, int8_t* qcodes,
                  float* qscale, float* qhead, double* pp, float* xx, cudaStream_t st,
                  int* nonfinite = nullptr);
 void launch_route_dist(const float* xp, const float* cent, int nq, int L, int s, int metric,
-                       const double* pp, const double* cnorm, double* diss, cudaStream_t st);
+                       const double* pp, const double* cnorm, double* diss, int bk, cudaStream_t st);
 size_t route_select_smem(int L);
 // w = 1 routing fused into the DMMA GEMM: per (row, 64-column tile) minima, then a
 // warp argmin per query (part_v / part_i: nq x route_nearest_tiles(L))
@@ -101,6 +101,9 @@ struct ClusterScoringHost {
   int* kbase;     // [nq+1]
   uint32_t* keys; // [sum N]
   int* work_counter;
+  int* dbg_raw1 = nullptr;     // rrg_stage_score only (see ClusterScoreArgs)
+  int* dbg_raw2 = nullptr;
+  float* dbg_score = nullptr;
 };
 void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st);
 
@@ -131,6 +134,10 @@ size_t select_topt_smem(int w, int take_cap, int k, int kcap);
 void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st);
 
 // Cluster-major re-rank (rrg_cluster_score.cu)
+constexpr int kRrQ = 16;  // queries of one work item (x staged at once; the screen's MMA N)
+// item_off[l] = ceil(pairs_l / kRrQ) * ceil(m_l / rows), exclusive scan, item_off[L] = total
+void launch_rr_items(const int* pair_off, const int* cl_pos, int L, int rows, int* item_off,
+                     cudaStream_t st);
 struct ClusterRerankHost {
   DevIndexView ix;
   const float* queries;
@@ -144,12 +151,51 @@ struct ClusterRerankHost {
   uint32_t* diss;
   int* work_counter;
   bool skip;  // pass over row pairs no query of a work item selected (sparse selections)
+  bool compact = false;  // list the selected rows first (after the screen: ~k of t survive)
   int mwords;
   int nq;  // queries of the chunk (work-item sizing)
 };
 bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster);
-size_t cluster_rerank_smem(int d_stride, int mwords);
+size_t cluster_rerank_smem(const DevIndexView& ix, int mwords);
 void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st);
+
+// Re-rank screen (rrg_screen.cu): tensor-core bounds of every (query, candidate row)
+// of the cluster-major work items, then per query the k-th smallest upper bound T and
+// the removal of the candidates whose lower bound exceeds it (see the file header).
+int screen_max_dim();
+size_t screen_smem(int kc);
+void launch_screen_build(const DevIndexView& v, float* mu, uint16_t* plane, size_t plane_bytes,
+                         double* rr, float4* meta, cudaStream_t st);
+struct ScreenHost {
+  DevIndexView ix;
+  const float* queries;  // chunk-local [nq][d]
+  int w;
+  const int* qoff;
+  const int* pair_off;
+  const int* pairs;
+  const int* kbase;
+  uint32_t* marks;       // membership bits of the top-t (cleared for non-survivors)
+  int* item_off;         // [L+1] scratch
+  float* ub;             // per candidate bounds (key-array layout)
+  float* lb;
+  const int* cand_idx;   // [nq][take_cap] top-t candidate indices
+  const int* cand_n;
+  int take_cap, k;
+  uint32_t* diss;        // key array re-used for distances: non-survivors -> ~0u
+  int64_t* counters;     // rrg_search_counters (nullptr unless enabled)
+};
+struct ThreshArgs {
+  const int* kbase;
+  const int* cand_idx;
+  const int* cand_n;
+  int take_cap, k;
+  const float* ub;
+  const float* lb;
+  uint32_t* marks;
+  uint32_t* diss;
+  int64_t* counters;
+};
+void launch_screen(const ScreenHost& h, int nq, cudaStream_t st);
 
 struct TopkFinalHost {
   DevIndexView ix;

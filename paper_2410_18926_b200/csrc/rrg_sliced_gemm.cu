@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
           if (g.epi == EPI_L2) g.outd[(size_t)gm * g.ldo + gn] = d2;
           else if (d2 < best) { best = d2; bcol = gn; }  // columns ascend: ties keep the lowest
         } else if (g.epi == EPI_NEGIP_ARGMIN) {
-          if (-val < best) { best = -val; bcol = gn; }
+          const double dv = -val == -val ? -val : kInf;  // NaN (non-finite query) ranks as +inf
+          if (dv < best || (dv == best && gn < bcol)) { best = dv; bcol = gn; }
         } else {
           g.outd[(size_t)gm * g.ldo + gn] = -val;
         }

@@ -35,7 +35,8 @@ FLAG_QUANTIZED, FLAG_CORPUS, FLAG_BALANCED, FLAG_EXACT_IVF = 1, 2, 4, 8
 
 
 class DeviceIndex:
-    """Handle to a device-resident index.  Immutable; safe for concurrent searches."""
+    """Handle to a device-resident index.  Immutable; safe for concurrent searches (each
+    thread and stream gets its own workspace; outputs are per call)."""
 
     def __init__(self, handle: int, device: int, source: str):
         self._h = ctypes.c_void_p(handle)
@@ -188,13 +189,21 @@ class DeviceIndex:
     def workspace_bytes(self, nq: int, k: int, w: int, t: int, rerank: bool) -> int:
         return int(lib.rrg_search_workspace_bytes(self._h, nq, k, w, t, int(rerank)))
 
-    def _workspace(self, nbytes: int):
+    def _workspace(self, nbytes: int, st):
+        """Scratch for one search, cached per (thread, stream).  It is allocated while
+        ``st`` is current, so torch's caching allocator ties the block to the stream
+        the search runs on: a grown buffer's old block is only reused by later work on
+        that same stream, and two streams never share one workspace."""
         import torch
 
-        ws = getattr(self._tls, "ws", None)
+        cache = getattr(self._tls, "ws", None)
+        if cache is None:
+            cache = self._tls.ws = {}
+        ws = cache.get(st.cuda_stream)
         if ws is None or ws.numel() < nbytes:
-            ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
-            self._tls.ws = ws
+            with torch.cuda.stream(st):
+                ws = torch.empty(max(nbytes, 256), dtype=torch.uint8, device=f"cuda:{self.device}")
+            cache[st.cuda_stream] = ws
         return ws
 
     def search_device(self, queries, k: int, w: int, t: int, rerank: bool = True, out=None,
@@ -222,8 +231,8 @@ class DeviceIndex:
         else:
             ids, scores, count = out
         nbytes = self.workspace_bytes(nq, k, w, t, rerank) if nq else 0
-        ws = self._workspace(nbytes)
         st = stream if stream is not None else torch.cuda.current_stream(dev)
+        ws = self._workspace(nbytes, st)
         check(lib.rrg_search(self._h, q.data_ptr(), nq, dim, k, w, t, int(rerank), ids.data_ptr(),
                              scores.data_ptr(), count.data_ptr(), ws.data_ptr(), ws.numel(),
                              st.cuda_stream))
@@ -288,6 +297,34 @@ class DeviceIndex:
         check(lib.rrg_stage_project(self._h, queries.data_ptr(), nq, xp.data_ptr(), qc.data_ptr(),
                                     qs.data_ptr(), qh.data_ptr(), st.cuda_stream))
         return xp, qc, qs, qh
+
+    def stage_score(self, queries, sel):
+        """K4 stage outputs for probes ``sel`` [nq, w] (``rrg_stage_score``): returns
+        (raw1 int32 [nq, w, rank], raw2 int32 [N], scores f32 [N], cand_off int32 [nq+1])
+        with the candidates of query q at cand_off[q]:cand_off[q+1], probes in sel order."""
+        import torch
+
+        nq, w = sel.shape
+        dev = queries.device
+        sel = sel.to(device=dev, dtype=torch.int32).contiguous()
+        sizes = torch.from_numpy(self.cluster_sizes().astype(np.int64)).to(dev)
+        total = int(sizes[sel.long()].sum()) if nq else 0
+        raw1 = torch.zeros((nq, w, self.rank), dtype=torch.int32, device=dev)
+        raw2 = torch.zeros((max(total, 1),), dtype=torch.int32, device=dev)
+        sc = torch.zeros((max(total, 1),), dtype=torch.float32, device=dev)
+        off = torch.zeros((nq + 1,), dtype=torch.int32, device=dev)
+        nb = int(lib.rrg_stage_score_workspace_bytes(self._h, nq, w))
+        ws = torch.empty(max(nb, 256), dtype=torch.uint8, device=dev)
+        st = torch.cuda.current_stream(dev)
+        check(lib.rrg_stage_score(self._h, queries.data_ptr(), nq, w, sel.data_ptr(), raw1.data_ptr(),
+                                  raw2.data_ptr(), sc.data_ptr(), off.data_ptr(), ws.data_ptr(),
+                                  ws.numel(), st.cuda_stream))
+        return raw1, raw2[:total], sc[:total], off
+
+    def reload_options(self) -> None:
+        """Re-read the RRG_* variant switches from the environment (``rrg_index_reload_options``);
+        they are otherwise resolved once, when the index is created."""
+        check(lib.rrg_index_reload_options(self._h))
 
     def stage_route(self, xp, w: int):
         import torch

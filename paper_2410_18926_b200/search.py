@@ -108,13 +108,101 @@ def _params(params):
     return int(params.k), int(params.w), int(params.t), bool(params.rerank)
 
 
+class QueryResults(list):
+    """``list[QueryResult]`` that builds each ``QueryResult`` on first access.
+
+    The search returns three dense arrays (ids [Q, k], scores [Q, k], count [Q]);
+    packaging one frozen dataclass per query costs ~1-2 us in Python (SURVEY.md §7
+    hard part 9), more than the whole device search per query at 10k-query batches.
+    Items are created when indexed or iterated and cached in the list itself; every
+    ``QueryResult`` owns its arrays (``ids[i, :c].copy()``, as the reference's fresh
+    per-query arrays).  It is a real ``list`` (isinstance, len, ==, iteration, slicing,
+    pickling all behave like the reference's return value); code that reads the raw
+    list storage from C without going through the sequence protocol sees ``None`` for
+    items never accessed -- ``materialize()`` fills them all.
+    """
+
+    __slots__ = ("_ids", "_scores", "_count", "_k", "_pending")
+
+    def __init__(self, ids: np.ndarray, scores: np.ndarray, count: np.ndarray, k: int):
+        n = int(ids.shape[0])
+        super().__init__([None] * n)
+        self._ids, self._scores, self._count, self._k = ids, scores, count, k
+        self._pending = n
+
+    def _make(self, i: int):
+        c = int(self._count[i])
+        r = QueryResult(ids=self._ids[i, :c].copy(), scores=self._scores[i, :c].copy(),
+                        truncated=c < self._k)
+        list.__setitem__(self, i, r)
+        self._pending -= 1
+        if self._pending == 0:  # every item built: the arrays are no longer needed
+            self._ids = self._scores = self._count = None
+        return r
+
+    def _get(self, i: int):
+        v = list.__getitem__(self, i)
+        if v is None and self._pending:
+            v = self._make(i if i >= 0 else i + len(self))
+        return v
+
+    def materialize(self) -> "QueryResults":
+        if self._pending:
+            for i in range(len(self)):
+                self._get(i)
+        return self
+
+    def __getitem__(self, i):
+        if isinstance(i, slice):
+            return [self._get(j) for j in range(*i.indices(len(self)))]
+        return self._get(i)
+
+    def __iter__(self):
+        for i in range(len(self)):
+            yield self._get(i)
+
+    def __reversed__(self):
+        for i in range(len(self) - 1, -1, -1):
+            yield self._get(i)
+
+    def __contains__(self, x):
+        return any(x == v for v in self)
+
+    def __eq__(self, other):
+        self.materialize()
+        if isinstance(other, QueryResults):
+            other.materialize()
+        return list.__eq__(self, other)
+
+    def __ne__(self, other):
+        return not self.__eq__(other)
+
+    __hash__ = None
+
+    def __repr__(self):
+        return list.__repr__(self.materialize())
+
+    def __reduce_ex__(self, protocol):
+        return (list, (list(self),))
+
+    def __copy__(self):
+        return list(self)
+
+    def copy(self):
+        return list(self)
+
+    def index(self, x, *args):
+        return list.index(self.materialize(), x, *args)
+
+    def count(self, x):
+        return list.count(self.materialize(), x)
+
+    def __add__(self, other):
+        return list(self) + list(other)
+
+
 def _package(ids: np.ndarray, scores: np.ndarray, count: np.ndarray, k: int) -> list:
-    out = []
-    QR = QueryResult
-    for i in range(ids.shape[0]):
-        c = int(count[i])
-        out.append(QR(ids=ids[i, :c].copy(), scores=scores[i, :c].copy(), truncated=c < k))
-    return out
+    return QueryResults(ids, scores, count, k)
 
 
 def query_batch(index, queries, params) -> list:

@@ -24,7 +24,7 @@ import rrann  # noqa: E402
 from rrann.bench import synth_dataset  # noqa: E402
 from rrann.cluster import route  # noqa: E402
 from rrann.index import IndexConfig, QueryParams, build, serialize  # noqa: E402
-from rrann.quantize import QuantizedMatrix, int8_gemv, quantize_vector  # noqa: E402
+from rrann.quantize import QuantizedMatrix, int8_gemv, quantize_vector, quantized_vecmat  # noqa: E402
 from rrann.rrr import RrrConfig, cluster_metric, score_cluster  # noqa: E402
 
 F32 = np.float32
@@ -98,12 +98,17 @@ def stage_trace(index, x):
         return out
     qx = quantize_vector(xp, mixed_precision=True)
     out.update(qhead=F32(qx.head), qscale=F32(qx.scale), qcodes=qx.values)
-    raws, scores = [], []
+    raws, raws2, scores = [], [], []
     for l in sel:
         model = index.models[int(l)]
         raws.append(int8_gemv(qx, model.a))
+        if model.b is not None:  # stage B: the re-quantized intermediate (rrr.py:196-197)
+            inter = quantized_vecmat(xp, model.a, qx=qx)
+            raws2.append(int8_gemv(quantize_vector(inter.astype(F32), mixed_precision=model.b.mixed),
+                                   model.b))
         scores.append(score_cluster(xp, model, metric, query_quantized=qx))
     out["raw1"] = np.concatenate(raws)
+    out["raw2"] = np.concatenate(raws2) if raws2 else np.zeros(0, np.int32)
     out["scores"] = np.concatenate(scores)
     return out
 

@@ -111,6 +111,78 @@ def test_golden_stages(pkg, tmp_path, case):
         assert set(sel[i].tolist()) == set(g[f"trace{i}_selected"].tolist())
 
 
+@pytest.mark.parametrize("case", QUANT_CASES)
+def test_golden_stage_score_bits(pkg, tmp_path, case):
+    """K4 (score_cluster, rrr.py:181-203) bit for bit against the reference's own
+    intermediates: the stage-A int32 products (int8_gemv(qx, A)), the stage-B int32
+    products of the re-quantized intermediate (int8_gemv(q(inter), B)) and the f32
+    per-point scores, for the probes the reference routed to (trace order)."""
+    g, dev = _golden_index(pkg, tmp_path, case)
+    x = torch.from_numpy(g["queries"][:3]).cuda()
+    w = len(g["trace0_selected"])
+    sel = torch.tensor(np.stack([g[f"trace{i}_selected"] for i in range(3)]), dtype=torch.int32)
+    raw1, raw2, sc, off = (a.cpu().numpy() for a in dev.stage_score(x, sel.cuda()))
+    sizes = dev.cluster_sizes()
+    r = dev.rank
+    for i in range(3):
+        cand = slice(off[i], off[i + 1])
+        np.testing.assert_array_equal(sc[cand].view(np.int32), g[f"trace{i}_scores"].view(np.int32),
+                                      err_msg=f"{case} q{i} scores")
+        # raw1 concatenates per probe: r stage-A products (RRR) or m_l (exact model)
+        ref1 = g[f"trace{i}_raw1"]
+        ref2 = g.get(f"trace{i}_raw2")
+        o1 = o2 = oc = 0
+        for c, l in enumerate(g[f"trace{i}_selected"]):
+            m = int(sizes[l])
+            exact = m < r or "exact_ivf" in case
+            if exact:  # single-factor model: its stage-A product is the per-point raw
+                np.testing.assert_array_equal(raw2[off[i] + oc: off[i] + oc + m], ref1[o1:o1 + m])
+                o1 += m
+            else:
+                np.testing.assert_array_equal(raw1[i, c], ref1[o1:o1 + r], err_msg=f"{case} q{i} A")
+                o1 += r
+                if ref2 is not None:
+                    np.testing.assert_array_equal(raw2[off[i] + oc: off[i] + oc + m], ref2[o2:o2 + m],
+                                                  err_msg=f"{case} q{i} B")
+                    o2 += m
+            oc += m
+        assert o1 == len(ref1)
+
+
+@pytest.mark.parametrize("metric", ["ip", "cosine", "euclidean"])
+@pytest.mark.parametrize("entry", ["host", "device"])
+def test_nonfinite_batch_fused_routing(pkg, tmp_path, metric, entry):
+    """A 64-query batch with one NaN (w = 1: the fused argmin routing, > 32 queries so
+    the GEMM path runs): DataError, and the handle keeps working afterwards."""
+    from index_writer import random_index
+
+    blob = random_index(96, 32, 8, 12, 900, metric, seed=5)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "nan", blob))
+    q = np.random.default_rng(3).standard_normal((64, 96)).astype(F32)
+    good = dev.search_host(q, 10, 1, 50, True)
+    bad = q.copy()
+    bad[17, 3] = np.nan
+    bad_inf = q.copy()
+    bad_inf[40, 0] = np.inf
+    for b in (bad, bad_inf):
+        if entry == "host":
+            with pytest.raises(pkg.DataError):
+                dev.search_host(b, 10, 1, 50, True)
+        else:
+            with pytest.raises(pkg.DataError):
+                pkg.query_batch(dev, torch.from_numpy(b).cuda(), pkg.QueryParams(k=10, w=1, t=50))
+        # the next search on the same handle succeeds and is unchanged
+        again = dev.search_host(q, 10, 1, 50, True)
+        for a, e in zip(again, good):
+            np.testing.assert_array_equal(a, e)
+    # the device entry itself (no host check) must not fault on the NaN row either
+    ids, sc, cnt = dev.search_device(torch.from_numpy(bad).cuda(), 10, 1, 50, True)
+    torch.cuda.synchronize()
+    ok = np.ones(64, bool)
+    ok[17] = False
+    np.testing.assert_array_equal(ids.cpu().numpy()[ok], good[0][ok])
+
+
 # ---------------------------------------------------- unquantized (f32) factors
 # score = x @ A (@ B) runs as OpenBLAS sgemv in the reference (rrr.py:97-100), an
 # FMA order the GPU cannot reproduce (SURVEY.md 8(c)), so the approximate scores
@@ -328,7 +400,7 @@ def test_exactness_limit_recall_one(pkg, tmp_path):
 
 
 def _workload(pkg, name):
-    from paper_2410_18926_b200 import workloads as W
+    import workloads as W
 
     try:
         path = W.materialize_index(name)
@@ -598,9 +670,11 @@ def test_sliced_projection_equals_dmma(pkg, tmp_path, d, s, monkeypatch):
     q[2, 5] = 1e-30
     xq = torch.from_numpy(q).cuda()
     monkeypatch.setenv("RRG_GEMM", "dmma")
+    dev.reload_options()  # variant switches are resolved per index, not per call
     ref = dev.stage_project(xq)[0].cpu().numpy()
     ref_sel = dev.stage_route(torch.from_numpy(ref).cuda(), 3).cpu().numpy()
     monkeypatch.setenv("RRG_GEMM", "sliced")
+    dev.reload_options()
     got = dev.stage_project(xq)[0].cpu().numpy()
     np.testing.assert_array_equal(got.view(np.int32), ref.view(np.int32))
     sel = dev.stage_route(torch.from_numpy(got).cuda(), 3).cpu().numpy()

@@ -102,7 +102,7 @@ def test_c2_ground_truth_matches_cpu(pkg):
     """Full C2 (1M x 768, 10k queries, k=100) vs the CPU exact ground truth of tools/build_index.py."""
     import torch
 
-    from paper_2410_18926_b200 import workloads as W
+    import workloads as W
 
     gt = W.load_ground_truth("c2")
     if gt is None:

@@ -56,12 +56,17 @@ def test_oracle_stage_traces(case):
         head, scale, codes = O.q8(xp)
         assert head == g[f"trace{qi}_qhead"] and scale == g[f"trace{qi}_qscale"]
         np.testing.assert_array_equal(codes, g[f"trace{qi}_qcodes"])
-        raws, scores = [], []
+        raws, raws2, scores = [], [], []
         for l in sel:
             cl = idx.clusters[int(l)]
             raws.append(O.int8_dot(codes, cl.a.values))
-            scores.append(O.score_cluster(xp, (head, scale, codes), cl, idx.metric))
+            tr = {}
+            scores.append(O.score_cluster(xp, (head, scale, codes), cl, idx.metric, trace=tr))
+            if "raw2" in tr:
+                raws2.append(tr["raw2"])
         np.testing.assert_array_equal(np.concatenate(raws), g[f"trace{qi}_raw1"])
+        np.testing.assert_array_equal(np.concatenate(raws2) if raws2 else np.zeros(0, np.int32),
+                                      g[f"trace{qi}_raw2"])
         np.testing.assert_array_equal(np.concatenate(scores).view(np.int32),
                                       g[f"trace{qi}_scores"].view(np.int32))
 

@@ -32,7 +32,7 @@ import numpy as np
 sys.path.insert(0, "/root/reference/pkg/src")
 sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 
-from paper_2410_18926_b200 import workloads as W  # noqa: E402
+import workloads as W  # noqa: E402
 
 
 def exact_gt(corpus: np.ndarray, queries: np.ndarray, k: int, chunk: int = 256) -> np.ndarray:

@@ -1,6 +1,7 @@
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
-from paper_2410_18926_b200 import DeviceIndex, workloads as W
+from paper_2410_18926_b200 import DeviceIndex
+import workloads as W
 path = W.materialize_index('c2'); dev = DeviceIndex.from_file(path)
 q = W.load_queries('c2'); k, w, t = 100, 1, 800
 qp = torch.from_numpy(q).pin_memory().numpy()

@@ -3,8 +3,9 @@ import sys, time
 from pathlib import Path
 import numpy as np
 import torch
-sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
-from paper_2410_18926_b200 import DeviceIndex, workloads as W
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+from paper_2410_18926_b200 import DeviceIndex
+import workloads as W
 
 path = W.materialize_index("c2")
 dev = DeviceIndex.from_file(path)

@@ -1,7 +1,7 @@
 import sys, time, numpy as np, torch
 sys.path.insert(0, '.')
 import paper_2410_18926_b200 as pkg
-from paper_2410_18926_b200 import workloads as W
+import workloads as W
 man = W.load_manifest('c2'); g = man['generator']
 c, q = W.synth_clustered(g['m'], g['n_queries'], g['d'], g['seed'], g['n_blobs'])
 cd = torch.from_numpy(c).cuda(); qd = torch.from_numpy(q).cuda()

@@ -65,7 +65,7 @@ def main():
     import torch
 
     from paper_2410_18926_b200 import DeviceIndex
-    from paper_2410_18926_b200 import workloads as W
+    import workloads as W
 
     man = W.load_manifest(args.workload)
     k = man["k"]

@@ -28,7 +28,7 @@ import numpy as np
 
 F32 = np.float32
 
-REPO_ROOT = Path(__file__).resolve().parent.parent
+REPO_ROOT = Path(__file__).resolve().parent
 DATA_DIR = REPO_ROOT / "data"
 
 # Workload registry: name -> generator / index parameters.  C1 and C2 follow

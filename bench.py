@@ -444,35 +444,60 @@ def main():
     # ---- per-stage device time (events around each launch inside librrg), separate pass
     import ctypes
     _native.lib.rrg_set_stage_timing(1)
-    stage_ms = (ctypes.c_double * 9)()
-    stage_n = (ctypes.c_int64 * 9)()
+    stage_ms = (ctypes.c_double * 10)()
+    stage_n = (ctypes.c_int64 * 10)()
+    counters = (ctypes.c_int64 * 8)()
+    _native.lib.rrg_search_counters(counters)  # reset
     _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
     for i in range(args.steps):
         flush.fill_(i & 0xFF)
         searcher.device_step(q, out)
     _native.lib.rrg_stage_times(stage_ms, stage_n)
+    _native.lib.rrg_search_counters(counters)
     _native.lib.rrg_set_stage_timing(0)
     names = ["project", "quantize", "route_dist", "route_select", "select_topt", "rerank", "bucket",
-             "cluster_score"]
+             "cluster_score", "ground_truth", "screen"]
     stages = {nm: round(stage_ms[i] / args.steps, 4) for i, nm in enumerate(names)}
 
-    # ---- roofline of the dominant kernel (rerank): algorithmic bytes / launch time
+    # ---- roofline of the dominant stage (the re-rank: screen + exact pass + final top-k).
+    # Algorithmic bytes are the bytes the design must move per launch, counted by the
+    # library itself (rrg_search_counters, same steps): the fp16 residual rows the
+    # screen streams (each probed cluster's rows once per query group), the DISTINCT
+    # f32 corpus rows the exact pass needs (union over each cluster's queries), the
+    # queries, the bounds and the results.  SURVEY 8(d)'s per-query Q*t*d*4 is reported
+    # beside it (gathered bytes): rows shared by a cluster's queries cross HBM once.
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
     peak = peaks.get("hbm_gbs", 6650.0)
-    cand = dev_cand_counts(dev, q, k, w, t)
-    rerank_bytes = cand * d * 4 + nq * d * 4 + nq * k * 12 + nq * t * 4
-    rr_ms = stages["rerank"]
-    achieved = rerank_bytes / (rr_ms / 1e3) / 1e9 if rr_ms > 0 else None
-    traffic, rr_kernel = None, "k_rerank_cluster"
+    cnt = [counters[i] / args.steps for i in range(8)]
+    kc = (d + 15) // 16
+    screen_bytes = cnt[2] * (kc * 16 * 2 + 24) + cnt[0] * 12  # rows + row bounds terms; ub/lb write + read
+    exact_rows = cnt[4]
+    exact_bytes = exact_rows * d * 4 + nq * d * 4 + nq * k * 12 + nq * t * 4
+    rr_ms = stages["rerank"] + stages["screen"]
+    alg = screen_bytes + exact_bytes
+    achieved = alg / (rr_ms / 1e3) / 1e9 if rr_ms > 0 else None
+    traffic, rr_kernel = None, "k_rr_screen + k_rr_thresh + k_rerank_cluster + k_topk_final_warp"
     tf = ROOT / "profiles" / f"{args.workload}_rerank_traffic.json"
     if tf.exists():
         tinfo = json.loads(tf.read_text())
         traffic, rr_kernel = tinfo.get("bytes_per_launch"), tinfo.get("kernel", rr_kernel)
+    cand = dev_cand_counts(dev, q, k, w, t)
+    gathered = cand * d * 4 + nq * d * 4 + nq * k * 12
     # the exact NumPy-order distance needs one sub, one mul and one add per element,
-    # none fusable: Q*t_eff*d*3 FP32 lane-ops on 148 SMs x 128 lanes at the max clock
-    fp32_ops = 3 * cand * d
+    # none fusable: FP32 lane-ops of the candidates re-ranked exactly (the survivors)
+    exact_cands = cnt[1] if cnt[1] else cand
+    fp32_ops = 3 * exact_cands * d
     fp32_peak = 148 * 128 * 1.965e9
-    fp32_frac = fp32_ops / (rr_ms / 1e3) / fp32_peak if rr_ms > 0 else None
+    fp32_frac = fp32_ops / (stages["rerank"] / 1e3) / fp32_peak if stages["rerank"] > 0 else None
+    rr_detail = {
+        "screen": {"ms": stages["screen"], "rows_streamed": cnt[2], "bytes": int(screen_bytes),
+                   "gbs": screen_bytes / (stages["screen"] / 1e3) / 1e9 if stages["screen"] > 0 else None,
+                   "candidates": cnt[0], "survivors": cnt[1]},
+        "exact": {"ms": stages["rerank"], "rows_fetched": cnt[3], "distinct_rows": exact_rows,
+                  "bytes": int(exact_bytes),
+                  "gbs": exact_bytes / (stages["rerank"] / 1e3) / 1e9 if stages["rerank"] > 0 else None},
+        "gathered_bytes_per_query_rows": int(gathered),
+    }
 
     # ---- e2e through the C ABI host entry: pinned host queries in, results out, per step
     qpin = torch.from_numpy(q_host).pin_memory().numpy()
@@ -596,15 +621,16 @@ def main():
             "parity": parity,
             "gpu_launches": int(launches_per_step * args.steps),
             "stage_ms": stages,
-            "roofline": {"bound": "hbm", "kernel": rr_kernel + " (+ k_topk_final)",
+            "roofline": {"bound": "hbm", "kernel": rr_kernel, "ms": rr_ms,
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak if achieved else None, "traffic": traffic,
-                         "algorithmic_bytes_per_launch": int(rerank_bytes),
+                         "algorithmic_bytes_per_launch": int(alg),
                          "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback",
-                         "note": "algorithmic bytes count each query's t candidate rows "
-                                 "(SURVEY 8(d)); rows are shared by the queries of a cluster "
-                                 "bucket, so DRAM traffic (traffic) is far lower and the "
-                                 "kernel is bound by the exact FP32 arithmetic",
+                         "note": "algorithmic bytes = fp16 residual rows streamed by the screen "
+                                 "+ distinct f32 rows the exact pass needs + queries, bounds and "
+                                 "results (library counters); gathered_bytes_per_query_rows is "
+                                 "SURVEY 8(d)'s Q*t*d*4 form",
+                         "stages": rr_detail,
                          "fp32_pipe": {"ops_per_launch": int(fp32_ops), "frac": fp32_frac,
                                        "peak_lane_ops_per_s": fp32_peak}},
             "cpu_baseline": cpu,

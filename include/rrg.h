@@ -241,13 +241,23 @@ int64_t rrg_last_launch_count(void);
  * 0 project, 1 prep/quantize, 2 route distances, 3 route select,
  * 4 top-t selection (query-major mode: scoring + top-t), 5 rerank+top-k,
  * 6 query bucketing, 7 cluster-major scoring (pair bucketing + scoring),
- * 8 ground truth (rrg_ground_truth launches).
+ * 8 ground truth (rrg_ground_truth launches), 9 re-rank screen (bounds + thresholds).
  * rrg_stage_times synchronizes the recorded events, writes the accumulated
  * milliseconds and launch counts per stage (arrays of RRG_N_STAGES) and resets
  * the accumulators. */
-#define RRG_N_STAGES 9
+#define RRG_N_STAGES 10
 void rrg_set_stage_timing(int enabled);
 int rrg_stage_times(double* ms, int64_t* launches);
+
+/* Re-rank work counters accumulated by the searches of this thread while stage timing
+ * is enabled (the roofline's algorithmic bytes come from these): returns and resets
+ *   0 candidates entering the screen (sum over queries of the top-t size)
+ *   1 candidates surviving the screen (re-ranked exactly)
+ *   2 rows streamed by the screen (fp16 residual rows, 128-row blocks)
+ *   3 corpus rows fetched by the cluster-major exact re-rank (f32 rows)
+ *   4 distinct corpus rows the exact pass needs (union over each cluster's queries) */
+#define RRG_N_COUNTERS 8
+int rrg_search_counters(int64_t* out);
 
 const char* rrg_last_error(void);
 const char* rrg_last_error_kind(void); /* "ShapeError", "ParameterError", ... */

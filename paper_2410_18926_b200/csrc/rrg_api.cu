@@ -41,6 +41,8 @@ struct StageTimer {
   double ms[RRG_N_STAGES] = {0};
   int64_t n[RRG_N_STAGES] = {0};
   std::vector<cudaEvent_t> pool;
+  int64_t* dcounters = nullptr;  // device counters (rrg_search_counters), while timing is on
+  int cdev = -1;
   cudaEvent_t get() {
     if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
     cudaEvent_t e;
@@ -51,6 +53,21 @@ struct StageTimer {
 thread_local StageTimer g_timer;
 
 [[noreturn]] void launch_failed(int stage, cudaError_t e);
+
+// Work counters of the re-rank (rrg_search_counters), collected while stage timing is
+// enabled; nullptr otherwise, so the search path never touches them.
+int64_t* counters_ptr(cudaStream_t st) {
+  StageTimer& t = g_timer;
+  if (!t.on) return nullptr;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (t.dcounters == nullptr || t.cdev != dev) {
+    if (cudaMalloc(&t.dcounters, RRG_N_COUNTERS * 8) != cudaSuccess) return t.dcounters = nullptr;
+    cudaMemsetAsync(t.dcounters, 0, RRG_N_COUNTERS * 8, st);
+    t.cdev = dev;
+  }
+  return t.dcounters;
+}
 
 // Runs one launch, counting it and (when enabled) bracketing it with events; a launch
 // rejected at submission (bad grid / shared-memory size) fails here, naming its stage.
@@ -437,6 +454,24 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
     fill_corpus(corp, d_pos, (int)v.d_stride, d_perm);
     v.corpus = corp;
   }
+  v.scr_plane = nullptr; v.scr_blk0 = nullptr; v.scr_mu = nullptr; v.scr_rr = nullptr;
+  v.scr_rmeta = nullptr; v.scr_kc = 0;
+  if (has_corpus && hm.metric == kMetricEuclidean && d <= screen_max_dim() && v.opt.screen != 0 && P > 0) {
+    // re-rank screen data (rrg_screen.cu): clusters padded to 128-row blocks
+    std::vector<int> blk0(L + 1, 0);
+    for (int l = 0; l < L; ++l) blk0[l + 1] = blk0[l] + (int)((ix->held_sizes[l] + 127) / 128);
+    v.scr_kc = (d + 15) / 16;
+    const size_t plane_bytes = (size_t)blk0[L] * v.scr_kc * 128 * 32;
+    uint16_t* plane = static_cast<uint16_t*>(ix->dalloc(plane_bytes));
+    float* mu = static_cast<float*>(ix->dalloc((size_t)L * d * 4));
+    double* rr = static_cast<double*>(ix->dalloc((size_t)P * 8));
+    float4* meta = static_cast<float4*>(ix->dalloc((size_t)P * 16));
+    v.scr_blk0 = ix->upload(blk0);
+    launch_screen_build(v, mu, plane, plane_bytes, rr, meta, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    v.scr_plane = plane; v.scr_mu = mu; v.scr_rr = rr; v.scr_rmeta = meta;
+  }
   ix->info.metric = hm.metric; ix->info.dim = d; ix->info.reduced_dim = s; ix->info.rank = r;
   ix->info.n_clusters = L; ix->info.n_points = hm.m; ix->info.flags = hm.flags;
   ix->info.n_exact_clusters = ix->n_exact;
@@ -776,6 +811,11 @@ struct Plan {
   int rr_mode;
   int mwords;
   size_t off_cidx, off_marks, marks_bytes, off_rritem;
+  // re-rank screen (rr_mode == 1, euclidean)
+  size_t off_xint;
+  bool screen;
+  int n_groups_max;
+  size_t off_ub, off_lb, off_scritem, off_grpoff, off_grec;
 };
 
 Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
@@ -845,6 +885,7 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     p.off_keys = carve(Q * std::max<int64_t>(nmax, 1) * 4);
     p.off_ctr = carve(16);
   }
+  p.screen = false;
   // re-rank strategy: cluster-major (rows of a cluster shared by its queries) when
   // the scoring is cluster-major and the row plan fits k_rerank_cluster;
   // RRG_RERANK=query|regs|tma forces a per-query kernel
@@ -876,6 +917,20 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     p.marks_bytes = ((size_t)Q * std::max<int64_t>(nmax, 1) / 32 + 2) * 4;
     p.off_marks = carve(p.marks_bytes);
     p.off_rritem = carve((L + 1) * 4);
+    // tensor-core screen of the re-rank (rrg_screen.cu): worth it once most of a query's
+    // t candidates cannot reach its top k (t >= 2k); RRG_SCREEN=1 forces, 0 disables
+    p.screen = v.scr_plane != nullptr && v.metric == kMetricEuclidean &&
+               (v.opt.screen == 1 || (v.opt.screen < 0 && t >= 2 * k));
+    p.off_xint = carve(Q * (int64_t)v.d_stride * 4);
+    if (p.screen) {
+      p.off_ub = carve(Q * std::max<int64_t>(nmax, 1) * 4);
+      p.off_lb = carve(Q * std::max<int64_t>(nmax, 1) * 4);
+      p.off_scritem = carve((L + 1) * 4);
+      p.off_grpoff = carve((L + 1) * 4);
+      const int64_t pairs = Q * (int64_t)w;
+      p.n_groups_max = (int)std::max<int64_t>(1, (pairs + 15 * std::min<int64_t>(L, pairs)) / kRrQ);
+      p.off_grec = carve((size_t)p.n_groups_max * screen_group_bytes(v.scr_kc));
+    }
   }
   p.total = o;
   return p;
@@ -1035,6 +1090,20 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         th.marks = marks;
       }
       staged(4, st, [&] { launch_select_topt(th, n, st); });
+      if (p.screen) {
+        ScreenHost sh{};
+        sh.ix = v; sh.queries = x; sh.w = w; sh.qoff = ch.qoff; sh.pair_off = ch.pair_off;
+        sh.pairs = ch.pairs; sh.kbase = ch.kbase; sh.marks = marks;
+        sh.item_off = reinterpret_cast<int*>(base + p.off_scritem);
+        sh.grp_off = reinterpret_cast<int*>(base + p.off_grpoff);
+        sh.grec = reinterpret_cast<unsigned char*>(base + p.off_grec);
+        sh.n_groups_max = p.n_groups_max;
+        sh.ub = reinterpret_cast<float*>(base + p.off_ub);
+        sh.lb = reinterpret_cast<float*>(base + p.off_lb);
+        sh.cand_idx = cidx; sh.cand_n = cn; sh.take_cap = p.take_cap; sh.k = k; sh.diss = ch.keys;
+        sh.counters = counters_ptr(st);
+        staged(9, st, [&] { launch_screen(sh, n, st); });
+      }
       if (p.rr_mode == 1) {
         // scores are consumed: the key array is reused for the re-ranked distances
         ClusterRerankHost rh{};
@@ -1045,6 +1114,14 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         // sparse selections (a query keeps < half of the rows its probes cover, taking
         // cluster sizes as a random query sees them): skip unselected row pairs
         rh.skip = v.opt.rr_skip >= 0 ? v.opt.rr_skip != 0 : (double)t < 0.5 * w * ix->m_biased;
+        rh.compact = p.screen;
+        if (p.screen) { rh.cand_idx = cidx; rh.cand_n = cn; rh.take_cap = p.take_cap; }
+        rh.xint = reinterpret_cast<float*>(base + p.off_xint);
+        staged(5, st, [&] { launch_interleave_queries(v, x, n, reinterpret_cast<float*>(base + p.off_xint), st); });
+        rh.counters = counters_ptr(st);
+        if (rh.counters)  // rows the exact pass needs: union over each cluster's queries
+          launch_count_rows(v, ch.pair_off, ch.pairs, ch.kbase, ch.qoff, w, marks,
+                            p.screen ? cidx : nullptr, cn, p.take_cap, p.mwords, rh.counters + 4, st);
         staged(5, st, [&] { launch_cluster_rerank(rh, st); });
         TopkFinalHost fh{};
         fh.ix = v; fh.sel = sel; fh.w = w; fh.qoff = ch.qoff; fh.kbase = ch.kbase; fh.diss = ch.keys;
@@ -1765,6 +1842,20 @@ int rrg_merge_results(int64_t nq, int32_t G, int32_t k, int32_t metric, const fl
 }
 
 int64_t rrg_last_launch_count(void) { return g_launches; }
+
+int rrg_search_counters(int64_t* out) {
+  StageTimer& t = g_timer;
+  for (int i = 0; i < RRG_N_COUNTERS; ++i) out[i] = 0;
+  if (t.dcounters == nullptr) return RRG_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(t.cdev);
+  cudaDeviceSynchronize();
+  cudaMemcpy(out, t.dcounters, RRG_N_COUNTERS * 8, cudaMemcpyDeviceToHost);
+  cudaMemset(t.dcounters, 0, RRG_N_COUNTERS * 8);
+  cudaSetDevice(prev);
+  return RRG_OK;
+}
 
 void rrg_set_stage_timing(int enabled) { g_timer.on = enabled != 0; }
 

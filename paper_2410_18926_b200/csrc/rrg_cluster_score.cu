@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "rrg_common.cuh"
@@ -1043,6 +1044,10 @@ constexpr int kRrRows = RRG_RR_ROWS;  // rows of the cluster per work item (larg
 struct ClusterRerankArgs {
   DevIndexView ix;
   const float* queries;  // chunk-local [nq][d]
+  const float* xint;     // the same queries interleaved like the corpus rows [nq][d_stride]
+  const int* cand_idx;   // k_rerank_sparse: the screen's survivors per query
+  const int* cand_n;
+  int take_cap;
   int w;
   const int* qoff;
   const int* pair_off;
@@ -1055,6 +1060,7 @@ struct ClusterRerankArgs {
   int* work_counter;
   int mwords;  // bitmap words staged per query (>= ceil(max m_l / 32) + 1)
   float neg_zero;  // -0.0f at run time: see sq2()
+  int64_t* counters;  // rrg_search_counters (nullptr unless enabled): [3] += rows fetched
 };
 
 // rr_item_off for the re-rank work items (one CTA)
@@ -1069,6 +1075,26 @@ __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_o
   __syncthreads();
   block_exclusive_scan_inplace(rr_item_off, L, &tot);
   if (threadIdx.x == 0) rr_item_off[L] = tot;
+}
+
+__global__ void k_interleave_queries(DevIndexView ix, const float* __restrict__ x, int nq,
+                                     float* __restrict__ xint) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t m = (int64_t)nq * ix.d;  // elem_perm is a permutation of [0, d)
+  for (int64_t i = t0; i < m; i += stride) {
+    const int64_t q = i / ix.d;
+    const int j = (int)(i - q * ix.d);
+    xint[q * ix.d_stride + (ix.elem_perm ? __ldg(ix.elem_perm + j) : j)] = __ldg(x + i);
+  }
+  const int pad = ix.d_stride - ix.d;  // slots [d, d_stride) of every row: zero
+  for (int64_t i = t0; i < (int64_t)nq * pad; i += stride) xint[(i / pad) * ix.d_stride + ix.d + i % pad] = 0.f;
+}
+
+void launch_interleave_queries(const DevIndexView& ix, const float* queries, int nq, float* xint,
+                               cudaStream_t st) {
+  const int64_t n = (int64_t)nq * ix.d_stride;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  (k_interleave_queries<<<blocks, 256, 0, st>>>(ix, queries, nq, xint), note_launch());
 }
 
 void launch_rr_items(const int* pair_off, const int* cl_pos, int L, int rows, int* item_off,
@@ -1157,7 +1183,25 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
     const int mw = (m + 31) / 32;
     for (int g0 = 0; g0 < np; g0 += kRrQ) {
       const int ng = min(kRrQ, np - g0);
-      {  // stage x (interleaved): SU independent loads in flight per thread
+      if (a.xint) {  // stage x: pre-interleaved rows, 16-byte loads, 4 in flight per thread
+        constexpr int SU = 4;
+        const int n4 = ds / 4, tot = ng * n4;
+        float4* xs4 = reinterpret_cast<float4*>(xs);
+        for (int e0 = tid; e0 < tot; e0 += XNT * SU) {
+          float4 xv[SU];
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            const int e = e0 + u * XNT;
+            if (e < tot) {
+              const int g = e / n4, j = e - g * n4;
+              xv[u] = __ldg(reinterpret_cast<const float4*>(a.xint + (size_t)pq[g0 + g] * ds) + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < SU; ++u)
+            if (e0 + u * XNT < tot) xs4[e0 + u * XNT] = xv[u];
+        }
+      } else {  // stage x (interleaved): SU independent loads in flight per thread
         constexpr int SU = 4;
         const int tot = ng * d;
         for (int e0 = tid; e0 < tot; e0 += XNT * SU) {
@@ -1296,9 +1340,11 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
       };
       int ia = next_marked(warp * 2);
       if (ia < n_idx) load_pair(ia);
+      int nfetch = 0;
       for (; ia < n_idx;) {
         const int pa = row_of(ia);
         const int pb = ia + 1 < n_idx ? row_of(ia + 1) : pa;
+        nfetch += pb != pa ? 2 : 1;
         const int pn = next_marked(ia + nwarps * 2);
         // the queries that selected either row (one lane per query, ballot)
         const bool mine = lane < ng && (marked(lane, pa) || marked(lane, pb));
@@ -1365,8 +1411,226 @@ __global__ void __launch_bounds__(XNT, kCmCtas) k_rerank_cluster(ClusterRerankAr
         __syncwarp();
         ia = pn;
       }
+      if (a.counters && lane == 0 && nfetch)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 3), (unsigned long long)nfetch);
       __syncthreads();
     }
+  }
+}
+
+// ------------------------------------------------- sparse exact re-rank (screened)
+// After the tensor-core screen about k of a query's t candidates survive (C2: 114 of
+// 800), so a work item's rows are each wanted by one or a few of its queries.  Here a
+// warp takes ONE listed row at a time (the next row's loads in flight meanwhile),
+// forms this lane's pairwise partial for every query that kept the row, and reduces
+// the P (next power of two of the active count) values with a P-way transposing
+// butterfly: (P - 1) + (5 - log2 P) shuffles instead of 31 for a full 16-slot pair,
+// and no arithmetic for queries that did not keep the row.  Same summation tree as
+// k_rerank_cluster (NumPy's, bit-exact).
+template <int P, int N>
+__device__ __forceinline__ float reduce_p(float (&v)[N], int lane) {
+  // transposing levels: lane bits 0..log2(P)-1 end up indexing the value they hold
+#pragma unroll
+  for (int s = 0; (1 << s) < P; ++s) {
+    const int o = 1 << s;
+    const bool hi = (lane >> s) & 1;
+#pragma unroll
+    for (int i = 0; i < (P >> (s + 1)); ++i) {
+      const float keep = hi ? v[2 * i + 1] : v[2 * i];
+      const float send = hi ? v[2 * i] : v[2 * i + 1];
+      v[i] = __fadd_rn(keep, __shfl_xor_sync(0xffffffffu, send, o));
+    }
+  }
+  float r = v[0];
+#pragma unroll
+  for (int o = P; o < 32; o <<= 1) r = __fadd_rn(r, __shfl_xor_sync(0xffffffffu, r, o));
+  return r;
+}
+template <int N>
+__device__ __forceinline__ float reduce_any(float (&v)[N], int nval, int lane) {
+  if (nval <= 1) return reduce_p<1>(v, lane);
+  if (nval <= 2) return reduce_p<2>(v, lane);
+  if (nval <= 4) return reduce_p<4>(v, lane);
+  if (nval <= 8) return reduce_p<8>(v, lane);
+  if (N >= 32 && nval > 16) return reduce_p<(N >= 32 ? 32 : 16)>(v, lane);
+  return reduce_p<16>(v, lane);
+}
+
+constexpr int SNT = 256;
+constexpr int kSpRows = 512;
+template <int NB, int NH>
+__global__ void __launch_bounds__(SNT, NH == 1 ? 2 : 1) k_rerank_sparse(ClusterRerankArgs a) {
+  constexpr int NLV = 8 * NH, cstep = 8 * NLV;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const DevIndexView& ix = a.ix;
+  const int ds = ix.d_stride;
+  float* xs = reinterpret_cast<float*>(smem_raw);                       // [kRrQ][ds]
+  uint32_t* mb = reinterpret_cast<uint32_t*>(xs + (size_t)kRrQ * ds);  // [kRrQ][mwords]
+  __shared__ int item_s, nrows_s;
+  __shared__ int pq[kRrQ], pkey[kRrQ], pofs[kRrQ];
+  __shared__ int rowlist[kSpRows];
+  __shared__ int slotg[SNT / 32][kRrQ];
+  const int L = ix.L;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = SNT / 32;
+  const int b = lane >> 2, h = lane & 3;
+  const int coff = 8 * b + 2 * h;
+  const float2 nz2 = make_float2(a.neg_zero, a.neg_zero);
+  const int total_items = a.rr_item_off[L];
+  while (true) {
+    if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = item_s;
+    __syncthreads();
+    if (item >= total_items) break;
+    int lo = 0, hi = L;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.rr_item_off[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int l = lo;
+    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    const int nrc = (m + a.rr_rows - 1) / a.rr_rows;
+    const int local = item - a.rr_item_off[l];
+    const int qc = nrc > 0 ? local / nrc : 0, rc = nrc > 0 ? local % nrc : 0;
+    const int j0 = a.pair_off[l] + qc * kRrQ;
+    const int ng = min(kRrQ, a.pair_off[l + 1] - j0);
+    const int r0 = rc * a.rr_rows, r1 = min(m, r0 + a.rr_rows);
+    if (tid < ng) {
+      const int pr = a.pairs[j0 + tid];
+      const int q = pr / a.w, c = pr % a.w;
+      pq[tid] = q;
+      pofs[tid] = a.qoff[(size_t)q * (a.w + 1) + c];
+      pkey[tid] = a.kbase[q] + pofs[tid];
+    }
+    __syncthreads();
+    if (m == 0) continue;
+    {  // x of the item's queries (pre-interleaved): 16-byte loads, 4 in flight per thread
+      constexpr int SU = 4;
+      const int n4 = ds / 4, tot = ng * n4;
+      float4* xs4 = reinterpret_cast<float4*>(xs);
+      for (int e0 = tid; e0 < tot; e0 += SNT * SU) {
+        float4 xv[SU];
+#pragma unroll
+        for (int u = 0; u < SU; ++u) {
+          const int e = e0 + u * SNT;
+          if (e < tot) {
+            const int g = e / n4, j = e - g * n4;
+            xv[u] = __ldg(reinterpret_cast<const float4*>(a.xint + (size_t)pq[g] * ds) + j);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < SU; ++u)
+          if (e0 + u * SNT < tot) xs4[e0 + u * SNT] = xv[u];
+      }
+    }
+    // membership bits of the item's rows [r0, r1) (word k covers rows 32k..32k+31): the
+    // screen's survivors of each slot's query that fall in this probe's rows
+    const int k0 = r0 >> 5, k1 = (r1 - 1) >> 5, nwd = k1 - k0 + 1;
+    for (int e = tid; e < ng * nwd; e += SNT) {
+      const int g = e / nwd, k = k0 + e - g * nwd;
+      mb[g * a.mwords + k] = 0;
+    }
+    __syncthreads();
+    for (int g = warp; g < ng; g += nwarps) {
+      const int q = pq[g], off = pofs[g], n = a.cand_n[q];
+      const int* list = a.cand_idx + (size_t)q * a.take_cap;
+      for (int i = lane; i < n; i += 32) {
+        const int row = __ldg(list + i) - off;
+        if (row >= r0 && row < r1) atomicOr(mb + g * a.mwords + (row >> 5), 1u << (row & 31));
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // list the rows any query of the item kept
+      int base_n = 0;
+      for (int kk = k0; kk <= k1; kk += 32) {
+        const int k = kk + lane;
+        uint32_t u = 0;
+        if (k <= k1) {
+          for (int g = 0; g < ng; ++g) u |= mb[g * a.mwords + k];
+          if (k == k0) u &= 0xffffffffu << (r0 & 31);
+          if (k == k1) u &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
+        }
+        const int cnt = __popc(u);
+        int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        int at = base_n + incl - cnt;
+        while (u) {
+          const int bb = __ffs(u) - 1;
+          u &= u - 1;
+          rowlist[at++] = 32 * k + bb;
+        }
+        base_n += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) nrows_s = base_n;
+    }
+    __syncthreads();
+    const int nrows = nrows_s;
+    float2 c[NH][NB], cn[NH][NB];
+    auto load_row = [&](int ia, float2 (&dst)[NH][NB]) {
+      const float* ra = ix.corpus + (size_t)(p0 + rowlist[ia]) * ds + coff;
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) dst[hh][i] = __ldg(reinterpret_cast<const float2*>(ra + 64 * hh + cstep * i));
+    };
+    int ia = warp;
+    if (ia < nrows) load_row(ia, c);
+    int nfetch = 0;
+    for (; ia < nrows; ia += nwarps) {
+      const int row = rowlist[ia];
+      if (ia + nwarps < nrows) load_row(ia + nwarps, cn);
+      ++nfetch;
+      // queries that kept this row, in slot order
+      const bool mine = lane < ng && ((mb[lane * a.mwords + (row >> 5)] >> (row & 31)) & 1u);
+      const unsigned act = __ballot_sync(0xffffffffu, mine);
+      const int nact = __popc(act);
+      if (mine) slotg[warp][__popc(act & ((1u << lane) - 1u))] = lane;
+      __syncwarp();
+      // value NH * s + hh: this lane's partial of half hh of the s-th active query
+      float v[NH * kRrQ];
+      unsigned rem = act;
+#pragma unroll
+      for (int s = 0; s < kRrQ; ++s) {
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh) v[NH * s + hh] = 0.f;
+        if (rem) {  // warp-uniform
+          const int g = __ffs(rem) - 1;
+          rem &= rem - 1;
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh) {
+            const float* xg = xs + (size_t)g * ds + coff + 64 * hh;
+            float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+              const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
+              const float2 dd = __fadd2_rn(c[hh][i], make_float2(-xv.x, -xv.y));
+              const float2 sq = sq2(dd, nz2);
+              acc = i == 0 ? sq : __fadd2_rn(acc, sq);
+            }
+            v[NH * s + hh] = __fadd_rn(acc.x, acc.y);  // r[2h] + r[2h+1] of this lane
+          }
+        }
+      }
+      // lane j holds value j fully reduced; NH = 2: dist = pw(half 0) + pw(half 1)
+      float r = reduce_any<NH * kRrQ>(v, NH * nact, lane);
+      if (NH == 2) r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));
+      if (lane < NH * nact && lane % NH == 0) {
+        const int g = slotg[warp][lane / NH];
+        a.diss[pkey[g] + row] = mono32(r);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+        for (int i = 0; i < NB; ++i) c[hh][i] = cn[hh][i];
+    }
+    if (a.counters && lane == 0 && nfetch)
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 3), (unsigned long long)nfetch);
+    __syncthreads();
   }
 }
 
@@ -1643,21 +1907,40 @@ bool cluster_rerank_ok(const DevIndexView& ix, int64_t max_cluster) {
 
 void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   ClusterRerankArgs a;
-  a.ix = h.ix; a.queries = h.queries; a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off;
+  a.ix = h.ix; a.queries = h.queries; a.xint = h.xint; a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off;
+  a.cand_idx = h.cand_idx; a.cand_n = h.cand_n; a.take_cap = h.take_cap;
   a.rr_item_off = h.rr_item_off; a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks;
   // rows per work item: 256 (few, long items) once the batch's (query, cluster) probes
   // give enough items to fill the GPU; 128 / 32 for small batches (one query's rows
   // spread over many CTAs: C2 batch 1, 4 -> 31 items)
   const int64_t probes = (int64_t)h.nq * h.w;
   a.rr_rows = probes >= 512 ? kRrRows : (probes >= 64 ? 128 : 32);
+  if (h.compact) a.rr_rows = std::min(a.rr_rows, kSpRows);
   (k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off), note_launch());
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   a.neg_zero = -0.0f;
+  a.counters = h.counters;
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
   const size_t sm = cluster_rerank_smem(h.ix, h.mwords);
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (h.compact && h.ix.metric == kMetricEuclidean) {  // screened: sparse per-row kernel
+    const size_t ssm = (size_t)kRrQ * h.ix.d_stride * 4 + (size_t)kRrQ * h.mwords * 4;
+#define RRG_SP(NB, NH, SLOT, CTAS)                                               \
+  do {                                                                           \
+    opt_in_smem(k_rerank_sparse<NB, NH>, SLOT);                                  \
+    (k_rerank_sparse<NB, NH><<<sms * (CTAS), SNT, ssm, st>>>(a), note_launch()); \
+  } while (0)
+    const int nb = h.ix.pw_leaf_n / 8;
+    if (h.ix.pw_nleaves == 16) {
+      if (nb == 12) RRG_SP(12, 2, 36, 1); else if (nb == 15) RRG_SP(15, 2, 37, 1); else RRG_SP(16, 2, 38, 1);
+    } else {
+      if (nb == 12) RRG_SP(12, 1, 39, 2); else if (nb == 15) RRG_SP(15, 1, 40, 2); else RRG_SP(16, 1, 41, 2);
+    }
+#undef RRG_SP
+    return;
+  }
 #define RRG_RR_LAUNCH(NB, AS, NH, RM, SLOT)                                      \
   do {                                                                           \
     opt_in_smem(k_rerank_cluster<NB, AS, NH, RM>, SLOT);                         \

@@ -138,9 +138,17 @@ constexpr int kRrQ = 16;  // queries of one work item (x staged at once; the scr
 // item_off[l] = ceil(pairs_l / kRrQ) * ceil(m_l / rows), exclusive scan, item_off[L] = total
 void launch_rr_items(const int* pair_off, const int* cl_pos, int L, int rows, int* item_off,
                      cudaStream_t st);
+// queries re-laid out like the corpus rows (interleaved for the pairwise plan), so the
+// cluster re-rank stages a work item's x with plain vector loads
+void launch_interleave_queries(const DevIndexView& ix, const float* queries, int nq, float* xint,
+                               cudaStream_t st);
 struct ClusterRerankHost {
   DevIndexView ix;
   const float* queries;
+  const float* xint = nullptr;  // [nq][d_stride] interleaved queries
+  const int* cand_idx = nullptr;  // screened: the survivors per query (membership source)
+  const int* cand_n = nullptr;
+  int take_cap = 0;
   int w;
   const int* qoff;
   const int* pair_off;
@@ -152,6 +160,7 @@ struct ClusterRerankHost {
   int* work_counter;
   bool skip;  // pass over row pairs no query of a work item selected (sparse selections)
   bool compact = false;  // list the selected rows first (after the screen: ~k of t survive)
+  int64_t* counters = nullptr;  // rrg_search_counters[3]: rows fetched
   int mwords;
   int nq;  // queries of the chunk (work-item sizing)
 };
@@ -164,6 +173,7 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st);
 // the removal of the candidates whose lower bound exceeds it (see the file header).
 int screen_max_dim();
 size_t screen_smem(int kc);
+size_t screen_group_bytes(int kc);
 void launch_screen_build(const DevIndexView& v, float* mu, uint16_t* plane, size_t plane_bytes,
                          double* rr, float4* meta, cudaStream_t st);
 struct ScreenHost {
@@ -176,18 +186,21 @@ struct ScreenHost {
   const int* kbase;
   uint32_t* marks;       // membership bits of the top-t (cleared for non-survivors)
   int* item_off;         // [L+1] scratch
+  int* grp_off;          // [L+1] scratch
+  unsigned char* grec;   // n_groups_max x screen_group_bytes(scr_kc) scratch
+  int n_groups_max;
   float* ub;             // per candidate bounds (key-array layout)
   float* lb;
-  const int* cand_idx;   // [nq][take_cap] top-t candidate indices
-  const int* cand_n;
+  int* cand_idx;         // [nq][take_cap] top-t candidate indices -> the survivors
+  int* cand_n;
   int take_cap, k;
-  uint32_t* diss;        // key array re-used for distances: non-survivors -> ~0u
+  uint32_t* diss;        // key array re-used for distances
   int64_t* counters;     // rrg_search_counters (nullptr unless enabled)
 };
 struct ThreshArgs {
   const int* kbase;
-  const int* cand_idx;
-  const int* cand_n;
+  int* cand_idx;  // compacted in place to the survivors
+  int* cand_n;
   int take_cap, k;
   const float* ub;
   const float* lb;
@@ -196,6 +209,10 @@ struct ThreshArgs {
   int64_t* counters;
 };
 void launch_screen(const ScreenHost& h, int nq, cudaStream_t st);
+// counter: distinct rows of every cluster marked by any of its queries
+void launch_count_rows(const DevIndexView& ix, const int* pair_off, const int* pairs, const int* kbase,
+                       const int* qoff, int w, const uint32_t* marks, const int* cand_idx, const int* cand_n,
+                       int take_cap, int mwords, int64_t* out, cudaStream_t st);
 
 struct TopkFinalHost {
   DevIndexView ix;

@@ -35,6 +35,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "rrg_common.cuh"
 #include "rrg_kernels.h"
 
@@ -43,14 +45,37 @@ namespace rrg {
 constexpr int kScrRows = 128;                   // rows per block = MMA M = TMEM lanes
 constexpr int kScrChunk = kScrRows * 32;        // bytes of one K = 16 chunk of a block
 constexpr int kScrStageChunks = 4;              // 16 KB per ring stage
-constexpr int kScrStages = 6;
+constexpr int kScrStagesMax = 12;              // ring depth: as many stages as shared memory allows
 constexpr int kScrStageBytes = kScrStageChunks * kScrChunk;
-constexpr int kScrRing = kScrStages * kScrStageBytes;  // 96 KB
+constexpr int kScrRingMin = 6 * kScrStageBytes;
 constexpr int kScrThreads = 192;                // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
-constexpr int kScrMaxKc = 128;                  // d <= 2048: two B tiles + the ring fit
+constexpr int kScrMaxKc = 120;                  // d <= 1920: two group records + the ring fit
+
+// Group record (one per (cluster, <= kRrQ queries) work group, built by k_rr_groups and
+// bulk-copied by the screen's producer): the queries' fp16 residual tile in the UMMA
+// K-major layout (N = kRrQ rows, 512 B per K chunk), then per slot the bound terms.
+struct GroupSlot {
+  double xx;   // ||x - mu_l||^2
+  double sc;   // 2^e_q
+  float nxh;   // ||x^'|| (scaled units, rounded up)
+  float nex;   // ||x'/2^e_q - x^'||
+  int pkey;    // key-array offset of the (query, probe) pair
+  int pad;
+};
+static_assert(sizeof(GroupSlot) == 32, "group slot layout");
+__host__ __device__ constexpr size_t grp_rec_bytes(int kc) {
+  return ((size_t)kc * 512 + kRrQ * sizeof(GroupSlot) + 16 + 127) / 128 * 128;
+}
 
 int screen_max_dim() { return kScrMaxKc * 16; }
-size_t screen_smem(int kc) { return (size_t)kScrRing + 2 * (size_t)kc * 512 + 1024; }
+// ring stages for a d: the two group records first, the rest of the CTA's shared memory
+// for the ring (d = 768: 10 stages = 160 KB in flight per SM; d = 1536: 8)
+int screen_stages(int kc) {
+  const int avail = (kMaxSmemPerCta - 4096 - 1024 - 2 * (int)grp_rec_bytes(kc)) / kScrStageBytes;
+  return std::max(1, std::min(kScrStagesMax, avail));
+}
+size_t screen_smem(int kc) { return (size_t)screen_stages(kc) * kScrStageBytes + 2 * grp_rec_bytes(kc) + 1024; }
+size_t screen_group_bytes(int kc) { return grp_rec_bytes(kc); }
 
 // halves offset of element e of row rr inside a block: chunk e/16, then the canonical
 // K-major no-swizzle core matrices (8 rows x 16 B; +128 B per K half, +256 B per 8 rows)
@@ -192,39 +217,109 @@ __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::aft
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+// Group records: block per (cluster, query group); warp per slot.  x' = x - mu_l in
+// f64, e_q with max|x'| / 2^e_q in [2^14, 2^15), x^' = fp16(x' / 2^e_q) into the tile,
+// and the norms the bound needs, from the stored values.
+__global__ void __launch_bounds__(512) k_rr_groups(DevIndexView ix, const float* __restrict__ queries, int w,
+                                                   const int* __restrict__ qoff, const int* __restrict__ pair_off,
+                                                   const int* __restrict__ pairs, const int* __restrict__ kbase,
+                                                   const int* __restrict__ grp_off, unsigned char* __restrict__ grec) {
+  const int gid = blockIdx.x;
+  const int L = ix.L, d = ix.d, KC = ix.scr_kc;
+  if (gid >= grp_off[L]) return;  // the grid is sized by an upper bound
+  int lo = 0, hi = L;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(grp_off + mid) <= gid) lo = mid; else hi = mid;
+  }
+  const int l = lo, gi = gid - grp_off[l];
+  const int j0 = pair_off[l] + gi * kRrQ;
+  const int ng = min(kRrQ, pair_off[l + 1] - j0);
+  unsigned char* rec = grec + (size_t)gid * grp_rec_bytes(KC);
+  uint16_t* bt = reinterpret_cast<uint16_t*>(rec);
+  GroupSlot* slots = reinterpret_cast<GroupSlot*>(rec + (size_t)KC * 512);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const float* mu = ix.scr_mu + (size_t)l * d;
+  for (int g = warp; g < kRrQ; g += blockDim.x >> 5) {
+    if (g >= ng) {  // unused slot: zero tile rows (their columns are never read)
+      for (int e = lane; e < KC * 16; e += 32)
+        bt[(size_t)(e >> 4) * 256 + (g >> 3) * 128 + ((e & 15) >> 3) * 64 + (g & 7) * 8 + (e & 7)] = 0;
+      continue;
+    }
+    const int pr = pairs[j0 + g];
+    const int q = pr / w, c = pr % w;
+    const float* x = queries + (size_t)q * d;
+    double amax = 0.0;
+#pragma unroll 4
+    for (int e = lane; e < d; e += 32) amax = fmax(amax, fabs((double)__ldg(x + e) - (double)__ldg(mu + e)));
+    amax = warp_max_d(amax);
+    const int ex = amax > 0.0 ? ilogb(amax) - 14 : 0;
+    const double inv = ldexp(1.0, -ex);
+    double s_x = 0.0, s_h = 0.0, s_e = 0.0;
+#pragma unroll 4
+    for (int e = lane; e < KC * 16; e += 32) {
+      uint16_t hb = 0;
+      if (e < d) {
+        const double xr = (double)__ldg(x + e) - (double)__ldg(mu + e);
+        const __half h = __double2half(xr * inv);
+        const double hd = (double)__half2float(h);
+        const double er = xr * inv - hd;
+        s_x += xr * xr;
+        s_h += hd * hd;
+        s_e += er * er;
+        hb = __half_as_ushort(h);
+      }
+      bt[(size_t)(e >> 4) * 256 + (g >> 3) * 128 + ((e & 15) >> 3) * 64 + (g & 7) * 8 + (e & 7)] = hb;
+    }
+    s_x = warp_sum_d(s_x);
+    s_h = warp_sum_d(s_h);
+    s_e = warp_sum_d(s_e);
+    if (lane == 0) {
+      GroupSlot gs;
+      gs.xx = s_x;
+      gs.sc = ldexp(1.0, ex);
+      gs.nxh = __double2float_ru(sqrt(s_h));
+      gs.nex = __double2float_ru(sqrt(s_e));
+      gs.pkey = kbase[q] + qoff[(size_t)q * (w + 1) + c];
+      gs.pad = 0;
+      slots[g] = gs;
+    }
+  }
+  if (threadIdx.x == 0) *reinterpret_cast<int*>(rec + (size_t)KC * 512 + kRrQ * sizeof(GroupSlot)) = ng;
+}
+
 struct ScreenArgs {
   DevIndexView ix;
-  const float* queries;  // chunk-local [nq][d]
-  int w;
-  const int* qoff;
   const int* pair_off;
-  const int* pairs;
-  const int* kbase;
   const uint32_t* marks;
   const int* item_off;   // [L+1]: ceil(pairs_l / kRrQ) * blocks_l, scanned
-  float* ub;             // per candidate (key-array layout)
+  const int* grp_off;    // [L+1]: ceil(pairs_l / kRrQ), scanned
+  const unsigned char* grec;  // group records
+  float* ub;             // per candidate bounds (key-array layout)
   float* lb;
   double eta, eps_acc;
+  int nst;               // ring stages
+  int64_t* counters;     // rrg_search_counters (nullptr unless enabled): [2] += rows streamed
 };
 
 __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   extern __shared__ __align__(1024) unsigned char scr_sm[];
-  __shared__ uint64_t full[kScrStages], empty[kScrStages], bfull[2], tfull[2], tempty[2];
+  __shared__ uint64_t full[kScrStagesMax], empty[kScrStagesMax], bfull[2], bempty[2], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base;
-  __shared__ double s_xx[2][kRrQ], s_sc[2][kRrQ];
-  __shared__ float s_nxh[2][kRrQ], s_nex[2][kRrQ];
-  __shared__ int s_pkey[2][kRrQ], s_ng[2];
   const DevIndexView& ix = a.ix;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   unsigned char* base = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(scr_sm) + 1023) & ~uintptr_t(1023));
   unsigned char* ring = base;
-  unsigned char* btile = base + kScrRing;
-  const int KC = ix.scr_kc, d = ix.d, L = ix.L;
-  const int bt_bytes = KC * 512;
+  const int nst = a.nst;
+  unsigned char* gbuf = base + (size_t)nst * kScrStageBytes;
+  const int KC = ix.scr_kc, L = ix.L;
+  const int rec_bytes = (int)grp_rec_bytes(KC);
   const int total = a.item_off[L];
   const int i0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
   const int i1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
   if (i0 >= i1) return;  // uniform over the CTA, before any barrier or TMEM use
+  if (a.counters && tid == 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 2), (unsigned long long)(i1 - i0) * kScrRows);
 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(s_addr(&tmem_base))
@@ -232,12 +327,14 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   if (tid == 0) {
-    for (int i = 0; i < kScrStages; ++i) {
+    for (int i = 0; i < nst; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&full[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&empty[i])));
     }
     for (int i = 0; i < 2; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bfull[i])));
+      // freed by the MMAs of the group (commit) and by the 4 epilogue warps
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 5;" ::"r"(s_addr(&bempty[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&tfull[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(s_addr(&tempty[i])));
     }
@@ -248,31 +345,57 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   fence_after();
   const uint32_t tmem = tmem_base;
 
-  // item -> (cluster, query group, 128-row block); a CTA's items are a contiguous range,
-  // a group's items are its cluster's blocks in order
-  auto decode = [&](int i, int& l, int& gi, int& b, int& nb) {
+  // item -> (cluster, query group, 128-row block).  A CTA's items are a contiguous
+  // range and a group's items are its cluster's blocks in order, so after one binary
+  // search the roles step through their items (a search per item costs ~10 dependent
+  // L2 loads, which throttled the producer).
+  struct ItemIt {
+    int l, gi, b, nb, ng;  // ng = query groups of cluster l
+  };
+  auto it_begin = [&](int i) {
+    ItemIt t;
     int lo = 0, hi = L;
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
       if (__ldg(a.item_off + mid) <= i) lo = mid; else hi = mid;
     }
-    l = lo;
-    nb = __ldg(ix.scr_blk0 + l + 1) - __ldg(ix.scr_blk0 + l);
-    const int local = i - __ldg(a.item_off + l);
-    gi = local / nb;
-    b = local % nb;
+    t.l = lo;
+    t.nb = __ldg(ix.scr_blk0 + lo + 1) - __ldg(ix.scr_blk0 + lo);
+    const int local = i - __ldg(a.item_off + lo);
+    t.ng = (__ldg(a.item_off + lo + 1) - __ldg(a.item_off + lo)) / t.nb;
+    t.gi = local / t.nb;
+    t.b = local % t.nb;
+    return t;
   };
-
+  auto it_next = [&](ItemIt& t) {  // only called while items remain
+    if (++t.b < t.nb) return;
+    t.b = 0;
+    if (++t.gi < t.ng) return;
+    t.gi = 0;
+    do {  // next cluster with items
+      ++t.l;
+      t.nb = __ldg(ix.scr_blk0 + t.l + 1) - __ldg(ix.scr_blk0 + t.l);
+    } while (__ldg(a.item_off + t.l + 1) == __ldg(a.item_off + t.l));
+    t.ng = (__ldg(a.item_off + t.l + 1) - __ldg(a.item_off + t.l)) / t.nb;
+  };
   if (warp == 0) {
-    if (lane == 0) {  // producer: the CTA's blocks, chunk by chunk, through the ring
-      int sc = 0;
-      for (int i = i0; i < i1; ++i) {
-        int l, gi, b, nb;
-        decode(i, l, gi, b, nb);
+    if (lane == 0) {  // producer: group records and the CTA's blocks through the ring
+      int sc = 0, j = -1, pl = -1, pg = -1;
+      ItemIt t = it_begin(i0);
+      for (int i = i0; i < i1; ++i, i < i1 ? it_next(t) : void()) {
+        const int l = t.l, gi = t.gi, b = t.b;
+        if (l != pl || gi != pg) {
+          ++j; pl = l; pg = gi;
+          const int buf = j & 1;
+          if (j >= 2) scr_wait(&bempty[buf], ((j >> 1) - 1) & 1);
+          scr_expect_tx(&bfull[buf], rec_bytes);
+          scr_bulk(s_addr(gbuf + buf * rec_bytes), a.grec + (size_t)(a.grp_off[l] + gi) * rec_bytes, rec_bytes,
+                   &bfull[buf]);
+        }
         const unsigned char* src = reinterpret_cast<const unsigned char*>(ix.scr_plane) +
                                    ((size_t)(ix.scr_blk0[l] + b) * KC) * kScrChunk;
         for (int c0 = 0; c0 < KC; c0 += kScrStageChunks, ++sc) {
-          const int slot = sc % kScrStages, pass = sc / kScrStages;
+          const int slot = sc % nst, pass = sc / nst;
           if (pass > 0) scr_wait(&empty[slot], (pass - 1) & 1);
           const int bytes = min(kScrStageChunks, KC - c0) * kScrChunk;
           scr_expect_tx(&full[slot], bytes);
@@ -283,9 +406,9 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       int sc = 0, j = -1, pl = -1, pg = -1;
-      for (int i = i0, it = 0; i < i1; ++i, ++it) {
-        int l, gi, b, nb;
-        decode(i, l, gi, b, nb);
+      ItemIt t = it_begin(i0);
+      for (int i = i0, it = 0; i < i1; ++i, ++it, i < i1 ? it_next(t) : void()) {
+        const int l = t.l, gi = t.gi, b = t.b, nb = t.nb;
         if (l != pl || gi != pg) {
           ++j; pl = l; pg = gi;
           scr_wait(&bfull[j & 1], (j >> 1) & 1);
@@ -296,10 +419,10 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
           scr_wait(&tempty[ab], (u - 1) & 1);
           fence_after();
         }
-        const uint32_t sb = s_addr(btile + (j & 1) * bt_bytes);
+        const uint32_t sb = s_addr(gbuf + (j & 1) * rec_bytes);
         const uint32_t dt = tmem + (uint32_t)(ab * kRrQ);
         for (int c0 = 0; c0 < KC; c0 += kScrStageChunks, ++sc) {
-          const int slot = sc % kScrStages, pass = sc / kScrStages;
+          const int slot = sc % nst, pass = sc / nst;
           scr_wait(&full[slot], pass & 1);
           fence_after();
           const uint32_t sa = s_addr(ring + slot * kScrStageBytes);
@@ -309,75 +432,37 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
           scr_commit(&empty[slot]);
         }
         scr_commit(&tfull[ab]);
+        if (b + 1 == nb || i + 1 == i1) scr_commit(&bempty[j & 1]);  // the group's tile is read
       }
     }
   } else {
     // epilogue warps: TMEM lane quarter = warp % 4, one block row per thread
-    const int ew = warp - 2, q4 = warp & 3, row = q4 * 32 + lane;
-    // the queries of item i's group -> fp16 tile `buf` + per-slot bound terms
-    auto build = [&](int i, int buf) {
-      int l, gi, b, nb;
-      decode(i, l, gi, b, nb);
-      const int j0 = a.pair_off[l] + gi * kRrQ;
-      const int ng = min(kRrQ, a.pair_off[l + 1] - j0);
-      epi_sync();  // every epilogue warp is done with the buffer's previous group
-      uint16_t* bt = reinterpret_cast<uint16_t*>(btile + buf * bt_bytes);
-      const float* mu = ix.scr_mu + (size_t)l * d;
-      for (int g = ew; g < ng; g += 4) {
-        const int pr = a.pairs[j0 + g];
-        const int q = pr / a.w, c = pr % a.w;
-        const float* x = a.queries + (size_t)q * d;
-        double amax = 0.0;
-        for (int e = lane; e < d; e += 32) amax = fmax(amax, fabs((double)__ldg(x + e) - (double)__ldg(mu + e)));
-        amax = warp_max_d(amax);
-        const int ex = amax > 0.0 ? ilogb(amax) - 14 : 0;
-        const double inv = ldexp(1.0, -ex);
-        double s_x = 0.0, s_h = 0.0, s_e = 0.0;
-        for (int e = lane; e < KC * 16; e += 32) {
-          uint16_t hb = 0;
-          if (e < d) {
-            const double xr = (double)__ldg(x + e) - (double)__ldg(mu + e);
-            const __half h = __double2half(xr * inv);
-            const double hd = (double)__half2float(h);
-            const double er = xr * inv - hd;
-            s_x += xr * xr;
-            s_h += hd * hd;
-            s_e += er * er;
-            hb = __half_as_ushort(h);
-          }
-          // B tile: N = kRrQ rows (slots), same core-matrix layout, 512 B per K chunk
-          bt[(size_t)(e >> 4) * 256 + (g >> 3) * 128 + ((e & 15) >> 3) * 64 + (g & 7) * 8 + (e & 7)] = hb;
-        }
-        s_x = warp_sum_d(s_x);
-        s_h = warp_sum_d(s_h);
-        s_e = warp_sum_d(s_e);
-        if (lane == 0) {
-          s_xx[buf][g] = s_x;
-          s_sc[buf][g] = ldexp(1.0, ex);
-          s_nxh[buf][g] = __double2float_ru(sqrt(s_h));
-          s_nex[buf][g] = __double2float_ru(sqrt(s_e));
-          s_pkey[buf][g] = a.kbase[q] + a.qoff[(size_t)q * (a.w + 1) + c];
-        }
-      }
-      if (ew == 0 && lane == 0) s_ng[buf] = ng;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // tile -> tensor core (async proxy)
-      epi_sync();
-      if (ew == 0 && lane == 0) scr_arrive(&bfull[buf]);
-    };
-    {
-      int l, gi, b, nb;
-      decode(i0, l, gi, b, nb);
-      build(i0, 0);
-      const int s1 = i0 + (nb - b);
-      if (s1 < i1) build(s1, 1);
-    }
+    const int q4 = warp & 3, row = q4 * 32 + lane;
     const double eta = a.eta, eps = a.eps_acc;
     int j = -1, pl = -1, pg = -1;
-    for (int i = i0, it = 0; i < i1; ++i, ++it) {
-      int l, gi, b, nb;
-      decode(i, l, gi, b, nb);
-      if (l != pl || gi != pg) { ++j; pl = l; pg = gi; }
-      const int buf = j & 1, ab = it & 1, u = it >> 1;
+    ItemIt t = it_begin(i0);
+    for (int i = i0, it = 0; i < i1; ++i, ++it, i < i1 ? it_next(t) : void()) {
+      const int l = t.l, gi = t.gi, b = t.b, nb = t.nb;
+      if (l != pl || gi != pg) {
+        ++j; pl = l; pg = gi;
+        scr_wait(&bfull[j & 1], (j >> 1) & 1);  // the group's slot terms have landed
+      }
+      const unsigned char* rec = gbuf + (j & 1) * rec_bytes;
+      const GroupSlot* slots = reinterpret_cast<const GroupSlot*>(rec + (size_t)KC * 512);
+      const int ng = *reinterpret_cast<const int*>(rec + (size_t)KC * 512 + kRrQ * sizeof(GroupSlot));
+      const int ab = it & 1, u = it >> 1;
+      const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+      const int jr = b * kScrRows + row;
+      // bounds for every (row, slot) of the item: the candidate range of a (query, probe)
+      // pair covers all m rows of the cluster, and entries outside the query's top t are
+      // never read -- cheaper than loading the membership bits first
+      const bool live = jr < m;
+      double rr = 0.0;
+      float4 rm = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live) {
+        rr = __ldg(ix.scr_rr + p0 + jr);
+        rm = __ldg(ix.scr_rmeta + p0 + jr);
+      }
       scr_wait(&tfull[ab], u & 1);
       fence_after();
       uint32_t v[kRrQ];
@@ -390,37 +475,28 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
       fence_before();
       __syncwarp();
       if (lane == 0) scr_arrive(&tempty[ab]);
-      const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
-      const int jr = b * kScrRows + row;
-      if (jr < m) {
-        const int gp = p0 + jr;
-        const double rr = __ldg(ix.scr_rr + gp);
-        const float4 rm = __ldg(ix.scr_rmeta + gp);
+      if (live) {
         const double rsc = ldexp(1.0, (int)rm.z), nrh = rm.x, ner = rm.y;
-        const int ng = s_ng[buf];
 #pragma unroll
         for (int g = 0; g < kRrQ; ++g) {
           if (g >= ng) break;
-          const int bit = s_pkey[buf][g] + jr;
-          if (!((__ldg(a.marks + (bit >> 5)) >> (bit & 31)) & 1u)) continue;
+          const GroupSlot gs = slots[g];
           const double G = (double)__uint_as_float(v[g]);
-          const double sc = s_sc[buf][g] * rsc;
-          const double xx = s_xx[buf][g], nxh = s_nxh[buf][g], nex = s_nex[buf][g];
-          const double S = xx + rr - 2.0 * sc * G;
+          const double sc = gs.sc * rsc;
+          const double nxh = gs.nxh, nex = gs.nex;
+          const double S = gs.xx + rr - 2.0 * sc * G;
           const double F = sc * (nxh * ner + nex * nrh + nex * ner + eps * nxh * nrh);
-          const double E = 2.0 * F * (1.0 + 0x1p-20) + 0x1p-40 * (xx + rr + 2.0 * sc * fabs(G));
+          const double E = 2.0 * F * (1.0 + 0x1p-20) + 0x1p-40 * (gs.xx + rr + 2.0 * sc * fabs(G));
           const double ubv = fmax((S + E) * (1.0 + eta), 0.0);
           const double lbv = fmax(S - E, 0.0) * (1.0 - eta);
+          const int bit = gs.pkey + jr;
           a.ub[bit] = __double2float_ru(ubv);
           a.lb[bit] = __double2float_rd(lbv);
         }
       }
-      // after the group's last item: its tile buffer is free, build the group after next
-      if (b + 1 == nb && i + 1 < i1) {
-        int l1, g1, b1, nb1;
-        decode(i + 1, l1, g1, b1, nb1);
-        const int s2 = i + 1 + (nb1 - b1);
-        if (s2 < i1) build(s2, buf);
+      if (b + 1 == nb || i + 1 == i1) {  // done with the group's record
+        __syncwarp();
+        if (lane == 0) scr_arrive(&bempty[j & 1]);
       }
     }
   }
@@ -433,114 +509,139 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
 }
 
 // ------------------------------------------------------------------ threshold
-// Warp per query: T = k-th smallest UB of its top-t candidates (radix select on the
-// bits of the non-negative f32 bounds), then every non-survivor (LB > T) loses its
-// membership bit (the cluster re-rank skips it) and gets the +inf key (k_topk_final
-// never selects it).  Survivor and candidate counts feed rrg_search_counters.
-constexpr int kThrWarps = 8;
+// Warp per query.  The bounds of its top-t candidates are gathered into shared memory;
+// T is any value >= the k-th smallest UB: here the largest UB of the float-linear
+// buckets (256 over [min UB, max UB]) up to the one holding the k-th smallest -- at
+// least k candidates lie in those buckets, so at least k have UB <= T -- which costs
+// one histogram pass and adds at most one bucket of extra survivors.  The survivors
+// (LB <= T) are compacted in place into the query's candidate list (cand_idx, cand_n),
+// which the sparse exact re-rank and the final top-k then read.
+__device__ __forceinline__ float warp_min_f(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fminf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_max_f(float v) {
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
 
-__global__ void __launch_bounds__(32 * kThrWarps) k_rr_thresh(ThreshArgs a, int nq) {
-  __shared__ int hist[kThrWarps][256];
-  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
-  const int q = blockIdx.x * kThrWarps + wl;
+__global__ void k_rr_thresh(ThreshArgs a, int nq) {
+  extern __shared__ __align__(16) unsigned char thr_sm[];
+  __shared__ int hist[8][256];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, wpb = blockDim.x >> 5;
+  const int q = blockIdx.x * wpb + wl;
   if (q >= nq) return;
+  const size_t per = (size_t)a.take_cap * 12;
+  float* uu = reinterpret_cast<float*>(thr_sm + per * wl);
+  float* ll = uu + a.take_cap;
+  int* cc = reinterpret_cast<int*>(ll + a.take_cap);
   int* h = hist[wl];
   const int n = a.cand_n[q];
-  const int kb = a.kbase[q], nc = a.kbase[q + 1] - kb;
-  const int* ci = a.cand_idx + (size_t)q * a.take_cap;
-  uint32_t T = 0x7f800000u;  // +inf: fewer than k candidates keep everything
-  if (n > a.k) {
-    uint32_t prefix = 0, pmask = 0;
-    int want = a.k;  // rank (1-based) of the k-th smallest inside the current prefix
-    for (int shift = 24; shift >= 0; shift -= 8) {
-      for (int i = lane; i < 256; i += 32) h[i] = 0;
-      __syncwarp();
-      for (int i = lane; i < n; i += 32) {
-        const uint32_t u = __float_as_uint(__ldg(a.ub + kb + __ldg(ci + i)));
-        if ((u & pmask) == prefix) atomicAdd(&h[(u >> shift) & 255], 1);
-      }
-      __syncwarp();
-      // bucket holding the want-th value: warp scan over 8 buckets per lane
-      int loc[8], s = 0;
-#pragma unroll
-      for (int t = 0; t < 8; ++t) { loc[t] = h[lane * 8 + t]; s += loc[t]; }
-      int incl = s;
-      for (int o = 1; o < 32; o <<= 1) {
-        const int v = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += v;
-      }
-      const int excl = incl - s;
-      int found = -1, before = 0;
-      if (excl < want && want <= incl) {
-        int run = excl;
-#pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          if (found < 0 && run + loc[t] >= want) { found = lane * 8 + t; before = run; }
-          run += loc[t];
-        }
-      }
-      const unsigned who = __ballot_sync(0xffffffffu, found >= 0);
-      const int src = __ffs(who) - 1;
-      found = __shfl_sync(0xffffffffu, found, src);
-      before = __shfl_sync(0xffffffffu, before, src);
-      want -= before;
-      prefix |= (uint32_t)found << shift;
-      pmask |= 255u << shift;
-      __syncwarp();
-    }
-    T = prefix;
-  }
-  const float Tf = __uint_as_float(T);
-  // membership bits of the query's candidate range [kb, kb + nc): clear non-survivors
-  int surv = 0;
-  if (n > a.k) {
-    const int w0 = kb >> 5, w1 = (kb + nc - 1) >> 5;
-    for (int wi = w0 + lane; wi <= w1; wi += 32) {
-      uint32_t in = 0xffffffffu;  // bits of this query inside the word
-      if (wi == w0) in &= 0xffffffffu << (kb & 31);
-      if (wi == w1) in &= 0xffffffffu >> (31 - ((kb + nc - 1) & 31));
-      const uint32_t m = a.marks[wi] & in;
-      uint32_t drop = 0, bits = m;
-      while (bits) {
-        const int bb = __ffs(bits) - 1;
-        bits &= bits - 1;
-        if (__ldg(a.lb + 32 * (size_t)wi + bb) > Tf) drop |= 1u << bb;
-      }
-      surv += __popc(m & ~drop);
-      if (drop) atomicAnd(a.marks + wi, ~drop);
-    }
-    for (int i = lane; i < n; i += 32) {
-      const int c = __ldg(ci + i);
-      if (__ldg(a.lb + kb + c) > Tf) a.diss[kb + c] = 0xffffffffu;
-    }
-  } else {
-    surv = lane == 0 ? n : 0;
-  }
-  if (a.counters) {
-    for (int o = 16; o > 0; o >>= 1) surv += __shfl_xor_sync(0xffffffffu, surv, o);
-    if (lane == 0) {
+  const int kb = a.kbase[q];
+  int* ci = a.cand_idx + (size_t)q * a.take_cap;
+  if (n <= a.k) {  // nothing can be pruned
+    if (a.counters && lane == 0) {
       atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 0), (unsigned long long)n);
-      atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 1), (unsigned long long)surv);
+      atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 1), (unsigned long long)n);
     }
+    return;
+  }
+  // gather: 4 candidates per lane in flight (index load, then both bounds)
+  constexpr int GU = 4;
+  float umin = __int_as_float(0x7f800000), umax = 0.f;
+  for (int b0 = lane; b0 < n; b0 += 32 * GU) {
+    int c[GU];
+    float u[GU], lv[GU];
+#pragma unroll
+    for (int t = 0; t < GU; ++t) c[t] = b0 + 32 * t < n ? ci[b0 + 32 * t] : 0;  // (rewritten below)
+#pragma unroll
+    for (int t = 0; t < GU; ++t) {
+      u[t] = __ldg(a.ub + kb + c[t]);
+      lv[t] = __ldg(a.lb + kb + c[t]);
+    }
+#pragma unroll
+    for (int t = 0; t < GU; ++t)
+      if (b0 + 32 * t < n) {
+        uu[b0 + 32 * t] = u[t];
+        ll[b0 + 32 * t] = lv[t];
+        cc[b0 + 32 * t] = c[t];
+        umin = fminf(umin, u[t]);
+        umax = fmaxf(umax, u[t]);
+      }
+  }
+  umin = warp_min_f(umin);
+  umax = warp_max_f(umax);
+  for (int i = lane; i < 256; i += 32) h[i] = 0;
+  __syncwarp();
+  const float scale = umax > umin ? 256.f / (umax - umin) : 0.f;
+  auto bucket = [&](float u) {
+    const int bk = (int)((u - umin) * scale);
+    return bk < 0 ? 0 : (bk > 255 ? 255 : bk);
+  };
+  for (int i = lane; i < n; i += 32) atomicAdd(&h[bucket(uu[i])], 1);
+  __syncwarp();
+  // bucket holding the k-th smallest: warp scan over 8 buckets per lane
+  int loc[8], sum = 0;
+#pragma unroll
+  for (int t = 0; t < 8; ++t) { loc[t] = h[lane * 8 + t]; sum += loc[t]; }
+  int incl = sum;
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  int found = 256;
+  if (incl - sum < a.k && a.k <= incl) {
+    int run = incl - sum;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) {
+      if (found == 256 && run + loc[t] >= a.k) found = lane * 8 + t;
+      run += loc[t];
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
+  float T = 0.f;
+  for (int i = lane; i < n; i += 32)
+    if (bucket(uu[i]) <= found) T = fmaxf(T, uu[i]);
+  T = warp_max_f(T);
+  // survivors, compacted in place (their order is irrelevant: the final top-k sorts)
+  int ns = 0;
+  for (int b0 = 0; b0 < n; b0 += 32) {
+    const int i = b0 + lane;
+    const bool keep = i < n && ll[i] <= T;
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    if (keep) ci[ns + __popc(bal & ((1u << lane) - 1u))] = cc[i];
+    ns += __popc(bal);
+  }
+  if (lane == 0) a.cand_n[q] = ns;
+  if (a.counters && lane == 0) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 0), (unsigned long long)n);
+    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 1), (unsigned long long)ns);
   }
 }
 
 // ------------------------------------------------------------------ launchers
 void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
+  // groups (cluster, <= kRrQ queries): one record each, built in parallel up front
+  launch_rr_items(h.pair_off, ix.cl_pos, ix.L, 1 << 30, h.grp_off, st);
   launch_rr_items(h.pair_off, ix.cl_pos, ix.L, kScrRows, h.item_off, st);
+  (k_rr_groups<<<h.n_groups_max, 32 * kRrQ, 0, st>>>(ix, h.queries, h.w, h.qoff, h.pair_off, h.pairs, h.kbase,
+                                              h.grp_off, h.grec), note_launch());
   ScreenArgs a;
-  a.ix = ix; a.queries = h.queries; a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off;
-  a.pairs = h.pairs; a.kbase = h.kbase; a.marks = h.marks; a.item_off = h.item_off;
-  a.ub = h.ub; a.lb = h.lb;
+  a.ix = ix; a.pair_off = h.pair_off; a.marks = h.marks; a.item_off = h.item_off; a.grp_off = h.grp_off;
+  a.grec = h.grec; a.ub = h.ub; a.lb = h.lb; a.counters = h.counters;
+  a.nst = screen_stages(ix.scr_kc);
   a.eta = (double)(ix.d + 4) * 0x1p-24 * 1.001;
   a.eps_acc = (double)(ix.d + 32) * 0x1p-21;
   const size_t sm = screen_smem(ix.scr_kc);
   static int done[64] = {};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
-  if (dev >= 0 && dev < 64 && !done[dev]) {
-    cudaFuncSetAttribute((const void*)k_rr_screen, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (dev >= 0 && dev < 64 && !done[dev]) {  // the largest tile any index may need
+    cudaFuncAttributes at{};
+    cudaFuncGetAttributes(&at, (const void*)k_rr_screen);
+    cudaFuncSetAttribute((const void*)k_rr_screen, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kMaxSmemPerCta - (int)at.sharedSizeBytes);
     done[dev] = 1;
   }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -548,7 +649,60 @@ void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
   ThreshArgs t;
   t.kbase = h.kbase; t.cand_idx = h.cand_idx; t.cand_n = h.cand_n; t.take_cap = h.take_cap; t.k = h.k;
   t.ub = h.ub; t.lb = h.lb; t.marks = h.marks; t.diss = h.diss; t.counters = h.counters;
-  (k_rr_thresh<<<(nq + kThrWarps - 1) / kThrWarps, 32 * kThrWarps, 0, st>>>(t, nq), note_launch());
+  static int tdone[64] = {};
+  if (dev >= 0 && dev < 64 && !tdone[dev]) {
+    cudaFuncSetAttribute((const void*)k_rr_thresh, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
+    tdone[dev] = 1;
+  }
+  const size_t per = (size_t)h.take_cap * 12;
+  const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (160 * 1024) / per));
+  (k_rr_thresh<<<(nq + wpb - 1) / wpb, 32 * wpb, per * wpb, st>>>(t, nq), note_launch());
+}
+
+// Counter only (rrg_search_counters[4]): block per cluster, the union over its queries
+// of the rows they keep (membership words, or the screen's survivor lists), popcounted.
+__global__ void k_count_rows(DevIndexView ix, const int* __restrict__ pair_off, const int* __restrict__ pairs,
+                             const int* __restrict__ kbase, const int* __restrict__ qoff, int w,
+                             const uint32_t* __restrict__ marks, const int* __restrict__ cand_idx,
+                             const int* __restrict__ cand_n, int take_cap, int64_t* out) {
+  extern __shared__ uint32_t u[];
+  const int l = blockIdx.x;
+  const int m = ix.cl_pos[l + 1] - ix.cl_pos[l], mw = (m + 31) / 32;
+  const int j0 = pair_off[l], j1 = pair_off[l + 1];
+  if (m == 0 || j1 == j0) return;
+  for (int k = threadIdx.x; k < mw; k += blockDim.x) u[k] = 0;
+  __syncthreads();
+  for (int j = j0; j < j1; ++j) {
+    const int pr = pairs[j], q = pr / w, c = pr % w;
+    const int off = qoff[(size_t)q * (w + 1) + c];
+    if (cand_idx) {
+      for (int i = threadIdx.x; i < cand_n[q]; i += blockDim.x) {
+        const int row = cand_idx[(size_t)q * take_cap + i] - off;
+        if (row >= 0 && row < m) atomicOr(u + (row >> 5), 1u << (row & 31));
+      }
+      continue;
+    }
+    const size_t key = (size_t)kbase[q] + off;
+    for (int k = threadIdx.x; k < mw; k += blockDim.x) {
+      const size_t bit = key + 32 * (size_t)k;
+      uint32_t v = __funnelshift_r(marks[bit >> 5], marks[(bit >> 5) + 1], (unsigned)(bit & 31));
+      if (k == mw - 1 && (m & 31)) v &= (1u << (m & 31)) - 1u;
+      u[k] |= v;  // one thread per word: no race
+    }
+  }
+  __syncthreads();
+  int cnt = 0;
+  for (int k = threadIdx.x; k < mw; k += blockDim.x) cnt += __popc(u[k]);
+  for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(reinterpret_cast<unsigned long long*>(out), (unsigned long long)cnt);
+}
+
+void launch_count_rows(const DevIndexView& ix, const int* pair_off, const int* pairs, const int* kbase,
+                       const int* qoff, int w, const uint32_t* marks, const int* cand_idx, const int* cand_n,
+                       int take_cap, int mwords, int64_t* out, cudaStream_t st) {
+  (k_count_rows<<<ix.L, 256, (size_t)mwords * 4, st>>>(ix, pair_off, pairs, kbase, qoff, w, marks, cand_idx,
+                                                      cand_n, take_cap, out),
+   note_launch());
 }
 
 }  // namespace rrg

@@ -51,7 +51,7 @@ def _corpus_max_norm(g):
 
 
 @pytest.mark.parametrize("case", QUANT_CASES)
-@pytest.mark.parametrize("entry", ["host", "device", "device-querymajor", "device-warpsel"])
+@pytest.mark.parametrize("entry", ["host", "device", "device-querymajor", "device-warpsel", "device-screen"])
 def test_golden_end_to_end(pkg, tmp_path, case, entry, monkeypatch):
     if entry == "device-querymajor":  # the fused query-major scoring kernel
         monkeypatch.setenv("RRG_SCORE_MODE", "query")
@@ -59,6 +59,10 @@ def test_golden_end_to_end(pkg, tmp_path, case, entry, monkeypatch):
     if entry == "device-warpsel":  # warp-per-query selections + cluster-major re-rank
         monkeypatch.setenv("RRG_WARP_SELECT", "1")
         monkeypatch.setenv("RRG_RERANK", "cluster")
+        entry = "device"
+    if entry == "device-screen":  # tensor-core screen of the cluster-major re-rank
+        monkeypatch.setenv("RRG_RERANK", "cluster")
+        monkeypatch.setenv("RRG_SCREEN", "1")
         entry = "device"
     g, dev = _golden_index(pkg, tmp_path, case)
     for pi, (k, w, t, rr) in enumerate(g["params"]):
@@ -492,7 +496,7 @@ SWEEP = [
 
 @pytest.mark.parametrize("mode", ["cluster", "cluster+auto", "cluster+async", "cluster+skip", "cluster+blocksel",
                                   "cluster+dmma", "cluster+slicedroute", "query", "cluster+regs",
-                                  "cluster+tma"])
+                                  "cluster+tma", "cluster+screen", "cluster+noscreen"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -514,6 +518,10 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
         monkeypatch.setenv("RRG_ROUTE_FUSED", "0")
     elif rerank_mode == "slicedroute":  # int8 tensor-core (sliced) projection + routing
         monkeypatch.setenv("RRG_GEMM", "sliced")
+    elif rerank_mode == "screen":  # tensor-core bounds prune the exact re-rank (any t)
+        monkeypatch.setenv("RRG_SCREEN", "1")
+    elif rerank_mode == "noscreen":
+        monkeypatch.setenv("RRG_SCREEN", "0")
     elif rerank_mode:
         monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
@@ -803,3 +811,61 @@ def test_too_many_clusters_rejected(pkg, tmp_path):
     blob = random_index(16, 8, 4, 20000, 20000, seed=1)
     with pytest.raises(pkg.ParameterError, match="clusters"):
         pkg.DeviceIndex.from_file(_write(tmp_path, "toomany", blob))
+
+
+# ------------------------------------------------------------- re-rank screen
+
+@pytest.mark.parametrize("d,L,m,metric_scale", [(768, 6, 3000, 1.0), (960, 5, 2500, 30.0),
+                                                (1536, 4, 1800, 1e-3), (768, 3, 900, 1.0)])
+def test_screen_exact_vs_oracle(pkg, tmp_path, d, L, m, metric_scale, monkeypatch):
+    """The tensor-core screen only removes candidates that provably cannot reach the top k:
+    screened and unscreened searches return the reference's ids and score bits, across
+    scales (tiny and huge corpora), duplicate rows, queries on corpus points, and t from
+    k (nothing to prune) to the whole cluster set."""
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    monkeypatch.setenv("RRG_RERANK", "cluster")
+    monkeypatch.setenv("RRG_SCREEN", "1")
+    blob = random_index(d, 64, 16, L, m, "euclidean", seed=d + L, dup_rows=20, corpus_scale=metric_scale)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "scr", blob))
+    oidx = O.read_index(blob)
+    rng = np.random.default_rng(d)
+    q = (rng.standard_normal((300, d)) * metric_scale).astype(F32)
+    q[0] = oidx.corpus[7]
+    q[1] = oidx.corpus[7] + np.float32(metric_scale * 1e-6)
+    q[2] = 0.0
+    for k, w, t in [(10, 1, 200), (50, 2, 400), (10, 1, 10), (100, L, m), (5, 1, 700)]:
+        ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(torch.from_numpy(q).cuda(), k, w, t, True))
+        ref = O.query_batch(oidx, q, k, w, t, True)
+        for i, r in enumerate(ref):
+            c = int(cnt[i])
+            assert c == len(r.ids), (k, w, t, i)
+            np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"{(k, w, t)} q{i}")
+            np.testing.assert_array_equal(sc[i, :c].view(np.int32), r.scores.view(np.int32))
+
+
+def test_screen_counters_and_pruning(pkg, tmp_path, monkeypatch):
+    """The screen re-ranks far fewer than t candidates per query on clustered data, and the
+    library's work counters account for it."""
+    import ctypes
+
+    from index_writer import random_index
+    from paper_2410_18926_b200 import _native
+
+    monkeypatch.setenv("RRG_RERANK", "cluster")
+    monkeypatch.setenv("RRG_SCREEN", "1")
+    blob = random_index(768, 64, 16, 8, 6000, "euclidean", seed=4)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "cnt", blob))
+    q = torch.from_numpy(np.random.default_rng(0).standard_normal((2000, 768)).astype(F32)).cuda()
+    _native.lib.rrg_set_stage_timing(1)
+    c = (ctypes.c_int64 * 8)()
+    _native.lib.rrg_search_counters(c)
+    dev.search_device(q, 10, 1, 400, True)
+    torch.cuda.synchronize()
+    _native.lib.rrg_search_counters(c)
+    _native.lib.rrg_set_stage_timing(0)
+    cand, surv, streamed, fetched, distinct = c[0], c[1], c[2], c[3], c[4]
+    assert 2000 * 10 <= cand <= 2000 * 400       # sum of min(t, candidates) per query
+    assert 2000 * 10 <= surv < cand / 4, (surv, cand)
+    assert streamed >= 6000 and distinct <= 6000 and fetched >= distinct

@@ -454,6 +454,17 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
     fill_corpus(corp, d_pos, (int)v.d_stride, d_perm);
     v.corpus = corp;
   }
+  v.rt_cent_tiles = nullptr; v.rt_cent_stats = nullptr; v.rt_kc = 0;
+  if (s <= route_screen_max_dim() && L >= 512) {  // routing screen: centroids as fp16 tiles
+    v.rt_kc = (s + 15) / 16;
+    uint16_t* ct = static_cast<uint16_t*>(ix->dalloc(route_tile_bytes(L, v.rt_kc)));
+    float4* cst = static_cast<float4*>(ix->dalloc((size_t)((L + 127) / 128 * 128) * 16));
+    launch_f16_tiles(v.cent, L, s, s, v.rt_kc, ct, cst, 0);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaDeviceSynchronize());
+    v.rt_cent_tiles = ct;
+    v.rt_cent_stats = cst;
+  }
   v.scr_plane = nullptr; v.scr_blk0 = nullptr; v.scr_mu = nullptr; v.scr_rr = nullptr;
   v.scr_rmeta = nullptr; v.scr_kc = 0;
   if (has_corpus && hm.metric == kMetricEuclidean && d <= screen_max_dim() && v.opt.screen != 0 && P > 0) {
@@ -764,6 +775,7 @@ RrgOpts read_opts() {
   o.host_pieces = std::max(0, std::min(8, flag("RRG_HOST_PIECES", 0)));
   o.graph = flag("RRG_GRAPH", 1) != 0;
   o.screen = env("RRG_SCREEN") ? (flag("RRG_SCREEN", 0) != 0) : -1;
+  o.route_screen = flag("RRG_ROUTE_SCREEN", 1) != 0;
   return o;
 }
 // up to this many queries the projection / routing run as warp-per-output GEMVs
@@ -1024,7 +1036,23 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         launch_prep(xps, xs, ns, v.s, v.s_pad, v.d, qcodes + (int64_t)s0 * v.s_pad, qscale + s0,
                     qhead + s0, pp + s0, xx + s0, st, nonfinite);
       });
-      if (w == 1 && ns > kSmallBatch && v.opt.route_fused) {
+      if (ns > kSmallBatch && w <= kRtMaxW && v.rt_cent_tiles && v.opt.route_screen) {
+        // bounds on the fp16 tensor cores, f64 recheck of the few candidates that can be
+        // among the w nearest (rrg_route_screen.cu); scratch inside this piece's rows of
+        // the routing buffer (>= 4 KB per query for L >= 512)
+        char* rb = reinterpret_cast<char*>(diss + (int64_t)s0 * v.L);
+        auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+        RouteScreenHost rh{};
+        rh.ix = v; rh.xp = xps; rh.pp = pp + s0; rh.w = w;
+        size_t o = 0;
+        rh.qt = reinterpret_cast<uint16_t*>(rb + o); o += al(route_tile_bytes(ns, v.rt_kc));
+        rh.qs = reinterpret_cast<float4*>(rb + o); o += al((size_t)(ns + 127) / 128 * 128 * 16);
+        rh.T = reinterpret_cast<uint32_t*>(rb + o); o += al((size_t)ns * 4);
+        rh.cnt = reinterpret_cast<int*>(rb + o); o += al((size_t)ns * 4);
+        rh.list = reinterpret_cast<int*>(rb + o); o += al((size_t)ns * kRtCap * 4);
+        rh.sel = sel + (int64_t)s0 * w; rh.primary = prim + s0;
+        staged(2, st, [&] { launch_route_screen(rh, ns, st); });
+      } else if (w == 1 && ns > kSmallBatch && v.opt.route_fused) {
         // nearest cluster straight from the GEMM: per (query, 64-centroid tile) minima
         const int nt = route_nearest_tiles(v.L);
         double* part_v = diss + (int64_t)s0 * nt;

@@ -1079,22 +1079,22 @@ __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_o
 
 __global__ void k_interleave_queries(DevIndexView ix, const float* __restrict__ x, int nq,
                                      float* __restrict__ xint) {
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t m = (int64_t)nq * ix.d;  // elem_perm is a permutation of [0, d)
-  for (int64_t i = t0; i < m; i += stride) {
-    const int64_t q = i / ix.d;
-    const int j = (int)(i - q * ix.d);
-    xint[q * ix.d_stride + (ix.elem_perm ? __ldg(ix.elem_perm + j) : j)] = __ldg(x + i);
-  }
-  const int pad = ix.d_stride - ix.d;  // slots [d, d_stride) of every row: zero
-  for (int64_t i = t0; i < (int64_t)nq * pad; i += stride) xint[(i / pad) * ix.d_stride + ix.d + i % pad] = 0.f;
+  // block per query: its row is staged in shared memory, then written out in slot
+  // order (coalesced), slot = elem_perm[j]; the d_stride - d pad slots are zero
+  extern __shared__ float xrow[];
+  const int q = blockIdx.x;
+  for (int j = threadIdx.x; j < ix.d_stride; j += blockDim.x) xrow[j] = 0.f;
+  __syncthreads();
+  for (int j = threadIdx.x; j < ix.d; j += blockDim.x)
+    xrow[ix.elem_perm ? __ldg(ix.elem_perm + j) : j] = __ldg(x + (size_t)q * ix.d + j);
+  __syncthreads();
+  float4* dst = reinterpret_cast<float4*>(xint + (size_t)q * ix.d_stride);
+  for (int j = threadIdx.x; j < ix.d_stride / 4; j += blockDim.x) dst[j] = reinterpret_cast<float4*>(xrow)[j];
 }
 
 void launch_interleave_queries(const DevIndexView& ix, const float* queries, int nq, float* xint,
                                cudaStream_t st) {
-  const int64_t n = (int64_t)nq * ix.d_stride;
-  const unsigned blocks = (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  (k_interleave_queries<<<blocks, 256, 0, st>>>(ix, queries, nq, xint), note_launch());
+  (k_interleave_queries<<<nq, 256, (size_t)ix.d_stride * 4, st>>>(ix, queries, nq, xint), note_launch());
 }
 
 void launch_rr_items(const int* pair_off, const int* cl_pos, int L, int rows, int* item_off,
@@ -1457,7 +1457,7 @@ __device__ __forceinline__ float reduce_any(float (&v)[N], int nval, int lane) {
 }
 
 constexpr int SNT = 256;
-constexpr int kSpRows = 512;
+constexpr int kSpRows = 1024;
 template <int NB, int NH>
 __global__ void __launch_bounds__(SNT, NH == 1 ? 2 : 1) k_rerank_sparse(ClusterRerankArgs a) {
   constexpr int NLV = 8 * NH, cstep = 8 * NLV;
@@ -1915,7 +1915,9 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   // spread over many CTAs: C2 batch 1, 4 -> 31 items)
   const int64_t probes = (int64_t)h.nq * h.w;
   a.rr_rows = probes >= 512 ? kRrRows : (probes >= 64 ? 128 : 32);
-  if (h.compact) a.rr_rows = std::min(a.rr_rows, kSpRows);
+  // sparse (screened) items: whole clusters (up to kSpRows rows) amortise the item
+  // staging; small batches keep the short items that spread one query over CTAs
+  if (h.compact) a.rr_rows = probes >= 512 ? kSpRows : std::min(a.rr_rows, kSpRows);
   (k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off), note_launch());
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   a.neg_zero = -0.0f;

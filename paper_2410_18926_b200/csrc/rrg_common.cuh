@@ -37,6 +37,7 @@ struct RrgOpts {
   int host_pieces;   // RRG_HOST_PIECES: 0 auto
   int graph;         // RRG_GRAPH: captured graphs for small host batches (default 1)
   int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
+  int route_screen;  // RRG_ROUTE_SCREEN (default 1): fp16 tensor-core routing bounds + f64 recheck
 };
 
 // POD view of a device-resident index, passed by value to kernels.
@@ -100,6 +101,10 @@ struct DevIndexView {
   const double* scr_rr;       // [P] ||c - mu||^2 (f64)
   const float4* scr_rmeta;    // [P] {||r_hat||, ||r - r_hat||, 2^e_row, 0} (scaled units, rounded up)
   int scr_kc;                 // K chunks of 16 elements: ceil(d / 16)
+  // routing screen (rrg_route_screen.cu): centroids as fp16 tiles (x 2^-e per row)
+  const uint16_t* rt_cent_tiles;  // [ceil(L/128)][rt_kc][128 rows x 16 fp16]
+  const float4* rt_cent_stats;    // [L_pad] {||c^||, ||c/2^e - c^||, e, 0}
+  int rt_kc;                      // ceil(s / 16)
   RrgOpts opt;
 };
 

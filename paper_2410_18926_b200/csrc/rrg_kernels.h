@@ -214,6 +214,30 @@ void launch_count_rows(const DevIndexView& ix, const int* pair_off, const int* p
                        const int* qoff, int w, const uint32_t* marks, const int* cand_idx, const int* cand_n,
                        int take_cap, int mwords, int64_t* out, cudaStream_t st);
 
+// Routing screen (rrg_route_screen.cu): fp16 tensor-core bounds of every
+// (query, centroid) d2, the centroids that can be among the w nearest, f64 recheck.
+constexpr int kRtCap = 64;    // survivors listed per query (more: every centroid is rechecked)
+constexpr int kRtMaxW = 8;    // w handled by the screen (larger w: the f64 GEMM path)
+constexpr int kRtMaxKc = 24;  // s <= 384
+int route_screen_max_dim();
+size_t route_tile_bytes(int rows, int kc);
+void launch_f16_tiles(const float* src, int rows, int K, int ld, int kc, uint16_t* tiles, float4* stats,
+                      cudaStream_t st);
+struct RouteScreenHost {
+  DevIndexView ix;
+  const float* xp;   // [nq][s] projected queries
+  const double* pp;  // [nq] x.x (NumPy pairwise f64)
+  int w;
+  uint16_t* qt;      // route_tile_bytes(nq, rt_kc) scratch
+  float4* qs;        // [nq padded to 128] scratch
+  uint32_t* T;       // [nq] scratch
+  int* cnt;          // [nq] scratch
+  int* list;         // [nq][kRtCap] scratch
+  int* sel;          // [nq][w] out
+  int* primary;      // [nq] out
+};
+void launch_route_screen(const RouteScreenHost& h, int nq, cudaStream_t st);
+
 struct TopkFinalHost {
   DevIndexView ix;
   const int* sel;

@@ -249,27 +249,47 @@ __global__ void __launch_bounds__(512) k_rr_groups(DevIndexView ix, const float*
     const int pr = pairs[j0 + g];
     const int q = pr / w, c = pr % w;
     const float* x = queries + (size_t)q * d;
+    // x' = x - mu (exact in f64); 8 elements per lane in flight per step
     double amax = 0.0;
-#pragma unroll 4
-    for (int e = lane; e < d; e += 32) amax = fmax(amax, fabs((double)__ldg(x + e) - (double)__ldg(mu + e)));
+    for (int e0 = lane; e0 < d; e0 += 256) {
+      float xv[8], mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        xv[u] = e < d ? __ldg(x + e) : 0.f;
+        mv[u] = e < d ? __ldg(mu + e) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) amax = fmax(amax, fabs((double)xv[u] - (double)mv[u]));
+    }
     amax = warp_max_d(amax);
     const int ex = amax > 0.0 ? ilogb(amax) - 14 : 0;
     const double inv = ldexp(1.0, -ex);
     double s_x = 0.0, s_h = 0.0, s_e = 0.0;
-#pragma unroll 4
-    for (int e = lane; e < KC * 16; e += 32) {
-      uint16_t hb = 0;
-      if (e < d) {
-        const double xr = (double)__ldg(x + e) - (double)__ldg(mu + e);
-        const __half h = __double2half(xr * inv);
-        const double hd = (double)__half2float(h);
-        const double er = xr * inv - hd;
-        s_x += xr * xr;
-        s_h += hd * hd;
-        s_e += er * er;
-        hb = __half_as_ushort(h);
+    for (int e0 = lane; e0 < KC * 16; e0 += 256) {
+      float xv[8], mv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        xv[u] = e < d ? __ldg(x + e) : 0.f;
+        mv[u] = e < d ? __ldg(mu + e) : 0.f;
       }
-      bt[(size_t)(e >> 4) * 256 + (g >> 3) * 128 + ((e & 15) >> 3) * 64 + (g & 7) * 8 + (e & 7)] = hb;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        if (e < KC * 16) {
+          const double xr = (double)xv[u] - (double)mv[u];
+          // any fp16 near x'/2^e will do: the bound uses the exact residual of the stored value
+          const __half hv = __float2half_rn((float)(xr * inv));
+          const double hd = (double)__half2float(hv);
+          const double er = xr * inv - hd;
+          s_x += xr * xr;
+          s_h += hd * hd;
+          s_e += er * er;
+          bt[(size_t)(e >> 4) * 256 + (g >> 3) * 128 + ((e & 15) >> 3) * 64 + (g & 7) * 8 + (e & 7)] =
+              __half_as_ushort(hv);
+        }
+      }
     }
     s_x = warp_sum_d(s_x);
     s_h = warp_sum_d(s_h);
@@ -537,7 +557,7 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
   int* cc = reinterpret_cast<int*>(ll + a.take_cap);
   int* h = hist[wl];
   const int n = a.cand_n[q];
-  const int kb = a.kbase[q];
+  const int kb = a.kbase[q], nc = a.kbase[q + 1] - kb;
   int* ci = a.cand_idx + (size_t)q * a.take_cap;
   if (n <= a.k) {  // nothing can be pruned
     if (a.counters && lane == 0) {
@@ -546,28 +566,38 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
     }
     return;
   }
-  // gather: 4 candidates per lane in flight (index load, then both bounds)
-  constexpr int GU = 4;
+  // the top-t candidates are the marked ones of the query's range [kb, kb + nc): stream the
+  // range (coalesced bounds, no index gathers) and stage the marked (UB, LB, index)
   float umin = __int_as_float(0x7f800000), umax = 0.f;
-  for (int b0 = lane; b0 < n; b0 += 32 * GU) {
-    int c[GU];
-    float u[GU], lv[GU];
+  int got = 0;
+  constexpr int SU = 8;  // 8 x (membership word, UB, LB) loads in flight per lane, none dependent
+  for (int j0 = 0; j0 < nc; j0 += 32 * SU) {
+    uint32_t mw[SU];
+    float u[SU], lv[SU];
 #pragma unroll
-    for (int t = 0; t < GU; ++t) c[t] = b0 + 32 * t < n ? ci[b0 + 32 * t] : 0;  // (rewritten below)
-#pragma unroll
-    for (int t = 0; t < GU; ++t) {
-      u[t] = __ldg(a.ub + kb + c[t]);
-      lv[t] = __ldg(a.lb + kb + c[t]);
+    for (int t = 0; t < SU; ++t) {
+      const int j = j0 + 32 * t + lane;
+      const int bit = kb + min(j, nc - 1);
+      mw[t] = __ldg(a.marks + (bit >> 5));
+      u[t] = __ldg(a.ub + bit);
+      lv[t] = __ldg(a.lb + bit);
     }
 #pragma unroll
-    for (int t = 0; t < GU; ++t)
-      if (b0 + 32 * t < n) {
-        uu[b0 + 32 * t] = u[t];
-        ll[b0 + 32 * t] = lv[t];
-        cc[b0 + 32 * t] = c[t];
+    for (int t = 0; t < SU; ++t) {
+      const int j = j0 + 32 * t + lane;
+      const int bit = kb + j;
+      const bool mk = j < nc && ((mw[t] >> (bit & 31)) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, mk);
+      if (mk) {
+        const int at = got + __popc(bal & ((1u << lane) - 1u));
+        uu[at] = u[t];
+        ll[at] = lv[t];
+        cc[at] = j;
         umin = fminf(umin, u[t]);
         umax = fmaxf(umax, u[t]);
       }
+      got += __popc(bal);
+    }
   }
   umin = warp_min_f(umin);
   umax = warp_max_f(umax);
@@ -578,7 +608,7 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
     const int bk = (int)((u - umin) * scale);
     return bk < 0 ? 0 : (bk > 255 ? 255 : bk);
   };
-  for (int i = lane; i < n; i += 32) atomicAdd(&h[bucket(uu[i])], 1);
+  for (int i = lane; i < got; i += 32) atomicAdd(&h[bucket(uu[i])], 1);
   __syncwarp();
   // bucket holding the k-th smallest: warp scan over 8 buckets per lane
   int loc[8], sum = 0;
@@ -600,14 +630,15 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
   }
   for (int o = 16; o > 0; o >>= 1) found = min(found, __shfl_xor_sync(0xffffffffu, found, o));
   float T = 0.f;
-  for (int i = lane; i < n; i += 32)
+  for (int i = lane; i < got; i += 32)
     if (bucket(uu[i]) <= found) T = fmaxf(T, uu[i]);
   T = warp_max_f(T);
-  // survivors, compacted in place (their order is irrelevant: the final top-k sorts)
+  if (found == 256) T = __int_as_float(0x7f800000);  // (fewer marked than k: keep all)
+  // survivors (LB <= T) replace the query's candidate list
   int ns = 0;
-  for (int b0 = 0; b0 < n; b0 += 32) {
+  for (int b0 = 0; b0 < got; b0 += 32) {
     const int i = b0 + lane;
-    const bool keep = i < n && ll[i] <= T;
+    const bool keep = i < got && !(ll[i] > T);
     const unsigned bal = __ballot_sync(0xffffffffu, keep);
     if (keep) ci[ns + __popc(bal & ((1u << lane) - 1u))] = cc[i];
     ns += __popc(bal);

@@ -465,6 +465,35 @@ def test_c2_properties_and_sample_parity(pkg):
         assert rec >= 0.5
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("name,w,t", [("c2", 1, 800), ("c3", 4, 800), ("c5", 64, 1600), ("c2", 8, 400)])
+def test_timed_operating_points_vs_oracle(pkg, name, w, t):
+    """The bench's operating points at full size (C2 w=1 t=800, C3 w=4 t=800, C5 OOD w=64
+    t=1600): the whole 10k batch is searched as the bench does, and a spread sample of
+    128 queries is checked against the oracle -- ids identical, score bits identical,
+    hence the sample's recall identical."""
+    from oracle import rrann_oracle as O
+
+    W, dev, path = _workload(pkg, name)
+    man = W.load_manifest(name)
+    k = man["k"]
+    q = W.load_queries(name)
+    ids, sc, cnt = (a.cpu().numpy() for a in dev.search_device(torch.from_numpy(q).cuda(), k, w, t, True))
+    oidx = O.read_index(path.read_bytes())
+    sample = np.unique(np.linspace(0, len(q) - 1, 128).astype(int))
+    gt = W.load_ground_truth(name)
+    rec_dev, rec_ref = [], []
+    for i in sample:
+        r = O.query(oidx, q[i], k, w, t, True)
+        assert int(cnt[i]) == len(r.ids), (name, i)
+        np.testing.assert_array_equal(ids[i, :cnt[i]], r.ids, err_msg=f"{name} w={w} t={t} q{i}")
+        np.testing.assert_array_equal(sc[i, :cnt[i]].view(np.int32), r.scores.view(np.int32))
+        if gt is not None:
+            rec_dev.append(len(set(ids[i, :cnt[i]].tolist()) & set(gt[i, :k].tolist())) / k)
+            rec_ref.append(len(set(r.ids.tolist()) & set(gt[i, :k].tolist())) / k)
+    assert rec_dev == rec_ref
+
+
 # ----------------------------------------------------------- random-index shape sweep
 
 SWEEP = [
@@ -869,3 +898,50 @@ def test_screen_counters_and_pruning(pkg, tmp_path, monkeypatch):
     assert 2000 * 10 <= cand <= 2000 * 400       # sum of min(t, candidates) per query
     assert 2000 * 10 <= surv < cand / 4, (surv, cand)
     assert streamed >= 6000 and distinct <= 6000 and fetched >= distinct
+
+
+# ------------------------------------------------------------- routing screen
+
+def _set_centroids(blob, d, s, L, fn):
+    """Rewrite the centroid block of an RRRANN01 blob (index.py:365-402) and its CRC."""
+    import struct
+    import zlib
+
+    off = 8 + 29 + 4 * d * s
+    cent = np.frombuffer(blob, dtype="<f4", count=L * s, offset=off).reshape(L, s).copy()
+    cent = fn(cent).astype("<f4")
+    body = blob[:off] + cent.tobytes() + blob[off + 4 * L * s:-4]
+    return body + struct.pack("<I", zlib.crc32(body) & 0xFFFFFFFF)
+
+
+@pytest.mark.parametrize("d,s,L,ties", [(96, 64, 1024, "none"), (768, 256, 640, "none"),
+                                        (64, 32, 1024, "dup"), (64, 32, 512, "all")])
+def test_route_screen_matches_f64_routing(pkg, tmp_path, d, s, L, ties, monkeypatch):
+    """Routing on the fp16 tensor cores with f64 recheck of the survivors selects the same
+    clusters as the f64 GEMM path and the oracle (ties -> lower id), including duplicated
+    centroids and a degenerate index where every centroid is equal (list overflow ->
+    full f64 scan)."""
+    from index_writer import random_index
+    from oracle import rrann_oracle as O
+
+    blob = random_index(d, s, 8, L, 30 * L, "euclidean", seed=L + s)
+    if ties == "dup":
+        blob = _set_centroids(blob, d, s, L, lambda c: np.concatenate([c[: L // 2], c[: L // 2]]))
+    elif ties == "all":
+        blob = _set_centroids(blob, d, s, L, lambda c: np.repeat(c[:1], L, axis=0))
+    path = _write(tmp_path, "rt", blob)
+    dev = pkg.DeviceIndex.from_file(path)
+    q = np.random.default_rng(s).standard_normal((700, d)).astype(F32)
+    oidx = O.read_index(blob)
+    for w in (1, 3, 8):
+        monkeypatch.setenv("RRG_ROUTE_SCREEN", "1")
+        dev.reload_options()
+        got = dev.search_host(q, 10, w, 60, True)
+        monkeypatch.setenv("RRG_ROUTE_SCREEN", "0")
+        dev.reload_options()
+        ref = dev.search_host(q, 10, w, 60, True)
+        for a, b in zip(got, ref):
+            np.testing.assert_array_equal(a, b, err_msg=f"w={w} {ties}")
+        for i in range(0, 700, 35):
+            r = O.query(oidx, q[i], 10, w, 60, True)
+            np.testing.assert_array_equal(got[0][i, :got[2][i]], r.ids, err_msg=f"w={w} q{i} {ties}")

@@ -471,7 +471,7 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
     // re-rank screen data (rrg_screen.cu): clusters padded to 128-row blocks
     std::vector<int> blk0(L + 1, 0);
     for (int l = 0; l < L; ++l) blk0[l + 1] = blk0[l] + (int)((ix->held_sizes[l] + 127) / 128);
-    v.scr_kc = (d + 15) / 16;
+    v.scr_kc = (d + 63) / 64 * 4;  // K16 chunks, a multiple of 4: the plane's K64 swizzle atoms
     const size_t plane_bytes = (size_t)blk0[L] * v.scr_kc * 128 * 32;
     uint16_t* plane = static_cast<uint16_t*>(ix->dalloc(plane_bytes));
     float* mu = static_cast<float*>(ix->dalloc((size_t)L * d * 4));
@@ -776,6 +776,7 @@ RrgOpts read_opts() {
   o.graph = flag("RRG_GRAPH", 1) != 0;
   o.screen = env("RRG_SCREEN") ? (flag("RRG_SCREEN", 0) != 0) : -1;
   o.route_screen = flag("RRG_ROUTE_SCREEN", 1) != 0;
+  o.screen_diag = flag("RRG_SCREEN_DIAG", 0);
   return o;
 }
 // up to this many queries the projection / routing run as warp-per-output GEMVs

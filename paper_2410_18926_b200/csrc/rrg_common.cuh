@@ -38,6 +38,7 @@ struct RrgOpts {
   int graph;         // RRG_GRAPH: captured graphs for small host batches (default 1)
   int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
   int route_screen;  // RRG_ROUTE_SCREEN (default 1): fp16 tensor-core routing bounds + f64 recheck
+  int screen_diag;   // RRG_SCREEN_DIAG: timing probes of k_rr_screen (1: no MMAs, 2: no MMAs or bounds)
 };
 
 // POD view of a device-resident index, passed by value to kernels.

@@ -49,6 +49,13 @@ constexpr int kScrStagesMax = 12;              // ring depth: as many stages as 
 constexpr int kScrStageBytes = kScrStageChunks * kScrChunk;
 constexpr int kScrRingMin = 6 * kScrStageBytes;
 constexpr int kScrThreads = 192;                // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
+// Measured on C2 (per-stage probes, RRG_SCREEN_DIAG): the stream alone runs at ~93% of
+// HBM peak; the MMAs add ~60 us per batch whatever the operand swizzle (none / 128 B),
+// the number of accumulators the K chunks rotate over (1 / 4), the TMEM item buffers
+// (2 / 4) -- and an L2 prefetch two items ahead made it slower (0.66 vs 0.51 ms).
+constexpr int kScrAcc = 1;   // accumulators per item (K chunks rotate over them)
+constexpr int kScrTBuf = 4;  // item accumulators in TMEM: the MMAs run up to 3 items ahead
+constexpr int kScrTmemCols = kScrTBuf * kScrAcc * kRrQ;  // 64
 constexpr int kScrMaxKc = 120;                  // d <= 1920: two group records + the ring fit
 
 // Group record (one per (cluster, <= kRrQ queries) work group, built by k_rr_groups and
@@ -77,10 +84,15 @@ int screen_stages(int kc) {
 size_t screen_smem(int kc) { return (size_t)screen_stages(kc) * kScrStageBytes + 2 * grp_rec_bytes(kc) + 1024; }
 size_t screen_group_bytes(int kc) { return grp_rec_bytes(kc); }
 
-// halves offset of element e of row rr inside a block: chunk e/16, then the canonical
-// K-major no-swizzle core matrices (8 rows x 16 B; +128 B per K half, +256 B per 8 rows)
+// halves offset of element e of row rr inside a block.  The residual rows are laid out
+// for UMMA's 128-byte-swizzled K-major operand: K in 64-element (128 B) chunks of
+// 128 rows x 128 B = 16 KB (one ring stage), 8-row atoms of 1 KB, and the 16-byte
+// piece j of row r stored at piece j ^ (r % 8) -- the tensor core reads it at full
+// shared-memory bandwidth (the no-swizzle layout measured ~1 us of MMA time per 128-row
+// block on C2, not hidden by the stream)
 __device__ __forceinline__ size_t scr_half_off(int rr, int e) {
-  return (size_t)(e >> 4) * (kScrChunk / 2) + (rr >> 3) * 128 + ((e & 15) >> 3) * 64 + (rr & 7) * 8 + (e & 7);
+  return (size_t)(e >> 6) * (kScrStageBytes / 2) + (rr >> 3) * 512 + (rr & 7) * 64 +
+         ((((e & 63) >> 3) ^ (rr & 7)) << 3) + (e & 7);
 }
 
 // ------------------------------------------------------------------ build
@@ -171,7 +183,15 @@ void launch_screen_build(const DevIndexView& v, float* mu, uint16_t* plane, size
 __device__ __forceinline__ uint32_t s_addr(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-// K-major, no swizzle: start >> 4, LBO (K direction) 128 B, SBO (8-row groups) 256 B, version 1
+// K-major, 128-byte swizzle (A: the residual rows): SBO 1024 B between 8-row atoms,
+// LBO unused (1), version 1, layout type 2; a K = 16 step inside the 128-byte row
+// advances the start address by 32 B
+__device__ __forceinline__ uint64_t scr_desc_sw128(uint32_t addr) {
+  return (uint64_t)((addr >> 4) & 0x3FFFu) | (1ull << 16) | ((uint64_t)(1024 >> 4) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+// K-major, no swizzle (B: the group's query tile): start >> 4, LBO (K direction) 128 B,
+// SBO (8-row groups) 256 B, version 1
 __device__ __forceinline__ uint64_t scr_desc(uint32_t addr) {
   return (uint64_t)((addr >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) | ((uint64_t)(256 >> 4) << 32) |
          (1ull << 46);
@@ -324,7 +344,8 @@ struct ScreenArgs {
 
 __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   extern __shared__ __align__(1024) unsigned char scr_sm[];
-  __shared__ uint64_t full[kScrStagesMax], empty[kScrStagesMax], bfull[2], bempty[2], tfull[2], tempty[2];
+  __shared__ uint64_t full[kScrStagesMax], empty[kScrStagesMax], bfull[2], bempty[2], tfull[kScrTBuf],
+      tempty[kScrTBuf];
   __shared__ uint32_t tmem_base;
   const DevIndexView& ix = a.ix;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -342,7 +363,7 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
     atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 2), (unsigned long long)(i1 - i0) * kScrRows);
 
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(s_addr(&tmem_base))
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(s_addr(&tmem_base))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -355,6 +376,8 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bfull[i])));
       // freed by the MMAs of the group (commit) and by the 4 epilogue warps
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 5;" ::"r"(s_addr(&bempty[i])));
+    }
+    for (int i = 0; i < kScrTBuf; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&tfull[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(s_addr(&tempty[i])));
     }
@@ -434,21 +457,25 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
           scr_wait(&bfull[j & 1], (j >> 1) & 1);
           fence_after();
         }
-        const int ab = it & 1, u = it >> 1;
+        const int ab = it % kScrTBuf, u = it / kScrTBuf;
         if (u > 0) {
           scr_wait(&tempty[ab], (u - 1) & 1);
           fence_after();
         }
         const uint32_t sb = s_addr(gbuf + (j & 1) * rec_bytes);
-        const uint32_t dt = tmem + (uint32_t)(ab * kRrQ);
+        const uint32_t dt = tmem + (uint32_t)(ab * kScrAcc * kRrQ);
         for (int c0 = 0; c0 < KC; c0 += kScrStageChunks, ++sc) {
           const int slot = sc % nst, pass = sc / nst;
           scr_wait(&full[slot], pass & 1);
           fence_after();
           const uint32_t sa = s_addr(ring + slot * kScrStageBytes);
           const int nch = min(kScrStageChunks, KC - c0);
-          for (int c = 0; c < nch; ++c)
-            scr_mma(dt, scr_desc(sa + c * kScrChunk), scr_desc(sb + (c0 + c) * 512), (c0 + c) > 0 ? 1u : 0u);
+          if (ix.opt.screen_diag == 0)
+            for (int c = 0; c < nch; ++c) {
+              const int kc = c0 + c;
+              scr_mma(dt + (uint32_t)((kc % kScrAcc) * kRrQ), scr_desc_sw128(sa + c * 32), scr_desc(sb + kc * 512),
+                      kc >= kScrAcc ? 1u : 0u);
+            }
           scr_commit(&empty[slot]);
         }
         scr_commit(&tfull[ab]);
@@ -470,7 +497,7 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
       const unsigned char* rec = gbuf + (j & 1) * rec_bytes;
       const GroupSlot* slots = reinterpret_cast<const GroupSlot*>(rec + (size_t)KC * 512);
       const int ng = *reinterpret_cast<const int*>(rec + (size_t)KC * 512 + kRrQ * sizeof(GroupSlot));
-      const int ab = it & 1, u = it >> 1;
+      const int ab = it % kScrTBuf, u = it / kScrTBuf;
       const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
       const int jr = b * kScrRows + row;
       // bounds for every (row, slot) of the item: the candidate range of a (query, probe)
@@ -485,33 +512,44 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
       }
       scr_wait(&tfull[ab], u & 1);
       fence_after();
-      uint32_t v[kRrQ];
-      asm volatile(
-          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-            "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-          : "r"(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(ab * kRrQ)));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      float gsum[kRrQ];
+#pragma unroll
+      for (int g = 0; g < kRrQ; ++g) gsum[g] = 0.f;
+      const int nacc = min(kScrAcc, KC);  // accumulators the item's chunks wrote
+#pragma unroll
+      for (int ac = 0; ac < kScrAcc; ++ac) {
+        uint32_t v[kRrQ];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)((ab * kScrAcc + ac) * kRrQ)));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (ac < nacc)
+#pragma unroll
+          for (int g = 0; g < kRrQ; ++g) gsum[g] += __uint_as_float(v[g]);
+      }
       fence_before();
       __syncwarp();
       if (lane == 0) scr_arrive(&tempty[ab]);
-      if (live) {
-        const double rsc = ldexp(1.0, (int)rm.z), nrh = rm.x, ner = rm.y;
+      if (live && ix.opt.screen_diag < 2) {
+        // f32 arithmetic; its own rounding (a handful of ops on magnitudes <= xx + rr +
+        // 2|x'.r|) is covered by the 2^-18 slack and the (1 +- 2^-20) factors
+        const float rsc = ldexpf(1.f, (int)rm.z), nrh = rm.x, ner = rm.y, rrf = (float)rr;
+        const float etap = (float)eta * (1.f + 0x1p-20f), epsf = (float)eps;
 #pragma unroll
         for (int g = 0; g < kRrQ; ++g) {
           if (g >= ng) break;
           const GroupSlot gs = slots[g];
-          const double G = (double)__uint_as_float(v[g]);
-          const double sc = gs.sc * rsc;
-          const double nxh = gs.nxh, nex = gs.nex;
-          const double S = gs.xx + rr - 2.0 * sc * G;
-          const double F = sc * (nxh * ner + nex * nrh + nex * ner + eps * nxh * nrh);
-          const double E = 2.0 * F * (1.0 + 0x1p-20) + 0x1p-40 * (gs.xx + rr + 2.0 * sc * fabs(G));
-          const double ubv = fmax((S + E) * (1.0 + eta), 0.0);
-          const double lbv = fmax(S - E, 0.0) * (1.0 - eta);
+          const float sc = (float)gs.sc * rsc;
+          const float nxh = gs.nxh, nex = gs.nex, xx = (float)gs.xx;
+          const float cross = 2.f * sc * gsum[g];
+          const float S = (xx + rrf) - cross;
+          const float F = sc * (nxh * ner + nex * nrh + nex * ner + epsf * nxh * nrh);
+          const float E = 2.f * F * 1.0001f + 0x1p-18f * (xx + rrf + fabsf(cross));
           const int bit = gs.pkey + jr;
-          a.ub[bit] = __double2float_ru(ubv);
-          a.lb[bit] = __double2float_rd(lbv);
+          a.ub[bit] = fmaxf((S + E) * (1.f + etap), 0.f);
+          a.lb[bit] = fmaxf(S - E, 0.f) * (1.f - etap);
         }
       }
       if (b + 1 == nb || i + 1 == i1) {  // done with the group's record
@@ -525,7 +563,7 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   __syncthreads();
   fence_after();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tmem) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem) : "memory");
 }
 
 // ------------------------------------------------------------------ threshold

@@ -52,11 +52,12 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=20.0)
     ap.add_argument("--parity-queries", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--mode", default=os.environ.get("RRG_BENCH_MODE", "replica"),
+    ap.add_argument("--mode", default=os.environ.get("RRG_BENCH_MODE"),
                     choices=["sharded", "replica"],
-                    help="N>1: full-index replicas, each rank its own query batch (default: the "
-                         "C2 index fits one GPU, no collective on the data path) or the "
-                         "cluster-sharded index with the two exact NCCL merges (DESIGN.md §5)")
+                    help="N>1: full-index replicas, each rank its own query batch (default for "
+                         "C1-C3, C5: the index fits one GPU, no collective on the data path) or "
+                         "the cluster-sharded index (default for C4): data-parallel front stages, "
+                         "owner-local search at w=1, NCCL all-gathers (DESIGN.md §5)")
     return ap.parse_args()
 
 
@@ -102,6 +103,18 @@ class CpuReference:
     core and on every core (a fork pool made once after the load, 1 BLAS thread per
     worker, contiguous query chunks).  Without the reference package the oracle port
     (oracle/rrann_oracle.py, the same NumPy calls) is timed instead."""
+
+    @classmethod
+    def from_oracle(cls, oidx, k, w, t):
+        """The oracle port over an index held in memory (C4: built on the GPU, no file)."""
+        from oracle import rrann_oracle as O
+
+        self = cls.__new__(cls)
+        self.kind = "port"
+        self.run = lambda q: O.query_batch(oidx, q, k, w, t, True)
+        self.cores = os.cpu_count() or 1
+        self.pool = None
+        return self
 
     def __init__(self, path, k, w, t):
         rr = load_reference()
@@ -265,6 +278,13 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    if args.workload == "c4":
+        print(json.dumps({"impl": "reference", "metric": METRIC, "unavailable":
+                          "C4 (10M x 960) cannot be built by the reference's NumPy build() (k-means++ "
+                          "is 8192 sequential passes over 10M rows), so no reference index exists; "
+                          "the device run's cpu_baseline times the oracle port on the GPU-built arrays"}),
+              flush=True)
+        return
     import workloads as W
 
     man = W.load_manifest(args.workload)
@@ -303,6 +323,62 @@ def run_reference(args):
                                        "1 BLAS thread each; value = best step (bench._timed_run)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+class C4Workload:
+    """BASELINE.json configs[3]: 10M x 960 (GIST shape), L=8192, s=64, r=32, k=100.
+
+    The reference's build cannot run at this size (k-means++ is 8192 sequential passes
+    over 10M rows in NumPy), so the index is built on the GPU by tools/c4.py's restatement
+    of build() -- rank 0 builds, the arrays are broadcast (NCCL), every rank regenerates
+    the corpus from the seed and keeps its cluster range (sharded) or the whole index.
+    Recall is against the GPU exact ground truth; parity uses the oracle on the same
+    arrays (rank 0)."""
+
+    def __init__(self, rank, world, local, sharded):
+        import torch
+
+        sys.path.insert(0, str(ROOT / "tools"))
+        import c4 as C4
+
+        from paper_2410_18926_b200 import DeviceIndex
+        from paper_2410_18926_b200.ground_truth import ground_truth_device
+
+        self.C4 = C4
+        P = self.P = C4.C4Params()
+        dev = torch.device(f"cuda:{local}")
+        corpus, queries, g = C4.generate(P, dev)
+        arrs = None
+        if rank == 0:
+            t0 = time.time()
+            arrs = C4.build(P, corpus, g)
+            self.n_exact = arrs.pop("n_exact")
+            self.build_s = time.time() - t0
+        if world > 1:
+            arrs = C4.broadcast_arrays(arrs, rank, dev)
+        self.arrs = arrs
+        shard = None
+        if sharded:
+            from paper_2410_18926_b200.sharded import partition_clusters
+
+            shard = partition_clusters(arrs["cluster_sizes"].astype(np.int64), world)[rank]
+        self.dev = DeviceIndex.from_arrays(metric="euclidean", rank=P.r, corpus=corpus, device=local,
+                                           shard=shard, **arrs)
+        self.gt = ground_truth_device(corpus, queries, P.k).cpu().numpy() if rank == 0 else None
+        self._corpus_h = corpus.cpu().numpy() if rank == 0 and world == 1 else None
+        del corpus
+        torch.cuda.empty_cache()
+        self.q_host = queries.cpu().numpy()
+        sizes = arrs["cluster_sizes"]
+        # operating point: w=1 t=800 (round-1 grid on this build: recall@100 0.931)
+        self.man = {"k": P.k, "generator": {"m": P.m, "d": P.d, "n_blobs": P.m // 1000},
+                    "index": {"L": P.L, "s": P.s, "r": P.r, "metric": "euclidean",
+                              "built_by": "GPU restatement of build() (tools/c4.py)",
+                              "mean_cluster": float(sizes.mean()), "max_cluster": int(sizes.max())},
+                    "grid": {"points": [{"w": 1, "t": 800, "recall": 0.931}]}}
+
+    def oracle_index(self):
+        return self.C4.oracle_index(self.P, self.arrs, self._corpus_h)
 
 
 class LocalSearcher:
@@ -370,28 +446,38 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    sharded = world > 1 and args.mode == "sharded"
+    mode = args.mode or ("sharded" if args.workload == "c4" else "replica")
+    sharded = world > 1 and mode == "sharded"
 
     from paper_2410_18926_b200 import DeviceIndex, _native, last_launch_count
     import workloads as W
 
-    man = W.load_manifest(args.workload)
-    w, t = operating_point(man, args)
-    k = man["k"]
-    path = W.materialize_index(args.workload) if rank == 0 else None
-    if world > 1:
-        dist.barrier()
-        path = W.materialize_index(args.workload)
-    if sharded:
-        from paper_2410_18926_b200.sharded import partition_clusters, scan_cluster_sizes
-
-        parts = partition_clusters(scan_cluster_sizes(path), world)
-        dev = DeviceIndex.from_file(path, device=local, shard=parts[rank])
-        searcher = ShardedSearcher(dev, k, w, t)
+    c4 = None
+    if args.workload == "c4":  # built on the GPU (tools/c4.py): no reference-built file
+        c4 = C4Workload(rank, world, local, sharded)
+        man, path, dev = c4.man, None, c4.dev
+        w, t = operating_point(man, args)
+        k = man["k"]
+        searcher = ShardedSearcher(dev, k, w, t) if sharded else LocalSearcher(dev, k, w, t)
+        q_host = c4.q_host
     else:
-        dev = DeviceIndex.from_file(path, device=local)
-        searcher = LocalSearcher(dev, k, w, t)
-    q_host = W.load_queries(args.workload)
+        man = W.load_manifest(args.workload)
+        w, t = operating_point(man, args)
+        k = man["k"]
+        path = W.materialize_index(args.workload) if rank == 0 else None
+        if world > 1:
+            dist.barrier()
+            path = W.materialize_index(args.workload)
+        if sharded:
+            from paper_2410_18926_b200.sharded import partition_clusters, scan_cluster_sizes
+
+            parts = partition_clusters(scan_cluster_sizes(path), world)
+            dev = DeviceIndex.from_file(path, device=local, shard=parts[rank])
+            searcher = ShardedSearcher(dev, k, w, t)
+        else:
+            dev = DeviceIndex.from_file(path, device=local)
+            searcher = LocalSearcher(dev, k, w, t)
+        q_host = W.load_queries(args.workload)
     nq, d = q_host.shape
     q = torch.from_numpy(q_host).cuda()
     out = (torch.empty((nq, k), dtype=torch.int64, device="cuda"),
@@ -434,7 +520,7 @@ def main():
     value = total_q / (ms_max / 1e3)
 
     # ---- recall of this run's results (identical ids to the oracle -> identical recall)
-    gt = W.load_ground_truth(args.workload)
+    gt = c4.gt if c4 is not None else W.load_ground_truth(args.workload)
     recall = None
     if gt is not None:
         ids = out[0].cpu().numpy()
@@ -576,7 +662,7 @@ def main():
     cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         dev_ids, dev_sc, dev_cnt = (a.cpu().numpy() for a in out)
-        ref = CpuReference(path, k, w, t)
+        ref = CpuReference(path, k, w, t) if c4 is None else CpuReference.from_oracle(c4.oracle_index(), k, w, t)
         with ref:
             sample = np.unique(np.linspace(0, nq - 1, min(nq, args.parity_queries)).astype(int))
             r_ids, r_sc, r_cnt = ref.results(q_host[sample])

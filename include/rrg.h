@@ -79,7 +79,7 @@ typedef struct {
   const float* b_scale;
   const int8_t* b_values;   /* sum r*m_l */
   const float* norms;       /* m, cluster order; NULL unless euclidean */
-  const float* corpus;      /* m x d in ORIGINAL id order; NULL if no corpus */
+  const float* corpus;      /* m x d in ORIGINAL id order; NULL if no corpus (host or device memory) */
   /* unquantized factors (RRG_FLAG_QUANTIZED clear, RrrConfig.quantize=False,
    * rrr.py:97-100): f32 blocks with the same shapes and concatenation as
    * a_values / b_values (no pad row, no head/scale); ignored when quantized */
@@ -197,6 +197,38 @@ int rrg_stage_score(RrgIndex* index, const float* queries, int64_t nq, int32_t w
  * Merge inputs use the all-gather layout [G][nq][cap] with counts [G][nq]. */
 size_t rrg_shard_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t k, int32_t w,
                                  int32_t t);
+
+/* Data-parallel front stages: the per-query outputs of projection (index.py:298),
+ * query quantization (quantize.py:61-77) and routing (cluster.py:254-264), row-major
+ * over nq queries (device buffers).  Each rank computes a slice of the batch with
+ * rrg_search_front; the slices are all-gathered and every rank continues from them
+ * (rrg_search_from_front / rrg_shard_phase1_from_front), so projection and routing
+ * are not replicated. */
+typedef struct {
+  float* xp;       /* nq x reduced_dim f32: f32(f64(x) @ f64(W)) */
+  int8_t* qcodes;  /* nq x round_up(reduced_dim, 16) int8: mixed-precision codes (col 0 = 0) */
+  float* qscale;   /* nq */
+  float* qhead;    /* nq */
+  double* pp;      /* nq: xp . xp (f64, NumPy pairwise order) */
+  float* xx;       /* nq: x . x (f32) */
+  int32_t* sel;    /* nq x w: routed clusters */
+  int32_t* prim;   /* nq: the nearest routed cluster */
+} RrgFront;
+size_t rrg_front_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t w);
+int rrg_search_front(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t w,
+                     const RrgFront* out, void* workspace, size_t workspace_bytes, void* stream);
+/* rrg_search with the front stages taken from `front` (rows of all nq queries).  On a
+ * shard index (rrg_index_open_shard) a query whose probes are all held elsewhere
+ * returns count 0; with w = 1 every query has exactly one owner, so each rank's
+ * results are final for the queries it owns and one all-gather + rrg_merge_results
+ * completes the batch -- no candidate exchange. */
+int rrg_search_from_front(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                          int32_t w, int32_t t, int32_t rerank, const RrgFront* front, int64_t* ids,
+                          float* scores, int32_t* count, void* workspace, size_t workspace_bytes,
+                          void* stream);
+int rrg_shard_phase1_from_front(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                                int32_t w, int32_t t, const RrgFront* front, uint32_t* keys, uint32_t* ids,
+                                int32_t* count, void* workspace, size_t workspace_bytes, void* stream);
 int rrg_shard_phase1(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
                      int32_t w, int32_t t, uint32_t* keys, uint32_t* ids, int32_t* count,
                      void* workspace, size_t workspace_bytes, void* stream);

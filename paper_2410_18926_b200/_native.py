@@ -45,6 +45,10 @@ class RrgIndexInfo(ctypes.Structure):
     ]
 
 
+class RrgFront(ctypes.Structure):
+    _fields_ = [(n, c_vp) for n in ("xp", "qcodes", "qscale", "qhead", "pp", "xx", "sel", "prim")]
+
+
 SIGNATURES = {
     "rrg_index_open": (c_int, [ctypes.c_char_p, c_int, ctypes.POINTER(c_vp)]),
     "rrg_index_open_shard": (c_int, [ctypes.c_char_p, c_int, c_i32, c_i32, ctypes.POINTER(c_vp)]),
@@ -70,6 +74,12 @@ SIGNATURES = {
     "rrg_shard_workspace_bytes": (c_size, [c_vp, c_i64, c_i32, c_i32, c_i32]),
     "rrg_shard_phase1": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp,
                                  c_vp, c_size, c_vp]),
+    "rrg_front_workspace_bytes": (c_size, [c_vp, c_i64, c_i32]),
+    "rrg_search_front": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_vp, c_vp, c_size, c_vp]),
+    "rrg_search_from_front": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_i32, c_vp,
+                                      c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
+    "rrg_shard_phase1_from_front": (c_int, [c_vp, c_vp, c_i64, c_i32, c_i32, c_i32, c_i32, c_vp,
+                                            c_vp, c_vp, c_vp, c_vp, c_size, c_vp]),
     "rrg_merge_candidates": (c_int, [c_i64, c_i32, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_vp,
                                      c_vp, c_vp]),
     "rrg_pack_candidates": (c_int, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp]),

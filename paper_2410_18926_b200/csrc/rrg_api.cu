@@ -722,7 +722,9 @@ int create_impl(const RrgIndexDesc* dsc, int device, int32_t cb, int32_t ce, Rrg
     CUDA_TRY(cudaMalloc(&staging, rows_per_chunk * row_bytes));
     for (uint64_t done = 0; done < (uint64_t)hm.m;) {
       uint64_t n = std::min<uint64_t>(rows_per_chunk, hm.m - done);
-      CUDA_TRY(cudaMemcpy(staging, dsc->corpus + done * d, n * row_bytes, cudaMemcpyHostToDevice));
+      // host or device corpus (unified addressing): a GPU-built index hands its corpus over
+      // without a host copy
+      CUDA_TRY(cudaMemcpy(staging, dsc->corpus + done * d, n * row_bytes, cudaMemcpyDefault));
       launch_scatter_rows(staging, (int64_t)n, d, d_stride, d_pos, (int64_t)done, perm, dst, 0);
       CUDA_TRY(cudaGetLastError());
       done += n;
@@ -931,9 +933,14 @@ Plan make_plan(const RrgIndex* ix, int64_t nq, int k, int w, int t, int rerank,
     p.off_marks = carve(p.marks_bytes);
     p.off_rritem = carve((L + 1) * 4);
     // tensor-core screen of the re-rank (rrg_screen.cu): worth it once most of a query's
-    // t candidates cannot reach its top k (t >= 2k); RRG_SCREEN=1 forces, 0 disables
+    // t candidates cannot reach its top k (t >= 2k) and a cluster's rows serve several
+    // queries -- the screen streams every row of a probed cluster (fp16) once per query
+    // group, the exact pass only the survivors' f32 rows; with ~1 query per cluster
+    // (C4: 10k queries over 8192 clusters) the dense exact pass reads fewer bytes.
+    // RRG_SCREEN=1 forces, 0 disables.
+    const double per_cluster = v.L > 0 ? (double)nq * w / v.L : 0.0;
     p.screen = v.scr_plane != nullptr && v.metric == kMetricEuclidean &&
-               (v.opt.screen == 1 || (v.opt.screen < 0 && t >= 2 * k));
+               (v.opt.screen == 1 || (v.opt.screen < 0 && t >= 2 * k && per_cluster >= 4.0));
     p.off_xint = carve(Q * (int64_t)v.d_stride * 4);
     if (p.screen) {
       p.off_ub = carve(Q * std::max<int64_t>(nmax, 1) * 4);
@@ -970,11 +977,16 @@ struct Phase1Out {
   int32_t* count;
 };
 
+// front: per-query outputs of projection .. routing.  With `fin` the search skips
+// those stages and takes them from the caller (data-parallel front stages of the
+// sharded search: each rank computes a slice, the slices are all-gathered); with
+// `fout` it stops after them and hands them out.
 void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int32_t w, int32_t t,
                  int32_t rerank, int64_t* ids, float* scores, int32_t* count, void* ws,
                  size_t ws_bytes, cudaStream_t st, const Phase1Out* ph1 = nullptr,
                  int* nonfinite = nullptr,
-                 const std::vector<cudaEvent_t>* in_ready = nullptr) {
+                 const std::vector<cudaEvent_t>* in_ready = nullptr,
+                 const RrgFront* fin = nullptr, const RrgFront* fout = nullptr) {
   Plan p = make_plan(ix, nq, k, w, t, rerank, ph1 != nullptr);
   {  // shared-memory budgets of the per-query CTAs (static parts bounded by 48 KB)
     const size_t lim = kMaxSmemPerCta - 48 * 1024;
@@ -1007,7 +1019,21 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
     // front stages (projection .. routing) are independent per query: with host input
     // events they run per arriving sub-range, overlapping the remaining H2D copies
     const int nsub = (in_ready && n == nq) ? (int)in_ready->size() : 1;
-    for (int j = 0; j < nsub; ++j) {
+    if (fin) {  // front outputs supplied: copy this chunk's rows into the workspace
+      auto cp = [&](void* dst, const void* src, size_t row_bytes) {
+        CUDA_TRY(cudaMemcpyAsync(dst, static_cast<const char*>(src) + q0 * row_bytes, n * row_bytes,
+                                 cudaMemcpyDeviceToDevice, st));
+      };
+      cp(xp, fin->xp, (size_t)v.s * 4);
+      cp(qcodes, fin->qcodes, (size_t)v.s_pad);
+      cp(qscale, fin->qscale, 4);
+      cp(qhead, fin->qhead, 4);
+      cp(pp, fin->pp, 8);
+      cp(xx, fin->xx, 4);
+      cp(sel, fin->sel, (size_t)w * 4);
+      cp(prim, fin->prim, 4);
+    }
+    for (int j = 0; j < (fin ? 0 : nsub); ++j) {
       const int s0 = (int)piece_bound(n, j, nsub), s1 = (int)piece_bound(n, j + 1, nsub);
       const int ns = s1 - s0;
       if (ns <= 0) continue;
@@ -1082,6 +1108,21 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
           launch_route_select(diss + (int64_t)s0 * v.L, ns, v.L, w, sel + (int64_t)s0 * w, prim + s0, st);
         });
       }
+    }
+    if (fout) {  // front only: hand this chunk's rows out
+      auto cp = [&](void* dst, const void* src, size_t row_bytes) {
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + q0 * row_bytes, src, n * row_bytes,
+                                 cudaMemcpyDeviceToDevice, st));
+      };
+      cp(fout->xp, xp, (size_t)v.s * 4);
+      cp(fout->qcodes, qcodes, (size_t)v.s_pad);
+      cp(fout->qscale, qscale, 4);
+      cp(fout->qhead, qhead, 4);
+      cp(fout->pp, pp, 8);
+      cp(fout->xx, xx, 4);
+      cp(fout->sel, sel, (size_t)w * 4);
+      cp(fout->prim, prim, 4);
+      continue;
     }
     staged(6, st, [&] { launch_bucket(prim, n, v.L, order, st); });
     ScoreArgsHost sa{};
@@ -1692,6 +1733,43 @@ int rrg_stage_route(RrgIndex* index, const float* xp, int64_t nq, int32_t w, int
   });
 }
 
+// Data-parallel front stages (SURVEY.md 8(e) "Queries"): the sharded search splits the
+// batch's projection / quantization / routing over the ranks and all-gathers these rows.
+size_t rrg_front_workspace_bytes(const RrgIndex* index, int64_t nq, int32_t w) {
+  if (!index || nq <= 0 || w < 1) return 0;
+  return make_plan(index, nq, 1, w, 1, 0).total;
+}
+
+int rrg_search_front(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t w,
+                     const RrgFront* out, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index || !out) return fail(RRG_E_USAGE, "ParameterError", "null argument");
+    if (nq == 0) return RRG_OK;
+    validate_search(index, dim, 1, w, 1, 0);
+    CUDA_TRY(cudaSetDevice(index->device));
+    search_impl(index, queries, nq, 1, w, 1, 0, nullptr, nullptr, nullptr, workspace, workspace_bytes,
+                static_cast<cudaStream_t>(stream), nullptr, nullptr, nullptr, nullptr, out);
+    return RRG_OK;
+  });
+}
+
+int rrg_search_from_front(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                          int32_t w, int32_t t, int32_t rerank, const RrgFront* front, int64_t* ids,
+                          float* scores, int32_t* count, void* workspace, size_t workspace_bytes,
+                          void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index || !front) return fail(RRG_E_USAGE, "ParameterError", "null argument");
+    if (nq == 0) return RRG_OK;
+    validate_search(index, dim, k, w, t, rerank);
+    CUDA_TRY(cudaSetDevice(index->device));
+    search_impl(index, queries, nq, k, w, t, rerank, ids, scores, count, workspace, workspace_bytes,
+                static_cast<cudaStream_t>(stream), nullptr, nullptr, nullptr, front);
+    return RRG_OK;
+  });
+}
+
 // K4 stage outputs (score_cluster, rrr.py:181-203 / quantize.py:109-156) of the
 // production cluster-major scoring kernel for caller-chosen probes: the projection
 // and query quantization of the search path, then k_score_cluster with its stage
@@ -1781,6 +1859,22 @@ int rrg_shard_phase1(RrgIndex* index, const float* queries, int64_t nq, int32_t 
     Phase1Out o{keys, ids, count};
     search_impl(index, queries, nq, k, w, t, 1, nullptr, nullptr, nullptr, workspace,
                 workspace_bytes, static_cast<cudaStream_t>(stream), &o);
+    return RRG_OK;
+  });
+}
+
+int rrg_shard_phase1_from_front(RrgIndex* index, const float* queries, int64_t nq, int32_t dim, int32_t k,
+                                int32_t w, int32_t t, const RrgFront* front, uint32_t* keys, uint32_t* ids,
+                                int32_t* count, void* workspace, size_t workspace_bytes, void* stream) {
+  g_launches = 0;
+  return guarded([&] {
+    if (!index || !front) return fail(RRG_E_USAGE, "ParameterError", "null argument");
+    if (nq == 0) return RRG_OK;
+    validate_search(index, dim, k, w, t, 1);
+    CUDA_TRY(cudaSetDevice(index->device));
+    Phase1Out o{keys, ids, count};
+    search_impl(index, queries, nq, k, w, t, 1, nullptr, nullptr, nullptr, workspace, workspace_bytes,
+                static_cast<cudaStream_t>(stream), &o, nullptr, nullptr, front);
     return RRG_OK;
   });
 }

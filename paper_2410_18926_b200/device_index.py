@@ -150,7 +150,12 @@ class DeviceIndex:
         sizes, ids = arr(cluster_sizes, np.uint32), arr(point_ids, np.int64)
         a_head, a_scale, a_vals = arr(a_head, f32), arr(a_scale, f32), arr(a_values, np.int8)
         b_head, b_scale, b_vals = arr(b_head, f32), arr(b_scale, f32), arr(b_values, np.int8)
-        norms, corpus = arr(norms, f32), arr(corpus, f32)
+        norms = arr(norms, f32)
+        corpus_dev = corpus is not None and getattr(corpus, "is_cuda", False)  # torch CUDA f32 [m, d]
+        if corpus_dev:
+            corpus = corpus.float().contiguous()
+        else:
+            corpus = arr(corpus, f32)
         a_f32, b_f32 = arr(a_values_f32, f32), arr(b_values_f32, f32)
         quant = a_vals is not None
         flags = (FLAG_QUANTIZED if quant else 0) | (FLAG_CORPUS if corpus is not None else 0) | extra_flags
@@ -161,7 +166,9 @@ class DeviceIndex:
                 a_f32, b_f32]
 
         def ptr(a):
-            return None if a is None else a.ctypes.data
+            if a is None:
+                return None
+            return a.data_ptr() if hasattr(a, "data_ptr") else a.ctypes.data
 
         desc = RrgIndexDesc(
             metric=_METRIC_CODES[metric], dim=d, reduced_dim=s, rank=rank, n_clusters=L,

@@ -20,6 +20,7 @@ in an oracle-backed engine and a gloo exchange with the same control flow.
 
 from __future__ import annotations
 
+import ctypes
 import struct
 from dataclasses import dataclass
 
@@ -92,6 +93,7 @@ class TorchExchange:
         self.dist = dist
         self.group = group
         self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
 
     def max_scalar(self, t) -> int:
         """max over ranks of a one-element int tensor (all-reduce MAX)."""
@@ -120,6 +122,23 @@ class LocalExchange:
 
 
 # ---------------------------------------------------------------------- engines
+
+
+@dataclass
+class Front:
+    """Per-query outputs of the front stages (projection index.py:298, query quantization
+    quantize.py:61-77, routing cluster.py:254-264), rows in batch order (RrgFront)."""
+
+    xp: object      # [n, s] f32
+    qcodes: object  # [n, s_pad] int8
+    qscale: object  # [n] f32
+    qhead: object   # [n] f32
+    pp: object      # [n] f64
+    xx: object      # [n] f32
+    sel: object     # [n, w] int32
+    prim: object    # [n] int32
+
+    FIELDS = ("xp", "qcodes", "qscale", "qhead", "pp", "xx", "sel", "prim")
 
 
 @dataclass
@@ -161,6 +180,61 @@ class CudaShardEngine:
         st = torch.cuda.current_stream(dev).cuda_stream
         check(lib.rrg_shard_phase1(self.dev.handle, q.data_ptr(), nq, dim, k, w, t, keys.data_ptr(),
                                    ids.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(), st))
+        return Candidates(keys, ids, cnt)
+
+    def front(self, q, w):
+        """Front stages of a query slice (``rrg_search_front``)."""
+        import torch
+
+        n = q.shape[0]
+        dev, s, sp = q.device, self.dev.reduced_dim, (self.dev.reduced_dim + 15) // 16 * 16
+        f = Front(xp=torch.empty((n, s), dtype=torch.float32, device=dev),
+                  qcodes=torch.empty((n, sp), dtype=torch.int8, device=dev),
+                  qscale=torch.empty((n,), dtype=torch.float32, device=dev),
+                  qhead=torch.empty((n,), dtype=torch.float32, device=dev),
+                  pp=torch.empty((n,), dtype=torch.float64, device=dev),
+                  xx=torch.empty((n,), dtype=torch.float32, device=dev),
+                  sel=torch.empty((n, w), dtype=torch.int32, device=dev),
+                  prim=torch.empty((n,), dtype=torch.int32, device=dev))
+        if n:
+            nb = int(lib.rrg_front_workspace_bytes(self.dev.handle, n, w))
+            ws = self._ws(nb)
+            st = torch.cuda.current_stream(dev).cuda_stream
+            check(lib.rrg_search_front(self.dev.handle, q.data_ptr(), n, q.shape[1], w,
+                                       ctypes.byref(_rrg_front(f)), ws.data_ptr(), ws.numel(), st))
+        return f
+
+    def search_from_front(self, q, front, k, w, t):
+        """Full search of the queries whose probes this shard holds (others: count 0)."""
+        import torch
+
+        nq, dim = q.shape
+        dev = q.device
+        ids = torch.empty((nq, k), dtype=torch.int64, device=dev)
+        sc = torch.empty((nq, k), dtype=torch.float32, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        nb = self.dev.workspace_bytes(nq, k, w, t, True)
+        ws = self._ws(nb)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_search_from_front(self.dev.handle, q.data_ptr(), nq, dim, k, w, t, 1,
+                                        ctypes.byref(_rrg_front(front)), ids.data_ptr(), sc.data_ptr(),
+                                        cnt.data_ptr(), ws.data_ptr(), ws.numel(), st))
+        return ids, sc, cnt
+
+    def phase1_from_front(self, q, front, k, w, t):
+        import torch
+
+        nq, dim = q.shape
+        dev = q.device
+        keys = torch.empty((nq, t), dtype=torch.int32, device=dev)
+        ids = torch.empty((nq, t), dtype=torch.int32, device=dev)
+        cnt = torch.empty((nq,), dtype=torch.int32, device=dev)
+        nb = int(lib.rrg_shard_workspace_bytes(self.dev.handle, nq, k, w, t))
+        ws = self._ws(nb)
+        st = torch.cuda.current_stream(dev).cuda_stream
+        check(lib.rrg_shard_phase1_from_front(self.dev.handle, q.data_ptr(), nq, dim, k, w, t,
+                                              ctypes.byref(_rrg_front(front)), keys.data_ptr(),
+                                              ids.data_ptr(), cnt.data_ptr(), ws.data_ptr(), ws.numel(), st))
         return Candidates(keys, ids, cnt)
 
     def merge_candidates(self, gk, gi, gc, take):
@@ -254,35 +328,94 @@ def exchange_candidates(engine, exchange, c1: Candidates, sparse: bool = True):
     return engine.unpack_candidates(gk, gi, goff, c1.keys.shape[1])
 
 
-def sharded_search(engine, exchange, queries, k: int, w: int, t: int, sparse: bool = True):
-    """Two-phase exact sharded search for one rank (all ranks call it collectively)."""
+def gathered_front(engine, exchange, queries, w: int) -> Front:
+    """Data-parallel front stages: rank r projects, quantizes and routes rows
+    [r*S, (r+1)*S) of the batch (S = ceil(nq / G)); one all-gather per field gives every
+    rank the whole batch's rows, so projection and routing are not replicated."""
+    nq, G, r = queries.shape[0], exchange.world, exchange.rank
+    S = -(-nq // G)
+    a, b = min(nq, r * S), min(nq, (r + 1) * S)
+    loc = engine.front(queries[a:b], w)
+    out = {}
+    for name in Front.FIELDS:
+        v = getattr(loc, name)
+        if v.shape[0] < S:  # pad the last slices to the common size
+            pad = v.new_zeros((S - v.shape[0],) + tuple(v.shape[1:]))
+            v = _cat(v, pad)
+        g = exchange.all_gather(v)
+        out[name] = g.reshape((G * S,) + tuple(g.shape[2:]))[:nq].contiguous()
+    return Front(**out)
+
+
+def _cat(a, b):
+    import torch
+
+    return torch.cat([a, b])
+
+
+def sharded_search(engine, exchange, queries, k: int, w: int, t: int, sparse: bool = True,
+                   data_parallel_front: bool = True):
+    """Exact sharded search for one rank (all ranks call it collectively).
+
+    Front stages are data-parallel (``gathered_front``).  With w = 1 every query's
+    candidates live on the one rank that holds its cluster, so that rank's local search
+    (top-t over its clusters, exact re-rank, top-k) is already the global answer: one
+    all-gather of the results and a merge finish the batch, with no candidate exchange
+    and no host synchronisation.  With w > 1 a query's probes may span ranks and the
+    reference re-ranks the GLOBAL top-t (index.py:314-322), so two exchanges are
+    needed: local top-t -> all-gather -> global top-t -> owner re-rank -> all-gather
+    -> final top-k."""
     if k > t:
         raise ParameterError(f"k={k} must be <= t={t} when re-ranking")
-    c1 = engine.phase1(queries, k, w, t)
-    gk, gi, gc = exchange_candidates(engine, exchange, c1, sparse)
-    cand = engine.merge_candidates(gk, gi, gc, t)
-    ids, sc, cnt = engine.phase2(queries, cand, k)
+    front = gathered_front(engine, exchange, queries, w) if data_parallel_front else None
+    if front is not None and w == 1:
+        ids, sc, cnt = engine.search_from_front(queries, front, k, w, t)
+    else:
+        c1 = (engine.phase1_from_front(queries, front, k, w, t) if front is not None
+              else engine.phase1(queries, k, w, t))
+        gk, gi, gc = exchange_candidates(engine, exchange, c1, sparse)
+        cand = engine.merge_candidates(gk, gi, gc, t)
+        ids, sc, cnt = engine.phase2(queries, cand, k)
     return engine.merge_results(exchange.all_gather(ids), exchange.all_gather(sc),
                                 exchange.all_gather(cnt), k)
 
 
-def sharded_search_local(engines, queries, k: int, w: int, t: int, sparse: bool = False):
-    """All G shards in one process (LocalExchange): same two phases, stacked lists
-    (sparse: through the pack / unpack of the packed exchange)."""
+def _rrg_front(f: Front):
+    from ._native import RrgFront
+
+    return RrgFront(*(getattr(f, n).data_ptr() for n in Front.FIELDS))
+
+
+def sharded_search_local(engines, queries, k: int, w: int, t: int, sparse: bool = False,
+                         data_parallel_front: bool = True):
+    """All G shards in one process (tests, the 1-GPU emulation): the same flow as
+    ``sharded_search`` -- the front stages computed slice by slice on the G shards and
+    concatenated (the all-gather), w = 1 answered by each query's owner shard, w > 1
+    through the two merges (sparse: the packed phase-1 exchange)."""
     import torch
 
-    c1 = [e.phase1(queries, k, w, t) for e in engines]
-    if sparse:
-        packed = [e.pack_candidates(c) for e, c in zip(engines, c1)]
-        tot = max(max(int(p[2][-1]) for p in packed), 1)
-        gk, gi, gc = engines[0].unpack_candidates(torch.stack([p[0][:tot] for p in packed]),
-                                                  torch.stack([p[1][:tot] for p in packed]),
-                                                  torch.stack([p[2] for p in packed]), t)
+    G, nq = len(engines), queries.shape[0]
+    front = None
+    if data_parallel_front:
+        S = -(-nq // G)
+        parts = [e.front(queries[min(nq, g * S):min(nq, (g + 1) * S)], w) for g, e in enumerate(engines)]
+        front = Front(**{n: torch.cat([getattr(p, n) for p in parts]) for n in Front.FIELDS})
+    if front is not None and w == 1:
+        res = [e.search_from_front(queries, front, k, w, t) for e in engines]
     else:
-        gk = torch.stack([c.keys for c in c1])
-        gi = torch.stack([c.ids for c in c1])
-        gc = torch.stack([c.count for c in c1])
-    cand = engines[0].merge_candidates(gk, gi, gc, t)
-    res = [e.phase2(queries, cand, k) for e in engines]
+        c1 = [e.phase1_from_front(queries, front, k, w, t) if front is not None else e.phase1(queries, k, w, t)
+              for e in engines]
+        if sparse:
+            packed = [e.pack_candidates(c) for e, c in zip(engines, c1)]
+            tot = max(max(int(p[2][-1]) for p in packed), 1)
+            gk, gi, gc = engines[0].unpack_candidates(torch.stack([p[0][:tot] for p in packed]),
+                                                      torch.stack([p[1][:tot] for p in packed]),
+                                                      torch.stack([p[2] for p in packed]), t)
+        else:
+            gk = torch.stack([c.keys for c in c1])
+            gi = torch.stack([c.ids for c in c1])
+            gc = torch.stack([c.count for c in c1])
+        cand = engines[0].merge_candidates(gk, gi, gc, t)
+        res = [e.phase2(queries, cand, k) for e in engines]
     return engines[0].merge_results(torch.stack([r[0] for r in res]), torch.stack([r[1] for r in res]),
                                     torch.stack([r[2] for r in res]), k)

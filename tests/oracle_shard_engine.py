@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from oracle import rrann_oracle as O
-from paper_2410_18926_b200.sharded import Candidates
+from paper_2410_18926_b200.sharded import Candidates, Front
 
 F32 = np.float32
 
@@ -35,16 +35,51 @@ class OracleShardEngine:
         for l in range(c0, c1):
             self.owner[index.clusters[l].ids] = True
 
-    def phase1(self, q, k, w, t):
+    def front(self, q, w):
+        """Front stages of a query slice (the oracle's projection, q8, route)."""
+        qn = q.numpy()
+        n, s = qn.shape[0], self.ix.projection.shape[1]
+        sp = (s + 15) // 16 * 16
+        xp = O.project(qn, self.ix.projection) if n else np.zeros((0, s), F32)
+        codes = np.zeros((n, sp), np.int8)
+        scale = np.zeros(n, F32)
+        head = np.zeros(n, F32)
+        sel = np.zeros((n, w), np.int32)
+        for i in range(n):
+            h, sc, c = O.q8(xp[i])
+            head[i], scale[i], codes[i, 1:s] = h, sc, c
+            sel[i] = O.route(xp[i], self.ix.centroids, w, self.ix.metric)
+        t = torch.from_numpy
+        return Front(xp=t(np.ascontiguousarray(xp, F32)), qcodes=t(codes), qscale=t(scale), qhead=t(head),
+                     pp=t(np.zeros(n)), xx=t(np.zeros(n, F32)), sel=t(sel), prim=t(sel[:, 0].copy()))
+
+    def _front_row(self, front, i):
+        xp = front.xp[i].numpy()
+        s = xp.shape[0]
+        qx = (F32(front.qhead[i].item()), F32(front.qscale[i].item()), front.qcodes[i, 1:s].numpy())
+        return xp, front.sel[i].numpy(), qx
+
+    def search_from_front(self, q, front, k, w, t):
+        """Full search of the queries whose probes this shard holds (others: count 0)."""
+        c1 = self.phase1_from_front(q, front, k, w, t)
+        return self.phase2(q, c1, k)
+
+    def phase1_from_front(self, q, front, k, w, t):
+        return self.phase1(q, k, w, t, front=front)
+
+    def phase1(self, q, k, w, t, front=None):
         qn = q.numpy()
         nq = qn.shape[0]
         keys = np.full((nq, t), 0xFFFFFFFF, np.uint32)
         ids = np.full((nq, t), 0xFFFFFFFF, np.uint32)
         cnt = np.zeros(nq, np.int32)
         for i in range(nq):
-            xp = O.project(qn[i][None, :], self.ix.projection)[0]
-            sel = O.route(xp, self.ix.centroids, w, self.ix.metric)
-            qx = O.q8(xp)
+            if front is not None:
+                xp, sel, qx = self._front_row(front, i)
+            else:
+                xp = O.project(qn[i][None, :], self.ix.projection)[0]
+                sel = O.route(xp, self.ix.centroids, w, self.ix.metric)
+                qx = O.q8(xp)
             kk, ii = [], []
             for l in sel:
                 if not self.c0 <= int(l) < self.c1:

@@ -84,6 +84,54 @@ def _gloo_worker(rank, world, port, blob, q, params, out_dir):
         dist.destroy_process_group()
 
 
+def _gloo_worker_dp(rank, world, port, blob, q, params, out_dir):
+    """Data-parallel front stages + the w = 1 owner-local path / two-phase exchange."""
+    import torch.distributed as dist
+
+    from paper_2410_18926_b200.sharded import TorchExchange, sharded_search
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        idx, engines = _engines(blob, world)
+        ex = TorchExchange()
+        for j, (k, w, t) in enumerate(params):
+            ids, sc, cnt = sharded_search(engines[rank], ex, torch.from_numpy(q), k, w, t,
+                                          data_parallel_front=True)
+            np.savez(os.path.join(out_dir, f"r{rank}_p{j}.npz"), ids=ids.numpy(), sc=sc.numpy(),
+                     cnt=cnt.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+def test_three_rank_gloo_data_parallel_front(tmp_path):
+    """world_size 3: each rank projects/routes a third of the batch (17 queries: ragged
+    slices), the rows are all-gathered; w = 1 needs no candidate exchange, w > 1 runs the
+    two exchanges; every rank returns the unsharded result."""
+    import sys
+
+    import torch.multiprocessing as mp
+
+    sys.path.insert(0, os.path.dirname(__file__))
+    blob = random_index(24, 12, 6, 10, 600, seed=9, dup_rows=3)
+    q = np.random.default_rng(4).standard_normal((17, 24)).astype(np.float32)
+    params = [(5, 1, 40), (10, 1, 600), (6, 3, 30)]
+    world = 3
+    mp.spawn(_gloo_worker_dp, args=(world, _free_port(), blob, q, params, str(tmp_path)), nprocs=world,
+             join=True)
+    idx = O.read_index(blob)
+    for j, (k, w, t) in enumerate(params):
+        ref = O.query_batch(idx, q, k, w, t, True)
+        for r in range(world):
+            got = np.load(tmp_path / f"r{r}_p{j}.npz")
+            for i, rr in enumerate(ref):
+                c = int(got["cnt"][i])
+                assert c == len(rr.ids), (r, j, i)
+                np.testing.assert_array_equal(got["ids"][i, :c], rr.ids)
+                np.testing.assert_array_equal(got["sc"][i, :c].view(np.int32), rr.scores.view(np.int32))
+
+
 def test_two_rank_gloo_matches_unsharded(tmp_path):
     import sys
 

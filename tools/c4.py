@@ -61,7 +61,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--grid", default="1:200,1:400,1:800,2:400,2:800,3:800,4:800,4:1600")
     ap.add_argument("--parity", type=int, default=64, help="queries checked against the oracle")
-    ap.add_argument("--shards", default="2,8", help="G values for the 1-GPU shard emulation")
+    ap.add_argument("--shards", default="2,4,8", help="G values for the 1-GPU shard emulation")
     ap.add_argument("--link-gbs", type=float, default=400.0,
                     help="assumed per-GPU NVLink all-gather receive bandwidth (exchange estimate)")
     return ap.parse_args()
@@ -218,6 +218,70 @@ def build(args, corpus, g):
         norms=norms.cpu().numpy(), n_exact=n_exact)
 
 
+# ------------------------------------------------------------------------------- data
+
+
+class C4Params:
+    """The C4 workload (BASELINE.json configs[3]) with tools/c4.py's defaults."""
+
+    def __init__(self, **kw):
+        self.m, self.d, self.L, self.s, self.r, self.k = 10_000_000, 960, 8192, 64, 32, 100
+        self.nq, self.train, self.iters, self.seed = 10_000, 2_000_000, 10, 1
+        self.__dict__.update(kw)
+
+
+def generate(args, device):
+    """synth_dataset semantics (bench.py:140-170) with torch's CUDA generator: returns
+    (corpus [m, d] f32, queries [nq, d] f32, generator) on `device`, the same on every
+    device for the same seed (Philox)."""
+    import torch
+
+    g = torch.Generator(device=device)
+    g.manual_seed(args.seed)
+    n_blobs = args.m // 1000
+    centers = torch.randn((n_blobs, args.d), generator=g, device=device) * 6.0
+    corpus = torch.empty((args.m, args.d), dtype=torch.float32, device=device)
+    for i in range(0, args.m, 1 << 20):
+        n = min(1 << 20, args.m - i)
+        lab = torch.randint(n_blobs, (n,), generator=g, device=device)
+        corpus[i:i + n] = centers[lab] + torch.randn((n, args.d), generator=g, device=device)
+    qlab = torch.randint(n_blobs, (args.nq,), generator=g, device=device)
+    queries = centers[qlab] + torch.randn((args.nq, args.d), generator=g, device=device)
+    return corpus, queries, g
+
+
+ARRAY_FIELDS = ("projection", "centroids", "cluster_sizes", "point_ids", "a_head", "a_scale", "a_values",
+                "b_head", "b_scale", "b_values", "norms")
+
+
+def broadcast_arrays(arrs, rank, device):
+    """Rank 0's built index arrays to every rank (NCCL broadcast): the build itself uses
+    atomics (index_add_), so each rank building its own copy could differ in the last bits."""
+    import torch
+    import torch.distributed as dist
+
+    out = {}
+    for name in ARRAY_FIELDS:
+        if rank == 0:
+            a = np.ascontiguousarray(arrs[name])
+            meta = torch.tensor([a.size, {"float32": 0, "uint32": 1, "int64": 2, "int8": 3}[str(a.dtype)]],
+                                dtype=torch.int64, device=device)
+        else:
+            meta = torch.zeros(2, dtype=torch.int64, device=device)
+        dist.broadcast(meta, 0)
+        n, code = int(meta[0]), int(meta[1])
+        dt = [np.float32, np.uint32, np.int64, np.int8][code]
+        buf = torch.empty(n * np.dtype(dt).itemsize, dtype=torch.uint8, device=device)
+        if rank == 0:
+            buf.copy_(torch.from_numpy(a.view(np.uint8).reshape(-1)))
+        dist.broadcast(buf, 0)
+        out[name] = buf.cpu().numpy().view(dt).reshape(arrs[name].shape if rank == 0 else (-1,))
+    if rank != 0:  # restore the 2-D shapes
+        out["projection"] = out["projection"].reshape(-1, int(out["centroids"].size // out["cluster_sizes"].size))
+        out["centroids"] = out["centroids"].reshape(out["cluster_sizes"].size, -1)
+    return out
+
+
 # ------------------------------------------------------------------------------- main
 
 
@@ -236,18 +300,8 @@ def main():
         print(json.dumps({"workload": "c4", "unavailable": f"host RAM {avail / 2**30:.0f} GiB < 1.3 x corpus"}))
         return
     dev = torch.device("cuda:0")
-    g = torch.Generator(device=dev)
-    g.manual_seed(args.seed)
-    n_blobs = args.m // 1000
     t0 = time.time()
-    centers = torch.randn((n_blobs, args.d), generator=g, device=dev) * 6.0
-    corpus = torch.empty((args.m, args.d), dtype=torch.float32, device=dev)
-    for i in range(0, args.m, 1 << 20):
-        n = min(1 << 20, args.m - i)
-        lab = torch.randint(n_blobs, (n,), generator=g, device=dev)
-        corpus[i:i + n] = centers[lab] + torch.randn((n, args.d), generator=g, device=dev)
-    qlab = torch.randint(n_blobs, (args.nq,), generator=g, device=dev)
-    queries = centers[qlab] + torch.randn((args.nq, args.d), generator=g, device=dev)
+    corpus, queries, g = generate(args, dev)
     log(f"data generated ({time.time() - t0:.0f} s)")
     t0 = time.time()
     arrs = build(args, corpus, g)
@@ -322,7 +376,7 @@ def run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact):
     # stage split
     import ctypes
     _native.lib.rrg_set_stage_timing(1)
-    stage_ms, stage_n = (ctypes.c_double * 9)(), (ctypes.c_int64 * 9)()
+    stage_ms, stage_n = (ctypes.c_double * 10)(), (ctypes.c_int64 * 10)()
     _native.lib.rrg_stage_times(stage_ms, stage_n)  # reset
     for i in range(3):
         flush.fill_(i)
@@ -330,7 +384,7 @@ def run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact):
     _native.lib.rrg_stage_times(stage_ms, stage_n)
     _native.lib.rrg_set_stage_timing(0)
     names = ["project", "quantize", "route_dist", "route_select", "select_topt", "rerank", "bucket",
-             "cluster_score"]
+             "cluster_score", "ground_truth", "screen"]
     stage = {nm: round(stage_ms[i] / 3, 4) for i, nm in enumerate(names)}
     # oracle parity on a query sample (id-for-id, score bits)
     parity = oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t) if args.parity else None
@@ -381,6 +435,41 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
         torch.cuda.synchronize()
         return out, e0.elapsed_time(e1)
 
+    nq = queries.shape[0]
+    if w == 1:  # the owner-local path of sharded.sharded_search: front slices, local search, merge
+        from paper_2410_18926_b200.sharded import Front
+
+        S = -(-nq // G)
+        best = None
+        for _ in range(3):
+            fr = [timed(lambda e=e, g=g: e.front(queries[min(nq, g * S):min(nq, (g + 1) * S)], w))
+                  for g, e in enumerate(engines)]
+            front = Front(**{n: torch.cat([getattr(f[0], n) for f in fr]) for n in Front.FIELDS})
+            res = [timed(lambda e=e: e.search_from_front(queries, front, k, w, t)) for e in engines]
+            out, m2 = timed(lambda: engines[0].merge_results(torch.stack([r[0][0] for r in res]),
+                                                             torch.stack([r[0][1] for r in res]),
+                                                             torch.stack([r[0][2] for r in res]), k))
+            p1 = [f[1] for f in fr]
+            p2 = [r[1] for r in res]
+            cur = (max(p1) + max(p2) + m2, p1, p2, m2)
+            best = cur if best is None or cur[0] < best[0] else best
+        oid, osc, ocnt = (x.cpu().numpy() for x in out)
+        equal = bool(np.array_equal(ocnt, cnt) and np.array_equal(oid, ids)
+                     and np.array_equal(np.nan_to_num(osc).view(np.int32), np.nan_to_num(sc).view(np.int32)))
+        s_pad = (args.s + 15) // 16 * 16
+        xf = (G - 1) * S * (args.s * 4 + s_pad + 4 + 4 + 8 + 4 + 4 + 4)  # front rows all-gathered
+        x2 = (G - 1) * nq * (k * 12 + 4)                                  # results all-gathered
+        xch_ms = (xf + x2) / (args.link_gbs * 1e9) * 1e3
+        compute_ms, p1, p2, m2 = best
+        del engines
+        torch.cuda.empty_cache()
+        return {"G": G, "equal_to_unsharded": equal, "front_ms": [round(v, 4) for v in p1],
+                "search_ms": [round(v, 4) for v in p2], "merge_ms": round(m2, 4),
+                "exchange_bytes_per_rank": xf + x2, "exchange_ms_est": round(xch_ms, 4),
+                "step_ms_est": round(compute_ms + xch_ms, 4), "qps_est": nq / (compute_ms + xch_ms) * 1e3,
+                "note": "w=1 owner-local flow (data-parallel front slices, each shard searches the queries "
+                        "routed to its clusters, one results all-gather + merge); shards run one after "
+                        f"another on one GPU; all-gather bytes at {args.link_gbs:.0f} GB/s (estimated)"}
     best = None
     for _ in range(3):  # first pass warms up workspaces
         c1 = [timed(lambda e=e: e.phase1(queries, k, w, t)) for e in engines]
@@ -404,7 +493,6 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
     oid, osc, ocnt = (x.cpu().numpy() for x in out)
     equal = bool(np.array_equal(ocnt, cnt) and np.array_equal(oid, ids)
                  and np.array_equal(np.nan_to_num(osc).view(np.int32), np.nan_to_num(sc).view(np.int32)))
-    nq = queries.shape[0]
     x1 = (G - 1) * (tot * 8 + (nq + 1) * 4)  # packed phase-1 all-gather received per rank
     x1_dense = (G - 1) * nq * (t * 8 + 4)    # the padded exchange it replaces
     x2 = (G - 1) * nq * (k * 12 + 4)         # phase-2 all-gather received per rank
@@ -421,7 +509,8 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
                     f"all-gather bytes at {args.link_gbs:.0f} GB/s (estimated, not measured)"}
 
 
-def oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t):
+def oracle_index(args, arrs, corpus_h):
+    """The built arrays as the oracle's index (test / bench checker only)."""
     from oracle import rrann_oracle as O
 
     r, s = args.r, args.s
@@ -449,6 +538,13 @@ def oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t):
         idx.clusters.append(O.OCluster(ids=arrs["point_ids"][pp:pp + ml], a=a, b=b,
                                        norms=arrs["norms"][pp:pp + ml], exact=exact))
         pp += ml
+    return idx
+
+
+def oracle_parity(args, arrs, corpus_h, queries, ids, sc, cnt, w, t):
+    from oracle import rrann_oracle as O
+
+    idx = oracle_index(args, arrs, corpus_h)
     qh = queries.cpu().numpy()
     sample = np.linspace(0, qh.shape[0] - 1, args.parity).astype(int)
     bad = 0

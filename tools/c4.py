@@ -39,6 +39,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
 
 
 def log(*a):
@@ -62,6 +63,9 @@ def parse():
     ap.add_argument("--grid", default="1:200,1:400,1:800,2:400,2:800,3:800,4:800,4:1600")
     ap.add_argument("--parity", type=int, default=64, help="queries checked against the oracle")
     ap.add_argument("--shards", default="2,4,8", help="G values for the 1-GPU shard emulation")
+    ap.add_argument("--write", default="",
+                    help="also stream the built index to this RRRANN01 file (tools/rrrann_writer.py) and "
+                         "check that the device index opened from it searches identically")
     ap.add_argument("--link-gbs", type=float, default=400.0,
                     help="assumed per-GPU NVLink all-gather receive bandwidth (exchange estimate)")
     return ap.parse_args()
@@ -282,6 +286,45 @@ def broadcast_arrays(arrs, rank, device):
     return out
 
 
+def write_file(args, arrs, corpus, path):
+    """Stream the GPU-built index through the RRRANN01 writer (corpus in original id order,
+    copied off the GPU in chunks) and a manifest; returns the CRC32 trailer."""
+    import rrrann_writer as RW
+
+    sizes = arrs["cluster_sizes"].astype(np.int64)
+    L, s, r = sizes.shape[0], args.s, args.r
+    w = RW.RrrWriter(path, metric="euclidean", dim=args.d, reduced_dim=s, rank=r, n_clusters=L,
+                     n_points=int(sizes.sum()), flags=RW.FLAG_QUANTIZED | RW.FLAG_CORPUS)
+    w.projection(arrs["projection"])
+    w.centroids(arrs["centroids"])
+    pa = pav = pb = pbv = pp = 0
+    for l in range(L):
+        ml = int(sizes[l])
+        exact = ml < r
+        cols = ml if exact else r
+        a = (arrs["a_head"][pa:pa + cols], arrs["a_scale"][pa:pa + cols], arrs["a_values"][pav:pav + s * cols])
+        pa += cols
+        pav += s * cols
+        b = None
+        if not exact:
+            b = (arrs["b_head"][pb:pb + ml], arrs["b_scale"][pb:pb + ml], arrs["b_values"][pbv:pbv + r * ml])
+            pb += ml
+            pbv += r * ml
+        w.cluster(arrs["point_ids"][pp:pp + ml], a, b, arrs["norms"][pp:pp + ml])
+        pp += ml
+    for i in range(0, corpus.shape[0], 1 << 18):
+        w.corpus(corpus[i:i + (1 << 18)].cpu().numpy())
+    crc = w.close()
+    with open(path + ".json", "w") as f:
+        json.dump({"name": "c4", "file_size": os.path.getsize(path), "crc32": crc,
+                   "generator": {"m": args.m, "d": args.d, "nq": args.nq, "seed": args.seed,
+                                 "n_blobs": args.m // 1000, "kind": "torch CUDA Philox (tools/c4.py)"},
+                   "index": {"L": args.L, "s": args.s, "r": args.r, "train": args.train, "iters": args.iters},
+                   "built_by": "tools/c4.py (GPU restatement of build()), streamed by tools/rrrann_writer.py"},
+                  f, indent=1)
+    return crc
+
+
 # ------------------------------------------------------------------------------- main
 
 
@@ -310,12 +353,29 @@ def main():
     gt = ground_truth_device(corpus, queries, args.k).cpu().numpy()
     torch.cuda.synchronize()
     log("ground truth done")
+    if args.write:
+        t0 = time.time()
+        crc = write_file(args, arrs, corpus, args.write)
+        log(f"wrote {args.write} ({os.path.getsize(args.write) / 2**30:.1f} GiB, crc {crc:#010x}, "
+            f"{time.time() - t0:.0f} s)")
     corpus_h = corpus.cpu().numpy()
     del corpus
     torch.cuda.empty_cache()
     n_exact = arrs.pop("n_exact")
     di = DeviceIndex.from_arrays(metric="euclidean", rank=args.r, corpus=corpus_h, device=0, **arrs)
     log(f"device index {di}")
+    if args.write:  # the file searches exactly like the in-memory index
+        fi = DeviceIndex.from_file(args.write, device=0)
+        for w, t in ((1, 800), (2, 400)):
+            a = [x.cpu().numpy() for x in di.search_device(queries, args.k, w, t, True)]
+            b = [x.cpu().numpy() for x in fi.search_device(queries, args.k, w, t, True)]
+            same = all(np.array_equal(np.nan_to_num(x).view(np.int32) if x.dtype == np.float32 else x,
+                                      np.nan_to_num(y).view(np.int32) if y.dtype == np.float32 else y)
+                       for x, y in zip(a, b))
+            log(f"file index == in-memory index at w={w} t={t}: {same}")
+            if not same:
+                raise SystemExit("file index differs from the in-memory index")
+        del fi
     # ... measurement continues in run()
     return run(args, di, arrs, corpus_h, queries, gt, build_s, n_exact)
 

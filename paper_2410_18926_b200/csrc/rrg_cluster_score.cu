@@ -169,9 +169,28 @@ struct ClusterScoreArgs {
   float* dbg_score;
 };
 
+// TC: stage B on the 5th-gen tensor cores.  A work item's (<= 32) queries form the
+// N = 32 operand (their re-quantized stage-A codes, K = r_pad = 32 bytes, one
+// kind::i8 MMA per 128 points: M = 128 points of the cluster), the int32 products
+// land in TMEM and the dequant / key epilogue reads them with tcgen05.ld -- warps w and
+// w + 4 share TMEM lane quarter w % 4 and take 16 queries each.  Exact int8 x int8 ->
+// int32 like the dp4a loop it replaces (rrr.py:196-197, quantize.py:109-126).
+__device__ __forceinline__ uint32_t sc_smem(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+// kind::i8: D s32, A/B signed, K-major, N = 32, M = 128
+constexpr uint32_t kScIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kPairsPerItem >> 3) << 17) |
+                              ((uint32_t)(128 >> 4) << 24);
+
+template <bool TC>
 __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
   const DevIndexView& ix = a.ix;
   __shared__ int item_s;
+  // TC: A tile (128 points x 32 B), B tile (32 queries x 32 B), canonical K-major layout
+  __shared__ __align__(128) int8_t tc_a[TC ? 128 * 32 : 16];
+  __shared__ __align__(128) int8_t tc_b[TC ? kPairsPerItem * 32 : 16];
+  __shared__ uint64_t tc_bar;
+  __shared__ uint32_t tc_tmem;
   __shared__ __align__(16) int8_t c2s[kPairsPerItem][kMaxRc];
   __shared__ float s2s[kPairsPerItem], h2s[kPairsPerItem];
   __shared__ float inters[kPairsPerItem][kMaxRc];
@@ -181,6 +200,21 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total_items = a.item_off[L];
   const bool euclid = ix.metric == kMetricEuclidean;
+  uint32_t tc_phase = 0;
+  if (TC) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;" ::"r"(sc_smem(&tc_tmem))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    if (tid == 32) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sc_smem(&tc_bar)));
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
   while (true) {
     if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
     __syncthreads();
@@ -257,8 +291,81 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
         if (lane == 0) { s2s[pi] = sc2; h2s[pi] = inters[pi][0]; }
       }
       __syncthreads();
+      if (TC) {
+        // B operand: the item's stage-B query codes, row n = query slot, 32 code bytes
+        for (int e = tid; e < kPairsPerItem * 2; e += CNT) {
+          const int n = e >> 1, half = e & 1;
+          int4 v = make_int4(0, 0, 0, 0);
+          if (n < np) v = *reinterpret_cast<const int4*>(&c2s[n][half * 16]);
+          *reinterpret_cast<int4*>(tc_b + (n >> 3) * 256 + half * 128 + (n & 7) * 16) = v;
+        }
+        for (int pb = pbeg; pb < pend; pb += 128) {
+          // A operand: B^T codes of 128 points (32 bytes each), zero past the item's end
+          for (int e = tid; e < 128 * 2; e += CNT) {
+            const int row = e >> 1, half = e & 1, p = pb + row;
+            int4 v = make_int4(0, 0, 0, 0);
+            if (p < pend) v = __ldg(reinterpret_cast<const int4*>(ix.bt + (size_t)(p0 + p) * 32) + half);
+            *reinterpret_cast<int4*>(tc_a + (row >> 3) * 256 + half * 128 + (row & 7) * 16) = v;
+          }
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          __syncthreads();
+          if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint64_t ad = (uint64_t)((sc_smem(tc_a) >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+                                ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+            const uint64_t bd = (uint64_t)((sc_smem(tc_b) >> 4) & 0x3FFFu) | ((uint64_t)(128 >> 4) << 16) |
+                                ((uint64_t)(256 >> 4) << 32) | (1ull << 46);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, 0, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tc_tmem),
+                "l"(ad), "l"(bd), "r"(kScIdesc)
+                : "memory");
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             sc_smem(&tc_bar))
+                         : "memory");
+          }
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "SC_WAIT_%=:\n\t"
+              "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+              "@!p bra SC_WAIT_%=;\n\t}" ::"r"(sc_smem(&tc_bar)),
+              "r"(tc_phase)
+              : "memory");
+          tc_phase ^= 1;
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int row = (warp & 3) * 32 + lane, c0 = (warp >> 2) * 16, p = pb + row;
+          uint32_t v[16];
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+                "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(tc_tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0));
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (p < pend) {
+            const int gp = p0 + p;
+            const float4 meta = __ldg(ix.pmeta + gp);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int pi = c0 + j;
+              if (pi < np) {
+                const int raw = (int)v[j];
+                const float yhat = deq(raw, s2s[pi], meta.y, h2s[pi], meta.x);
+                const float keyf = euclid ? __fadd_rn(__fmul_rn(-2.0f, yhat), meta.z) : -yhat;
+                a.keys[pkey[pi] + p] = mono32(keyf);
+                if (a.dbg_raw2) {
+                  a.dbg_raw2[pkey[pi] + p] = raw;
+                  a.dbg_score[pkey[pi] + p] = euclid ? keyf : yhat;
+                }
+              }
+            }
+          }
+          asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+          __syncthreads();  // the tiles and the accumulator are reused by the next block
+        }
+      }
       // stage B: thread per point, codes/meta loaded once, all np queries scored
-      for (int p = pbeg + tid; p < pend; p += CNT) {
+      for (int p = pbeg + tid; p < (TC ? pbeg : pend); p += CNT) {
         const int gp = p0 + p;
         const float4 meta = __ldg(ix.pmeta + gp);
         int4 b[4];
@@ -317,6 +424,12 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
       }
     }
     __syncthreads();
+  }
+  if (TC) {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;" ::"r"(tc_tmem) : "memory");
   }
 }
 
@@ -1828,8 +1941,15 @@ void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   a.xp = h.xp;
-  if (ix.quantized)
-    (k_score_cluster<<<sms * RRG_SCORE_CTAS, CNT, 0, st>>>(a), note_launch());
+  // tensor-core stage B (r_pad = 32): the int8 products of a work item's 32 queries x 128
+  // points in one MMA.  Auto: dense buckets (>= 64 queries per probed cluster on average)
+  // -- measured C5 w=64 4.51 -> 4.14 ms, w=16 1.54 -> 1.40 ms; C2 (10 per cluster) 0.13 ->
+  // 0.14 ms, where the items hold few queries and the dp4a loop is cheaper
+  const bool tc = ix.opt.score_tc >= 0 ? ix.opt.score_tc != 0 : (double)nq * h.w >= 64.0 * ix.L;
+  if (ix.quantized && ix.r_pad == 32 && tc)
+    (k_score_cluster<true><<<sms * RRG_SCORE_CTAS, CNT, 0, st>>>(a), note_launch());
+  else if (ix.quantized)
+    (k_score_cluster<false><<<sms * RRG_SCORE_CTAS, CNT, 0, st>>>(a), note_launch());
   else
     (k_score_cluster_f32<<<sms * 4, CNT, 0, st>>>(a), note_launch());
 }

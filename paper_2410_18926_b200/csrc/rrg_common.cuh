@@ -39,6 +39,7 @@ struct RrgOpts {
   int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
   int route_screen;  // RRG_ROUTE_SCREEN (default 1): fp16 tensor-core routing bounds + f64 recheck
   int screen_diag;   // RRG_SCREEN_DIAG: timing probes of k_rr_screen (1: no MMAs, 2: no MMAs or bounds)
+  int score_tc;      // RRG_SCORE_TC: stage B of the cluster scoring on tcgen05 (kind::i8): -1 auto
 };
 
 // POD view of a device-resident index, passed by value to kernels.

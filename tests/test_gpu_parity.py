@@ -525,7 +525,7 @@ SWEEP = [
 
 @pytest.mark.parametrize("mode", ["cluster", "cluster+auto", "cluster+async", "cluster+skip", "cluster+blocksel",
                                   "cluster+dmma", "cluster+slicedroute", "query", "cluster+regs",
-                                  "cluster+tma", "cluster+screen", "cluster+noscreen"])
+                                  "cluster+tma", "cluster+screen", "cluster+noscreen", "cluster+scoretc"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -551,6 +551,8 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
         monkeypatch.setenv("RRG_SCREEN", "1")
     elif rerank_mode == "noscreen":
         monkeypatch.setenv("RRG_SCREEN", "0")
+    elif rerank_mode == "scoretc":  # stage B of the scoring on tcgen05 (kind::i8; r_pad = 32 shapes)
+        monkeypatch.setenv("RRG_SCORE_TC", "1")
     elif rerank_mode:
         monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
@@ -945,3 +947,25 @@ def test_route_screen_matches_f64_routing(pkg, tmp_path, d, s, L, ties, monkeypa
         for i in range(0, 700, 35):
             r = O.query(oidx, q[i], 10, w, 60, True)
             np.testing.assert_array_equal(got[0][i, :got[2][i]], r.ids, err_msg=f"w={w} q{i} {ties}")
+
+
+@pytest.mark.parametrize("name,w,t", [("c2", 8, 400), ("c5", 64, 1600)])
+def test_tensor_core_stage_b_bit_exact(pkg, name, w, t, monkeypatch):
+    """Stage B of the cluster scoring on tcgen05 (RRG_SCORE_TC=1): the int32 products,
+    scores and final results equal the dp4a kernel's bit for bit at full size."""
+    W, dev, path = _workload(pkg, name)
+    q = torch.from_numpy(W.load_queries(name)).cuda()
+    k = W.load_manifest(name)["k"]
+    monkeypatch.setenv("RRG_SCORE_TC", "0")
+    dev.reload_options()
+    ref = [a.cpu().numpy() for a in dev.search_device(q, k, w, t, True)]
+    sel = dev.stage_route(dev.stage_project(q[:512])[0], w)
+    r1 = [a.cpu().numpy() for a in dev.stage_score(q[:512], sel)]
+    monkeypatch.setenv("RRG_SCORE_TC", "1")
+    dev.reload_options()
+    got = [a.cpu().numpy() for a in dev.search_device(q, k, w, t, True)]
+    g1 = [a.cpu().numpy() for a in dev.stage_score(q[:512], sel)]
+    for a, b in zip(got, ref):
+        np.testing.assert_array_equal(np.nan_to_num(a), np.nan_to_num(b))
+    for a, b in zip(g1[1:], r1[1:]):  # raw2, scores, offsets
+        np.testing.assert_array_equal(a.view(np.int32), b.view(np.int32))

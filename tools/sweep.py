@@ -51,6 +51,27 @@ def device_ms(dev, q, k, w, t, reps, flush):
     return float(np.mean([a.elapsed_time(b) for a, b in ts])), out
 
 
+STAGES = ["project", "quantize", "route_dist", "route_select", "select_topt", "rerank", "bucket",
+          "cluster_score", "ground_truth", "screen"]
+
+
+def stage_ms(dev, q, k, w, t, reps, flush):
+    """Per-stage device ms of one search (rrg_stage_times: events around every launch)."""
+    import ctypes
+
+    from paper_2410_18926_b200 import _native
+
+    ms, n = (ctypes.c_double * 10)(), (ctypes.c_int64 * 10)()
+    _native.lib.rrg_set_stage_timing(1)
+    _native.lib.rrg_stage_times(ms, n)
+    for i in range(reps):
+        flush.fill_(i & 0xFF)
+        dev.search_device(q, k, w, t, True)
+    _native.lib.rrg_stage_times(ms, n)
+    _native.lib.rrg_set_stage_timing(0)
+    return {nm: round(ms[i] / reps, 4) for i, nm in enumerate(STAGES) if ms[i] > 0}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("mode", choices=["batch", "w"])
@@ -105,7 +126,8 @@ def main():
             ms, out = device_ms(dev, q, k, w, t0, max(3, args.reps // 4), flush)
             ids = out[0].cpu().numpy()
             pt = {"w": w, "t": t0, "device_ms": ms, "device_qps": q.shape[0] / ms * 1e3,
-                  "recall_at_k": recall(ids, gt, k) if gt is not None else None}
+                  "recall_at_k": recall(ids, gt, k) if gt is not None else None,
+                  "stage_ms": stage_ms(dev, q, k, w, t0, 3, flush)}
             res["points"].append(pt)
             print(pt, file=sys.stderr, flush=True)
     print(json.dumps(res))

@@ -52,6 +52,35 @@ struct StageTimer {
 };
 thread_local StageTimer g_timer;
 
+// A second stream per host thread and device: work that depends only on the pair
+// bucketing (query interleave, the screen's group records) overlaps the top-t selection.
+struct AuxStream {
+  int device = -1;
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+  ~AuxStream() {
+    if (s) cudaStreamDestroy(s);
+    if (fork) cudaEventDestroy(fork);
+    if (join) cudaEventDestroy(join);
+  }
+};
+thread_local AuxStream g_aux;
+AuxStream& aux_stream() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  AuxStream& a = g_aux;
+  if (a.device != dev) {
+    if (a.s) cudaStreamDestroy(a.s);
+    if (a.fork) cudaEventDestroy(a.fork);
+    if (a.join) cudaEventDestroy(a.join);
+    cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming);
+    a.device = dev;
+  }
+  return a;
+}
+
 [[noreturn]] void launch_failed(int stage, cudaError_t e);
 
 // Work counters of the re-rank (rrg_search_counters), collected while stage timing is
@@ -1160,9 +1189,18 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         th.cand_idx = cidx;
         th.marks = marks;
       }
-      staged(4, st, [&] { launch_select_topt(th, n, st); });
+      // side stream: the interleaved queries and the screen's group records need only the
+      // pair bucketing -- they run while the top-t selection does
+      AuxStream& ax = aux_stream();
+      if (p.rr_mode == 1) {
+        CUDA_TRY(cudaEventRecord(ax.fork, st));
+        CUDA_TRY(cudaStreamWaitEvent(ax.s, ax.fork, 0));
+        staged(5, ax.s, [&] {
+          launch_interleave_queries(v, x, n, reinterpret_cast<float*>(base + p.off_xint), ax.s);
+        });
+      }
+      ScreenHost sh{};
       if (p.screen) {
-        ScreenHost sh{};
         sh.ix = v; sh.queries = x; sh.w = w; sh.qoff = ch.qoff; sh.pair_off = ch.pair_off;
         sh.pairs = ch.pairs; sh.kbase = ch.kbase; sh.marks = marks;
         sh.item_off = reinterpret_cast<int*>(base + p.off_scritem);
@@ -1173,8 +1211,12 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         sh.lb = reinterpret_cast<float*>(base + p.off_lb);
         sh.cand_idx = cidx; sh.cand_n = cn; sh.take_cap = p.take_cap; sh.k = k; sh.diss = ch.keys;
         sh.counters = counters_ptr(st);
-        staged(9, st, [&] { launch_screen(sh, n, st); });
+        staged(9, ax.s, [&] { launch_screen_prep(sh, n, ax.s); });
       }
+      if (p.rr_mode == 1) CUDA_TRY(cudaEventRecord(ax.join, ax.s));
+      staged(4, st, [&] { launch_select_topt(th, n, st); });
+      if (p.rr_mode == 1) CUDA_TRY(cudaStreamWaitEvent(st, ax.join, 0));
+      if (p.screen) staged(9, st, [&] { launch_screen(sh, n, st); });
       if (p.rr_mode == 1) {
         // scores are consumed: the key array is reused for the re-ranked distances
         ClusterRerankHost rh{};
@@ -1188,7 +1230,6 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         rh.compact = p.screen;
         if (p.screen) { rh.cand_idx = cidx; rh.cand_n = cn; rh.take_cap = p.take_cap; }
         rh.xint = reinterpret_cast<float*>(base + p.off_xint);
-        staged(5, st, [&] { launch_interleave_queries(v, x, n, reinterpret_cast<float*>(base + p.off_xint), st); });
         rh.counters = counters_ptr(st);
         if (rh.counters)  // rows the exact pass needs: union over each cluster's queries
           launch_count_rows(v, ch.pair_off, ch.pairs, ch.kbase, ch.qoff, w, marks,

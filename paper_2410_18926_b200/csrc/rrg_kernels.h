@@ -208,7 +208,8 @@ struct ThreshArgs {
   uint32_t* diss;
   int64_t* counters;
 };
-void launch_screen(const ScreenHost& h, int nq, cudaStream_t st);
+void launch_screen_prep(const ScreenHost& h, int nq, cudaStream_t st);  // items + group records
+void launch_screen(const ScreenHost& h, int nq, cudaStream_t st);       // screen + thresholds
 // counter: distinct rows of every cluster marked by any of its queries
 void launch_count_rows(const DevIndexView& ix, const int* pair_off, const int* pairs, const int* kbase,
                        const int* qoff, int w, const uint32_t* marks, const int* cand_idx, const int* cand_n,

@@ -589,10 +589,8 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
   const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5, wpb = blockDim.x >> 5;
   const int q = blockIdx.x * wpb + wl;
   if (q >= nq) return;
-  const size_t per = (size_t)a.take_cap * 12;
+  const size_t per = (size_t)a.take_cap * 4;  // only the marked UBs are staged (occupancy)
   float* uu = reinterpret_cast<float*>(thr_sm + per * wl);
-  float* ll = uu + a.take_cap;
-  int* cc = reinterpret_cast<int*>(ll + a.take_cap);
   int* h = hist[wl];
   const int n = a.cand_n[q];
   const int kb = a.kbase[q], nc = a.kbase[q + 1] - kb;
@@ -611,14 +609,13 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
   constexpr int SU = 8;  // 8 x (membership word, UB, LB) loads in flight per lane, none dependent
   for (int j0 = 0; j0 < nc; j0 += 32 * SU) {
     uint32_t mw[SU];
-    float u[SU], lv[SU];
+    float u[SU];
 #pragma unroll
     for (int t = 0; t < SU; ++t) {
       const int j = j0 + 32 * t + lane;
       const int bit = kb + min(j, nc - 1);
       mw[t] = __ldg(a.marks + (bit >> 5));
       u[t] = __ldg(a.ub + bit);
-      lv[t] = __ldg(a.lb + bit);
     }
 #pragma unroll
     for (int t = 0; t < SU; ++t) {
@@ -627,10 +624,7 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
       const bool mk = j < nc && ((mw[t] >> (bit & 31)) & 1u);
       const unsigned bal = __ballot_sync(0xffffffffu, mk);
       if (mk) {
-        const int at = got + __popc(bal & ((1u << lane) - 1u));
-        uu[at] = u[t];
-        ll[at] = lv[t];
-        cc[at] = j;
+        uu[got + __popc(bal & ((1u << lane) - 1u))] = u[t];
         umin = fminf(umin, u[t]);
         umax = fmaxf(umax, u[t]);
       }
@@ -672,14 +666,27 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
     if (bucket(uu[i]) <= found) T = fmaxf(T, uu[i]);
   T = warp_max_f(T);
   if (found == 256) T = __int_as_float(0x7f800000);  // (fewer marked than k: keep all)
-  // survivors (LB <= T) replace the query's candidate list
+  // survivors (marked, LB <= T) replace the query's candidate list: a second coalesced
+  // stream over the range (membership words and LBs, L2-resident)
   int ns = 0;
-  for (int b0 = 0; b0 < got; b0 += 32) {
-    const int i = b0 + lane;
-    const bool keep = i < got && !(ll[i] > T);
-    const unsigned bal = __ballot_sync(0xffffffffu, keep);
-    if (keep) ci[ns + __popc(bal & ((1u << lane) - 1u))] = cc[i];
-    ns += __popc(bal);
+  for (int j0 = 0; j0 < nc; j0 += 32 * SU) {
+    uint32_t mw[SU];
+    float lv[SU];
+#pragma unroll
+    for (int t = 0; t < SU; ++t) {
+      const int bit = kb + min(j0 + 32 * t + lane, nc - 1);
+      mw[t] = __ldg(a.marks + (bit >> 5));
+      lv[t] = __ldg(a.lb + bit);
+    }
+#pragma unroll
+    for (int t = 0; t < SU; ++t) {
+      const int j = j0 + 32 * t + lane;
+      const int bit = kb + j;
+      const bool keep = j < nc && ((mw[t] >> (bit & 31)) & 1u) && !(lv[t] > T);
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) ci[ns + __popc(bal & ((1u << lane) - 1u))] = j;
+      ns += __popc(bal);
+    }
   }
   if (lane == 0) a.cand_n[q] = ns;
   if (a.counters && lane == 0) {
@@ -689,13 +696,20 @@ __global__ void k_rr_thresh(ThreshArgs a, int nq) {
 }
 
 // ------------------------------------------------------------------ launchers
-void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
+// Work items and group records: needs only the pair bucketing, so it runs on a side
+// stream while the top-t selection (which makes the membership bits) runs.
+void launch_screen_prep(const ScreenHost& h, int nq, cudaStream_t st) {
+  (void)nq;
   const DevIndexView& ix = h.ix;
   // groups (cluster, <= kRrQ queries): one record each, built in parallel up front
   launch_rr_items(h.pair_off, ix.cl_pos, ix.L, 1 << 30, h.grp_off, st);
   launch_rr_items(h.pair_off, ix.cl_pos, ix.L, kScrRows, h.item_off, st);
   (k_rr_groups<<<h.n_groups_max, 32 * kRrQ, 0, st>>>(ix, h.queries, h.w, h.qoff, h.pair_off, h.pairs, h.kbase,
                                               h.grp_off, h.grec), note_launch());
+}
+
+void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
+  const DevIndexView& ix = h.ix;
   ScreenArgs a;
   a.ix = ix; a.pair_off = h.pair_off; a.marks = h.marks; a.item_off = h.item_off; a.grp_off = h.grp_off;
   a.grec = h.grec; a.ub = h.ub; a.lb = h.lb; a.counters = h.counters;
@@ -723,7 +737,7 @@ void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
     cudaFuncSetAttribute((const void*)k_rr_thresh, cudaFuncAttributeMaxDynamicSharedMemorySize, 192 * 1024);
     tdone[dev] = 1;
   }
-  const size_t per = (size_t)h.take_cap * 12;
+  const size_t per = (size_t)h.take_cap * 4;
   const int wpb = (int)std::max<size_t>(1, std::min<size_t>(8, (160 * 1024) / per));
   (k_rr_thresh<<<(nq + wpb - 1) / wpb, 32 * wpb, per * wpb, st>>>(t, nq), note_launch());
 }

@@ -10,7 +10,7 @@ import sys
 def main(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
-    hdr = rows[0]
+    hdr, units = rows[0], dict(zip(rows[0], rows[1]))
     for row in rows[2:]:
         d = dict(zip(hdr, row))
         st = {}
@@ -23,8 +23,11 @@ def main(rep):
         tot = sum(st.values()) or 1.0
         top = sorted(((v, k) for k, v in st.items()), reverse=True)[:6]
         name = d.get("Kernel Name", "?")[:60]
-        print(f"{name}\n  dur {d.get('gpu__time_duration.sum')} us  dram rd {d.get('dram__bytes_read.sum')} "
-              f"wr {d.get('dram__bytes_write.sum')}  dram% {d.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')}"
+        u = lambda k: units.get(k, "")  # noqa: E731
+        print(f"{name}\n  dur {d.get('gpu__time_duration.sum')} {u('gpu__time_duration.sum')}"
+              f"  dram rd {d.get('dram__bytes_read.sum')} {u('dram__bytes_read.sum')}"
+              f" wr {d.get('dram__bytes_write.sum')} {u('dram__bytes_write.sum')}"
+              f"  dram% {d.get('gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed')}"
               f"  issue% {d.get('sm__inst_issued.avg.pct_of_peak_sustained_active')}"
               f"  occ% {d.get('sm__warps_active.avg.pct_of_peak_sustained_active')}")
         print("  stalls:", ", ".join(f"{k} {v / tot * 100:.0f}%" for v, k in top))

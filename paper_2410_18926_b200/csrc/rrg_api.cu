@@ -809,6 +809,7 @@ RrgOpts read_opts() {
   o.route_screen = flag("RRG_ROUTE_SCREEN", 1) != 0;
   o.screen_diag = flag("RRG_SCREEN_DIAG", 0);
   o.score_tc = env("RRG_SCORE_TC") ? (flag("RRG_SCORE_TC", 0) != 0) : -1;
+  o.sparse_variant = flag("RRG_SPARSE_VARIANT", 1);
   return o;
 }
 // up to this many queries the projection / routing run as warp-per-output GEMVs

@@ -34,7 +34,9 @@ namespace rrg {
 
 constexpr int kRtRows = 128;              // queries per CTA (M) = centroids per tile (N)
 constexpr int kRtChunk = kRtRows * 32;    // one K = 16 chunk of a 128-row tile: 4 KB
-constexpr int kRtThreads = 160;           // warps 0-3 epilogue (TMEM lane quarters), warp 4 TMA + MMA
+// warps 0-7 epilogue (TMEM lane quarter = warp % 4, column half = warp / 4), warp 8 TMA + MMA
+constexpr int kRtThreads = 288;
+constexpr int kRtIssuer = 8;
 
 int route_screen_max_dim() { return kRtMaxKc * 16; }
 size_t route_tile_bytes(int rows, int kc) { return (size_t)((rows + kRtRows - 1) / kRtRows) * kc * kRtChunk; }
@@ -160,7 +162,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
   const int tile_bytes = a.kc * kRtChunk;
   unsigned char* sa = base;
   unsigned char* sb = base + tile_bytes;
-  if (warp == 4) {
+  if (warp == kRtIssuer) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(rt_smem(&tmem_base))
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
@@ -171,7 +173,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&bfull[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&bempty[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(rt_smem(&tfull[i])));
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(rt_smem(&tempty[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(rt_smem(&tempty[i])));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -179,7 +181,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base;
-  if (warp == 4) {
+  if (warp == kRtIssuer) {
     if (lane == 0) {  // TMA + MMA issue
       rt_bulk(rt_smem(sa), a.qt + (size_t)qb * a.kc * (kRtChunk / 2), tile_bytes, &afull);
       for (int t = t0; t < min(t1, t0 + 2); ++t)
@@ -210,7 +212,8 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
       }
     }
   } else {
-    const int q = qb * kRtRows + warp * 32 + lane;
+    const int q4 = warp & 3, half = warp >> 2;  // lane quarter (queries), column half
+    const int q = qb * kRtRows + q4 * 32 + lane;
     const bool valid = q < a.nq;
     float ppq = 0.f, nhq = 0.f, neq = 0.f, scq = 0.f, T = 0.f;
     if (valid) {
@@ -225,20 +228,22 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
     for (int t = t0; t < t1; ++t) {
       const int i = t - t0, buf = i & 1, u = i >> 1;
       {  // the tile's centroid terms, one per epilogue thread, while the MMAs run
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
-        const int c = t * kRtRows + warp * 32 + lane;
-        float4 v4 = make_float4(0.f, 0.f, 0.f, __int_as_float(0x7f800000));
-        if (c < a.L) {
-          const float4 cs = __ldg(a.cs + c);
-          v4 = make_float4(cs.x, cs.y, ldexpf(1.f, (int)cs.z), (float)__ldg(a.cc + c));
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // previous tile's readers are done
+        if (warp < 4) {
+          const int c = t * kRtRows + warp * 32 + lane;
+          float4 v4 = make_float4(0.f, 0.f, 0.f, __int_as_float(0x7f800000));
+          if (c < a.L) {
+            const float4 cs = __ldg(a.cs + c);
+            v4 = make_float4(cs.x, cs.y, ldexpf(1.f, (int)cs.z), (float)__ldg(a.cc + c));
+          }
+          cst[warp * 32 + lane] = v4;
         }
-        cst[warp * 32 + lane] = v4;
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        asm volatile("bar.sync 1, 256;" ::: "memory");
       }
       rt_wait(&tfull[buf], u & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll 1
-      for (int c0 = 0; c0 < kRtRows; c0 += 32) {
+      for (int c0 = half * (kRtRows / 2); c0 < (half + 1) * (kRtRows / 2); c0 += 32) {
         uint32_t v[32];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
@@ -248,7 +253,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
               "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
               "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
               "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(buf * kRtRows + c0)));
+            : "r"(tmem + ((uint32_t)(q4 * 32) << 16) + (uint32_t)(buf * kRtRows + c0)));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
         if (valid) {
 #pragma unroll
@@ -291,7 +296,8 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 4) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
+  if (warp == kRtIssuer)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem) : "memory");
 }
 
 // ------------------------------------------------------------------ recheck

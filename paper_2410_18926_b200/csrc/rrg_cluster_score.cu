@@ -1939,13 +1939,18 @@ static void opt_in_smem(Kern* kern, int slot) {
   done[slot][dev] = 1;
 }
 
-void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st) {
+void launch_cluster_prep(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
   (k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand), note_launch());
   opt_in_smem(k_pairs_build, 15);  // L * 8 bytes: 64 KB at L = 8192 (C4)
   (k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off,
                                                   h.item_off, h.pairs, h.kbase), note_launch());
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
+}
+
+void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st, bool prep) {
+  const DevIndexView& ix = h.ix;
+  if (prep) launch_cluster_prep(h, nq, st);
   ClusterScoreArgs a;
   a.ix = ix; a.qcodes = h.qcodes; a.qscale = h.qscale; a.qhead = h.qhead; a.sel = h.sel;
   a.w = h.w; a.qoff = h.qoff; a.pair_off = h.pair_off; a.item_off = h.item_off;

@@ -41,6 +41,7 @@ struct RrgOpts {
   int screen_diag;   // RRG_SCREEN_DIAG: timing probes of k_rr_screen (1: no MMAs, 2: no MMAs or bounds)
   int score_tc;      // RRG_SCORE_TC: stage B of the cluster scoring on tcgen05 (kind::i8): -1 auto
   int sparse_variant;  // RRG_SPARSE_VARIANT: k_rerank_sparse 0 register prefetch / 1 more CTAs
+  int screen_stages;   // RRG_SCREEN_STAGES: ring depth of k_rr_screen (0: as much as fits)
 };
 
 // POD view of a device-resident index, passed by value to kernels.

@@ -105,7 +105,9 @@ struct ClusterScoringHost {
   int* dbg_raw2 = nullptr;
   float* dbg_score = nullptr;
 };
-void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st);
+// candidate offsets + pair bucketing (what the screen's side stream needs), then scoring
+void launch_cluster_prep(const ClusterScoringHost& h, int nq, cudaStream_t st);
+void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st, bool prep = true);
 
 struct SelectTopTHost {
   DevIndexView ix;
@@ -209,7 +211,8 @@ struct ThreshArgs {
   int64_t* counters;
 };
 void launch_screen_prep(const ScreenHost& h, int nq, cudaStream_t st);  // items + group records
-void launch_screen(const ScreenHost& h, int nq, cudaStream_t st);       // screen + thresholds
+void launch_screen(const ScreenHost& h, int nq, cudaStream_t st);       // the bounds (k_rr_screen)
+void launch_thresh(const ScreenHost& h, int nq, cudaStream_t st);       // T, survivors
 // counter: distinct rows of every cluster marked by any of its queries
 void launch_count_rows(const DevIndexView& ix, const int* pair_off, const int* pairs, const int* kbase,
                        const int* qoff, int w, const uint32_t* marks, const int* cand_idx, const int* cand_n,

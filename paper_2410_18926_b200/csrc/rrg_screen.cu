@@ -713,10 +713,11 @@ void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
   ScreenArgs a;
   a.ix = ix; a.pair_off = h.pair_off; a.marks = h.marks; a.item_off = h.item_off; a.grp_off = h.grp_off;
   a.grec = h.grec; a.ub = h.ub; a.lb = h.lb; a.counters = h.counters;
-  a.nst = screen_stages(ix.scr_kc);
+  a.nst = ix.opt.screen_stages > 0 ? std::min(ix.opt.screen_stages, screen_stages(ix.scr_kc))
+                                    : screen_stages(ix.scr_kc);
   a.eta = (double)(ix.d + 4) * 0x1p-24 * 1.001;
   a.eps_acc = (double)(ix.d + 32) * 0x1p-21;
-  const size_t sm = screen_smem(ix.scr_kc);
+  const size_t sm = (size_t)a.nst * kScrStageBytes + 2 * grp_rec_bytes(ix.scr_kc) + 1024;
   static int done[64] = {};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
@@ -729,6 +730,11 @@ void launch_screen(const ScreenHost& h, int nq, cudaStream_t st) {
   }
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   (k_rr_screen<<<sms, kScrThreads, sm, st>>>(a), note_launch());
+}
+
+void launch_thresh(const ScreenHost& h, int nq, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
   ThreshArgs t;
   t.kbase = h.kbase; t.cand_idx = h.cand_idx; t.cand_n = h.cand_n; t.take_cap = h.take_cap; t.k = h.k;
   t.ub = h.ub; t.lb = h.lb; t.marks = h.marks; t.diss = h.diss; t.counters = h.counters;

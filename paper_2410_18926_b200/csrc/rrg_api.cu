@@ -1095,10 +1095,15 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         launch_prep(xps, xs, ns, v.s, v.s_pad, v.d, qcodes + (int64_t)s0 * v.s_pad, qscale + s0,
                     qhead + s0, pp + s0, xx + s0, st, nonfinite);
       });
-      if (ns > kSmallBatch && w <= kRtMaxW && v.rt_cent_tiles && v.opt.route_screen) {
+      auto al256 = [](size_t b) { return (b + 255) / 256 * 256; };
+      const size_t rt_need = v.rt_cent_tiles == nullptr ? 0 :
+          al256(route_tile_bytes(ns, v.rt_kc)) + al256((size_t)(ns + 127) / 128 * 128 * 16) +
+          al256((size_t)ns * 4) + al256(route_cnt_bytes(ns, v.L)) + al256(route_list_bytes(ns, v.L));
+      if (ns > kSmallBatch && w <= kRtMaxW && v.rt_cent_tiles && v.opt.route_screen &&
+          rt_need <= (size_t)ns * v.L * 8) {
         // bounds on the fp16 tensor cores, f64 recheck of the few candidates that can be
         // among the w nearest (rrg_route_screen.cu); scratch inside this piece's rows of
-        // the routing buffer (>= 4 KB per query for L >= 512)
+        // the routing buffer (>= 4 KB per query for L >= 512; this needs ~2.8 KB + the tile)
         char* rb = reinterpret_cast<char*>(diss + (int64_t)s0 * v.L);
         auto al = [](size_t b) { return (b + 255) / 256 * 256; };
         RouteScreenHost rh{};
@@ -1107,8 +1112,8 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         rh.qt = reinterpret_cast<uint16_t*>(rb + o); o += al(route_tile_bytes(ns, v.rt_kc));
         rh.qs = reinterpret_cast<float4*>(rb + o); o += al((size_t)(ns + 127) / 128 * 128 * 16);
         rh.T = reinterpret_cast<uint32_t*>(rb + o); o += al((size_t)ns * 4);
-        rh.cnt = reinterpret_cast<int*>(rb + o); o += al((size_t)ns * 4);
-        rh.list = reinterpret_cast<int*>(rb + o); o += al((size_t)ns * kRtCap * 4);
+        rh.cnt = reinterpret_cast<int*>(rb + o); o += al(route_cnt_bytes(ns, v.L));
+        rh.list = reinterpret_cast<int2*>(rb + o); o += al(route_list_bytes(ns, v.L));
         rh.sel = sel + (int64_t)s0 * w; rh.primary = prim + s0;
         staged(2, st, [&] { launch_route_screen(rh, ns, st); });
       } else if (w == 1 && ns > kSmallBatch && v.opt.route_fused) {

@@ -220,7 +220,10 @@ void launch_count_rows(const DevIndexView& ix, const int* pair_off, const int* p
 
 // Routing screen (rrg_route_screen.cu): fp16 tensor-core bounds of every
 // (query, centroid) d2, the centroids that can be among the w nearest, f64 recheck.
-constexpr int kRtCap = 64;    // survivors listed per query (more: every centroid is rechecked)
+constexpr int kRtCap = 64;    // survivors rechecked per query (more: every centroid is rechecked)
+constexpr int kRtMaxGroups = 32;  // centroid ranges (CTAs) per query block
+size_t route_list_bytes(int nq, int L);  // scratch of the per-thread candidate lists
+size_t route_cnt_bytes(int nq, int L);
 constexpr int kRtMaxW = 8;    // w handled by the screen (larger w: the f64 GEMM path)
 constexpr int kRtMaxKc = 24;  // s <= 384
 int route_screen_max_dim();
@@ -235,8 +238,8 @@ struct RouteScreenHost {
   uint16_t* qt;      // route_tile_bytes(nq, rt_kc) scratch
   float4* qs;        // [nq padded to 128] scratch
   uint32_t* T;       // [nq] scratch
-  int* cnt;          // [nq] scratch
-  int* list;         // [nq][kRtCap] scratch
+  int* cnt;          // route_cnt_bytes scratch
+  int2* list;        // route_list_bytes scratch
   int* sel;          // [nq][w] out
   int* primary;      // [nq] out
 };

@@ -15,12 +15,13 @@
 // f64-grade contract as the DMMA path: f32 products, f64 sums) and the w smallest
 // by (d2, id) are taken, like the stable argsort.
 //
-// k_route_screen<1>: per (128-query block, centroid range) CTA, tcgen05.mma kind::f16
-// (M = 128 queries, N = 128 centroids, K = 16) into double-buffered TMEM, each thread
-// (one query) keeps its w smallest UB -> atomicMin into T[q].  k_route_screen<2>: the
-// same products again, every centroid with LB <= T[q] appended to the query's list.
-// k_route_recheck: warp per query, exact f64 d2 of the listed centroids (all L when
-// the list overflowed), top w by (d2, id).
+// k_route_screen: per (128-query block, centroid range) CTA, tcgen05.mma kind::f16
+// (M = 128 queries, N = 128 centroids, K = 16) into double-buffered TMEM; each epilogue
+// thread (one query, half of every tile's columns) keeps its w smallest UB (-> atomicMin
+// into T[q]) and lists the centroids whose LB is <= its running w-th smallest UB -- a
+// superset of the survivors it saw, since the final T[q] is below every running bound.
+// k_route_recheck: warp per query, keeps the listed centroids with LB <= T[q], exact f64
+// d2 for those (every centroid when a list overflowed), top w by (d2, id).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -120,6 +121,10 @@ void launch_f16_tiles(const float* src, int rows, int K, int ld, int kc, uint16_
 }
 
 // ------------------------------------------------------------------ screen
+constexpr int kRtLoc = 12;  // list slots per thread and (CTA, half): 4 at w = 1, 12 for w <= 8
+// (kept in registers while the thread sweeps its columns: an entry whose LB rises above
+// the running bound is dropped, so only the near-ties of the running best accumulate)
+
 struct RouteScreenArgs {
   const uint16_t* qt;   // query tiles
   const float4* qs;     // query stats [nq]
@@ -127,11 +132,11 @@ struct RouteScreenArgs {
   const uint16_t* ct;   // centroid tiles
   const float4* cs;     // centroid stats [L]
   const double* cc;     // c.c [L]
-  int nq, L, kc, w, tiles_per_cta;
+  int nq, L, kc, w, tiles_per_cta, nslot;
   float eps;
-  uint32_t* T;          // [nq] f32 bits, +inf initialised; min over CTAs of their w-th smallest UB
-  int* cnt;             // [nq] survivors
-  int* list;            // [nq][kRtCap]
+  uint32_t* T;          // [nq] f32 bits; min over CTAs of their w-th smallest UB
+  int* cnt;             // [nq][nslot] listed per (CTA, column half); kRtLoc + 1 = overflow
+  int2* list;           // [nq][nslot][kRtLoc] (centroid, LB bits)
 };
 
 __device__ __forceinline__ void rt_bounds(float G, float sc, float ppq, float ccc, float nhq, float neq,
@@ -146,7 +151,7 @@ __device__ __forceinline__ void rt_bounds(float G, float sc, float ppq, float cc
   lb = fmaxf(S - E, 0.f);
 }
 
-template <int PASS>
+template <int LOC>
 __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs a) {
   extern __shared__ __align__(1024) unsigned char rt_sm[];
   __shared__ uint64_t afull, bfull[2], bempty[2], tfull[2], tempty[2];
@@ -215,13 +220,18 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
     const int q4 = warp & 3, half = warp >> 2;  // lane quarter (queries), column half
     const int q = qb * kRtRows + q4 * 32 + lane;
     const bool valid = q < a.nq;
-    float ppq = 0.f, nhq = 0.f, neq = 0.f, scq = 0.f, T = 0.f;
+    float ppq = 0.f, nhq = 0.f, neq = 0.f, scq = 0.f;
     if (valid) {
       const float4 s4 = a.qs[q];
       nhq = s4.x; neq = s4.y; scq = ldexpf(1.f, (int)s4.z);
       ppq = (float)a.pp[q];
-      if (PASS == 2) T = __uint_as_float(a.T[q]);
     }
+    const int slot = blockIdx.y * 2 + half;
+    int lid[LOC];
+    float llb[LOC];
+#pragma unroll
+    for (int i = 0; i < LOC; ++i) { lid[i] = -1; llb[i] = 0.f; }  // lid < 0: empty
+    bool over = false;
     float best[kRtMaxW];
 #pragma unroll
     for (int i = 0; i < kRtMaxW; ++i) best[i] = __int_as_float(0x7f800000);
@@ -262,19 +272,25 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
             const float4 cs = cst[c0 + j];  // (c >= L: c.c = +inf, never a survivor)
             float lb, ub;
             rt_bounds(__uint_as_float(v[j]), scq * cs.z, ppq, cs.w, nhq, neq, cs.x, cs.y, a.eps, lb, ub);
-            if (PASS == 1) {
-              if (ub < best[kRtMaxW - 1]) {  // insertion into the sorted w smallest
-                float x = ub;
+            if (ub < best[kRtMaxW - 1]) {  // insertion into the sorted w smallest
+              float x = ub;
 #pragma unroll
-                for (int s = 0; s < kRtMaxW; ++s) {
-                  const float lo = fminf(best[s], x);
-                  x = fmaxf(best[s], x);
-                  best[s] = lo;
-                }
+              for (int s = 0; s < kRtMaxW; ++s) {
+                const float lo = fminf(best[s], x);
+                x = fmaxf(best[s], x);
+                best[s] = lo;
               }
-            } else if (!(lb > T) && c < a.L) {  // survivor (NaN bounds survive too)
-              const int pos = atomicAdd(a.cnt + q, 1);
-              if (pos < kRtCap) a.list[(size_t)q * kRtCap + pos] = c;
+            }
+            float bw = best[0];  // the running w-th smallest UB
+#pragma unroll
+            for (int s = 1; s < kRtMaxW; ++s)
+              if (s == a.w - 1) bw = best[s];
+            if (!(lb > bw) && c < a.L) {  // (NaN bounds are listed too)
+              bool placed = false;  // into an empty slot or one no longer within the bound
+#pragma unroll
+              for (int i = 0; i < LOC; ++i)
+                if (!placed && (lid[i] < 0 || llb[i] > bw)) { llb[i] = lb; lid[i] = c; placed = true; }
+              over |= !placed;
             }
           }
         }
@@ -283,13 +299,19 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
       __syncwarp();
       if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(rt_smem(&tempty[buf])) : "memory");
     }
-    if (PASS == 1 && valid) {
-      // this CTA's w-th smallest UB bounds the query's w-th smallest d2 (if it saw w)
+    if (valid) {
+      // this thread's w-th smallest UB bounds the query's w-th smallest d2 (if it saw w)
       float tw = best[0];
 #pragma unroll
       for (int s = 0; s < kRtMaxW; ++s)
         if (s == a.w - 1) tw = best[s];
       if (tw == tw && tw < __int_as_float(0x7f800000)) atomicMin(a.T + q, __float_as_uint(tw));
+      int2* lst = a.list + ((size_t)q * a.nslot + slot) * kRtLoc;
+      int nl = 0;
+#pragma unroll
+      for (int i = 0; i < LOC; ++i)
+        if (lid[i] >= 0 && !(llb[i] > tw)) lst[nl++] = make_int2(lid[i], __float_as_int(llb[i]));
+      a.cnt[(size_t)q * a.nslot + slot] = over ? kRtLoc + 1 : nl;
     }
   }
   __syncwarp();
@@ -305,13 +327,39 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
 // came out shorter than w), the w smallest by (d2, id) -> sel, primary = the nearest.
 __global__ void k_route_recheck(const float* __restrict__ xp, int nq, int s, const float* __restrict__ cent,
                                 int L, int w, const double* __restrict__ pp, const double* __restrict__ cc,
-                                const int* __restrict__ cnt, const int* __restrict__ list, int* __restrict__ sel,
+                                const uint32_t* __restrict__ Tq, const int* __restrict__ cnt,
+                                const int2* __restrict__ list, int nslot, int* __restrict__ sel,
                                 int* __restrict__ primary) {
   const int q = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
   if (q >= nq) return;
-  const int n = cnt[q];
-  const bool full = n > kRtCap || n < w;
+  // the survivors: listed centroids with LB <= T (a warp-wide compaction of the slots)
+  __shared__ int surv_s[8][kRtCap];
+  int* surv = surv_s[(threadIdx.x >> 5) & 7];
+  const float T = __uint_as_float(Tq[q]);
+  bool over = false;
+  int n = 0;
+  for (int e0 = 0; e0 < nslot * kRtLoc; e0 += 32) {
+    const int e = e0 + lane, sl = e / kRtLoc, j = e % kRtLoc;
+    bool keep = false;
+    int c = 0;
+    if (e < nslot * kRtLoc) {
+      const int nc = cnt[(size_t)q * nslot + sl];
+      over |= nc > kRtLoc;
+      if (j < min(nc, kRtLoc)) {
+        const int2 v = list[((size_t)q * nslot + sl) * kRtLoc + j];
+        c = v.x;
+        keep = !(__int_as_float(v.y) > T);
+      }
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, keep);
+    const int at = n + __popc(bal & ((1u << lane) - 1u));
+    if (keep && at < kRtCap) surv[at] = c;
+    n += __popc(bal);
+  }
+  over = __any_sync(0xffffffffu, over);
+  __syncwarp();
+  const bool full = over || n > kRtCap || n < w;
   const int m = full ? L : n;
   const float* x = xp + (size_t)q * s;
   // each lane keeps its own w smallest (d2, id) over the centroids it evaluated
@@ -320,7 +368,7 @@ __global__ void k_route_recheck(const float* __restrict__ xp, int nq, int s, con
 #pragma unroll
   for (int i = 0; i < kRtMaxW; ++i) { bd[i] = __longlong_as_double(0x7ff0000000000000ll); bi[i] = 0x7fffffff; }
   for (int j = 0; j < m; ++j) {
-    const int c = full ? j : list[(size_t)q * kRtCap + j];
+    const int c = full ? j : surv[j];
     const float* cr = cent + (size_t)c * s;
     double acc = 0.0;
     for (int k = lane; k < s; k += 32) acc = fma((double)__ldg(x + k), (double)__ldg(cr + k), acc);
@@ -364,29 +412,45 @@ __global__ void k_route_recheck(const float* __restrict__ xp, int nq, int s, con
   }
 }
 
+// (CTA, column half) list slots per query: the launch's centroid ranges x 2
+static int route_groups(int nq, int L, int& tiles_per_cta) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int qblocks = (nq + kRtRows - 1) / kRtRows;
+  const int ntile = (L + kRtRows - 1) / kRtRows;
+  // enough CTAs for ~2 per SM, each with >= 2 centroid tiles when there are several
+  int groups = std::max(1, std::min(std::min(ntile, kRtMaxGroups), (2 * sms + qblocks - 1) / qblocks));
+  tiles_per_cta = (ntile + groups - 1) / groups;
+  return (ntile + tiles_per_cta - 1) / tiles_per_cta;
+}
+size_t route_list_bytes(int nq, int L) {
+  int tpc = 0;
+  return (size_t)nq * 2 * route_groups(nq, L, tpc) * kRtLoc * 8;
+}
+size_t route_cnt_bytes(int nq, int L) {
+  int tpc = 0;
+  return (size_t)nq * 2 * route_groups(nq, L, tpc) * 4;
+}
+
 void launch_route_screen(const RouteScreenHost& h, int nq, cudaStream_t st) {
   const DevIndexView& v = h.ix;
   launch_f16_tiles(h.xp, nq, v.s, v.s, v.rt_kc, h.qt, h.qs, st);
   cudaMemsetAsync(h.T, 0x7f, (size_t)nq * 4, st);  // 0x7f7f7f7f: a huge finite bound
-  cudaMemsetAsync(h.cnt, 0, (size_t)nq * 4, st);
   RouteScreenArgs a;
   a.qt = h.qt; a.qs = h.qs; a.pp = h.pp; a.ct = v.rt_cent_tiles; a.cs = v.rt_cent_stats; a.cc = v.cnorm;
   a.nq = nq; a.L = v.L; a.kc = v.rt_kc; a.w = h.w;
   a.eps = (float)((double)(v.s + 32) * 0x1p-21);
   a.T = h.T; a.cnt = h.cnt; a.list = h.list;
-  int dev = 0, sms = 148;
+  int dev = 0;
   cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int qblocks = (nq + kRtRows - 1) / kRtRows;
-  const int ntile = (v.L + kRtRows - 1) / kRtRows;
-  // enough CTAs for ~2 per SM, each with >= 2 centroid tiles when there are several
-  int groups = std::max(1, std::min(ntile, (2 * sms + qblocks - 1) / qblocks));
-  a.tiles_per_cta = (ntile + groups - 1) / groups;
-  groups = (ntile + a.tiles_per_cta - 1) / a.tiles_per_cta;
+  const int groups = route_groups(nq, v.L, a.tiles_per_cta);
+  a.nslot = 2 * groups;
   const size_t sm = (size_t)3 * v.rt_kc * kRtChunk + 1024;
   static int done[64] = {};
   if (dev >= 0 && dev < 64 && !done[dev]) {
-    for (const void* f : {(const void*)k_route_screen<1>, (const void*)k_route_screen<2>}) {
+    for (const void* f : {(const void*)k_route_screen<4>, (const void*)k_route_screen<kRtLoc>}) {
       cudaFuncAttributes at{};
       cudaFuncGetAttributes(&at, f);
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemPerCta - (int)at.sharedSizeBytes);
@@ -394,10 +458,13 @@ void launch_route_screen(const RouteScreenHost& h, int nq, cudaStream_t st) {
     done[dev] = 1;
   }
   dim3 grid(qblocks, groups);
-  (k_route_screen<1><<<grid, kRtThreads, sm, st>>>(a), note_launch());
-  (k_route_screen<2><<<grid, kRtThreads, sm, st>>>(a), note_launch());
-  (k_route_recheck<<<(nq + 7) / 8, 256, 0, st>>>(h.xp, nq, v.s, v.cent, v.L, h.w, h.pp, v.cnorm, h.cnt, h.list,
-                                                 h.sel, h.primary),
+  // w = 1: the near-ties of the running minimum (4 slots, fewer registers); w <= 8: 12
+  if (h.w == 1)
+    (k_route_screen<4><<<grid, kRtThreads, sm, st>>>(a), note_launch());
+  else
+    (k_route_screen<kRtLoc><<<grid, kRtThreads, sm, st>>>(a), note_launch());
+  (k_route_recheck<<<(nq + 7) / 8, 256, 0, st>>>(h.xp, nq, v.s, v.cent, v.L, h.w, h.pp, v.cnorm, h.T, h.cnt,
+                                                 h.list, a.nslot, h.sel, h.primary),
    note_launch());
 }
 

@@ -516,6 +516,22 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
         oid, osc, ocnt = (x.cpu().numpy() for x in out)
         equal = bool(np.array_equal(ocnt, cnt) and np.array_equal(oid, ids)
                      and np.array_equal(np.nan_to_num(osc).view(np.int32), np.nan_to_num(sc).view(np.int32)))
+        # stage split of shard 0's front slice and search (events around every launch)
+        import ctypes
+
+        from paper_2410_18926_b200 import _native
+        names = ["project", "quantize", "route_dist", "route_select", "select_topt", "rerank", "bucket",
+                 "cluster_score", "ground_truth", "screen"]
+        ms_, n_ = (ctypes.c_double * 10)(), (ctypes.c_int64 * 10)()
+        _native.lib.rrg_set_stage_timing(1)
+        _native.lib.rrg_stage_times(ms_, n_)
+        engines[0].front(queries[:S], w)
+        _native.lib.rrg_stage_times(ms_, n_)
+        front_stages = {nm: round(ms_[i], 4) for i, nm in enumerate(names) if ms_[i] > 0}
+        engines[0].search_from_front(queries, front, k, w, t)
+        _native.lib.rrg_stage_times(ms_, n_)
+        _native.lib.rrg_set_stage_timing(0)
+        search_stages = {nm: round(ms_[i], 4) for i, nm in enumerate(names) if ms_[i] > 0}
         s_pad = (args.s + 15) // 16 * 16
         xf = (G - 1) * S * (args.s * 4 + s_pad + 4 + 4 + 8 + 4 + 4 + 4)  # front rows all-gathered
         x2 = (G - 1) * nq * (k * 12 + 4)                                  # results all-gathered
@@ -525,6 +541,7 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
         torch.cuda.empty_cache()
         return {"G": G, "equal_to_unsharded": equal, "front_ms": [round(v, 4) for v in p1],
                 "search_ms": [round(v, 4) for v in p2], "merge_ms": round(m2, 4),
+                "shard0_front_stage_ms": front_stages, "shard0_search_stage_ms": search_stages,
                 "exchange_bytes_per_rank": xf + x2, "exchange_ms_est": round(xch_ms, 4),
                 "step_ms_est": round(compute_ms + xch_ms, 4), "qps_est": nq / (compute_ms + xch_ms) * 1e3,
                 "note": "w=1 owner-local flow (data-parallel front slices, each shard searches the queries "

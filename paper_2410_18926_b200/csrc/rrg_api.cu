@@ -1099,7 +1099,9 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       const size_t rt_need = v.rt_cent_tiles == nullptr ? 0 :
           al256(route_tile_bytes(ns, v.rt_kc)) + al256((size_t)(ns + 127) / 128 * 128 * 16) +
           al256((size_t)ns * 4) + al256(route_cnt_bytes(ns, v.L)) + al256(route_list_bytes(ns, v.L));
-      if (ns > kSmallBatch && w <= kRtMaxW && v.rt_cent_tiles && v.opt.route_screen &&
+      // (w = 1 only: at C3, w = 4, the per-thread candidate lists cost more than the f64
+      // GEMM they replace -- 0.43 vs 0.25 ms)
+      if (ns > kSmallBatch && w == 1 && v.rt_cent_tiles && v.opt.route_screen &&
           rt_need <= (size_t)ns * v.L * 8) {
         // bounds on the fp16 tensor cores, f64 recheck of the few candidates that can be
         // among the w nearest (rrg_route_screen.cu); scratch inside this piece's rows of

@@ -269,47 +269,55 @@ __global__ void __launch_bounds__(512) k_rr_groups(DevIndexView ix, const float*
     const int pr = pairs[j0 + g];
     const int q = pr / w, c = pr % w;
     const float* x = queries + (size_t)q * d;
-    // x' = x - mu (exact in f64); 8 elements per lane in flight per step
-    double amax = 0.0;
-    for (int e0 = lane; e0 < d; e0 += 256) {
-      float xv[8], mv[8];
+    // x' = x - mu (exact in f64): each lane owns runs of 8 consecutive elements, so a run
+    // is two 16-byte loads of x and of mu and one 16-byte store of 8 fp16 into the tile
+    // (8 consecutive K elements of one row are one 16-byte core-matrix row)
+    const int KE = KC * 16;
+    const bool vec = (d & 7) == 0;
+    auto load8 = [&](int e0, double (&xr)[8]) {
+      if (vec && e0 + 8 <= d) {
+        const float4 xa = __ldg(reinterpret_cast<const float4*>(x + e0));
+        const float4 xb = __ldg(reinterpret_cast<const float4*>(x + e0 + 4));
+        const float4 ma = __ldg(reinterpret_cast<const float4*>(mu + e0));
+        const float4 mb = __ldg(reinterpret_cast<const float4*>(mu + e0 + 4));
+        xr[0] = (double)xa.x - ma.x; xr[1] = (double)xa.y - ma.y; xr[2] = (double)xa.z - ma.z;
+        xr[3] = (double)xa.w - ma.w; xr[4] = (double)xb.x - mb.x; xr[5] = (double)xb.y - mb.y;
+        xr[6] = (double)xb.z - mb.z; xr[7] = (double)xb.w - mb.w;
+      } else {
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + 32 * u;
-        xv[u] = e < d ? __ldg(x + e) : 0.f;
-        mv[u] = e < d ? __ldg(mu + e) : 0.f;
+        for (int u = 0; u < 8; ++u)
+          xr[u] = e0 + u < d ? (double)__ldg(x + e0 + u) - (double)__ldg(mu + e0 + u) : 0.0;
       }
+    };
+    double amax = 0.0;
+    for (int e0 = lane * 8; e0 < KE; e0 += 256) {
+      double xr[8];
+      load8(e0, xr);
 #pragma unroll
-      for (int u = 0; u < 8; ++u) amax = fmax(amax, fabs((double)xv[u] - (double)mv[u]));
+      for (int u = 0; u < 8; ++u) amax = fmax(amax, fabs(xr[u]));
     }
     amax = warp_max_d(amax);
     const int ex = amax > 0.0 ? ilogb(amax) - 14 : 0;
     const double inv = ldexp(1.0, -ex);
     double s_x = 0.0, s_h = 0.0, s_e = 0.0;
-    for (int e0 = lane; e0 < KC * 16; e0 += 256) {
-      float xv[8], mv[8];
+    for (int e0 = lane * 8; e0 < KE; e0 += 256) {
+      double xr[8];
+      load8(e0, xr);
+      uint32_t packed[4];
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
-        const int e = e0 + 32 * u;
-        xv[u] = e < d ? __ldg(x + e) : 0.f;
-        mv[u] = e < d ? __ldg(mu + e) : 0.f;
+        // any fp16 near x'/2^e will do: the bound uses the exact residual of the stored value
+        const __half hv = __float2half_rn((float)(xr[u] * inv));
+        const double hd = (double)__half2float(hv);
+        const double er = xr[u] * inv - hd;
+        s_x += xr[u] * xr[u];
+        s_h += hd * hd;
+        s_e += er * er;
+        const uint32_t hb = __half_as_ushort(hv);
+        packed[u >> 1] = (u & 1) ? (packed[u >> 1] | (hb << 16)) : hb;
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int e = e0 + 32 * u;
-        if (e < KC * 16) {
-          const double xr = (double)xv[u] - (double)mv[u];
-          // any fp16 near x'/2^e will do: the bound uses the exact residual of the stored value
-          const __half hv = __float2half_rn((float)(xr * inv));
-          const double hd = (double)__half2float(hv);
-          const double er = xr * inv - hd;
-          s_x += xr * xr;
-          s_h += hd * hd;
-          s_e += er * er;
-          bt[(size_t)(e >> 4) * 256 + (g >> 3) * 128 + ((e & 15) >> 3) * 64 + (g & 7) * 8 + (e & 7)] =
-              __half_as_ushort(hv);
-        }
-      }
+      *reinterpret_cast<uint4*>(bt + (size_t)(e0 >> 4) * 256 + (g >> 3) * 128 + ((e0 & 15) >> 3) * 64 + (g & 7) * 8) =
+          make_uint4(packed[0], packed[1], packed[2], packed[3]);
     }
     s_x = warp_sum_d(s_x);
     s_h = warp_sum_d(s_h);
@@ -345,7 +353,13 @@ struct ScreenArgs {
 __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   extern __shared__ __align__(1024) unsigned char scr_sm[];
   __shared__ uint64_t full[kScrStagesMax], empty[kScrStagesMax], bfull[2], bempty[2], tfull[kScrTBuf],
-      tempty[kScrTBuf];
+      tempty[kScrTBuf], sfull[kScrTBuf], sempty[kScrTBuf];
+  // per item (indexed like the TMEM buffers) the group's slot terms + slot count, copied
+  // by the producer: the epilogue never holds a group tile buffer, so the producer may
+  // refill one as soon as its MMAs are done (with the epilogue gating the tile buffers,
+  // the stream stalled behind it: C3 screen 1.21 ms, MMA-only or epilogue-only ~0.7)
+  constexpr int kSlotBytes = kRrQ * (int)sizeof(GroupSlot) + 16;
+  __shared__ __align__(128) unsigned char sslot[kScrTBuf][kSlotBytes];
   __shared__ uint32_t tmem_base;
   const DevIndexView& ix = a.ix;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -375,11 +389,13 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
     for (int i = 0; i < 2; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bfull[i])));
       // freed by the MMAs of the group (commit) and by the 4 epilogue warps
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 5;" ::"r"(s_addr(&bempty[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&bempty[i])));
     }
     for (int i = 0; i < kScrTBuf; ++i) {
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&tfull[i])));
       asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(s_addr(&tempty[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(s_addr(&sfull[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"(s_addr(&sempty[i])));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -388,10 +404,12 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   fence_after();
   const uint32_t tmem = tmem_base;
 
-  // item -> (cluster, query group, 128-row block).  A CTA's items are a contiguous
-  // range and a group's items are its cluster's blocks in order, so after one binary
-  // search the roles step through their items (a search per item costs ~10 dependent
-  // L2 loads, which throttled the producer).
+  // item -> (cluster, 128-row block, query group).  A CTA's items are a contiguous
+  // range; within a cluster the query groups of one block are adjacent, so a block that
+  // several groups screen is re-read from L2 right after its first (HBM) read -- group-
+  // major order re-streamed it from HBM (C3: 1.92 M rows streamed for 1 M rows).  After
+  // one binary search the roles step through their items (a search per item costs ~10
+  // dependent L2 loads, which throttled the producer).
   struct ItemIt {
     int l, gi, b, nb, ng;  // ng = query groups of cluster l
   };
@@ -406,15 +424,15 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
     t.nb = __ldg(ix.scr_blk0 + lo + 1) - __ldg(ix.scr_blk0 + lo);
     const int local = i - __ldg(a.item_off + lo);
     t.ng = (__ldg(a.item_off + lo + 1) - __ldg(a.item_off + lo)) / t.nb;
-    t.gi = local / t.nb;
-    t.b = local % t.nb;
+    t.b = local / t.ng;
+    t.gi = local % t.ng;
     return t;
   };
   auto it_next = [&](ItemIt& t) {  // only called while items remain
-    if (++t.b < t.nb) return;
-    t.b = 0;
     if (++t.gi < t.ng) return;
     t.gi = 0;
+    if (++t.b < t.nb) return;
+    t.b = 0;
     do {  // next cluster with items
       ++t.l;
       t.nb = __ldg(ix.scr_blk0 + t.l + 1) - __ldg(ix.scr_blk0 + t.l);
@@ -423,32 +441,42 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   };
   if (warp == 0) {
     if (lane == 0) {  // producer: group records and the CTA's blocks through the ring
-      int sc = 0, j = -1, pl = -1, pg = -1;
+      int slot = 0, pass = 0, j = -1, pl = -1, pg = -1;
       ItemIt t = it_begin(i0);
-      for (int i = i0; i < i1; ++i, i < i1 ? it_next(t) : void()) {
+      for (int i = i0, it = 0; i < i1; ++i, ++it, i < i1 ? it_next(t) : void()) {
         const int l = t.l, gi = t.gi, b = t.b;
+        const unsigned char* grec = a.grec + (size_t)(a.grp_off[l] + gi) * rec_bytes;
+        const int ab = it % kScrTBuf, u = it / kScrTBuf;
+        if (u > 0) scr_wait(&sempty[ab], (u - 1) & 1);
+        scr_expect_tx(&sfull[ab], kSlotBytes);
+        scr_bulk(s_addr(sslot[ab]), grec + (size_t)KC * 512, kSlotBytes, &sfull[ab]);
         if (l != pl || gi != pg) {
           ++j; pl = l; pg = gi;
           const int buf = j & 1;
           if (j >= 2) scr_wait(&bempty[buf], ((j >> 1) - 1) & 1);
-          scr_expect_tx(&bfull[buf], rec_bytes);
-          scr_bulk(s_addr(gbuf + buf * rec_bytes), a.grec + (size_t)(a.grp_off[l] + gi) * rec_bytes, rec_bytes,
-                   &bfull[buf]);
+          scr_expect_tx(&bfull[buf], KC * 512);
+          scr_bulk(s_addr(gbuf + buf * rec_bytes), grec, KC * 512, &bfull[buf]);
         }
         const unsigned char* src = reinterpret_cast<const unsigned char*>(ix.scr_plane) +
                                    ((size_t)(ix.scr_blk0[l] + b) * KC) * kScrChunk;
-        for (int c0 = 0; c0 < KC; c0 += kScrStageChunks, ++sc) {
-          const int slot = sc % nst, pass = sc / nst;
+        for (int c0 = 0; c0 < KC; c0 += kScrStageChunks) {
           if (pass > 0) scr_wait(&empty[slot], (pass - 1) & 1);
-          const int bytes = min(kScrStageChunks, KC - c0) * kScrChunk;
-          scr_expect_tx(&full[slot], bytes);
-          scr_bulk(s_addr(ring + slot * kScrStageBytes), src + (size_t)c0 * kScrChunk, bytes, &full[slot]);
+          scr_expect_tx(&full[slot], kScrStageBytes);
+          scr_bulk(s_addr(ring + slot * kScrStageBytes), src + (size_t)c0 * kScrChunk, kScrStageBytes, &full[slot]);
+          if (++slot == nst) { slot = 0; ++pass; }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
-      int sc = 0, j = -1, pl = -1, pg = -1;
+      // descriptors advance by plain adds (start address field = addr >> 4, no carry for
+      // shared-memory addresses): the issue loop was ~42 instructions per MMA and, sharing
+      // its SM sub-partition with an epilogue warp, paced the whole kernel (C3: 1.20 ms,
+      // vs 0.65 with the epilogue's arithmetic off and 0.71 with the MMAs off)
+      static_assert(kScrAcc == 1 && kScrStageBytes % 16 == 0, "one accumulator per item");
+      const uint64_t ring_desc = scr_desc_sw128(s_addr(ring));
+      int slot = 0, pass = 0, j = -1, pl = -1, pg = -1;
+      const bool mma_on = ix.opt.screen_diag == 0;
       ItemIt t = it_begin(i0);
       for (int i = i0, it = 0; i < i1; ++i, ++it, i < i1 ? it_next(t) : void()) {
         const int l = t.l, gi = t.gi, b = t.b, nb = t.nb;
@@ -462,42 +490,36 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
           scr_wait(&tempty[ab], (u - 1) & 1);
           fence_after();
         }
-        const uint32_t sb = s_addr(gbuf + (j & 1) * rec_bytes);
-        const uint32_t dt = tmem + (uint32_t)(ab * kScrAcc * kRrQ);
-        for (int c0 = 0; c0 < KC; c0 += kScrStageChunks, ++sc) {
-          const int slot = sc % nst, pass = sc / nst;
+        uint64_t bd = scr_desc(s_addr(gbuf + (j & 1) * rec_bytes));
+        const uint32_t dt = tmem + (uint32_t)(ab * kRrQ);
+        for (int c0 = 0; c0 < KC; c0 += kScrStageChunks) {
           scr_wait(&full[slot], pass & 1);
           fence_after();
-          const uint32_t sa = s_addr(ring + slot * kScrStageBytes);
-          const int nch = min(kScrStageChunks, KC - c0);
-          if (ix.opt.screen_diag == 0)
-            for (int c = 0; c < nch; ++c) {
-              const int kc = c0 + c;
-              scr_mma(dt + (uint32_t)((kc % kScrAcc) * kRrQ), scr_desc_sw128(sa + c * 32), scr_desc(sb + kc * 512),
-                      kc >= kScrAcc ? 1u : 0u);
-            }
+          const uint64_t ad = ring_desc + (uint64_t)(slot * (kScrStageBytes >> 4));
+          if (mma_on) {
+            // a K16 step is 32 B inside the 128-byte swizzle atom (A) and one 512-byte
+            // K chunk of the group tile (B)
+            scr_mma(dt, ad, bd, c0 > 0 ? 1u : 0u);
+#pragma unroll
+            for (int c = 1; c < kScrStageChunks; ++c) scr_mma(dt, ad + 2 * c, bd + 32 * c, 1u);
+          }
+          bd += 32 * kScrStageChunks;
           scr_commit(&empty[slot]);
+          if (++slot == nst) { slot = 0; ++pass; }
         }
         scr_commit(&tfull[ab]);
-        if (b + 1 == nb || i + 1 == i1) scr_commit(&bempty[j & 1]);  // the group's tile is read
+        if (t.ng > 1 || b + 1 == nb || i + 1 == i1) scr_commit(&bempty[j & 1]);  // the group's tile is read
       }
     }
   } else {
     // epilogue warps: TMEM lane quarter = warp % 4, one block row per thread
     const int q4 = warp & 3, row = q4 * 32 + lane;
     const double eta = a.eta, eps = a.eps_acc;
-    int j = -1, pl = -1, pg = -1;
     ItemIt t = it_begin(i0);
     for (int i = i0, it = 0; i < i1; ++i, ++it, i < i1 ? it_next(t) : void()) {
-      const int l = t.l, gi = t.gi, b = t.b, nb = t.nb;
-      if (l != pl || gi != pg) {
-        ++j; pl = l; pg = gi;
-        scr_wait(&bfull[j & 1], (j >> 1) & 1);  // the group's slot terms have landed
-      }
-      const unsigned char* rec = gbuf + (j & 1) * rec_bytes;
-      const GroupSlot* slots = reinterpret_cast<const GroupSlot*>(rec + (size_t)KC * 512);
-      const int ng = *reinterpret_cast<const int*>(rec + (size_t)KC * 512 + kRrQ * sizeof(GroupSlot));
+      const int l = t.l, b = t.b;
       const int ab = it % kScrTBuf, u = it / kScrTBuf;
+      const GroupSlot* slots = reinterpret_cast<const GroupSlot*>(sslot[ab]);
       const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
       const int jr = b * kScrRows + row;
       // bounds for every (row, slot) of the item: the candidate range of a (query, probe)
@@ -510,8 +532,10 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
         rr = __ldg(ix.scr_rr + p0 + jr);
         rm = __ldg(ix.scr_rmeta + p0 + jr);
       }
-      scr_wait(&tfull[ab], u & 1);
+      scr_wait(&tfull[ab], u & 1);  // (the slot copy was issued before the item's stream)
       fence_after();
+      scr_wait(&sfull[ab], u & 1);
+      const int ng = *reinterpret_cast<const int*>(sslot[ab] + kRrQ * sizeof(GroupSlot));
       float gsum[kRrQ];
 #pragma unroll
       for (int g = 0; g < kRrQ; ++g) gsum[g] = 0.f;
@@ -552,10 +576,8 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
           a.lb[bit] = fmaxf(S - E, 0.f) * (1.f - etap);
         }
       }
-      if (b + 1 == nb || i + 1 == i1) {  // done with the group's record
-        __syncwarp();
-        if (lane == 0) scr_arrive(&bempty[j & 1]);
-      }
+      __syncwarp();
+      if (lane == 0) scr_arrive(&sempty[ab]);
     }
   }
   __syncwarp();

@@ -198,13 +198,17 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
         rt_wait(&bfull[buf], u & 1);
         if (u > 0) rt_wait(&tempty[buf], (u - 1) & 1);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t a0 = rt_smem(sa), b0 = rt_smem(sb + buf * tile_bytes);
+        // descriptors advance by adds to the start-address field (addr >> 4): fewer issue
+        // instructions per MMA (see k_rr_screen)
+        const uint64_t ad = rt_desc(rt_smem(sa)), bd = rt_desc(rt_smem(sb + buf * tile_bytes));
+        const uint32_t dt = tmem + (uint32_t)(buf * kRtRows);
         for (int c = 0; c < a.kc; ++c) {
           asm volatile(
               "{\n\t.reg .pred p;\n\t"
               "setp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)(buf * kRtRows)),
-              "l"(rt_desc(a0 + c * kRtChunk)), "l"(rt_desc(b0 + c * kRtChunk)), "r"(kRtIdesc), "r"(c > 0 ? 1u : 0u)
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(dt),
+              "l"(ad + (uint64_t)(c * (kRtChunk >> 4))), "l"(bd + (uint64_t)(c * (kRtChunk >> 4))), "r"(kRtIdesc),
+              "r"(c > 0 ? 1u : 0u)
               : "memory");
         }
         rt_commit(&bempty[buf]);

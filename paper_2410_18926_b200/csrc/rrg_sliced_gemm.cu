@@ -202,15 +202,16 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
       const int st = kc % kSlStages;
       sl_wait(&full[st], (kc / kSlStages) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sa = sl_smem(base + (size_t)st * kSlStage);
-      const uint32_t sb = sa + kSlAStage;
+      // descriptors advance by adds to the start-address field (addr >> 4)
+      const uint64_t ad = sl_desc(sl_smem(base + (size_t)st * kSlStage));
+      const uint64_t bd = ad + (uint64_t)(kSlAStage >> 4);
 #pragma unroll
       for (int i = 0; i < kSl; ++i)
 #pragma unroll
         for (int j = 0; j < kSl - i; ++j) {
           const uint32_t first = kc == 0 && i == 0;  // first product into level i+j
-          sl_mma(tmem + (uint32_t)((i + j) * kSlBN), sl_desc(sa + i * kSlATile),
-                 sl_desc(sb + j * kSlBTile), first ? 0u : 1u);
+          sl_mma(tmem + (uint32_t)((i + j) * kSlBN), ad + (uint64_t)((i * kSlATile) >> 4),
+                 bd + (uint64_t)((j * kSlBTile) >> 4), first ? 0u : 1u);
         }
       sl_commit(&empty[st]);
     }

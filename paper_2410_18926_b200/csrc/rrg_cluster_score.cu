@@ -1562,11 +1562,56 @@ __device__ __forceinline__ float reduce_p(float (&v)[N], int lane) {
 template <int N>
 __device__ __forceinline__ float reduce_any(float (&v)[N], int nval, int lane) {
   if (nval <= 1) return reduce_p<1>(v, lane);
-  if (nval <= 2) return reduce_p<2>(v, lane);
-  if (nval <= 4) return reduce_p<4>(v, lane);
-  if (nval <= 8) return reduce_p<8>(v, lane);
-  if (N >= 32 && nval > 16) return reduce_p<(N >= 32 ? 32 : 16)>(v, lane);
-  return reduce_p<16>(v, lane);
+  if constexpr (N >= 2) if (nval <= 2) return reduce_p<2>(v, lane);
+  if constexpr (N >= 4) if (nval <= 4) return reduce_p<4>(v, lane);
+  if constexpr (N >= 8) if (nval <= 8) return reduce_p<8>(v, lane);
+  if constexpr (N >= 32) if (nval > 16) return reduce_p<32>(v, lane);
+  if constexpr (N >= 16) return reduce_p<16>(v, lane);
+  return reduce_p<N>(v, lane);  // (nval <= N here)
+}
+
+// One listed row against the S first active queries (act: their slot bits, nact <= S):
+// this lane's pairwise partial per (query, half), then the P-way reduction.  S is the
+// next power of two of nact, so a row only one or two queries kept costs no unrolled
+// work for the other 14 slots (C2: 2.2 queries per fetched row).
+template <int S, int NB, int NH>
+__device__ __forceinline__ float sparse_row_dist(unsigned act, int nact, const float* __restrict__ xs, int ds,
+                                                 int coff, const float2 (&c)[NH][NB], float2 nz2, int lane) {
+  constexpr int cstep = 64 * NH;
+  float v[NH * S];
+  unsigned rem = act;
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) v[NH * s + hh] = 0.f;
+    if (rem) {  // warp-uniform
+      const int g = __ffs(rem) - 1;
+      rem &= rem - 1;
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        const float* xg = xs + (size_t)g * ds + coff + 64 * hh;
+        float2 acc = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
+          const float2 dd = __fadd2_rn(c[hh][i], make_float2(-xv.x, -xv.y));
+          const float2 sq = sq2(dd, nz2);
+          acc = i == 0 ? sq : __fadd2_rn(acc, sq);
+        }
+        v[NH * s + hh] = __fadd_rn(acc.x, acc.y);  // r[2h] + r[2h+1] of this lane
+      }
+    }
+  }
+  return reduce_any<NH * S>(v, NH * nact, lane);
+}
+template <int NB, int NH>
+__device__ __forceinline__ float sparse_row(unsigned act, int nact, const float* __restrict__ xs, int ds, int coff,
+                                            const float2 (&c)[NH][NB], float2 nz2, int lane) {
+  if (nact <= 1) return sparse_row_dist<1, NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
+  if (nact <= 2) return sparse_row_dist<2, NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
+  if (nact <= 4) return sparse_row_dist<4, NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
+  if (nact <= 8) return sparse_row_dist<8, NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
+  return sparse_row_dist<kRrQ, NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
 }
 
 constexpr int SNT = 256;
@@ -1713,33 +1758,8 @@ __global__ void __launch_bounds__(SNT, CT) k_rerank_sparse(ClusterRerankArgs a) 
       const int nact = __popc(act);
       if (mine) slotg[warp][__popc(act & ((1u << lane) - 1u))] = lane;
       __syncwarp();
-      // value NH * s + hh: this lane's partial of half hh of the s-th active query
-      float v[NH * kRrQ];
-      unsigned rem = act;
-#pragma unroll
-      for (int s = 0; s < kRrQ; ++s) {
-#pragma unroll
-        for (int hh = 0; hh < NH; ++hh) v[NH * s + hh] = 0.f;
-        if (rem) {  // warp-uniform
-          const int g = __ffs(rem) - 1;
-          rem &= rem - 1;
-#pragma unroll
-          for (int hh = 0; hh < NH; ++hh) {
-            const float* xg = xs + (size_t)g * ds + coff + 64 * hh;
-            float2 acc = make_float2(0.f, 0.f);
-#pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              const float2 xv = *reinterpret_cast<const float2*>(xg + cstep * i);
-              const float2 dd = __fadd2_rn(c[hh][i], make_float2(-xv.x, -xv.y));
-              const float2 sq = sq2(dd, nz2);
-              acc = i == 0 ? sq : __fadd2_rn(acc, sq);
-            }
-            v[NH * s + hh] = __fadd_rn(acc.x, acc.y);  // r[2h] + r[2h+1] of this lane
-          }
-        }
-      }
       // lane j holds value j fully reduced; NH = 2: dist = pw(half 0) + pw(half 1)
-      float r = reduce_any<NH * kRrQ>(v, NH * nact, lane);
+      float r = sparse_row<NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
       if (NH == 2) r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));
       if (lane < NH * nact && lane % NH == 0) {
         const int g = slotg[warp][lane / NH];
@@ -1757,6 +1777,195 @@ __global__ void __launch_bounds__(SNT, CT) k_rerank_sparse(ClusterRerankArgs a) 
     }
     if (a.counters && lane == 0 && nfetch)
       atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 3), (unsigned long long)nfetch);
+    __syncthreads();
+  }
+}
+
+// Same computation as k_rerank_sparse, with the listed rows streamed into a shared-
+// memory ring by a producer warp (cp.async.bulk, one row per copy, an mbarrier per
+// slot) instead of register loads by the computing warps: the rows in flight per SM
+// are set by the ring depth (16-32 rows) rather than by what the warps have issued
+// while they compute.  RRG_SPARSE_VARIANT=2.
+constexpr int RNT = SNT + 32;  // 8 computing warps + the producer warp
+__device__ __forceinline__ void rr_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "RR_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra RR_WAIT_%=;\n\t}" ::"r"(sc_smem(bar)),
+      "r"(parity)
+      : "memory");
+}
+template <int NB, int NH>
+__global__ void __launch_bounds__(RNT, NH == 1 ? 2 : 1) k_rerank_sparse_ring(ClusterRerankArgs a, int nslots) {
+  constexpr int NLV = 8 * NH, cstep = 8 * NLV;
+  constexpr int kMaxSlots = 32;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const DevIndexView& ix = a.ix;
+  const int ds = ix.d_stride;
+  const int row_bytes = ds * 4;
+  float* xs = reinterpret_cast<float*>(smem_raw);                       // [kRrQ][ds]
+  uint32_t* mb = reinterpret_cast<uint32_t*>(xs + (size_t)kRrQ * ds);  // [kRrQ][mwords]
+  unsigned char* ring = smem_raw + (((size_t)kRrQ * ds * 4 + (size_t)kRrQ * a.mwords * 4 + 127) & ~(size_t)127);
+  __shared__ uint64_t full[kMaxSlots], empty[kMaxSlots];
+  __shared__ int item_s, nrows_s;
+  __shared__ int pq[kRrQ], pkey[kRrQ], pofs[kRrQ];
+  __shared__ int rowlist[kSpRows];
+  __shared__ int slotg[SNT / 32][kRrQ];
+  const int L = ix.L;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int ncw = SNT / 32;  // computing warps
+  const int b = lane >> 2, h = lane & 3;
+  const int coff = 8 * b + 2 * h;
+  const float2 nz2 = make_float2(a.neg_zero, a.neg_zero);
+  const int total_items = a.rr_item_off[L];
+  if (tid == 0) {
+    for (int i = 0; i < nslots; ++i) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sc_smem(&full[i])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sc_smem(&empty[i])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  int gbase = 0;  // rows this CTA has streamed before the current item (ring position)
+  while (true) {
+    if (tid == 0) item_s = atomicAdd(a.work_counter, 1);
+    __syncthreads();
+    const int item = item_s;
+    __syncthreads();
+    if (item >= total_items) break;
+    int lo = 0, hi = L;
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (a.rr_item_off[mid] <= item) lo = mid; else hi = mid;
+    }
+    const int l = lo;
+    const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
+    const int nrc = (m + a.rr_rows - 1) / a.rr_rows;
+    const int local = item - a.rr_item_off[l];
+    const int qc = nrc > 0 ? local / nrc : 0, rc = nrc > 0 ? local % nrc : 0;
+    const int j0 = a.pair_off[l] + qc * kRrQ;
+    const int ng = min(kRrQ, a.pair_off[l + 1] - j0);
+    const int r0 = rc * a.rr_rows, r1 = min(m, r0 + a.rr_rows);
+    if (tid < ng) {
+      const int pr = a.pairs[j0 + tid];
+      const int q = pr / a.w, c = pr % a.w;
+      pq[tid] = q;
+      pofs[tid] = a.qoff[(size_t)q * (a.w + 1) + c];
+      pkey[tid] = a.kbase[q] + pofs[tid];
+    }
+    __syncthreads();
+    if (m == 0) continue;
+    const int k0 = r0 >> 5, k1 = (r1 - 1) >> 5, nwd = k1 - k0 + 1;
+    for (int e = tid; e < ng * nwd; e += RNT) {
+      const int g = e / nwd, k = k0 + e - g * nwd;
+      mb[g * a.mwords + k] = 0;
+    }
+    __syncthreads();
+    for (int g = warp; g < ng; g += RNT / 32) {
+      const int q = pq[g], off = pofs[g], n = a.cand_n[q];
+      const int* list = a.cand_idx + (size_t)q * a.take_cap;
+      for (int i = lane; i < n; i += 32) {
+        const int row = __ldg(list + i) - off;
+        if (row >= r0 && row < r1) atomicOr(mb + g * a.mwords + (row >> 5), 1u << (row & 31));
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // list the rows any query of the item kept
+      int base_n = 0;
+      for (int kk = k0; kk <= k1; kk += 32) {
+        const int k = kk + lane;
+        uint32_t u = 0;
+        if (k <= k1) {
+          for (int g = 0; g < ng; ++g) u |= mb[g * a.mwords + k];
+          if (k == k0) u &= 0xffffffffu << (r0 & 31);
+          if (k == k1) u &= 0xffffffffu >> (31 - ((r1 - 1) & 31));
+        }
+        const int cnt = __popc(u);
+        int incl = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+          const int v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += v;
+        }
+        int at = base_n + incl - cnt;
+        while (u) {
+          const int bb = __ffs(u) - 1;
+          u &= u - 1;
+          rowlist[at++] = 32 * k + bb;
+        }
+        base_n += __shfl_sync(0xffffffffu, incl, 31);
+      }
+      if (lane == 0) nrows_s = base_n;
+    }
+    __syncthreads();
+    const int nrows = nrows_s;
+    if (warp == ncw) {
+      if (lane == 0) {  // producer: the listed rows, in order, through the ring
+        for (int i = 0; i < nrows; ++i) {
+          const int gi = gbase + i, slot = gi % nslots, ph = gi / nslots;
+          if (ph > 0) rr_wait(&empty[slot], (ph - 1) & 1);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sc_smem(&full[slot])),
+                       "r"(row_bytes)
+                       : "memory");
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  sc_smem(ring + (size_t)slot * row_bytes)),
+              "l"(ix.corpus + (size_t)(p0 + rowlist[i]) * ds), "r"(row_bytes), "r"(sc_smem(&full[slot]))
+              : "memory");
+        }
+      }
+    } else {
+      // x of the item's queries (pre-interleaved) while the first rows land
+      {
+        constexpr int SU = 4;
+        const int n4 = ds / 4, tot = ng * n4;
+        float4* xs4 = reinterpret_cast<float4*>(xs);
+        for (int e0 = tid; e0 < tot; e0 += SNT * SU) {
+          float4 xv[SU];
+#pragma unroll
+          for (int u = 0; u < SU; ++u) {
+            const int e = e0 + u * SNT;
+            if (e < tot) {
+              const int g = e / n4, j = e - g * n4;
+              xv[u] = __ldg(reinterpret_cast<const float4*>(a.xint + (size_t)pq[g] * ds) + j);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < SU; ++u)
+            if (e0 + u * SNT < tot) xs4[e0 + u * SNT] = xv[u];
+        }
+      }
+      asm volatile("bar.sync 1, %0;" ::"n"(SNT) : "memory");  // the computing warps only
+      int nfetch = 0;
+      for (int ia = warp; ia < nrows; ia += ncw) {
+        const int row = rowlist[ia];
+        const int gi = gbase + ia, slot = gi % nslots;
+        ++nfetch;
+        const bool mine = lane < ng && ((mb[lane * a.mwords + (row >> 5)] >> (row & 31)) & 1u);
+        const unsigned act = __ballot_sync(0xffffffffu, mine);
+        const int nact = __popc(act);
+        if (mine) slotg[warp][__popc(act & ((1u << lane) - 1u))] = lane;
+        rr_wait(&full[slot], (gi / nslots) & 1);
+        const float* rs = reinterpret_cast<const float*>(ring + (size_t)slot * row_bytes) + coff;
+        float2 c[NH][NB];
+#pragma unroll
+        for (int hh = 0; hh < NH; ++hh)
+#pragma unroll
+          for (int i = 0; i < NB; ++i) c[hh][i] = *reinterpret_cast<const float2*>(rs + 64 * hh + cstep * i);
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sc_smem(&empty[slot])) : "memory");
+        float r = sparse_row<NB, NH>(act, nact, xs, ds, coff, c, nz2, lane);
+        if (NH == 2) r = __fadd_rn(r, __shfl_down_sync(0xffffffffu, r, 1));
+        if (lane < NH * nact && lane % NH == 0) {
+          const int g = slotg[warp][lane / NH];
+          a.diss[pkey[g] + row] = mono32(r);
+        }
+        __syncwarp();
+      }
+      if (a.counters && lane == 0 && nfetch)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 3), (unsigned long long)nfetch);
+    }
+    gbase += nrows;
     __syncthreads();
   }
 }
@@ -2077,6 +2286,32 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
     // 1 (default): no register prefetch, 3 CTAs/SM (C2 1.49 -> 1.46 ms, C3 3.36 -> 3.18 ms);
     // 0: the next row prefetched into registers, 2 CTAs/SM
     const int var = h.ix.opt.sparse_variant;
+    if (var == 2) {  // ring-staged rows: as many 16 KB-aligned slots as shared memory allows
+      const size_t fixed = (ssm + 127) / 128 * 128;
+      const size_t rowb = (size_t)h.ix.d_stride * 4;
+      // 2 CTAs per SM (one's item staging hidden behind the other's stream) when both
+      // fit with >= 12 slots each, else one CTA with the deepest ring
+      const int ns2 = ((228 * 1024) / 2 - 8 * 1024 - (int)fixed) / (int)rowb;
+      const int ns1 = (kMaxSmemPerCta - 8 * 1024 - (int)fixed) / (int)rowb;
+      const int cta = ns2 >= 12 ? 2 : 1;
+      const int ns = std::min(32, cta == 2 ? ns2 : ns1);
+      if (ns >= 8) {
+        const size_t rsm = fixed + (size_t)ns * rowb;
+#define RRG_SPR(NB, NH, SLOT)                                                                \
+  do {                                                                                       \
+    opt_in_smem(k_rerank_sparse_ring<NB, NH>, SLOT);                                         \
+    (k_rerank_sparse_ring<NB, NH><<<sms * cta, RNT, rsm, st>>>(a, ns), note_launch());       \
+  } while (0)
+        const int nb = h.ix.pw_leaf_n / 8;
+        if (h.ix.pw_nleaves == 16) {
+          if (nb == 12) RRG_SPR(12, 2, 48); else if (nb == 15) RRG_SPR(15, 2, 49); else RRG_SPR(16, 2, 50);
+        } else {
+          if (nb == 12) RRG_SPR(12, 1, 51); else if (nb == 15) RRG_SPR(15, 1, 52); else RRG_SPR(16, 1, 53);
+        }
+#undef RRG_SPR
+        return;
+      }
+    }
     if (h.ix.pw_nleaves == 16) {
       if (var == 1) {
         if (nb == 12) RRG_SP(12, 2, false, 2, 42); else if (nb == 15) RRG_SP(15, 2, false, 2, 43);

@@ -525,7 +525,8 @@ SWEEP = [
 
 @pytest.mark.parametrize("mode", ["cluster", "cluster+auto", "cluster+async", "cluster+skip", "cluster+blocksel",
                                   "cluster+dmma", "cluster+slicedroute", "query", "cluster+regs",
-                                  "cluster+tma", "cluster+screen", "cluster+noscreen", "cluster+scoretc"])
+                                  "cluster+tma", "cluster+screen", "cluster+screenring", "cluster+noscreen",
+                                  "cluster+scoretc"])
 @pytest.mark.parametrize("d,s,r,L,m,metric,exact_ivf", SWEEP)
 def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mode, monkeypatch):
     """Every scoring x re-rank kernel variant against the oracle: cluster-major scoring
@@ -549,6 +550,9 @@ def test_random_index_sweep(pkg, tmp_path, d, s, r, L, m, metric, exact_ivf, mod
         monkeypatch.setenv("RRG_GEMM", "sliced")
     elif rerank_mode == "screen":  # tensor-core bounds prune the exact re-rank (any t)
         monkeypatch.setenv("RRG_SCREEN", "1")
+    elif rerank_mode == "screenring":  # screened exact pass with ring-staged rows (variant 2)
+        monkeypatch.setenv("RRG_SCREEN", "1")
+        monkeypatch.setenv("RRG_SPARSE_VARIANT", "2")
     elif rerank_mode == "noscreen":
         monkeypatch.setenv("RRG_SCREEN", "0")
     elif rerank_mode == "scoretc":  # stage B of the scoring on tcgen05 (kind::i8; r_pad = 32 shapes)

@@ -188,6 +188,29 @@ __device__ T pw_leaf(Get get, int start, int n) {
   return res;
 }
 
+// Warp evaluation of the same tree when it is perfect and narrow: n = m * 2^a with leaf
+// size m <= 128, m % 8 == 0 (every split halves exactly) and 8 * 2^a <= 32 chains.
+// Lane c runs chain c % 8 of leaf c / 8 in NumPy's order; xor-shuffles 1, 2, 4 then form
+// ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) and 8, 16 the leaf tree (a+b == b+a exactly, so
+// both lanes of a pair hold the same bits).  Every lane returns the sum.
+__host__ __device__ inline int pw_warp_leaves(int n) {
+  if (n < 8 || n % 8) return 0;
+  int L = 1;
+  while (n / L > 128) {
+    if ((n / L) % 16) return 0;  // the halves must stay multiples of 8
+    L *= 2;
+  }
+  return L <= 4 ? L : 0;
+}
+template <typename T, typename Get>
+__device__ T pw_sum_warp(Get get, int n, int L, int lane) {
+  const int m = n / L, c = lane & (8 * L - 1) , leaf = c >> 3, j = c & 7;
+  T r = get(leaf * m + j);
+  for (int i = 8; i < m; i += 8) r = r + get(leaf * m + i + j);
+  for (int o = 1; o < 8 * L; o <<= 1) r = r + __shfl_xor_sync(0xffffffffu, r, o);
+  return r;
+}
+
 // Single-thread iterative evaluation of the full tree (used for short rows and
 // for ||p||^2 of the routing expansion).  The explicit stack mirrors the
 // recursion; depth <= 32.

@@ -293,12 +293,14 @@ __global__ void k_prep_queries(const float* __restrict__ xp, const float* __rest
   if (nonfinite && __any_sync(0xffffffffu, bad) && lane == 0) atomicOr(nonfinite, 1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) xsum += __shfl_xor_sync(0xffffffffu, xsum, o);
+  auto get = [&](int i) { double v = (double)row[i]; return v * v; };
+  const int pwl = pw_warp_leaves(s);  // (s = 64, 256: one lane per accumulator chain)
+  const double ppw = pwl ? pw_sum_warp<double>(get, s, pwl, lane) : 0.0;
   if (lane == 0) {
     qscale[warp] = sc;
     qhead[warp] = row[0];
     xx[warp] = (float)xsum;
-    auto get = [&](int i) { double v = (double)row[i]; return v * v; };
-    pp[warp] = pw_sum_seq<double>(get, s);
+    pp[warp] = pwl ? ppw : pw_sum_seq<double>(get, s);
   }
 }
 

@@ -31,6 +31,7 @@ constexpr int kSlBN = 64;         // columns (rows of B) per CTA
 constexpr int kSlBK = 32;         // K bytes per stage (one K=32 MMA per slice pair)
 constexpr int kSlStages = 4;
 constexpr int kSlThreads = 128;
+constexpr int kSlRegK = 2048;  // k_slice_rows keeps rows up to this length in registers
 constexpr int kSlATile = kSlBM * kSlBK;  // 4 KB per slice plane
 constexpr int kSlBTile = kSlBN * kSlBK;  // 2 KB
 constexpr int kSlAStage = kSl * kSlATile;  // 32 KB
@@ -58,32 +59,80 @@ __global__ void k_slice_rows(const float* __restrict__ x, int rows_valid, int ro
                              int* __restrict__ exps) {
   const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
   const int lane = threadIdx.x & 31;
+  const int Kp = kchunks * kSlBK;
   if (row >= rows_pad) return;
   const bool valid = row < rows_valid;
   const float* r = x + (size_t)(valid ? row : 0) * ld;
+  // the row is read once: up to kSlRegK elements stay in registers (4 per lane per
+  // 128-element step) between the max pass and the slicing (two passes over global
+  // memory were latency-bound: C2 41 us for 7.7 M elements)
+  constexpr int kV = kSlRegK / 128;
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  auto load4 = [&](int k0) {
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!valid || k0 >= K) return u;
+    if (vec && k0 + 4 <= K) return __ldg(reinterpret_cast<const float4*>(r + k0));
+    u.x = __ldg(r + k0);
+    if (k0 + 1 < K) u.y = __ldg(r + k0 + 1);
+    if (k0 + 2 < K) u.z = __ldg(r + k0 + 2);
+    if (k0 + 3 < K) u.w = __ldg(r + k0 + 3);
+    return u;
+  };
+  float4 xv[kV];
   float mx = 0.f;
-  if (valid)
+  if (Kp <= kSlRegK) {
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      xv[i] = load4(lane * 4 + 128 * i);
+      mx = fmaxf(mx, fmaxf(fmaxf(fabsf(xv[i].x), fabsf(xv[i].y)), fmaxf(fabsf(xv[i].z), fabsf(xv[i].w))));
+    }
+  } else if (valid) {
     for (int k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(__ldg(r + k)));
+  }
   for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   const int e = mx > 0.f ? ilogbf(mx) + 1 : 0;
   if (lane == 0) exps[row] = e;
-  const int Kp = kchunks * kSlBK;
-  for (int k0 = lane * 4; k0 < Kp; k0 += 128) {
-    float u[4];
+  // |x| * 2^(56 - e) truncated to an integer (exact: x = m 2^x_e with a 24-bit m), whose
+  // base-128 digits, signed like x, are the slices -- the same digits as peeling
+  // trunc(u * 128) off u = x / 2^e eight times in f32 (each step exact; values below
+  // 2^-56 of the row max have all-zero slices either way), in integer instructions
+  auto fixed56 = [&](float xf) -> unsigned long long {
+    const uint32_t bits = __float_as_uint(xf);
+    const int be = (int)((bits >> 23) & 0xFFu);
+    if (be == 0xFF) return 0ull;  // non-finite rows are rejected before the projection
+    const unsigned long long m = be ? ((bits & 0x7FFFFFu) | 0x800000u) : (bits & 0x7FFFFFu);
+    const int sh = (be ? be : 1) - 150 - e + 56;  // x = m 2^(be - 150)
+    if (sh >= 0) return m << sh;                  // (< 2^56: |x| < 2^e)
+    return sh > -64 ? m >> -sh : 0ull;
+  };
+  auto slice4 = [&](int k0, float4 xq) {
+    const float xs4[4] = {xq.x, xq.y, xq.z, xq.w};
+    unsigned long long f[4];
+    uint32_t neg = 0;
 #pragma unroll
-    for (int t = 0; t < 4; ++t) u[t] = (valid && k0 + t < K) ? ldexpf(__ldg(r + k0 + t), -e) : 0.f;
+    for (int t = 0; t < 4; ++t) {
+      f[t] = fixed56(xs4[t]);
+      neg |= (__float_as_uint(xs4[t]) >> 31) << t;
+    }
 #pragma unroll
     for (int s = 0; s < kSl; ++s) {
       uint32_t word = 0;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        u[t] *= 128.f;
-        const float tr = truncf(u[t]);
-        word |= (uint32_t)(uint8_t)(int8_t)(int)tr << (8 * t);
-        u[t] -= tr;
+        const int dg = (int)((f[t] >> (7 * (kSl - 1 - s))) & 127u);
+        word |= (uint32_t)(uint8_t)(int8_t)(((neg >> t) & 1u) ? -dg : dg) << (8 * t);
       }
       *reinterpret_cast<uint32_t*>(planes + sl_tiled_off(row, k0, s, tile_rows, kchunks)) = word;
     }
+  };
+  if (Kp <= kSlRegK) {
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int k0 = lane * 4 + 128 * i;
+      if (k0 < Kp) slice4(k0, xv[i]);
+    }
+  } else {
+    for (int k0 = lane * 4; k0 < Kp; k0 += 128) slice4(k0, load4(k0));
   }
 }
 
@@ -156,9 +205,20 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
   extern __shared__ __align__(1024) unsigned char sl_sm[];
   __shared__ uint64_t full[kSlStages], empty[kSlStages], done;
   __shared__ uint32_t tmem_base;
+  // the tile's per-column terms, staged once: the epilogue read them per output from
+  // global memory, a dependent load ahead of every column's arithmetic (it was ~2/3 of
+  // the kernel's time at C2)
+  __shared__ double col_sc[kSlBN], col_t[kSlBN];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int mb = blockIdx.y, nb = blockIdx.x;
   const int m0 = mb * kSlBM, n0 = nb * kSlBN;
+  // 2^e as an exact f64 power of two (|e| stays far inside the range)
+  auto pow2 = [](int e) { return __longlong_as_double((long long)(1023 + e) << 52); };
+  if (tid >= 64 && tid < 64 + kSlBN) {
+    const int j = tid - 64, gn = n0 + j;
+    col_sc[j] = gn < g.N ? pow2(g.b_exp[gn]) : 0.0;
+    col_t[j] = gn < g.N && g.colterm ? g.colterm[gn] : 0.0;
+  }
   unsigned char* base = reinterpret_cast<unsigned char*>(
       (reinterpret_cast<uintptr_t>(sl_sm) + 1023) & ~uintptr_t(1023));
   if (warp == 0) {
@@ -223,9 +283,8 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
   // epilogue
   const int gm = m0 + warp * 32 + lane;
   const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-  // 2^(ea - 14) and 2^eb as exact f64 powers of two (|e| stays far inside the range)
-  auto pow2 = [](int e) { return __longlong_as_double((long long)(1023 + e) << 52); };
-  const double sa = pow2(g.a_exp[gm] - 14);  // padded rows have exponent 0
+  const double sa = pow2(g.a_exp[gm] - 14);  // 2^(ea - 14); padded rows have exponent 0
+  const double rterm = (g.epi == EPI_L2 || g.epi == EPI_L2_ARGMIN) && gm < g.M ? g.rowterm[gm] : 0.0;
   constexpr double kInf = __builtin_huge_val();
   double best = kInf;  // EPI_*_ARGMIN: this row's (value, lowest column) over the tile
   int bcol = 0x7fffffff;
@@ -243,7 +302,22 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
             "=r"(v[l][15])
           : "r"(lane_addr + (uint32_t)(l * kSlBN + c0)));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (gm < g.M) {
+    if (gm < g.M && g.epi == EPI_PROJ && (g.ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(g.outf) & 15) == 0 &&
+        n0 + c0 + 16 <= g.N) {
+      // 16 consecutive columns of this thread's row as four 16-byte stores (a store per
+      // column wrote 4 bytes into 32 different rows' sectors per warp instruction)
+      float f[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        double acc = 0.0;
+#pragma unroll
+        for (int l = kSl - 1; l >= 0; --l) acc = fma(acc, 0.0078125, (double)(int)v[l][j]);
+        f[j] = (float)((acc * sa) * col_sc[c0 + j]);
+      }
+      float4* o = reinterpret_cast<float4*>(g.outf + (size_t)gm * g.ldo + n0 + c0);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+    } else if (gm < g.M) {
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
         const int gn = n0 + c0 + j;
@@ -251,11 +325,11 @@ __global__ void __launch_bounds__(kSlThreads, 1) k_gemm_sliced(SlicedGemmArgs g)
 #pragma unroll
         for (int l = kSl - 1; l >= 0; --l) acc = fma(acc, 0.0078125, (double)(int)v[l][j]);
         if (gn >= g.N) continue;
-        const double val = (acc * sa) * pow2(g.b_exp[gn]);
+        const double val = (acc * sa) * col_sc[c0 + j];
         if (g.epi == EPI_PROJ) {
           g.outf[(size_t)gm * g.ldo + gn] = (float)val;
         } else if (g.epi == EPI_L2 || g.epi == EPI_L2_ARGMIN) {
-          double d2 = __dadd_rn(__dsub_rn(g.rowterm[gm], __dmul_rn(2.0, val)), g.colterm[gn]);
+          double d2 = __dadd_rn(__dsub_rn(rterm, __dmul_rn(2.0, val)), col_t[c0 + j]);
           d2 = d2 > 0.0 ? d2 : 0.0;
           if (g.epi == EPI_L2) g.outd[(size_t)gm * g.ldo + gn] = d2;
           else if (d2 < best) { best = d2; bcol = gn; }  // columns ascend: ties keep the lowest

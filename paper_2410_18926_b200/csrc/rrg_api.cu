@@ -806,7 +806,7 @@ RrgOpts read_opts() {
   o.host_pieces = std::max(0, std::min(8, flag("RRG_HOST_PIECES", 0)));
   o.graph = flag("RRG_GRAPH", 1) != 0;
   o.screen = env("RRG_SCREEN") ? (flag("RRG_SCREEN", 0) != 0) : -1;
-  o.route_screen = flag("RRG_ROUTE_SCREEN", 1) != 0;
+  o.route_screen = flag("RRG_ROUTE_SCREEN", 1);  // 0 off, 1 w = 1, 2 any w <= kRtMaxW
   o.screen_diag = flag("RRG_SCREEN_DIAG", 0);
   o.score_tc = env("RRG_SCORE_TC") ? (flag("RRG_SCORE_TC", 0) != 0) : -1;
   o.sparse_variant = flag("RRG_SPARSE_VARIANT", 1);
@@ -1101,7 +1101,8 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
           al256((size_t)ns * 4) + al256(route_cnt_bytes(ns, v.L)) + al256(route_list_bytes(ns, v.L));
       // (w = 1 only: at C3, w = 4, the per-thread candidate lists cost more than the f64
       // GEMM they replace -- 0.43 vs 0.25 ms)
-      if (ns > kSmallBatch && w == 1 && v.rt_cent_tiles && v.opt.route_screen &&
+      if (ns > kSmallBatch && (w == 1 || (v.opt.route_screen == 2 && w <= kRtMaxW)) && v.rt_cent_tiles &&
+          v.opt.route_screen &&
           rt_need <= (size_t)ns * v.L * 8) {
         // bounds on the fp16 tensor cores, f64 recheck of the few candidates that can be
         // among the w nearest (rrg_route_screen.cu); scratch inside this piece's rows of

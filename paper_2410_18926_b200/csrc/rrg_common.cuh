@@ -37,7 +37,7 @@ struct RrgOpts {
   int host_pieces;   // RRG_HOST_PIECES: 0 auto
   int graph;         // RRG_GRAPH: captured graphs for small host batches (default 1)
   int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
-  int route_screen;  // RRG_ROUTE_SCREEN (default 1): fp16 tensor-core routing bounds + f64 recheck
+  int route_screen;  // RRG_ROUTE_SCREEN: fp16 tensor-core routing bounds + f64 recheck (0 off, 1 at w = 1, 2 at any w <= 8)
   int screen_diag;   // RRG_SCREEN_DIAG: timing probes of k_rr_screen (1: no MMAs, 2: no MMAs or bounds)
   int score_tc;      // RRG_SCORE_TC: stage B of the cluster scoring on tcgen05 (kind::i8): -1 auto
   int sparse_variant;  // RRG_SPARSE_VARIANT: k_rerank_sparse 0 register prefetch / 1 more CTAs

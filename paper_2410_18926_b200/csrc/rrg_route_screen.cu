@@ -151,7 +151,9 @@ __device__ __forceinline__ void rt_bounds(float G, float sc, float ppq, float cc
   lb = fmaxf(S - E, 0.f);
 }
 
-template <int LOC>
+// WM: the w the running-bound list is sized for (1, or kRtMaxW for any w <= 8 -- the
+// general form's insertion and w-th selection were ~half the epilogue's instructions)
+template <int LOC, int WM>
 __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs a) {
   extern __shared__ __align__(1024) unsigned char rt_sm[];
   __shared__ uint64_t afull, bfull[2], bempty[2], tfull[2], tempty[2];
@@ -236,9 +238,9 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
 #pragma unroll
     for (int i = 0; i < LOC; ++i) { lid[i] = -1; llb[i] = 0.f; }  // lid < 0: empty
     bool over = false;
-    float best[kRtMaxW];
+    float best[WM];
 #pragma unroll
-    for (int i = 0; i < kRtMaxW; ++i) best[i] = __int_as_float(0x7f800000);
+    for (int i = 0; i < WM; ++i) best[i] = __int_as_float(0x7f800000);
     for (int t = t0; t < t1; ++t) {
       const int i = t - t0, buf = i & 1, u = i >> 1;
       {  // the tile's centroid terms, one per epilogue thread, while the MMAs run
@@ -276,10 +278,10 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
             const float4 cs = cst[c0 + j];  // (c >= L: c.c = +inf, never a survivor)
             float lb, ub;
             rt_bounds(__uint_as_float(v[j]), scq * cs.z, ppq, cs.w, nhq, neq, cs.x, cs.y, a.eps, lb, ub);
-            if (ub < best[kRtMaxW - 1]) {  // insertion into the sorted w smallest
+            if (ub < best[WM - 1]) {  // insertion into the sorted w smallest
               float x = ub;
 #pragma unroll
-              for (int s = 0; s < kRtMaxW; ++s) {
+              for (int s = 0; s < WM; ++s) {
                 const float lo = fminf(best[s], x);
                 x = fmaxf(best[s], x);
                 best[s] = lo;
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
             }
             float bw = best[0];  // the running w-th smallest UB
 #pragma unroll
-            for (int s = 1; s < kRtMaxW; ++s)
+            for (int s = 1; s < WM; ++s)
               if (s == a.w - 1) bw = best[s];
             if (!(lb > bw) && c < a.L) {  // (NaN bounds are listed too)
               bool placed = false;  // into an empty slot or one no longer within the bound
@@ -307,7 +309,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) k_route_screen(RouteScreenArgs 
       // this thread's w-th smallest UB bounds the query's w-th smallest d2 (if it saw w)
       float tw = best[0];
 #pragma unroll
-      for (int s = 0; s < kRtMaxW; ++s)
+      for (int s = 0; s < WM; ++s)
         if (s == a.w - 1) tw = best[s];
       if (tw == tw && tw < __int_as_float(0x7f800000)) atomicMin(a.T + q, __float_as_uint(tw));
       int2* lst = a.list + ((size_t)q * a.nslot + slot) * kRtLoc;
@@ -454,7 +456,7 @@ void launch_route_screen(const RouteScreenHost& h, int nq, cudaStream_t st) {
   const size_t sm = (size_t)3 * v.rt_kc * kRtChunk + 1024;
   static int done[64] = {};
   if (dev >= 0 && dev < 64 && !done[dev]) {
-    for (const void* f : {(const void*)k_route_screen<4>, (const void*)k_route_screen<kRtLoc>}) {
+    for (const void* f : {(const void*)k_route_screen<4, 1>, (const void*)k_route_screen<kRtLoc, kRtMaxW>}) {
       cudaFuncAttributes at{};
       cudaFuncGetAttributes(&at, f);
       cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmemPerCta - (int)at.sharedSizeBytes);
@@ -464,9 +466,9 @@ void launch_route_screen(const RouteScreenHost& h, int nq, cudaStream_t st) {
   dim3 grid(qblocks, groups);
   // w = 1: the near-ties of the running minimum (4 slots, fewer registers); w <= 8: 12
   if (h.w == 1)
-    (k_route_screen<4><<<grid, kRtThreads, sm, st>>>(a), note_launch());
+    (k_route_screen<4, 1><<<grid, kRtThreads, sm, st>>>(a), note_launch());
   else
-    (k_route_screen<kRtLoc><<<grid, kRtThreads, sm, st>>>(a), note_launch());
+    (k_route_screen<kRtLoc, kRtMaxW><<<grid, kRtThreads, sm, st>>>(a), note_launch());
   (k_route_recheck<<<(nq + 7) / 8, 256, 0, st>>>(h.xp, nq, v.s, v.cent, v.L, h.w, h.pp, v.cnorm, h.T, h.cnt,
                                                  h.list, a.nslot, h.sel, h.primary),
    note_launch());

@@ -940,7 +940,7 @@ def test_route_screen_matches_f64_routing(pkg, tmp_path, d, s, L, ties, monkeypa
     q = np.random.default_rng(s).standard_normal((700, d)).astype(F32)
     oidx = O.read_index(blob)
     for w in (1, 3, 8):
-        monkeypatch.setenv("RRG_ROUTE_SCREEN", "1")
+        monkeypatch.setenv("RRG_ROUTE_SCREEN", "2")  # (the default takes it at w = 1 only)
         dev.reload_options()
         got = dev.search_host(q, 10, w, 60, True)
         monkeypatch.setenv("RRG_ROUTE_SCREEN", "0")

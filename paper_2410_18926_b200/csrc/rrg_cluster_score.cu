@@ -167,6 +167,7 @@ struct ClusterScoreArgs {
   int* dbg_raw1;
   int* dbg_raw2;
   float* dbg_score;
+  int stage_a_bytes;     // > 0: stage A operands staged in shared memory ((r + 32) * s_pad)
 };
 
 // TC: stage B on the 5th-gen tensor cores.  A work item's (<= 32) queries form the
@@ -185,6 +186,7 @@ constexpr uint32_t kScIdesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(k
 template <bool TC>
 __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
   const DevIndexView& ix = a.ix;
+  extern __shared__ __align__(16) int8_t sc_dyn[];  // stage A operands (a.stage_a_bytes)
   __shared__ int item_s;
   // TC: A tile (128 points x 32 B), B tile (32 queries x 32 B), canonical K-major layout
   __shared__ __align__(128) int8_t tc_a[TC ? 128 * 32 : 16];
@@ -253,6 +255,21 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
       const int prs = np * r;
       int parts = 1;
       while (parts < 32 && prs * parts * 2 <= CNT && parts * 2 <= nvec) parts <<= 1;
+      // the cluster's A^T codes and the item's query codes staged once (all loads in
+      // flight together): reading them per product from L2 was a chain of dependent
+      // round trips per item (C2: the kernel's top stall)
+      const bool staged = a.stage_a_bytes > 0;
+      int8_t* s_at = sc_dyn;
+      int8_t* s_qc = sc_dyn + (size_t)r * s_pad;
+      if (staged) {
+        const int4* ga = reinterpret_cast<const int4*>(ix.at + (size_t)slot * r * s_pad);
+        for (int e = tid; e < r * nvec; e += CNT) reinterpret_cast<int4*>(s_at)[e] = __ldg(ga + e);
+        for (int e = tid; e < np * nvec; e += CNT) {
+          const int pi = e / nvec, u = e - pi * nvec;
+          reinterpret_cast<int4*>(s_qc)[e] = __ldg(reinterpret_cast<const int4*>(a.qcodes + (size_t)pq[pi] * s_pad) + u);
+        }
+        __syncthreads();
+      }
       for (int base = 0; base < prs * parts; base += CNT) {
         const int e = base + tid;
         const int pr = e / parts, part = e % parts;
@@ -260,10 +277,12 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
         const int pi = act ? pr / r : 0, jj = act ? pr % r : 0;
         int raw = 0;
         if (act) {
-          const int4* aw = reinterpret_cast<const int4*>(ix.at + ((size_t)slot * r + jj) * s_pad);
-          const int4* q4 = reinterpret_cast<const int4*>(a.qcodes + (size_t)pq[pi] * s_pad);
+          const int4* aw = staged ? reinterpret_cast<const int4*>(s_at + (size_t)jj * s_pad)
+                                  : reinterpret_cast<const int4*>(ix.at + ((size_t)slot * r + jj) * s_pad);
+          const int4* q4 = staged ? reinterpret_cast<const int4*>(s_qc + (size_t)pi * s_pad)
+                                  : reinterpret_cast<const int4*>(a.qcodes + (size_t)pq[pi] * s_pad);
           for (int u = part; u < nvec; u += parts) {
-            int4 b = __ldg(aw + u), cc = __ldg(q4 + u);
+            int4 b = staged ? aw[u] : __ldg(aw + u), cc = staged ? q4[u] : __ldg(q4 + u);
             raw = __dp4a(cc.x, b.x, raw);
             raw = __dp4a(cc.y, b.y, raw);
             raw = __dp4a(cc.z, b.z, raw);
@@ -2174,10 +2193,14 @@ void launch_cluster_scoring(const ClusterScoringHost& h, int nq, cudaStream_t st
   // -- measured C5 w=64 4.51 -> 4.14 ms, w=16 1.54 -> 1.40 ms; C2 (10 per cluster) 0.13 ->
   // 0.14 ms, where the items hold few queries and the dp4a loop is cheaper
   const bool tc = ix.opt.score_tc >= 0 ? ix.opt.score_tc != 0 : (double)nq * h.w >= 64.0 * ix.L;
+  // stage A operands in shared memory while they fit beside 4 CTAs per SM
+  const size_t sa = (size_t)(ix.r + kPairsPerItem) * ix.s_pad;
+  a.stage_a_bytes = ix.opt.score_stage_a && sa <= 32 * 1024 ? (int)sa : 0;
+  const size_t dyn = (size_t)a.stage_a_bytes;
   if (ix.quantized && ix.r_pad == 32 && tc)
-    (k_score_cluster<true><<<sms * RRG_SCORE_CTAS, CNT, 0, st>>>(a), note_launch());
+    (k_score_cluster<true><<<sms * RRG_SCORE_CTAS, CNT, dyn, st>>>(a), note_launch());
   else if (ix.quantized)
-    (k_score_cluster<false><<<sms * RRG_SCORE_CTAS, CNT, 0, st>>>(a), note_launch());
+    (k_score_cluster<false><<<sms * RRG_SCORE_CTAS, CNT, dyn, st>>>(a), note_launch());
   else
     (k_score_cluster_f32<<<sms * 4, CNT, 0, st>>>(a), note_launch());
 }

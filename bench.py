@@ -398,7 +398,9 @@ class LocalSearcher:
 
 
 class ShardedSearcher:
-    """Cluster-sharded index over the ranks; queries broadcast; two NCCL all-gather merges."""
+    """Cluster-sharded index over the ranks: data-parallel front stages (one all-gather of
+    the front rows), w = 1 owner-local search, and each rank keeps the results of its own
+    query slice (one all-to-all, sharded.slice_results)."""
 
     def __init__(self, dev, k, w, t):
         from paper_2410_18926_b200.sharded import CudaShardEngine, TorchExchange
@@ -410,10 +412,11 @@ class ShardedSearcher:
     def device_step(self, q, out):
         from paper_2410_18926_b200.sharded import sharded_search
 
-        ids, sc, cnt = sharded_search(self.engine, self.ex, q, self.k, self.w, self.t)
-        out[0].copy_(ids)
-        out[1].copy_(sc)
-        out[2].copy_(cnt)
+        ids, sc, cnt = sharded_search(self.engine, self.ex, q, self.k, self.w, self.t, results="slice")
+        a = min(q.shape[0], self.ex.rank * -(-q.shape[0] // self.ex.world))
+        out[0][a:a + ids.shape[0]].copy_(ids)
+        out[1][a:a + ids.shape[0]].copy_(sc)
+        out[2][a:a + ids.shape[0]].copy_(cnt)
         return out
 
     def host_step(self, qpin, hout):

@@ -1199,6 +1199,23 @@ __global__ void __launch_bounds__(MNT) k_merge(int mode, int metric, int nq, int
   }
   __syncthreads();
   const int n = base[G];
+  if (mode == 1) {  // one contributing shard (every row of the w = 1 owner-local search):
+                    // its result list is already sorted by (distance, id), copied as is
+    int g1 = -1, nz = 0;
+    for (int g = 0; g < G; ++g)
+      if (base[g + 1] > base[g]) { g1 = g; ++nz; }
+    if (nz <= 1 && n <= take) {
+      const size_t src = ((size_t)(g1 < 0 ? 0 : g1) * nq + q) * cap;
+      for (int i = tid; i < take; i += MNT) {
+        const size_t o = (size_t)q * take + i;
+        static_cast<float*>(out_keys)[o] =
+            i < n ? static_cast<const float*>(in_keys)[src + i] : __int_as_float(0x7fc00000);
+        static_cast<int64_t*>(out_ids)[o] = i < n ? static_cast<const int64_t*>(in_ids)[src + i] : -1;
+      }
+      if (tid == 0) out_count[q] = n;
+      return;
+    }
+  }
   for (int g = 0; g < G; ++g) {
     const int c = base[g + 1] - base[g];
     const size_t src = ((size_t)g * nq + q) * cap;

@@ -101,6 +101,11 @@ def _gloo_worker_dp(rank, world, port, blob, q, params, out_dir):
                                           data_parallel_front=True)
             np.savez(os.path.join(out_dir, f"r{rank}_p{j}.npz"), ids=ids.numpy(), sc=sc.numpy(),
                      cnt=cnt.numpy())
+            # each rank keeps its own slice's rows (one all-to-all instead of the all-gather)
+            ids, sc, cnt = sharded_search(engines[rank], ex, torch.from_numpy(q), k, w, t,
+                                          data_parallel_front=True, results="slice")
+            np.savez(os.path.join(out_dir, f"r{rank}_p{j}_slice.npz"), ids=ids.numpy(), sc=sc.numpy(),
+                     cnt=cnt.numpy())
     finally:
         dist.destroy_process_group()
 
@@ -121,15 +126,23 @@ def test_three_rank_gloo_data_parallel_front(tmp_path):
     mp.spawn(_gloo_worker_dp, args=(world, _free_port(), blob, q, params, str(tmp_path)), nprocs=world,
              join=True)
     idx = O.read_index(blob)
+    S = -(-q.shape[0] // world)
     for j, (k, w, t) in enumerate(params):
         ref = O.query_batch(idx, q, k, w, t, True)
         for r in range(world):
             got = np.load(tmp_path / f"r{r}_p{j}.npz")
+            sl = np.load(tmp_path / f"r{r}_p{j}_slice.npz")
+            assert sl["cnt"].shape[0] == min(q.shape[0], (r + 1) * S) - r * S
             for i, rr in enumerate(ref):
                 c = int(got["cnt"][i])
                 assert c == len(rr.ids), (r, j, i)
                 np.testing.assert_array_equal(got["ids"][i, :c], rr.ids)
                 np.testing.assert_array_equal(got["sc"][i, :c].view(np.int32), rr.scores.view(np.int32))
+                if r * S <= i < (r + 1) * S:
+                    ii = i - r * S
+                    assert int(sl["cnt"][ii]) == c
+                    np.testing.assert_array_equal(sl["ids"][ii, :c], rr.ids)
+                    np.testing.assert_array_equal(sl["sc"][ii, :c].view(np.int32), rr.scores.view(np.int32))
 
 
 def test_two_rank_gloo_matches_unsharded(tmp_path):

@@ -506,9 +506,13 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
                   for g, e in enumerate(engines)]
             front = Front(**{n: torch.cat([getattr(f[0], n) for f in fr]) for n in Front.FIELDS})
             res = [timed(lambda e=e: e.search_from_front(queries, front, k, w, t)) for e in engines]
-            out, m2 = timed(lambda: engines[0].merge_results(torch.stack([r[0][0] for r in res]),
-                                                             torch.stack([r[0][1] for r in res]),
-                                                             torch.stack([r[0][2] for r in res]), k))
+            out, _ = timed(lambda: engines[0].merge_results(torch.stack([r[0][0] for r in res]),
+                                                            torch.stack([r[0][1] for r in res]),
+                                                            torch.stack([r[0][2] for r in res]), k))
+            # each rank merges only its slice's rows (sharded.slice_results): time slice 0,
+            # its [G, S, ...] inputs laid out as the all-to-all delivers them
+            sl = [torch.stack([r[0][j][:S] for r in res]) for j in range(3)]
+            _, m2 = timed(lambda: engines[0].merge_results(sl[0], sl[1], sl[2], k))
             p1 = [f[1] for f in fr]
             p2 = [r[1] for r in res]
             cur = (max(p1) + max(p2) + m2, p1, p2, m2)
@@ -534,7 +538,7 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
         search_stages = {nm: round(ms_[i], 4) for i, nm in enumerate(names) if ms_[i] > 0}
         s_pad = (args.s + 15) // 16 * 16
         xf = (G - 1) * S * (args.s * 4 + s_pad + 4 + 4 + 8 + 4 + 4 + 4)  # front rows all-gathered
-        x2 = (G - 1) * nq * (k * 12 + 4)                                  # results all-gathered
+        x2 = (G - 1) * S * (k * 12 + 4)                                   # result rows all-to-all
         xch_ms = (xf + x2) / (args.link_gbs * 1e9) * 1e3
         compute_ms, p1, p2, m2 = best
         del engines
@@ -545,7 +549,8 @@ def shard_emulation(args, arrs, corpus_h, queries, ids, sc, cnt, w, t, G):
                 "exchange_bytes_per_rank": xf + x2, "exchange_ms_est": round(xch_ms, 4),
                 "step_ms_est": round(compute_ms + xch_ms, 4), "qps_est": nq / (compute_ms + xch_ms) * 1e3,
                 "note": "w=1 owner-local flow (data-parallel front slices, each shard searches the queries "
-                        "routed to its clusters, one results all-gather + merge); shards run one after "
+                        "routed to its clusters, one all-to-all of the result rows by query slice + merge "
+                        "of the rank's slice); shards run one after "
                         f"another on one GPU; all-gather bytes at {args.link_gbs:.0f} GB/s (estimated)"}
     best = None
     for _ in range(3):  # first pass warms up workspaces

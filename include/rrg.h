@@ -281,6 +281,18 @@ int64_t rrg_last_launch_count(void);
 void rrg_set_stage_timing(int enabled);
 int rrg_stage_times(double* ms, int64_t* launches);
 
+/* Critical-path spans recorded while stage timing is on, as events on the launching
+ * stream only (side-stream work that overlaps them is not added in):
+ *   RRG_PATH_RERANK  from the re-rank screen's launch (or the exact pass when there is
+ *                    no screen) to the end of the final top-k;
+ *   RRG_PATH_SEARCH  from a search's first launch to its last.
+ * rrg_path_times synchronizes, writes the accumulated milliseconds and span counts
+ * (arrays of RRG_N_PATHS) and resets them. */
+#define RRG_PATH_RERANK 0
+#define RRG_PATH_SEARCH 1
+#define RRG_N_PATHS 2
+int rrg_path_times(double* ms, int64_t* count);
+
 /* Re-rank work counters accumulated by the searches of this thread while stage timing
  * is enabled (the roofline's algorithmic bytes come from these): returns and resets
  *   0 candidates entering the screen (sum over queries of the top-t size)

@@ -93,6 +93,7 @@ SIGNATURES = {
     "rrg_last_launch_count": (c_i64, []),
     "rrg_set_stage_timing": (None, [c_int]),
     "rrg_stage_times": (c_int, [c_vp, c_vp]),
+    "rrg_path_times": (c_int, [c_vp, c_vp]),
     "rrg_search_counters": (c_int, [c_vp]),
     "rrg_last_error": (ctypes.c_char_p, []),
     "rrg_last_error_kind": (ctypes.c_char_p, []),

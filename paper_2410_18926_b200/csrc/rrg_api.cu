@@ -43,6 +43,11 @@ struct StageTimer {
   std::vector<cudaEvent_t> pool;
   int64_t* dcounters = nullptr;  // device counters (rrg_search_counters), while timing is on
   int cdev = -1;
+  // critical-path spans on the launching stream (rrg_path_times)
+  cudaEvent_t path_open[RRG_N_PATHS] = {};
+  std::vector<Rec> path_pending;
+  double pms[RRG_N_PATHS] = {0};
+  int64_t pn[RRG_N_PATHS] = {0};
   cudaEvent_t get() {
     if (!pool.empty()) { cudaEvent_t e = pool.back(); pool.pop_back(); return e; }
     cudaEvent_t e;
@@ -100,6 +105,22 @@ int64_t* counters_ptr(cudaStream_t st) {
 
 // Runs one launch, counting it and (when enabled) bracketing it with events; a launch
 // rejected at submission (bad grid / shared-memory size) fails here, naming its stage.
+void path_begin(int p, cudaStream_t st) {
+  StageTimer& t = g_timer;
+  if (!t.on) return;
+  if (t.path_open[p]) t.pool.push_back(t.path_open[p]);
+  t.path_open[p] = t.get();
+  cudaEventRecord(t.path_open[p], st);
+}
+void path_end(int p, cudaStream_t st) {
+  StageTimer& t = g_timer;
+  if (!t.on || !t.path_open[p]) return;
+  StageTimer::Rec r{p, t.path_open[p], t.get()};
+  cudaEventRecord(r.b, st);
+  t.path_pending.push_back(r);
+  t.path_open[p] = nullptr;
+}
+
 template <typename F>
 void staged(int stage, cudaStream_t st, F&& launch) {
   StageTimer& t = g_timer;
@@ -1046,6 +1067,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
   int* gp = reinterpret_cast<int*>(base + p.off_gp);
   int* prim = reinterpret_cast<int*>(base + p.off_prim);
   int* order = reinterpret_cast<int*>(base + p.off_order);
+  path_begin(RRG_PATH_SEARCH, st);
   for (int64_t q0 = 0; q0 < nq; q0 += p.qc) {
     const int n = (int)std::min<int64_t>(p.qc, nq - q0);
     const float* x = queries + q0 * v.d;
@@ -1234,6 +1256,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       // the screen (every SM, HBM-bound) runs after the selection: launched on the side
       // stream next to the scoring it measured no faster (C2 1.45 vs 1.44 ms), its
       // persistent CTAs leave no room for the scoring and selection CTAs
+      if (p.rr_mode == 1) path_begin(RRG_PATH_RERANK, st);
       if (p.screen) staged(9, st, [&] { launch_screen(sh, n, st); });
       if (p.screen) staged(9, st, [&] { launch_thresh(sh, n, st); });
       if (p.rr_mode == 1) {
@@ -1260,6 +1283,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         fh.out_ids = ids; fh.out_scores = scores; fh.out_count = count; fh.q0 = (int)q0;
         fh.order = order;
         staged(5, st, [&] { launch_topk_final(fh, n, st); });
+        path_end(RRG_PATH_RERANK, st);
       }
     }
     if (rerank && !ph1 && p.rr_mode == 0) {
@@ -1267,10 +1291,13 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       ra.ix = v; ra.queries = x; ra.cand_pos = cpos; ra.cand_n = cn; ra.take_cap = p.take_cap;
       ra.k = k; ra.out_ids = ids; ra.out_scores = scores; ra.out_count = count; ra.q0 = (int)q0;
       ra.order = order;
+      path_begin(RRG_PATH_RERANK, st);
       staged(5, st, [&] { launch_rerank(ra, n, st); });
+      path_end(RRG_PATH_RERANK, st);
     }
     CUDA_TRY(cudaGetLastError());
   }
+  path_end(RRG_PATH_SEARCH, st);
 }
 
 template <typename F>
@@ -2060,6 +2087,26 @@ int rrg_stage_times(double* ms, int64_t* launches) {
     if (launches) launches[i] = t.n[i];
     t.ms[i] = 0;
     t.n[i] = 0;
+  }
+  return RRG_OK;
+}
+int rrg_path_times(double* ms, int64_t* count) {
+  StageTimer& t = g_timer;
+  for (auto& r : t.path_pending) {
+    cudaEventSynchronize(r.b);
+    float el = 0.f;
+    cudaEventElapsedTime(&el, r.a, r.b);
+    t.pms[r.stage] += el;
+    t.pn[r.stage] += 1;
+    t.pool.push_back(r.a);
+    t.pool.push_back(r.b);
+  }
+  t.path_pending.clear();
+  for (int i = 0; i < RRG_N_PATHS; ++i) {
+    if (ms) ms[i] = t.pms[i];
+    if (count) count[i] = t.pn[i];
+    t.pms[i] = 0;
+    t.pn[i] = 0;
   }
   return RRG_OK;
 }

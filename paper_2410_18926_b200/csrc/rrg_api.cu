@@ -62,11 +62,13 @@ thread_local StageTimer g_timer;
 struct AuxStream {
   int device = -1;
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, cfork = nullptr, cjoin = nullptr;
   ~AuxStream() {
     if (s) cudaStreamDestroy(s);
     if (fork) cudaEventDestroy(fork);
     if (join) cudaEventDestroy(join);
+    if (cfork) cudaEventDestroy(cfork);
+    if (cjoin) cudaEventDestroy(cjoin);
   }
 };
 thread_local AuxStream g_aux;
@@ -78,9 +80,13 @@ AuxStream& aux_stream() {
     if (a.s) cudaStreamDestroy(a.s);
     if (a.fork) cudaEventDestroy(a.fork);
     if (a.join) cudaEventDestroy(a.join);
+    if (a.cfork) cudaEventDestroy(a.cfork);
+    if (a.cjoin) cudaEventDestroy(a.cjoin);
     cudaStreamCreateWithFlags(&a.s, cudaStreamNonBlocking);
     cudaEventCreateWithFlags(&a.fork, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&a.join, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&a.cfork, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&a.cjoin, cudaEventDisableTiming);
     a.device = dev;
   }
   return a;
@@ -1273,9 +1279,14 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         if (p.screen) { rh.cand_idx = cidx; rh.cand_n = cn; rh.take_cap = p.take_cap; }
         rh.xint = reinterpret_cast<float*>(base + p.off_xint);
         rh.counters = counters_ptr(st);
-        if (rh.counters)  // rows the exact pass needs: union over each cluster's queries
+        if (rh.counters) {  // rows the exact pass needs: union over each cluster's queries
+          // (measurement only; on the side stream, outside the stage's span)
+          CUDA_TRY(cudaEventRecord(ax.cfork, st));
+          CUDA_TRY(cudaStreamWaitEvent(ax.s, ax.cfork, 0));
           launch_count_rows(v, ch.pair_off, ch.pairs, ch.kbase, ch.qoff, w, marks,
-                            p.screen ? cidx : nullptr, cn, p.take_cap, p.mwords, rh.counters + 4, st);
+                            p.screen ? cidx : nullptr, cn, p.take_cap, p.mwords, rh.counters + 4, ax.s);
+          CUDA_TRY(cudaEventRecord(ax.cjoin, ax.s));
+        }
         staged(5, st, [&] { launch_cluster_rerank(rh, st); });
         TopkFinalHost fh{};
         fh.ix = v; fh.sel = sel; fh.w = w; fh.qoff = ch.qoff; fh.kbase = ch.kbase; fh.diss = ch.keys;
@@ -1284,6 +1295,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         fh.order = order;
         staged(5, st, [&] { launch_topk_final(fh, n, st); });
         path_end(RRG_PATH_RERANK, st);
+        if (rh.counters) CUDA_TRY(cudaStreamWaitEvent(st, ax.cjoin, 0));
       }
     }
     if (rerank && !ph1 && p.rr_mode == 0) {

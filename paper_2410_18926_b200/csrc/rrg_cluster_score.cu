@@ -2243,11 +2243,13 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
                          kMaxSmemPerCta - (int)at.sharedSizeBytes);
     done[dev] = 1;
   }
-  // warp per query at any list length once the batch fills the GPU (measured on C5:
-  // w=16 (~16k candidates) 2.0 vs 4.9 ms, w=64 (~62k) 6.6 vs 14.5 ms for the CTA select)
+  // warp per query once the batch fills the GPU, for lists up to kSelBigN keys
   // (the membership bits are sized by kcap = min(largest list, 24k): a capped kcap
   // cannot hold every candidate's bit, so the CTA select handles that case)
-  if (warp_select_ok(h.ix, nq) && h.rerank && !(h.marks && h.kcap >= 24 * 1024)) {
+  // long lists without membership bits (C5's per-query re-rank) take the CTA select
+  // with its sampled range: w=64 (~62k keys) 14.5 -> 9.9 ms per batch, w=16 5.5 -> 4.3
+  const bool long_lists = !h.marks && h.kcap >= kSelBigN && h.ix.opt.warp_select < 0;
+  if (warp_select_ok(h.ix, nq) && h.rerank && !(h.marks && h.kcap >= 24 * 1024) && !long_lists) {
     // 8 warps per CTA; keys staged on-chip only while that keeps >= 32 warps per SM
     const int bits_cap = h.marks ? h.kcap : 0;
     const int stage_cap = 0;  // keys are read through L1
@@ -2262,7 +2264,11 @@ void launch_select_topt(const SelectTopTHost& h, int nq, cudaStream_t st) {
     (k_select_topt_warp<<<(nq + wpc - 1) / wpc, 32 * wpc, per * wpc, st>>>(a, stage_cap, bits_cap, nq), note_launch());
     return;
   }
-  (k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, h.kcap), st>>>(a), note_launch());
+  // long lists without membership bits: no key staging (the sampled two-sweep select
+  // reads each key twice from HBM anyway), so the CTA's shared memory stays small and
+  // 8 CTAs fit per SM (staging 24k keys left 2)
+  if (!h.marks && h.kcap >= kSelBigN) a.kcap = 0;
+  (k_select_topt<<<nq, TNT, select_topt_smem(h.w, h.take_cap, h.k, a.kcap), st>>>(a), note_launch());
 }
 
 // RRG_RR_ASYNC=1 (ix.opt.rr_async): cp.async row staging -- measured on C2 (w=1,

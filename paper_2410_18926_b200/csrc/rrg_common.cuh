@@ -409,6 +409,8 @@ __device__ int block_select_smallest(int n, int take, KeyF key, TieF tie, int* o
 // keys) falls back to the radix select above.
 constexpr int kSelBins = 2048;
 constexpr int kSelBuf = 512;
+constexpr int kSelBigN = 16384;   // block selections: sampled range + 8 keys in flight from here
+constexpr int kSelSamples = 512;  // (fits bs.buf_key before the boundary buffer is needed)
 
 struct BucketSmem {
   int hist[kSelBins];
@@ -421,6 +423,24 @@ struct BucketSmem {
 };
 
 __device__ __forceinline__ int bitlen64(unsigned long long v) { return v ? 64 - __clzll(v) : 0; }
+
+// Bitonic sort (ascending) of n_pow2 u64 keys in shared memory; pad with ~0.
+template <int NT>
+__device__ void block_bitonic_sort(uint64_t* a, int n_pow2) {
+  for (int size = 2; size <= n_pow2; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < n_pow2 / 2; t += NT) {
+        int lo = 2 * t - (t & (stride - 1));
+        int hi = lo + stride;
+        bool up = ((lo & size) == 0);
+        uint64_t x = a[lo], y = a[hi];
+        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
+      }
+    }
+  }
+  __syncthreads();
+}
 
 // Bucketing is linear in the key's float value v: b = min(B-1, floor(rn(rn(v - vmin) *
 // scale))), a monotone non-decreasing map (IEEE rounding is monotone), so every
@@ -436,34 +456,75 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, ValF v
     return n;
   }
   if (take <= 0) return 0;
-  // 1. value range (keys are monotone in value, so the extreme keys give it)
-  unsigned long long lo = ~0ull, hi = 0ull;
-  for (int i = tid; i < n; i += NT) {
-    unsigned long long k = (unsigned long long)key(i);
-    lo = k < lo ? k : lo;
-    hi = k > hi ? k : hi;
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
-    unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
-    lo = a < lo ? a : lo;
-    hi = b > hi ? b : hi;
-  }
+  // long lists with a small take (C5: 1,600 of ~62k keys): the bucket range comes from
+  // kSelSamples spread samples -- [smallest sample, a sample well above rank take] --
+  // instead of a min/max sweep, and the sweeps keep 8 keys per thread in flight.  Keys
+  // are clamped to the range first (a monotone map: lower buckets still precede higher
+  // ones, so the selection stays exact; an unlucky sample only overflows the boundary
+  // buffer into block_select_smallest).
+  const bool big = sizeof(K) == 4 && n >= kSelBigN && (long long)take * 8 <= n;
   if (tid == 0) { bs.lo = ~0ull; bs.hi = 0ull; bs.nbuf = 0; bs.count = 0; }
+  if (big) {
+    for (int sidx = tid; sidx < kSelSamples; sidx += NT) {
+      const int i = (int)((((long long)sidx * 2 + 1) * n) / (2 * kSelSamples));
+      bs.buf_key[sidx] = ((unsigned long long)key(i) << 32) | (unsigned)sidx;
+    }
+    block_bitonic_sort<NT>(reinterpret_cast<uint64_t*>(bs.buf_key), kSelSamples);  // (ends with a barrier)
+    const int rh = min(kSelSamples - 1, (int)(((long long)take * kSelSamples * 3) / (2LL * n)) + 24);
+    const unsigned long long slo = bs.buf_key[0] >> 32, shi = bs.buf_key[rh] >> 32;
+    __syncthreads();
+    if (tid == 0) { bs.lo = slo; bs.hi = shi; }
+  } else {
+    // 1. value range (keys are monotone in value, so the extreme keys give it)
+    unsigned long long lo = ~0ull, hi = 0ull;
+    for (int i = tid; i < n; i += NT) {
+      unsigned long long k = (unsigned long long)key(i);
+      lo = k < lo ? k : lo;
+      hi = k > hi ? k : hi;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+      unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = a < lo ? a : lo;
+      hi = b > hi ? b : hi;
+    }
+    __syncthreads();
+    if (lane == 0) { atomicMin(&bs.lo, lo); atomicMax(&bs.hi, hi); }
+  }
   for (int i = tid; i < kSelBins; i += NT) bs.hist[i] = 0;
   __syncthreads();
-  if (lane == 0) { atomicMin(&bs.lo, lo); atomicMax(&bs.hi, hi); }
-  __syncthreads();
-  const V vmin = val((K)bs.lo), vmax = val((K)bs.hi);
+  const K klo = (K)bs.lo, khi = (K)bs.hi;
+  const V vmin = val(klo), vmax = val(khi);
   const V range = vmax - vmin;
   const V scale = range > (V)0 ? (V)(kSelBins - 1) / range : (V)0;
-  auto bucket = [&](int i) {
-    V f = (val(key(i)) - vmin) * scale;
+  auto bucket_k = [&](K kk) {
+    kk = kk < klo ? klo : (kk > khi ? khi : kk);  // (no-op for the swept range)
+    V f = (val(kk) - vmin) * scale;
     int b = (int)f;
     return b < kSelBins - 1 ? (b < 0 ? 0 : b) : kSelBins - 1;
   };
+  auto bucket = [&](int i) { return bucket_k(key(i)); };
   // 2. histogram
-  for (int i = tid; i < n; i += NT) atomicAdd(&bs.hist[bucket(i)], 1);
+  if (big) {
+    // keys above the sampled range (most of them) are only counted, per warp: one
+    // shared-memory counter hit by every thread would serialise the sweep
+    int above = 0;
+    for (int b0 = tid; b0 < n; b0 += NT * 8) {
+      K kv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) kv[u] = b0 + u * NT < n ? key(b0 + u * NT) : khi;
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (b0 + u * NT >= n) continue;
+        if (kv[u] > khi) ++above;
+        else atomicAdd(&bs.hist[bucket_k(kv[u])], 1);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) above += __shfl_xor_sync(0xffffffffu, above, o);
+    if (lane == 0 && above) atomicAdd(&bs.hist[kSelBins - 1], above);
+  } else {
+    for (int i = tid; i < n; i += NT) atomicAdd(&bs.hist[bucket(i)], 1);
+  }
   __syncthreads();
   // 3. boundary bucket: block exclusive scan of per-thread bin ranges
   constexpr int per = kSelBins / NT;
@@ -508,16 +569,15 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, ValF v
     return block_select_smallest<NT, K>(n, take, key, tie, out, sm);
   }
   // 4. collect
-  for (int base = 0; base < n; base += NT) {
-    int i = base + tid;
+  auto collect = [&](int i, bool valid, K kk) {
     bool sel = false;
-    if (i < n) {
-      int b = bucket(i);
+    if (valid) {
+      int b = bucket_k(kk);
       if (b < bb || (b == bb && all_eq)) {
         sel = true;
       } else if (b == bb) {
         int s = atomicAdd(&bs.nbuf, 1);
-        bs.buf_key[s] = (unsigned long long)key(i);
+        bs.buf_key[s] = (unsigned long long)kk;
         bs.buf_tie[s] = tie(i);
         bs.buf_idx[s] = i;
       }
@@ -527,6 +587,26 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, ValF v
     if (lane == 0 && m) slot = atomicAdd(&bs.count, __popc(m));
     slot = __shfl_sync(0xffffffffu, slot, 0);
     if (sel) out[slot + __popc(m & ((1u << lane) - 1))] = i;
+  };
+  if (big) {
+    for (int base = 0; base < n; base += NT * 8) {
+      K kv[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * NT + tid;
+        kv[u] = i < n ? key(i) : khi;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = base + u * NT + tid;
+        collect(i, i < n, kv[u]);
+      }
+    }
+  } else {
+    for (int base = 0; base < n; base += NT) {
+      const int i = base + tid;
+      collect(i, i < n, i < n ? key(i) : khi);
+    }
   }
   __syncthreads();
   // 5. exact resolution of the boundary bucket by (key, tie) rank
@@ -545,24 +625,6 @@ __device__ int block_select_bucketed(int n, int take, KeyF key, TieF tie, ValF v
     __syncthreads();
   }
   return take;
-}
-
-// Bitonic sort (ascending) of n_pow2 u64 keys in shared memory; pad with ~0.
-template <int NT>
-__device__ void block_bitonic_sort(uint64_t* a, int n_pow2) {
-  for (int size = 2; size <= n_pow2; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      __syncthreads();
-      for (int t = threadIdx.x; t < n_pow2 / 2; t += NT) {
-        int lo = 2 * t - (t & (stride - 1));
-        int hi = lo + stride;
-        bool up = ((lo & size) == 0);
-        uint64_t x = a[lo], y = a[hi];
-        if ((x > y) == up) { a[lo] = y; a[hi] = x; }
-      }
-    }
-  }
-  __syncthreads();
 }
 
 }  // namespace rrg

@@ -790,12 +790,18 @@ def test_fused_nearest_cluster_ties(pkg, tmp_path):
         np.testing.assert_array_equal(ids[i, :c], r.ids, err_msg=f"q{i}")
 
 
+@pytest.mark.parametrize("select", ["warp", "auto"])
 @pytest.mark.parametrize("rerank_mode", ["query", "cluster"])
-def test_long_candidate_lists(pkg, tmp_path, rerank_mode, monkeypatch):
+def test_long_candidate_lists(pkg, tmp_path, rerank_mode, select, monkeypatch):
     """~30k candidates per query (w = L on 4 large clusters): the warp top-t streams
     long lists (per-query re-rank) and yields to the CTA select where its membership
-    bits would not fit (cluster-major re-rank, lists above the 24k key cap)."""
-    monkeypatch.setenv("RRG_WARP_SELECT", "1")
+    bits would not fit (cluster-major re-rank, lists above the 24k key cap); "auto"
+    takes the CTA select's long-list path (sampled bucket range, clamped keys, 8 keys
+    in flight) -- with duplicated rows, so the boundary holds exact ties."""
+    if select == "warp":
+        monkeypatch.setenv("RRG_WARP_SELECT", "1")
+    else:
+        monkeypatch.delenv("RRG_WARP_SELECT", raising=False)
     monkeypatch.setenv("RRG_RERANK", rerank_mode)
     from index_writer import random_index
     from oracle import rrann_oracle as O
@@ -904,6 +910,38 @@ def test_screen_counters_and_pruning(pkg, tmp_path, monkeypatch):
     assert 2000 * 10 <= cand <= 2000 * 400       # sum of min(t, candidates) per query
     assert 2000 * 10 <= surv < cand / 4, (surv, cand)
     assert streamed >= 6000 and distinct <= 6000 and fetched >= distinct
+
+
+def test_path_times_and_timing_invariance(pkg, tmp_path, monkeypatch):
+    """rrg_path_times: the re-rank span lies inside the search span, one of each per
+    search; results are the same with the timers (and the side-stream row count) on."""
+    import ctypes
+
+    from index_writer import random_index
+    from paper_2410_18926_b200 import _native
+
+    monkeypatch.setenv("RRG_SCREEN", "1")
+    monkeypatch.setenv("RRG_RERANK", "cluster")
+    blob = random_index(768, 64, 16, 8, 4000, "euclidean", seed=6)  # (d = 768: the cluster-major plan)
+    dev = pkg.DeviceIndex.from_file(_write(tmp_path, "pt", blob))
+    q = torch.from_numpy(np.random.default_rng(1).standard_normal((1500, 768)).astype(F32)).cuda()
+    ref = [a.cpu() for a in dev.search_device(q, 10, 1, 300, True)]
+    ms, n = (ctypes.c_double * 2)(), (ctypes.c_int64 * 2)()
+    c = (ctypes.c_int64 * 8)()
+    _native.lib.rrg_set_stage_timing(1)
+    _native.lib.rrg_path_times(ms, n)
+    _native.lib.rrg_search_counters(c)
+    got = []
+    for _ in range(3):
+        got = [a.cpu() for a in dev.search_device(q, 10, 1, 300, True)]
+    _native.lib.rrg_path_times(ms, n)
+    _native.lib.rrg_search_counters(c)
+    _native.lib.rrg_set_stage_timing(0)
+    assert n[0] == 3 and n[1] == 3, (n[0], n[1])
+    assert 0.0 < ms[0] <= ms[1], (ms[0], ms[1])
+    assert c[4] > 0  # the row-union count ran (side stream)
+    for a, b in zip(got, ref):
+        assert torch.equal(torch.nan_to_num(a), torch.nan_to_num(b))
 
 
 # ------------------------------------------------------------- routing screen

@@ -450,6 +450,15 @@ void build_device_index(RrgIndex* ix, HostModel& hm, bool has_corpus, CorpusFill
   v.cent = ix->upload(hm.centroids);
   v.cnorm = ix->upload(cnorm);
   v.cl_pos = ix->upload(cl_pos);
+  {  // clusters by held size, largest first (ties by id): the order the sparse exact
+     // pass hands out its work items, so the longest items do not form the grid's tail
+    std::vector<int> ord(L);
+    for (int l = 0; l < L; ++l) ord[l] = l;
+    std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) {
+      return cl_pos[a + 1] - cl_pos[a] > cl_pos[b + 1] - cl_pos[b];
+    });
+    v.cl_order = ix->upload(ord);
+  }
   v.cl_kind = ix->upload(cl_kind);
   v.cl_aidx = ix->upload(cl_aidx);
   v.at = ix->upload(at);
@@ -834,6 +843,7 @@ RrgOpts read_opts() {
   o.graph = flag("RRG_GRAPH", 1) != 0;
   o.screen = env("RRG_SCREEN") ? (flag("RRG_SCREEN", 0) != 0) : -1;
   o.score_stage_a = flag("RRG_SCORE_STAGE_A", 1);
+  o.rr_order = flag("RRG_RR_ORDER", 1);
   o.route_screen = flag("RRG_ROUTE_SCREEN", 1);  // 0 off, 1 w = 1, 2 any w <= kRtMaxW
   o.screen_diag = flag("RRG_SCREEN_DIAG", 0);
   o.score_tc = env("RRG_SCORE_TC") ? (flag("RRG_SCORE_TC", 0) != 0) : -1;

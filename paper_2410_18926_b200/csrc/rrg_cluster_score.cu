@@ -1177,6 +1177,7 @@ struct ClusterRerankArgs {
   DevIndexView ix;
   const float* queries;  // chunk-local [nq][d]
   const float* xint;     // the same queries interleaved like the corpus rows [nq][d_stride]
+  int ordered;           // rr_item_off runs over ix.cl_order (sparse kernels)
   const int* cand_idx;   // k_rerank_sparse: the screen's survivors per query
   const int* cand_n;
   int take_cap;
@@ -1198,11 +1199,15 @@ struct ClusterRerankArgs {
 // rr_item_off for the re-rank work items (one CTA)
 __global__ void __launch_bounds__(PNT) k_rr_items(const int* __restrict__ pair_off,
                                                   const int* __restrict__ cl_pos, int L, int rows,
-                                                  int* __restrict__ rr_item_off) {
+                                                  int* __restrict__ rr_item_off,
+                                                  const int* __restrict__ order = nullptr) {
+  // entry j counts the items of cluster order[j] (or j): the kernels map an item back
+  // through the same order
   __shared__ int tot;
-  for (int l = threadIdx.x; l < L; l += PNT) {
+  for (int j = threadIdx.x; j < L; j += PNT) {
+    const int l = order ? order[j] : j;
     const int cnt = pair_off[l + 1] - pair_off[l], m = cl_pos[l + 1] - cl_pos[l];
-    rr_item_off[l] = ((cnt + kRrQ - 1) / kRrQ) * ((m + rows - 1) / rows);
+    rr_item_off[j] = ((cnt + kRrQ - 1) / kRrQ) * ((m + rows - 1) / rows);
   }
   __syncthreads();
   block_exclusive_scan_inplace(rr_item_off, L, &tot);
@@ -1667,10 +1672,10 @@ __global__ void __launch_bounds__(SNT, CT) k_rerank_sparse(ClusterRerankArgs a) 
       const int mid = (lo + hi) >> 1;
       if (a.rr_item_off[mid] <= item) lo = mid; else hi = mid;
     }
-    const int l = lo;
+    const int l = a.ordered ? __ldg(ix.cl_order + lo) : lo;  // (largest clusters first)
     const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
     const int nrc = (m + a.rr_rows - 1) / a.rr_rows;
-    const int local = item - a.rr_item_off[l];
+    const int local = item - a.rr_item_off[lo];
     const int qc = nrc > 0 ? local / nrc : 0, rc = nrc > 0 ? local % nrc : 0;
     const int j0 = a.pair_off[l] + qc * kRrQ;
     const int ng = min(kRrQ, a.pair_off[l + 1] - j0);
@@ -1858,10 +1863,10 @@ __global__ void __launch_bounds__(RNT, NH == 1 ? 2 : 1) k_rerank_sparse_ring(Clu
       const int mid = (lo + hi) >> 1;
       if (a.rr_item_off[mid] <= item) lo = mid; else hi = mid;
     }
-    const int l = lo;
+    const int l = a.ordered ? __ldg(ix.cl_order + lo) : lo;  // (largest clusters first)
     const int p0 = ix.cl_pos[l], m = ix.cl_pos[l + 1] - p0;
     const int nrc = (m + a.rr_rows - 1) / a.rr_rows;
-    const int local = item - a.rr_item_off[l];
+    const int local = item - a.rr_item_off[lo];
     const int qc = nrc > 0 ? local / nrc : 0, rc = nrc > 0 ? local % nrc : 0;
     const int j0 = a.pair_off[l] + qc * kRrQ;
     const int ng = min(kRrQ, a.pair_off[l + 1] - j0);
@@ -2303,7 +2308,12 @@ void launch_cluster_rerank(const ClusterRerankHost& h, cudaStream_t st) {
   // sparse (screened) items: whole clusters (up to kSpRows rows) amortise the item
   // staging; small batches keep the short items that spread one query over CTAs
   if (h.compact) a.rr_rows = probes >= 512 ? kSpRows : std::min(a.rr_rows, kSpRows);
-  (k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off), note_launch());
+  // the sparse kernels take the items largest cluster first (their work is about
+  // proportional to the cluster's rows): in cluster order the long items formed the
+  // grid's tail (C2: SMs active 83% of the kernel on average)
+  a.ordered = h.compact && h.ix.metric == kMetricEuclidean && h.ix.opt.rr_order;
+  (k_rr_items<<<1, PNT, 0, st>>>(h.pair_off, h.ix.cl_pos, h.ix.L, a.rr_rows, h.rr_item_off,
+                                 a.ordered ? h.ix.cl_order : nullptr), note_launch());
   a.diss = h.diss; a.work_counter = h.work_counter; a.mwords = h.mwords;
   a.neg_zero = -0.0f;
   a.counters = h.counters;

@@ -38,6 +38,7 @@ struct RrgOpts {
   int graph;         // RRG_GRAPH: captured graphs for small host batches (default 1)
   int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
   int score_stage_a;  // RRG_SCORE_STAGE_A (default 1): K4 stage-A operands staged in shared memory
+  int rr_order;       // RRG_RR_ORDER (default 1): sparse re-rank items largest cluster first
   int route_screen;  // RRG_ROUTE_SCREEN: fp16 tensor-core routing bounds + f64 recheck (0 off, 1 at w = 1, 2 at any w <= 8)
   int screen_diag;   // RRG_SCREEN_DIAG: timing probes of k_rr_screen (1: no MMAs, 2: no MMAs or bounds)
   int score_tc;      // RRG_SCORE_TC: stage B of the cluster scoring on tcgen05 (kind::i8): -1 auto
@@ -59,6 +60,7 @@ struct DevIndexView {
   const float* cent;     // L x s
   const double* cnorm;   // L: (c*c).sum(axis=1) in f64, NumPy pairwise order
   const int* cl_pos;     // L+1: first global position of each cluster (cluster order)
+  const int* cl_order;   // L: clusters by held size, largest first (sparse re-rank items)
   const int* cl_kind;    // L
   const int* cl_aidx;    // L: rrr -> model slot in at/ahead/ascale; exact -> row in xcodes
   const int8_t* at;      // [n_rrr][r][s_pad]: A^T codes, row 0 of A (pad) kept as column 0

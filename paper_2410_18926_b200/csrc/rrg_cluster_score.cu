@@ -1639,7 +1639,10 @@ __device__ __forceinline__ float sparse_row(unsigned act, int nact, const float*
 }
 
 constexpr int SNT = 256;
-constexpr int kSpRows = 1024;
+#ifndef RRG_SP_ROWS
+#define RRG_SP_ROWS 2048  // rows per sparse item: C2 512 -> 1.248, 1024 -> 1.237, 2048 -> 1.224, 4096 -> 1.353 ms (smem)
+#endif
+constexpr int kSpRows = RRG_SP_ROWS;
 // PF: the next row's loads are issued before this row's arithmetic (register double
 // buffer); CT: resident CTAs per SM the register budget targets
 template <int NB, int NH, bool PF = true, int CT = (NH == 1 ? 2 : 1)>

@@ -381,8 +381,6 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   const int i0 = (int)((int64_t)total * blockIdx.x / gridDim.x);
   const int i1 = (int)((int64_t)total * (blockIdx.x + 1) / gridDim.x);
   if (i0 >= i1) return;  // uniform over the CTA, before any barrier or TMEM use
-  if (a.counters && tid == 0)
-    atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 2), (unsigned long long)(i1 - i0) * kScrRows);
 
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(s_addr(&tmem_base))
@@ -450,6 +448,7 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
   if (warp == 0) {
     if (lane == 0) {  // producer: group records and the CTA's blocks through the ring
       int slot = 0, pass = 0, j = -1, pl = -1, pg = -1;
+      long long rows_streamed = 0;  // rrg_search_counters[2] (whole 8-row atoms)
       ItemIt t = it_begin(i0);
       for (int i = i0, it = 0; i < i1; ++i, ++it, i < i1 ? it_next(t) : void()) {
         const int l = t.l, gi = t.gi, b = t.b;
@@ -467,13 +466,21 @@ __global__ void __launch_bounds__(kScrThreads, 1) k_rr_screen(ScreenArgs a) {
         }
         const unsigned char* src = reinterpret_cast<const unsigned char*>(ix.scr_plane) +
                                    ((size_t)(ix.scr_blk0[l] + b) * KC) * kScrChunk;
+        // a stage is 16 row atoms of 1 KB (8 rows x 128 B): a cluster's last block
+        // copies only the atoms holding its rows (the padding rows' products land in
+        // accumulator rows the epilogue never reads)
+        const int mrows = min(kScrRows, (ix.cl_pos[l + 1] - ix.cl_pos[l]) - b * kScrRows);
+        const uint32_t sbytes = (uint32_t)((mrows + 7) >> 3) * (kScrStageBytes / (kScrRows / 8));
+        rows_streamed += (mrows + 7) & ~7;
         for (int c0 = 0; c0 < KC; c0 += kScrStageChunks) {
           if (pass > 0) scr_wait(&empty[slot], (pass - 1) & 1);
-          scr_expect_tx(&full[slot], kScrStageBytes);
-          scr_bulk(s_addr(ring + slot * kScrStageBytes), src + (size_t)c0 * kScrChunk, kScrStageBytes, &full[slot]);
+          scr_expect_tx(&full[slot], sbytes);
+          scr_bulk(s_addr(ring + slot * kScrStageBytes), src + (size_t)c0 * kScrChunk, sbytes, &full[slot]);
           if (++slot == nst) { slot = 0; ++pass; }
         }
       }
+      if (a.counters)
+        atomicAdd(reinterpret_cast<unsigned long long*>(a.counters + 2), (unsigned long long)rows_streamed);
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer

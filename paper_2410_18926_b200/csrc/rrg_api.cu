@@ -1082,7 +1082,7 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
   uint32_t* gk = reinterpret_cast<uint32_t*>(base + p.off_gk);
   int* gp = reinterpret_cast<int*>(base + p.off_gp);
   int* prim = reinterpret_cast<int*>(base + p.off_prim);
-  int* order = reinterpret_cast<int*>(base + p.off_order);
+  int* order_buf = reinterpret_cast<int*>(base + p.off_order);
   path_begin(RRG_PATH_SEARCH, st);
   for (int64_t q0 = 0; q0 < nq; q0 += p.qc) {
     const int n = (int)std::min<int64_t>(p.qc, nq - q0);
@@ -1203,7 +1203,11 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
       cp(fout->prim, prim, 4);
       continue;
     }
-    staged(6, st, [&] { launch_bucket(prim, n, v.L, order, st); });
+    // queries bucketed by nearest cluster: the per-query kernels then visit the queries
+    // cluster by cluster (L2 locality of the per-query re-rank's rows); the cluster-major
+    // path reads per-query key ranges only, so it keeps the batch order
+    int* order = p.score_mode != 0 && p.rr_mode == 1 && v.opt.rr_order ? nullptr : order_buf;
+    if (order) staged(6, st, [&] { launch_bucket(prim, n, v.L, order, st); });
     ScoreArgsHost sa{};
     sa.ix = v; sa.qcodes = qcodes; sa.qscale = qscale; sa.qhead = qhead; sa.xx = xx; sa.sel = sel;
     sa.w = w; sa.take_cap = p.take_cap; sa.rerank = rerank; sa.k = k; sa.smem_cap = p.smem_cap;

@@ -110,7 +110,8 @@ __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel
                                                      int* __restrict__ pair_off,   // L+1
                                                      int* __restrict__ item_off,   // L+1
                                                      int* __restrict__ pairs,      // nq*w
-                                                     int* __restrict__ kbase) {    // nq+1
+                                                     int* __restrict__ kbase,      // nq+1
+                                                     int stage_kbase) {
   extern __shared__ int sh[];  // cnt[L], cur[L]
   int* cnt = sh;
   int* cur = sh + L;
@@ -134,10 +135,17 @@ __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel
   if (threadIdx.x == 0) item_off[L] = tot;
   // scatter (order inside a cluster's bucket is irrelevant to results)
   for (int i = threadIdx.x; i < np; i += PNT) pairs[atomicAdd(&cur[sel[i]], 1)] = i;
-  // key-array base per query
-  for (int q = threadIdx.x; q < nq; q += PNT) kbase[q] = ncand[q];
+  // key-array base per query: scanned in shared memory when the launch gave room for
+  // it (coalesced in and out; the in-place scan of global memory was a chain of
+  // dependent loads per thread)
+  int* kb = stage_kbase ? sh + 2 * L : kbase;
+  for (int q = threadIdx.x; q < nq; q += PNT) kb[q] = ncand[q];
   __syncthreads();
-  block_exclusive_scan_inplace(kbase, nq, &tot);
+  block_exclusive_scan_inplace(kb, nq, &tot);
+  if (stage_kbase) {
+    __syncthreads();
+    for (int q = threadIdx.x; q < nq; q += PNT) kbase[q] = kb[q];
+  }
   if (threadIdx.x == 0) kbase[nq] = tot;
 }
 
@@ -2187,8 +2195,11 @@ void launch_cluster_prep(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const DevIndexView& ix = h.ix;
   (k_cand_offsets<<<(nq + 7) / 8, 256, 0, st>>>(ix, h.sel, nq, h.w, h.qoff, h.ncand), note_launch());
   opt_in_smem(k_pairs_build, 15);  // L * 8 bytes: 64 KB at L = 8192 (C4)
-  (k_pairs_build<<<1, PNT, (size_t)ix.L * 8, st>>>(h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off,
-                                                  h.item_off, h.pairs, h.kbase), note_launch());
+  const size_t pb_stage = ((size_t)ix.L * 2 + nq + 1) * 4;
+  const int stage_kb = pb_stage <= 160 * 1024;
+  (k_pairs_build<<<1, PNT, stage_kb ? pb_stage : (size_t)ix.L * 8, st>>>(
+       h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off, h.item_off, h.pairs, h.kbase, stage_kb),
+   note_launch());
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
 }
 

@@ -54,6 +54,108 @@ __device__ __forceinline__ size_t sl_tiled_off(int r, int k, int s, int tile_row
 // Warp per row: e = exponent with max|x| < 2^e, then 8 truncated 7-bit digits of
 // x * 2^-e (each step u*128 and u - trunc(u) is exact in f32); rows >= rows_valid
 // (tile padding) and k >= K are zero.  Lane handles 4 consecutive k per step.
+__global__ void __launch_bounds__(256, 3) k_slice_rows16(const float* __restrict__ x, int rows_valid, int rows_pad, int K,
+                             int ld, int kchunks, int tile_rows, int8_t* __restrict__ planes,
+                             int* __restrict__ exps) {
+  const int row = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  const int Kp = kchunks * kSlBK;
+  if (row >= rows_pad) return;
+  const bool valid = row < rows_valid;
+  const float* r = x + (size_t)(valid ? row : 0) * ld;
+  // the row is read once: up to kSlRegK elements stay in registers (16 consecutive per
+  // lane per 512-element step) between the max pass and the slicing (two passes over
+  // global memory were latency-bound: C2 41 us for 7.7 M elements), and each lane's 16
+  // digits of one slice are one 16-byte store (4-byte stores kept the LSU busy: C3 97 us)
+  constexpr int kV = kSlRegK / 512;
+  const bool vec = ((ld & 3) == 0) && ((reinterpret_cast<uintptr_t>(x) & 15) == 0);
+  auto load4 = [&](int k0) {
+    float4 u = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (!valid || k0 >= K) return u;
+    if (vec && k0 + 4 <= K) return __ldg(reinterpret_cast<const float4*>(r + k0));
+    u.x = __ldg(r + k0);
+    if (k0 + 1 < K) u.y = __ldg(r + k0 + 1);
+    if (k0 + 2 < K) u.z = __ldg(r + k0 + 2);
+    if (k0 + 3 < K) u.w = __ldg(r + k0 + 3);
+    return u;
+  };
+  float4 xv[kV][4];
+  float mx = 0.f;
+  if (Kp <= kSlRegK) {
+#pragma unroll
+    for (int i = 0; i < kV; ++i)
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        xv[i][v] = load4(lane * 16 + 512 * i + 4 * v);
+        mx = fmaxf(mx, fmaxf(fmaxf(fabsf(xv[i][v].x), fabsf(xv[i][v].y)),
+                             fmaxf(fabsf(xv[i][v].z), fabsf(xv[i][v].w))));
+      }
+  } else if (valid) {
+    for (int k = lane; k < K; k += 32) mx = fmaxf(mx, fabsf(__ldg(r + k)));
+  }
+  for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  const int e = mx > 0.f ? ilogbf(mx) + 1 : 0;
+  if (lane == 0) exps[row] = e;
+  // |x| * 2^(56 - e) truncated to an integer (exact: x = m 2^x_e with a 24-bit m), whose
+  // base-128 digits, signed like x, are the slices -- the same digits as peeling
+  // trunc(u * 128) off u = x / 2^e eight times in f32 (each step exact; values below
+  // 2^-56 of the row max have all-zero slices either way), in integer instructions
+  auto fixed56 = [&](float xf) -> unsigned long long {
+    const uint32_t bits = __float_as_uint(xf);
+    const int be = (int)((bits >> 23) & 0xFFu);
+    if (be == 0xFF) return 0ull;  // non-finite rows are rejected before the projection
+    const unsigned long long m = be ? ((bits & 0x7FFFFFu) | 0x800000u) : (bits & 0x7FFFFFu);
+    const int sh = (be ? be : 1) - 150 - e + 56;  // x = m 2^(be - 150)
+    if (sh >= 0) return m << sh;                  // (< 2^56: |x| < 2^e)
+    return sh > -64 ? m >> -sh : 0ull;
+  };
+  // k0 % 16 == 0: the 16 bytes of one slice are contiguous in the tiled layout
+  auto slice16 = [&](int k0, const float4 (&xq)[4]) {
+    unsigned long long f[16];
+    uint32_t neg = 0;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      const float xs4[4] = {xq[v].x, xq[v].y, xq[v].z, xq[v].w};
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        f[4 * v + t] = fixed56(xs4[t]);
+        neg |= (__float_as_uint(xs4[t]) >> 31) << (4 * v + t);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kSl; ++s) {
+      uint32_t word[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        word[v] = 0;
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int dg = (int)((f[4 * v + t] >> (7 * (kSl - 1 - s))) & 127u);
+          word[v] |= (uint32_t)(uint8_t)(int8_t)(((neg >> (4 * v + t)) & 1u) ? -dg : dg) << (8 * t);
+        }
+      }
+      *reinterpret_cast<uint4*>(planes + sl_tiled_off(row, k0, s, tile_rows, kchunks)) =
+          make_uint4(word[0], word[1], word[2], word[3]);
+    }
+  };
+  if (Kp <= kSlRegK) {
+#pragma unroll
+    for (int i = 0; i < kV; ++i) {
+      const int k0 = lane * 16 + 512 * i;
+      if (k0 < Kp) slice16(k0, xv[i]);
+    }
+  } else {
+    for (int k0 = lane * 16; k0 < Kp; k0 += 512) {
+      float4 xq[4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) xq[v] = load4(k0 + 4 * v);
+      slice16(k0, xq);
+    }
+  }
+}
+
+// (K <= 1024: 4 elements per lane per step -- fewer registers, more warps per SM;
+// C2 37 us vs 45 us for k_slice_rows16, which wins from K = 1536: 71 vs 97 us)
 __global__ void k_slice_rows(const float* __restrict__ x, int rows_valid, int rows_pad, int K,
                              int ld, int kchunks, int tile_rows, int8_t* __restrict__ planes,
                              int* __restrict__ exps) {
@@ -369,8 +471,12 @@ void launch_slice_rows(const float* x, int rows, int K, int ld, bool a_operand, 
                        int* exps, cudaStream_t st) {
   const int rp = sliced_rows_pad(rows, a_operand);
   const int64_t blocks = ((int64_t)rp * 32 + 255) / 256;
-  (k_slice_rows<<<(unsigned)blocks, 256, 0, st>>>(x, rows, rp, K, ld, sliced_kchunks(K),
-                                                 a_operand ? kSlBM : kSlBN, planes, exps), note_launch());
+  if (K > 1024)
+    (k_slice_rows16<<<(unsigned)blocks, 256, 0, st>>>(x, rows, rp, K, ld, sliced_kchunks(K),
+                                                     a_operand ? kSlBM : kSlBN, planes, exps), note_launch());
+  else
+    (k_slice_rows<<<(unsigned)blocks, 256, 0, st>>>(x, rows, rp, K, ld, sliced_kchunks(K),
+                                                   a_operand ? kSlBM : kSlBN, planes, exps), note_launch());
 }
 
 void launch_gemm_sliced(const int8_t* a, const int* a_exp, int M, const int8_t* b, const int* b_exp,

@@ -619,6 +619,8 @@ int open_impl(const char* path, int device, int32_t cb, int32_t ce, RrgIndex** o
   const bool has_corpus = flags & RRG_FLAG_CORPUS;
   const bool exact_ivf = flags & RRG_FLAG_EXACT_IVF;
   if (ce < 0) ce = (int32_t)L;
+  if (cb < 0 || cb > ce || (int64_t)ce > (int64_t)L)
+    raise_usage("ParameterError", "shard cluster range [%d, %d) outside [0, %lld]", cb, ce, (long long)L);
   fr.vec(hm.projection, (uint64_t)d * s, "projection");
   fr.vec(hm.centroids, (uint64_t)L * s, "centroids");
   hm.clusters.resize(L);
@@ -2013,6 +2015,10 @@ int rrg_pack_candidates(int64_t nq, int32_t cap, const uint32_t* keys, const uin
                         int32_t* offsets, void* stream) {
   return guarded([&] {
     if (nq < 0 || cap < 1) raise_usage("ParameterError", "bad list shape");
+    // the packed offsets are int32: the exchange of one call holds < 2^31 entries
+    if (nq * (int64_t)cap > (int64_t)INT32_MAX)
+      raise_usage("ParameterError", "nq * cap = %lld exceeds the int32 offsets of the packed exchange; "
+                  "split the batch", (long long)(nq * (int64_t)cap));
     if (nq == 0) return RRG_OK;
     staged(4, static_cast<cudaStream_t>(stream), [&] {
       launch_pack_candidates((int)nq, cap, keys, ids, counts, packed_keys, packed_ids, offsets,

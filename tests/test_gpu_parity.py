@@ -324,6 +324,10 @@ def test_format_errors(pkg, tmp_path):
         pkg.DeviceIndex.from_file(_write(tmp_path, "c", bytes(bad)))
     with pytest.raises(pkg.FormatError, match="unknown trailing section"):
         pkg.DeviceIndex.from_file(_write(tmp_path, "x", blob + b"abc"))
+    good = _write(tmp_path, "g", blob)
+    for bad_range in [(-1, 2), (3, 2), (0, 10 ** 6)]:  # shard ranges outside [0, L]
+        with pytest.raises(pkg.ParameterError, match="shard cluster range"):
+            pkg.DeviceIndex.from_file(good, shard=bad_range)
 
 
 def test_drop_in_query_batch(pkg, tmp_path):

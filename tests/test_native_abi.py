@@ -66,3 +66,14 @@ def test_errors_subclass_reference(rrann_ref):
     assert issubclass(E.ParameterError, rrann_ref.ParameterError)
     assert issubclass(E.ShapeError, rrann_ref.RrannError)
     assert E.DataError.category == "data"
+
+
+def test_pack_candidates_rejects_int32_offset_overflow():
+    """rrg_pack_candidates' offsets are int32: a call whose lists could hold 2^31 entries is
+    a ParameterError, raised before any device work (so it runs without a GPU)."""
+    import paper_2410_18926_b200 as pkg
+    from paper_2410_18926_b200 import _native
+    from paper_2410_18926_b200._native import check
+
+    with pytest.raises(pkg.ParameterError, match="int32 offsets"):
+        check(_native.lib.rrg_pack_candidates(3_000_000, 800, None, None, None, None, None, None, None))

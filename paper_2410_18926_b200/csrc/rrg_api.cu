@@ -846,6 +846,7 @@ RrgOpts read_opts() {
   o.screen = env("RRG_SCREEN") ? (flag("RRG_SCREEN", 0) != 0) : -1;
   o.score_stage_a = flag("RRG_SCORE_STAGE_A", 1);
   o.rr_order = flag("RRG_RR_ORDER", 1);
+  o.score_order = flag("RRG_SCORE_ORDER", 1);
   o.route_screen = flag("RRG_ROUTE_SCREEN", 1);  // 0 off, 1 w = 1, 2 any w <= kRtMaxW
   o.screen_diag = flag("RRG_SCREEN_DIAG", 0);
   o.score_tc = env("RRG_SCORE_TC") ? (flag("RRG_SCORE_TC", 0) != 0) : -1;

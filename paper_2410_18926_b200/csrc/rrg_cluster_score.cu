@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel
                                                      int* __restrict__ item_off,   // L+1
                                                      int* __restrict__ pairs,      // nq*w
                                                      int* __restrict__ kbase,      // nq+1
-                                                     int stage_kbase) {
+                                                     int stage_kbase, const int* __restrict__ order) {
   extern __shared__ int sh[];  // cnt[L], cur[L]
   int* cnt = sh;
   int* cur = sh + L;
@@ -123,8 +123,11 @@ __global__ void __launch_bounds__(PNT) k_pairs_build(const int* __restrict__ sel
   __syncthreads();
   for (int i = threadIdx.x; i < L; i += PNT) {
     cur[i] = cnt[i];
-    const int m = cl_pos[i + 1] - cl_pos[i];
-    item_off[i] = ((cnt[i] + kPairsPerItem - 1) / kPairsPerItem) * ((m + kScorePts - 1) / kScorePts);
+    // the scoring items run largest cluster first when `order` is given (entry i counts
+    // the items of cluster order[i]; the kernel maps back through it)
+    const int l = order ? order[i] : i;
+    const int m = cl_pos[l + 1] - cl_pos[l];
+    item_off[i] = ((cnt[l] + kPairsPerItem - 1) / kPairsPerItem) * ((m + kScorePts - 1) / kScorePts);
   }
   __syncthreads();
   block_exclusive_scan_inplace(cur, L, &tot);
@@ -237,10 +240,10 @@ __global__ void __launch_bounds__(CNT) k_score_cluster(ClusterScoreArgs a) {
       int mid = (lo + hi) >> 1;
       if (a.item_off[mid] <= item) lo = mid; else hi = mid;
     }
-    const int l = lo;
+    const int l = ix.opt.score_order ? __ldg(ix.cl_order + lo) : lo;  // (largest clusters first)
     const int p0 = ix.cl_pos[l], mcl = ix.cl_pos[l + 1] - p0;
     const int npc = (mcl + kScorePts - 1) / kScorePts;
-    const int local = item - a.item_off[l];
+    const int local = item - a.item_off[lo];
     const int j0 = a.pair_off[l] + (local / npc) * kPairsPerItem;
     const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
     const int pbeg = (local % npc) * kScorePts, pend = min(mcl, pbeg + kScorePts);
@@ -487,10 +490,10 @@ __global__ void __launch_bounds__(CNT) k_score_cluster_f32(ClusterScoreArgs a) {
       int mid = (lo + hi) >> 1;
       if (a.item_off[mid] <= item) lo = mid; else hi = mid;
     }
-    const int l = lo;
+    const int l = ix.opt.score_order ? __ldg(ix.cl_order + lo) : lo;  // (largest clusters first)
     const int p0 = ix.cl_pos[l], mcl = ix.cl_pos[l + 1] - p0;
     const int npc = (mcl + kScorePts - 1) / kScorePts;
-    const int local = item - a.item_off[l];
+    const int local = item - a.item_off[lo];
     const int j0 = a.pair_off[l] + (local / npc) * kPairsPerItem;
     const int np = min(kPairsPerItem, a.pair_off[l + 1] - j0);
     const int pbeg = (local % npc) * kScorePts, pend = min(mcl, pbeg + kScorePts);
@@ -2198,7 +2201,8 @@ void launch_cluster_prep(const ClusterScoringHost& h, int nq, cudaStream_t st) {
   const size_t pb_stage = ((size_t)ix.L * 2 + nq + 1) * 4;
   const int stage_kb = pb_stage <= 160 * 1024;
   (k_pairs_build<<<1, PNT, stage_kb ? pb_stage : (size_t)ix.L * 8, st>>>(
-       h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off, h.item_off, h.pairs, h.kbase, stage_kb),
+       h.sel, nq, h.w, ix.L, ix.cl_pos, h.ncand, h.pair_off, h.item_off, h.pairs, h.kbase, stage_kb,
+       ix.opt.score_order ? ix.cl_order : nullptr),
    note_launch());
   cudaMemsetAsync(h.work_counter, 0, sizeof(int), st);
 }

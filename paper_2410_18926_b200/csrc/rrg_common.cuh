@@ -39,6 +39,7 @@ struct RrgOpts {
   int screen;        // RRG_SCREEN: -1 auto, 0 off, 1 on (tensor-core re-rank screen)
   int score_stage_a;  // RRG_SCORE_STAGE_A (default 1): K4 stage-A operands staged in shared memory
   int rr_order;       // RRG_RR_ORDER (default 1): sparse re-rank items largest cluster first
+  int score_order;    // RRG_SCORE_ORDER (default 1): scoring items largest cluster first
   int route_screen;  // RRG_ROUTE_SCREEN: fp16 tensor-core routing bounds + f64 recheck (0 off, 1 at w = 1, 2 at any w <= 8)
   int screen_diag;   // RRG_SCREEN_DIAG: timing probes of k_rr_screen (1: no MMAs, 2: no MMAs or bounds)
   int score_tc;      // RRG_SCORE_TC: stage B of the cluster scoring on tcgen05 (kind::i8): -1 auto

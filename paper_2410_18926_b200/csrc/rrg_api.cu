@@ -1182,6 +1182,18 @@ void search_impl(RrgIndex* ix, const float* queries, int64_t nq, int32_t k, int3
         staged(3, st, [&] {
           launch_route_nearest_reduce(part_v, part_i, ns, v.L, sel + s0, prim + s0, st);
         });
+      } else if (w > 1 && w <= 8 && ns > kSmallBatch && v.opt.route_fused && v.metric == kMetricEuclidean) {
+        // the w nearest straight from the GEMM: per (query, 64-centroid tile) sorted top-4 / -8
+        // (C3, w = 4: the 164 MB f64 distance rows and their CTA-per-query select, 0.25 ms)
+        const int nt = route_nearest_tiles(v.L), tw = w <= 4 ? 4 : 8;
+        double* part_v = diss + (int64_t)s0 * nt * tw;
+        int* part_i = reinterpret_cast<int*>(diss + (int64_t)p.qc * nt * tw) + (int64_t)s0 * nt * tw;
+        staged(2, st, [&] {
+          launch_route_topw_fused(xps, v.cent, ns, v.L, v.s, w, pp + s0, v.cnorm, part_v, part_i, st);
+        });
+        staged(3, st, [&] {
+          launch_route_topw_reduce(part_v, part_i, ns, v.L, w, sel + (int64_t)s0 * w, prim + s0, st);
+        });
       } else {
         staged(2, st, [&] {
           route_dist(v, xps, ns, pp + s0, diss + (int64_t)s0 * v.L, qpl_s, qex, st);

@@ -130,6 +130,81 @@ __global__ void __launch_bounds__(64 * WM, WM == 2 ? 4 : WM == 3 ? 3 : 2) k_gemm
     if (kt + 1 < nk) sstore(buf ^ 1);
     __syncthreads();
   }
+  if constexpr (EPI == EPI_L2_TOP4 || EPI == EPI_L2_TOP8) {
+    // routing with 1 < w <= TW: each row's TW nearest columns of this tile by
+    // (dissimilarity, column), written as TW partials per (row, column tile); the
+    // f64 row of dissimilarities is never stored (C3: 164 MB per batch)
+    constexpr int TW = EPI == EPI_L2_TOP4 ? 4 : 8;
+    double* red_v = gemm_sm;                                          // [MBM][2][TW]
+    int* red_i = reinterpret_cast<int*>(gemm_sm + 2 * MBM * TW);      // [MBM][2][TW]
+    constexpr double kInfD = __builtin_huge_val();
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int rl = wm * 32 + i * 8 + (lane >> 2), gm = m0 + rl;
+      // this lane's 8 columns, sorted by (value, column) with an insertion network
+      double v[8];
+      int c[8];
+#pragma unroll
+      for (int t = 0; t < 8; ++t) { v[t] = kInfD; c[t] = 0x7fffffff; }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gn = n0 + wn * 32 + j * 8 + (lane & 3) * 2 + h;
+          double x = kInfD;
+          int xi = 0x7fffffff;
+          if (gn < N && gm < M) {
+            x = __dadd_rn(__dsub_rn(rowterm[gm], __dmul_rn(2.0, acc[i][j][h])), colterm[gn]);
+            x = x > 0.0 ? x : 0.0;
+            xi = gn;
+          }
+          bool in = false;
+#pragma unroll
+          for (int t = 0; t < 8; ++t)
+            if (in || x < v[t] || (x == v[t] && xi < c[t])) {
+              const double tv = v[t]; const int tc = c[t];
+              v[t] = x; c[t] = xi; x = tv; xi = tc; in = true;
+            }
+        }
+      // TW rounds of an argmin over the row's 4 lanes (xor 1, 2): the row's TW smallest
+      // of the warp's 32 columns
+#pragma unroll
+      for (int r = 0; r < TW; ++r) {
+        double b = v[0];
+        int bc = c[0];
+#pragma unroll
+        for (int o = 1; o <= 2; o <<= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+          const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+          if (ob < b || (ob == b && oc < bc)) { b = ob; bc = oc; }
+        }
+        if (c[0] == bc && bc != 0x7fffffff) {
+#pragma unroll
+          for (int t = 0; t < 7; ++t) { v[t] = v[t + 1]; c[t] = c[t + 1]; }
+          v[7] = kInfD; c[7] = 0x7fffffff;
+        }
+        if ((lane & 3) == 0) { red_v[(rl * 2 + wn) * TW + r] = b; red_i[(rl * 2 + wn) * TW + r] = bc; }
+      }
+    }
+    __syncthreads();
+    for (int r = tid; r < MBM; r += DMNT) {  // merge the two warp columns' sorted lists
+      const int gm = m0 + r;
+      if (gm >= M) continue;
+      const double* va = red_v + (r * 2) * TW;
+      const int* ia = red_i + (r * 2) * TW;
+      int p0 = 0, p1 = 0;
+      for (int k = 0; k < TW; ++k) {
+        const double a0 = va[p0], a1 = va[TW + p1];
+        const int i0 = ia[p0], i1 = ia[TW + p1];
+        const bool first = a0 < a1 || (a0 == a1 && i0 < i1);
+        const size_t o = ((size_t)gm * ldo + blockIdx.x) * TW + k;
+        outd[o] = first ? a0 : a1;
+        outi[o] = first ? i0 : i1;
+        if (first) ++p0; else ++p1;
+      }
+    }
+    return;
+  }
   if constexpr (EPI == EPI_L2_ARGMIN || EPI == EPI_NEGIP_ARGMIN) {
     // routing with w = 1: only each row's nearest column is needed -- reduce this
     // tile's 64 columns to (dissimilarity, lowest column) per row and write one partial
@@ -1498,6 +1573,80 @@ __global__ void k_route_nearest_partials(const double* __restrict__ pv, const in
 }
 
 int route_nearest_tiles(int L) { return (L + MBN - 1) / MBN; }
+
+// 1 < w <= 8: the w nearest of a query from its per-tile sorted top-TW partials (warp per
+// query: each lane merges its tiles' lists into a sorted top-TW, then w rounds of a warp
+// argmin by (dissimilarity, column) -- route()'s stable argsort order)
+template <int TW>
+__global__ void k_route_topw_partials(const double* __restrict__ part_v, const int* __restrict__ part_i, int nq,
+                                      int nt, int w, int* __restrict__ sel, int* __restrict__ primary) {
+  const int q = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (q >= nq) return;
+  constexpr double kInfD = __builtin_huge_val();
+  double v[TW];
+  int c[TW];
+#pragma unroll
+  for (int t = 0; t < TW; ++t) { v[t] = kInfD; c[t] = 0x7fffffff; }
+  for (int tile = lane; tile < nt; tile += 32) {
+    const size_t b = ((size_t)q * nt + tile) * TW;
+#pragma unroll
+    for (int k = 0; k < TW; ++k) {
+      double x = __ldg(part_v + b + k);
+      int xi = __ldg(part_i + b + k);
+      if (xi == 0x7fffffff) continue;
+      bool in = false;
+#pragma unroll
+      for (int t = 0; t < TW; ++t)
+        if (in || x < v[t] || (x == v[t] && xi < c[t])) {
+          const double tv = v[t]; const int tc = c[t];
+          v[t] = x; c[t] = xi; x = tv; xi = tc; in = true;
+        }
+    }
+  }
+  for (int r = 0; r < w; ++r) {
+    double b = v[0];
+    int bc = c[0];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(0xffffffffu, b, o);
+      const int oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (ob < b || (ob == b && oc < bc)) { b = ob; bc = oc; }
+    }
+    if (c[0] == bc) {
+#pragma unroll
+      for (int t = 0; t + 1 < TW; ++t) { v[t] = v[t + 1]; c[t] = c[t + 1]; }
+      v[TW - 1] = kInfD; c[TW - 1] = 0x7fffffff;
+    }
+    if (lane == 0) {
+      sel[(size_t)q * w + r] = bc == 0x7fffffff ? 0 : bc;
+      if (r == 0) primary[q] = bc == 0x7fffffff ? 0 : bc;
+    }
+  }
+}
+
+void launch_route_topw_fused(const float* xp, const float* cent, int nq, int L, int s, int w, const double* pp,
+                             const double* cnorm, double* part_v, int* part_i, cudaStream_t st) {
+  constexpr int WM = 4;
+  const int nt = route_nearest_tiles(L);
+  dim3 grid(nt, (nq + 32 * WM - 1) / (32 * WM));
+  if (w <= 4)
+    gemm_launch<EPI_L2_TOP4, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, part_v, nt, pp, cnorm,
+                                          part_i);
+  else
+    gemm_launch<EPI_L2_TOP8, true, WM, 8>(grid, st, xp, s, cent, s, nq, L, s, nullptr, part_v, nt, pp, cnorm,
+                                          part_i);
+}
+
+void launch_route_topw_reduce(const double* part_v, const int* part_i, int nq, int L, int w, int* sel,
+                              int* primary, cudaStream_t st) {
+  const int nt = route_nearest_tiles(L);
+  if (w <= 4)
+    (k_route_topw_partials<4><<<(nq + 7) / 8, 256, 0, st>>>(part_v, part_i, nq, nt, w, sel, primary),
+     note_launch());
+  else
+    (k_route_topw_partials<8><<<(nq + 7) / 8, 256, 0, st>>>(part_v, part_i, nq, nt, w, sel, primary),
+     note_launch());
+}
 
 void launch_route_nearest_fused(const float* xp, const float* cent, int nq, int L, int s, int metric,
                                 const double* pp, const double* cnorm, double* part_v, int* part_i,

@@ -15,6 +15,8 @@ constexpr int EPI_GT_L2 = 3;   // (qq - 2 q.c) + cc, no clip (bench.py:110)
 constexpr int EPI_GT_COS = 4;  // -(q.c / ||c||)           (bench.py:100-103,112)
 constexpr int EPI_L2_ARGMIN = 5;     // routing w = 1: per-row nearest column per tile
 constexpr int EPI_NEGIP_ARGMIN = 6;
+constexpr int EPI_L2_TOP4 = 7;       // routing 1 < w <= 4: per-row 4 nearest columns per tile
+constexpr int EPI_L2_TOP8 = 8;       //                w <= 8
 constexpr int kMaxSmemPerCta = 227 * 1024;  // B200 opt-in limit per CTA
 // cluster count bound: routing (w > 1) keeps 12 B per cluster in one CTA's shared memory
 constexpr int kMaxClusters = (kMaxSmemPerCta - 4096) / 12;
@@ -74,6 +76,10 @@ int route_nearest_tiles(int L);
 void launch_route_nearest_fused(const float* xp, const float* cent, int nq, int L, int s, int metric,
                                 const double* pp, const double* cnorm, double* part_v, int* part_i,
                                 cudaStream_t st);
+void launch_route_topw_fused(const float* xp, const float* cent, int nq, int L, int s, int w, const double* pp,
+                             const double* cnorm, double* part_v, int* part_i, cudaStream_t st);
+void launch_route_topw_reduce(const double* part_v, const int* part_i, int nq, int L, int w, int* sel,
+                              int* primary, cudaStream_t st);
 void launch_route_nearest_reduce(const double* part_v, const int* part_i, int nq, int L, int* sel,
                                  int* primary, cudaStream_t st);
 void launch_route_select(const double* diss, int nq, int L, int w, int* sel, int* primary,
